@@ -1,0 +1,223 @@
+"""ctypes front-end for the parity checkers (TEST INFRASTRUCTURE ONLY).
+
+Two libraries are exposed with one numpy-level API:
+
+* ``port()`` — ``oracle/_build/liboracle.so``, the C restatement in
+  ``diloco_oracle.c`` (cites /root/reference/proj file:line per function).
+* ``reference()`` — ``oracle/_ref/libdiloco_ref.so``, the reference's own
+  ``fp16.cpp tensor.cpp optim.cpp reduce.cpp`` compiled by ``oracle/Makefile``
+  and wrapped by ``ref_shim.cpp``.  Present when it was built in the build
+  container (it travels to the GPU box with the snapshot); ``None`` otherwise.
+
+Only tests/, ``__graft_entry__.smoke()`` and bench.py's CPU-baseline /
+``--impl reference`` arm may import this module.  The product package never
+does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+PORT_SO = os.path.join(HERE, "_build", "liboracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libdiloco_ref.so")
+
+_f32p = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
+_u16p = np.ctypeslib.ndpointer(np.uint16, flags="C_CONTIGUOUS")
+_sz = C.c_size_t
+_u64 = C.c_uint64
+
+OK, ESHAPE, ECONFIG, ENUMERIC, ECOLLECTIVE = 0, 1, 2, 3, 4
+
+
+def build(ref: bool | None = None) -> None:
+    """Compile the restatement (always) and the reference (when present)."""
+    targets = [PORT_SO]
+    if ref is None:
+        ref = os.path.isdir("/root/reference/proj/src")
+    if ref:
+        targets.append("ref")
+    subprocess.run(["make", "-s", "-C", HERE] + targets, check=True)
+
+
+class _Lib:
+    """Common numpy API over either library (prefix 'orc_' or 'ref_')."""
+
+    def __init__(self, path: str, prefix: str):
+        self.path = path
+        self.kind = "port" if prefix == "orc_" else "reference"
+        L = C.CDLL(path)
+        self._L = L
+        p = prefix
+
+        def fn(name, res, *args):
+            f = getattr(L, p + name)
+            f.restype = res
+            f.argtypes = list(args)
+            return f
+
+        self._enc1 = fn("fp16_encode", C.c_uint16, C.c_float)
+        self._dec1 = fn("fp16_decode", C.c_float, C.c_uint16)
+        self._enc = fn("encode_fp16", C.c_int, _f32p, _sz, _u16p)
+        self._dec = fn("decode_fp16", None if p == "orc_" else C.c_int, _u16p, _sz, _f32p)
+        self._all_finite = fn("all_finite", C.c_int, _f32p, _sz)
+        self._axpy = fn("axpy", None if p == "orc_" else C.c_int, C.c_float, _f32p, _f32p, _sz, _f32p)
+        self._lr_at = fn("lr_at", C.c_float, _u64, _u64, C.c_float, C.c_int, _u64)
+        self._adamw = fn("adamw_step", C.c_int, _f32p, _f32p, _f32p, _f32p, _sz, C.c_float,
+                         C.c_float, C.c_float, C.c_float, C.POINTER(_u64), C.c_float, _f32p)
+        self._nest = fn("nesterov_step", C.c_int, _f32p, _f32p, _f32p, _sz, C.c_float, C.c_float, _f32p)
+        self._unscale = fn("scaler_unscale_and_check", C.c_int, C.c_float, _f32p, _sz, _f32p)
+        self._scaler_update = fn("scaler_update", None, C.POINTER(C.c_float), C.POINTER(_u64), _u64, C.c_int)
+        self._part = fn("partition_ranges", None, _sz, _sz, C.POINTER(_sz), C.POINTER(_sz))
+        self._ppb = fn("per_peer_reduce_bytes", _u64, _sz, _sz, _sz, C.c_int)
+        self._fleet = fn("fleet_reduce_bytes", _u64, _sz, _sz, C.c_int)
+        if p == "orc_":
+            self._reduce = fn("reduce_average", C.c_int, C.POINTER(C.c_void_p), _sz, _sz, C.c_int,
+                              C.c_void_p, _f32p)
+            self._key = fn("rng_key", _u64, _u64, C.c_char_p, _u64)
+            self._fill = fn("rng_fill", None, _u64, _u64, _sz, C.c_float, C.c_float, _f32p)
+        else:
+            self._reduce = fn("reduce_average", C.c_int, C.POINTER(C.c_void_p), _sz, _sz, C.c_int, _f32p)
+            self._bench_outer = fn("bench_outer", C.c_int, C.c_int, _sz, _sz, C.c_int, C.c_int,
+                                   C.c_float, C.c_float, C.POINTER(C.c_double))
+            self._bench_inner = fn("bench_inner", C.c_int, C.c_int, _sz, C.c_int, C.POINTER(C.c_double))
+
+    # -- codec ---------------------------------------------------------------
+    def fp16_encode_scalar(self, x: float) -> int:
+        return int(self._enc1(float(x)))
+
+    def fp16_decode_scalar(self, b: int) -> float:
+        return float(self._dec1(int(b)))
+
+    def encode_fp16(self, v):
+        v = np.ascontiguousarray(v, np.float32)
+        out = np.empty(v.size, np.uint16)
+        ov = self._enc(v, v.size, out)
+        return out, bool(ov)
+
+    def decode_fp16(self, b):
+        b = np.ascontiguousarray(b, np.uint16)
+        out = np.empty(b.size, np.float32)
+        self._dec(b, b.size, out)
+        return out
+
+    # -- tensor ----------------------------------------------------------------
+    def all_finite(self, v) -> bool:
+        v = np.ascontiguousarray(v, np.float32)
+        return bool(self._all_finite(v, v.size))
+
+    def axpy(self, alpha, x, y):
+        x = np.ascontiguousarray(x, np.float32)
+        y = np.ascontiguousarray(y, np.float32)
+        out = np.empty_like(y)
+        self._axpy(alpha, x, y, x.size, out)
+        return out
+
+    # -- optim -----------------------------------------------------------------
+    def lr_at(self, warmup, total, base_lr, cosine, step) -> float:
+        return float(self._lr_at(warmup, total, base_lr, int(cosine), step))
+
+    def adamw_step(self, p, g, m, v, step_count, lr, b1=0.9, b2=0.95, eps=1e-8, wd=0.1):
+        """Returns (status, p_new, step_count); m and v are updated in place."""
+        p = np.ascontiguousarray(p, np.float32)
+        g = np.ascontiguousarray(g, np.float32)
+        assert m.dtype == np.float32 and v.dtype == np.float32
+        sc = _u64(step_count)
+        out = np.empty_like(p)
+        st = self._adamw(p, g, m, v, p.size, b1, b2, eps, wd, C.byref(sc), lr, out)
+        return st, out, int(sc.value)
+
+    def nesterov_step(self, p, g, buf, lr, mu):
+        p = np.ascontiguousarray(p, np.float32)
+        g = np.ascontiguousarray(g, np.float32)
+        out = np.empty_like(p)
+        st = self._nest(p, g, buf, p.size, lr, mu, out)
+        return st, out
+
+    def scaler_unscale_and_check(self, scale, g):
+        g = np.ascontiguousarray(g, np.float32)
+        out = np.empty_like(g)
+        ov = self._unscale(scale, g, g.size, out)
+        return out, bool(ov)
+
+    def scaler_update(self, scale, good, growth, overflow):
+        s = C.c_float(scale)
+        gd = _u64(good)
+        self._scaler_update(C.byref(s), C.byref(gd), growth, int(overflow))
+        return float(s.value), int(gd.value)
+
+    # -- reduce ----------------------------------------------------------------
+    def reduce_average(self, contribs, precision: int):
+        cs = [np.ascontiguousarray(c, np.float32) for c in contribs]
+        k, n = len(cs), (cs[0].size if cs else 0)
+        arr = (C.c_void_p * max(k, 1))(*[c.ctypes.data for c in cs])
+        out = np.empty(n, np.float32)
+        if self.kind == "port":
+            scratch = np.empty(max(k * n, 1), np.float32)
+            st = self._reduce(arr, k, n, precision, scratch.ctypes.data, out)
+        else:
+            st = self._reduce(arr, k, n, precision, out)
+        return st, out
+
+    def partition_ranges(self, n, k):
+        off = (_sz * k)()
+        ln = (_sz * k)()
+        self._part(n, k, off, ln)
+        return [(off[i], ln[i]) for i in range(k)]
+
+    def per_peer_reduce_bytes(self, n, k, rank, precision):
+        return int(self._ppb(n, k, rank, precision))
+
+    def fleet_reduce_bytes(self, n, k, precision):
+        return int(self._fleet(n, k, precision))
+
+    # -- CPU baseline harness (reference only) -----------------------------------
+    def bench_outer(self, threads, slice_len, k, precision, iters, lr=0.7, mu=0.9):
+        t = C.c_double(0)
+        st = self._bench_outer(threads, slice_len, k, precision, iters, lr, mu, C.byref(t))
+        if st:
+            raise RuntimeError(f"ref_bench_outer failed with status {st}")
+        return float(t.value)
+
+    def bench_inner(self, threads, slice_len, iters):
+        t = C.c_double(0)
+        st = self._bench_inner(threads, slice_len, iters, C.byref(t))
+        if st:
+            raise RuntimeError(f"ref_bench_inner failed with status {st}")
+        return float(t.value)
+
+
+_port = None
+_ref = None
+
+
+def port() -> _Lib:
+    global _port
+    if _port is None:
+        if not os.path.exists(PORT_SO):
+            build(ref=False)
+        _port = _Lib(PORT_SO, "orc_")
+    return _port
+
+
+def reference():
+    """The compiled reference, or None when oracle/_ref was never built."""
+    global _ref
+    if _ref is None and os.path.exists(REF_SO):
+        _ref = _Lib(REF_SO, "ref_")
+    return _ref
+
+
+# -- synthetic inputs, generated identically on CPU and GPU --------
+
+def rng_key(seed: int, purpose: str, index: int) -> int:
+    return int(port()._key(seed, purpose.encode(), index))
+
+
+def rng_fill(seed: int, purpose: str, index: int, n: int, lo: float, hi: float, first: int = 0):
+    out = np.empty(n, np.float32)
+    port()._fill(rng_key(seed, purpose, index), first, n, lo, hi, out)
+    return out

@@ -1,0 +1,322 @@
+// ref_shim.cpp — extern "C" wrappers around the REFERENCE implementation.
+//
+// TEST INFRASTRUCTURE ONLY.  oracle/Makefile compiles this file together with
+// the reference's own hot-path sources, straight from /root/reference/proj/src
+// (fp16.cpp tensor.cpp optim.cpp reduce.cpp), into oracle/_ref/libdiloco_ref.so
+// with the reference's flags (-ffp-contract=off, proj/CMakeLists.txt:18).  No
+// reference source is copied into this repository.  The .so is linked with
+// hidden visibility so only the ref_* symbols below are exported.
+//
+// Uses: (1) pin the C restatement (oracle/diloco_oracle.c) bit-for-bit,
+// (2) generate tests/golden fixtures, (3) the CPU baseline / `bench.py --impl
+// reference` arm (ref_bench_*), timing the reference's own functions.
+#include <atomic>
+#include <barrier>
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <thread>
+#include <vector>
+
+#include "diloco/fp16.hpp"
+#include "diloco/optim.hpp"
+#include "diloco/reduce.hpp"
+#include "diloco/rng.hpp"
+#include "diloco/tensor.hpp"
+
+#define REF_API extern "C" __attribute__((visibility("default")))
+
+using namespace diloco;
+
+namespace {
+
+enum { kOk = 0, kShape = 1, kConfig = 2, kNumeric = 3, kCollective = 4, kOther = 9 };
+
+ParamVector pv(const float* data, size_t n) {
+  return ParamVector(Layout::single("p", n), std::vector<float>(data, data + n));
+}
+
+void put(const ParamVector& v, float* out) {
+  std::memcpy(out, v.values().data(), v.size() * sizeof(float));
+}
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return kOk;
+  } catch (const ShapeError&) {
+    return kShape;
+  } catch (const ConfigError&) {
+    return kConfig;
+  } catch (const NumericError&) {
+    return kNumeric;
+  } catch (const CollectiveError&) {
+    return kCollective;
+  } catch (const std::exception&) {
+    return kOther;
+  }
+}
+
+}  // namespace
+
+REF_API uint16_t ref_fp16_encode(float v) { return fp16_encode(v); }
+REF_API float ref_fp16_decode(uint16_t b) { return fp16_decode(b); }
+
+REF_API int ref_encode_fp16(const float* v, size_t n, uint16_t* out) {
+  const Fp16Buffer b = encode_fp16(pv(v, n));
+  std::memcpy(out, b.bits.data(), n * sizeof(uint16_t));
+  return b.overflow ? 1 : 0;
+}
+
+REF_API int ref_decode_fp16(const uint16_t* b, size_t n, float* out) {
+  Fp16Buffer buf;
+  buf.bits.assign(b, b + n);
+  return guarded([&] { put(decode_fp16(buf, Layout::single("p", n)), out); });
+}
+
+REF_API int ref_all_finite(const float* v, size_t n) { return pv(v, n).all_finite() ? 1 : 0; }
+
+REF_API int ref_axpy(float alpha, const float* x, const float* y, size_t n, float* out) {
+  return guarded([&] { put(axpy(alpha, pv(x, n), pv(y, n)), out); });
+}
+
+REF_API float ref_lr_at(uint64_t warmup, uint64_t total, float base_lr, int cosine,
+                        uint64_t step) {
+  LrSchedule s;
+  s.warmup_steps = warmup;
+  s.total_steps = total;
+  s.base_lr = base_lr;
+  s.decay = cosine ? LrDecay::cosine : LrDecay::none;
+  return lr_at(s, step);
+}
+
+// adamw_step (optim.hpp:61-62): p -> out; m, v, step_count updated in place.
+REF_API int ref_adamw_step(const float* p, const float* g, float* m, float* v, size_t n,
+                           float b1, float b2, float eps, float wd, uint64_t* step_count,
+                           float lr, float* out) {
+  auto layout = Layout::single("p", n);
+  AdamWState st;
+  st.m = ParamVector(layout, std::vector<float>(m, m + n));
+  st.v = ParamVector(layout, std::vector<float>(v, v + n));
+  st.step_count = *step_count;
+  st.beta1 = b1;
+  st.beta2 = b2;
+  st.eps = eps;
+  st.weight_decay = wd;
+  const ParamVector params(layout, std::vector<float>(p, p + n));
+  const ParamVector grad(layout, std::vector<float>(g, g + n));
+  return guarded([&] {
+    const ParamVector o = adamw_step(st, params, grad, lr);
+    put(o, out);
+    put(st.m, m);
+    put(st.v, v);
+    *step_count = st.step_count;
+  });
+}
+
+// nesterov_step (optim.hpp:65-66): p -> out; momentum buffer in place.
+REF_API int ref_nesterov_step(const float* p, const float* g, float* buf, size_t n,
+                              float lr, float mu, float* out) {
+  auto layout = Layout::single("p", n);
+  NesterovState st;
+  st.momentum_buf = ParamVector(layout, std::vector<float>(buf, buf + n));
+  st.lr = lr;
+  st.momentum = mu;
+  const ParamVector params(layout, std::vector<float>(p, p + n));
+  const ParamVector grad(layout, std::vector<float>(g, g + n));
+  return guarded([&] {
+    const ParamVector o = nesterov_step(st, params, grad);
+    put(o, out);
+    put(st.momentum_buf, buf);
+  });
+}
+
+REF_API int ref_scaler_unscale_and_check(float scale, const float* g, size_t n, float* out) {
+  LossScaler s;
+  s.scale = scale;
+  const UnscaleResult r = scaler_unscale_and_check(s, pv(g, n));
+  put(r.grad, out);
+  return r.overflow ? 1 : 0;
+}
+
+REF_API void ref_scaler_update(float* scale, uint64_t* good, uint64_t growth, int overflow) {
+  LossScaler s;
+  s.scale = *scale;
+  s.consecutive_good = *good;
+  s.growth_interval = growth;
+  scaler_update(s, overflow != 0);
+  *scale = s.scale;
+  *good = s.consecutive_good;
+}
+
+// reduce_average (reduce.hpp:65-66) over k contributions of n floats.
+REF_API int ref_reduce_average(const float* const* contribs, size_t k, size_t n,
+                               int precision, float* out) {
+  auto layout = Layout::single("delta", n);
+  std::vector<ParamVector> vs;
+  vs.reserve(k);
+  for (size_t j = 0; j < k; ++j) {
+    vs.emplace_back(layout, std::vector<float>(contribs[j], contribs[j] + n));
+  }
+  std::vector<const ParamVector*> ptrs;
+  for (const auto& v : vs) ptrs.push_back(&v);
+  return guarded([&] {
+    put(reduce_average(ptrs, precision ? Precision::fp16 : Precision::fp32), out);
+  });
+}
+
+REF_API void ref_partition_ranges(size_t n, size_t k, size_t* offsets, size_t* lengths) {
+  const std::vector<Range> r = partition_ranges(n, k);
+  for (size_t i = 0; i < k; ++i) {
+    offsets[i] = r[i].offset;
+    lengths[i] = r[i].length;
+  }
+}
+
+REF_API uint64_t ref_per_peer_reduce_bytes(size_t n, size_t k, size_t rank, int precision) {
+  return per_peer_reduce_bytes(n, k, rank, precision ? Precision::fp16 : Precision::fp32);
+}
+
+REF_API uint64_t ref_fleet_reduce_bytes(size_t n, size_t k, int precision) {
+  return fleet_reduce_bytes(n, k, precision ? Precision::fp16 : Precision::fp32);
+}
+
+// SoloCollective::all_reduce_avg (reduce.cpp:113-126).
+REF_API int ref_solo_all_reduce_avg(const float* delta, size_t n, int precision, float* out) {
+  SoloCollective solo;
+  PseudoGradient pg;
+  pg.delta = pv(delta, n);
+  pg.precision = precision ? Precision::fp16 : Precision::fp32;
+  return guarded([&] { put(solo.all_reduce_avg(pg, nullptr).delta, out); });
+}
+
+// ---------------------------------------------------------------------------
+// CPU baseline harness: the reference's own functions, one engine set per
+// host thread on a disjoint slice (every op on the path is elementwise, so a
+// slice is an exact sub-problem).  Inputs follow SURVEY.md §8(d):
+//   theta_0 ~ U(-0.05, 0.05)  CounterRng(4242, "theta", 0)
+//   theta_local_w = theta_0 - U(-1e-3, 1e-3)  CounterRng(4242, "local", w)
+//   grad_w ~ U(-1e-2, 1e-2)   CounterRng(4242, "grad", w)
+// Returns seconds per outer step (max over threads of the per-iteration wall
+// time, averaged over iters) in *sec_per_iter.
+// ---------------------------------------------------------------------------
+
+namespace {
+
+std::vector<float> fill(uint64_t seed, const char* purpose, uint64_t stream, size_t first,
+                        size_t n, float lo, float hi) {
+  CounterRng rng(seed, purpose, stream);
+  for (size_t i = 0; i < first; ++i) rng.next_u64();
+  std::vector<float> out(n);
+  for (float& f : out) f = rng.next_uniform(lo, hi);
+  return out;
+}
+
+}  // namespace
+
+REF_API int ref_bench_outer(int threads, size_t slice, size_t k, int precision, int iters,
+                            float lr, float mu, double* sec_per_iter) {
+  if (threads < 1 || k < 1 || iters < 1 || slice < 1) return kConfig;
+  const Precision prec = precision ? Precision::fp16 : Precision::fp32;
+  std::barrier sync(threads + 1);
+  std::vector<double> t_thread(threads, 0.0);
+  std::atomic<int> err{0};
+  auto work = [&](int tid) {
+    try {
+      auto layout = Layout::single("p", slice);
+      const std::vector<float> theta0 = fill(4242, "theta", 0, tid * slice, slice, -0.05f, 0.05f);
+      std::vector<ParamVector> theta_t, local, pristine;
+      std::vector<NesterovState> outer;
+      for (size_t w = 0; w < k; ++w) {
+        std::vector<float> noise = fill(4242, "local", w, tid * slice, slice, -1e-3f, 1e-3f);
+        std::vector<float> loc(slice);
+        for (size_t i = 0; i < slice; ++i) loc[i] = theta0[i] - noise[i];
+        theta_t.emplace_back(layout, theta0);
+        pristine.emplace_back(layout, std::move(loc));
+        local.push_back(pristine.back());
+        outer.push_back(NesterovState::init(layout, lr, mu));
+      }
+      for (int it = 0; it < iters; ++it) {
+        for (size_t w = 0; w < k; ++w) local[w] = pristine[w];  // untimed: fresh window
+        sync.arrive_and_wait();
+        const auto t0 = std::chrono::steady_clock::now();
+        // run_simulated's outer round (netsim.cpp:325-357) on this slice.
+        std::vector<ParamVector> deltas;
+        deltas.reserve(k);
+        for (size_t w = 0; w < k; ++w) deltas.push_back(axpy(-1.0f, local[w], theta_t[w]));
+        std::vector<const ParamVector*> ptrs;
+        for (const auto& d : deltas) ptrs.push_back(&d);
+        const ParamVector dbar = reduce_average(ptrs, prec);
+        for (size_t w = 0; w < k; ++w) {  // DilocoEngine::outer_step, engine.cpp:136-144
+          if (dbar.all_finite()) theta_t[w] = nesterov_step(outer[w], theta_t[w], dbar);
+          local[w] = theta_t[w];
+        }
+        t_thread[tid] += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        sync.arrive_and_wait();
+      }
+    } catch (...) {
+      err = 1;
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 0; t < threads; ++t) pool.emplace_back(work, t);
+  for (int it = 0; it < iters; ++it) {
+    sync.arrive_and_wait();
+    sync.arrive_and_wait();
+  }
+  for (auto& th : pool) th.join();
+  if (err) return kOther;
+  double worst = 0.0;
+  for (double t : t_thread) worst = t > worst ? t : worst;
+  *sec_per_iter = worst / iters;
+  return kOk;
+}
+
+// Inner step per thread: scale_gradient (engine.cpp:20-27) +
+// scaler_unscale_and_check + adamw_step (engine.cpp:50-69) on a slice.
+REF_API int ref_bench_inner(int threads, size_t slice, int iters, double* sec_per_iter) {
+  if (threads < 1 || iters < 1 || slice < 1) return kConfig;
+  std::barrier sync(threads + 1);
+  std::vector<double> t_thread(threads, 0.0);
+  std::atomic<int> err{0};
+  auto work = [&](int tid) {
+    try {
+      auto layout = Layout::single("p", slice);
+      ParamVector params(layout, fill(4242, "theta", 0, tid * slice, slice, -0.05f, 0.05f));
+      const ParamVector grad(layout, fill(4242, "grad", 0, tid * slice, slice, -1e-2f, 1e-2f));
+      AdamWState adam = AdamWState::init(layout, 0.9f, 0.95f, 1e-8f, 0.1f);
+      LossScaler scaler;
+      LrSchedule sched;
+      for (int it = 0; it < iters; ++it) {
+        sync.arrive_and_wait();
+        const auto t0 = std::chrono::steady_clock::now();
+        std::vector<float> scaled(slice);
+        const auto g = grad.values();
+        for (size_t i = 0; i < slice; ++i) scaled[i] = g[i] * scaler.scale;
+        UnscaleResult un = scaler_unscale_and_check(scaler, ParamVector(layout, std::move(scaled)));
+        if (!un.overflow) {
+          params = adamw_step(adam, params, un.grad, lr_at(sched, adam.step_count + 1));
+        }
+        scaler_update(scaler, un.overflow);
+        t_thread[tid] += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        sync.arrive_and_wait();
+      }
+    } catch (...) {
+      err = 1;
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 0; t < threads; ++t) pool.emplace_back(work, t);
+  for (int it = 0; it < iters; ++it) {
+    sync.arrive_and_wait();
+    sync.arrive_and_wait();
+  }
+  for (auto& th : pool) th.join();
+  if (err) return kOther;
+  double worst = 0.0;
+  for (double t : t_thread) worst = t > worst ? t : worst;
+  *sec_per_iter = worst / iters;
+  return kOk;
+}
