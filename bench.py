@@ -1,0 +1,316 @@
+#!/usr/bin/env python
+"""bench.py — DiLoCo outer-sync throughput on B200 (one worker per GPU).
+
+Metric (BASELINE.json): outer-sync params/sec & ms/outer-step at 1/2/4/8 B200;
+inner AdamW HBM GB/s vs peak.
+
+Workload (configs[3]/[4] of BASELINE.json, one DiLoCo worker per GPU): a 1.1B
+flat FP32 parameter vector per worker, FP16 pseudo-gradient cast + FP16
+average (ordered NCCL scatter / rank-order fold / all-gather), outer Nesterov
+lr=0.7 momentum=0.9.  One timed *step* = one outer step: K2 pseudo-grad ->
+C1 cross-worker average -> K4 Nesterov + theta_local refresh, on that step's
+synthetic end-of-window weights (two device-resident variants alternate, so
+every step sees a fresh, non-zero delta).  `value` = workers x params /
+outer-step time (weak scaling: every GPU holds a full replica).  The inner
+AdamW step (K1: unscale + overflow check + AdamW, one HBM pass) is timed in the
+same run and reported under "inner_adamw".
+
+Arms: default = this repo's CUDA path; `--impl reference` = the reference's own
+CPU implementation (oracle/_ref, compiled from /root/reference/proj/src) on the
+host cores.  Under torchrun (N>1) one process drives one GPU; timings are CUDA
+events on the engine stream, max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "outer-sync params/sec & ms/outer-step at 1/2/4/8 B200; inner AdamW HBM GB/s vs peak"
+PEAK_FALLBACK_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--params", type=int, default=1_100_000_000)
+    ap.add_argument("--precision", choices=["fp16", "fp32"], default="fp16")
+    ap.add_argument("--mode", choices=["ordered", "allreduce"], default="ordered")
+    ap.add_argument("--inner-mode", choices=["pingpong", "inplace"], default="pingpong")
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-clocks", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return PEAK_FALLBACK_GBS, "fallback"
+
+
+# ---- clocks sampler (B200_PROFILING.md "clocks DURING the timed region") -----------------
+
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int, enabled: bool = True):
+        self.proc = None
+        self.device = device
+        if enabled:
+            try:
+                self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                              "-i", str(device), "-lms", "100"], stdout=subprocess.PIPE,
+                                             stderr=subprocess.DEVNULL, text=True)
+            except FileNotFoundError:
+                self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        rows = [r.split(", ") for r in out.strip().splitlines() if r.count(",") >= 8]
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].strip() == "Active"})
+        pw = [float(r[3]) for r in rows if r[3].replace(".", "").isdigit()]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows), "power_w_max": max(pw) if pw else None}
+
+
+# ---- CPU baseline: the reference's own functions on host threads --------------------------
+
+def cpu_reference_outer(k: int, prec: int, iters: int, warmup: int = 0, budget_gb: float = 8.0):
+    """Returns (params_per_s, seconds/iter list, dict describing the sample)."""
+    from oracle import oracle as O
+    lib = O.reference()
+    kind = "reference"
+    if lib is None:
+        return None
+    threads = os.cpu_count() or 1
+    per_thread = int(budget_gb * 1e9 / (threads * k * 20))
+    slice_len = max(1 << 16, min((16 << 20) // k, per_thread))
+    if warmup:
+        lib.bench_outer(threads, slice_len, k, prec, warmup)
+    secs = [lib.bench_outer(threads, slice_len, k, prec, 1) for _ in range(iters)]
+    units = k * threads * slice_len
+    sample = (f"{threads} threads x {slice_len} params/thread x {k} workers "
+              f"({'fp16' if prec else 'fp32'}), per step: K x axpy + reduce_average + K x nesterov/outer_step "
+              f"(netsim.cpp:325-357), {iters} steps")
+    return units / statistics.mean(secs), secs, {"kind": kind, "cores": threads, "sample": sample}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    k = args.gpus if world == 1 else world
+    prec = 1 if args.precision == "fp16" else 0
+    res = cpu_reference_outer(k, prec, args.steps, args.warmup)
+    if res is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return 0
+    value, secs, desc = res
+    ms = statistics.mean(secs) * 1e3
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "params/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": workload_config(args, k),
+            "cpu_baseline": dict(desc, value=value, unit="params/s"),
+            "e2e": {"value": value, "unit": "params/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+def workload_config(args, k):
+    return {"workload": f"DiLoCo outer step, {args.params / 1e9:.3g}B flat params per worker, {k} worker(s) "
+                        f"(1 per GPU), {args.precision} pseudo-grad + {args.precision} average "
+                        f"({args.mode}), Nesterov lr=0.7 mu=0.9",
+            "params_per_worker": args.params, "workers": k, "precision": args.precision, "reduce_mode": args.mode,
+            "inner_mode": args.inner_mode, "parallelism": f"diloco-dp{k}",
+            "l2": "inputs larger than L2 (every vector >= 126 MB)" if args.params * 2 > 126e6 else "L2-resident"}
+
+
+# ---- our arm -----------------------------------------------------------------------------
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2407_07852_b200 as D
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("gloo")
+    D.lib.dlc_set_device(local)
+    k = world
+    n = args.params
+    prec = D.FP16 if args.precision == "fp16" else D.FP32
+    mode = D.MODE_ORDERED if args.mode == "ordered" else D.MODE_ALLREDUCE
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    coll = None
+    if k > 1:
+        uid = [D.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        coll = D.NcclCollective(rank, world, uid[0], local, mode)
+
+    cfg = D.DilocoConfig(local_steps_h=1, num_workers_k=k, reduce_precision=prec, total_inner_steps=1 << 40)
+    hp = D.OptimHyperparams()
+    inner_mode = D.INNER_PINGPONG if args.inner_mode == "pingpong" else D.INNER_INPLACE
+    eng = D.DilocoEngine(cfg, hp, n, local, inner_mode)
+    eng.rng_fill(D.THETA_T, 4242, "theta", 0, -0.05, 0.05)
+    # two synthetic end-of-window weight sets per worker (theta_t - U(-1e-3, 1e-3))
+    xs = [torch.empty(n, dtype=torch.float32, device=f"cuda:{local}") for _ in range(2)]
+    for i, x in enumerate(xs):
+        eng.rng_perturb(4242, "local", rank * 16 + i, -1e-3, 1e-3, dst_dev_ptr=x.data_ptr())
+    eng.rng_fill(D.GRAD, 4242, "grad", rank, -1e-2 * 65536.0, 1e-2 * 65536.0)  # loss-scaled grads
+    gptr = eng.device_ptr(D.GRAD)
+    eng.synchronize()
+    stream = torch.cuda.ExternalStream(eng.stream, device=f"cuda:{local}")
+
+    def timed(fn, steps):
+        barrier()
+        eng.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for s in range(steps):
+            fn(s)
+        b.record(stream)
+        b.synchronize()
+        eng.synchronize()
+        barrier()
+        return max_over_ranks(a.elapsed_time(b))
+
+    outer = lambda s: eng.outer_step_from(coll, xs[s % 2].data_ptr())  # noqa: E731
+    inner = lambda s: eng.inner_step(gptr, grad_is_scaled=True)  # noqa: E731
+    for s in range(args.warmup):
+        outer(s)
+        inner(s)
+    eng.synchronize()
+
+    clocks = Clocks(local, enabled=not args.no_clocks)
+    eng.set_timing(True)
+    eng.phase_times()
+    outer_ms = timed(outer, args.steps)
+    ph_ms, ph_n = eng.phase_times()
+    inner_total = timed(inner, args.steps)
+    ph2_ms, ph2_n = eng.phase_times()
+    clk = clocks.stop()
+    eng.set_timing(False)
+
+    ms_step = outer_ms / args.steps
+    inner_ms = inner_total / args.steps
+    peak, peak_kind = measured_peak()
+    wire = 2 if prec == D.FP16 else 4
+    # algorithmic bytes per parameter
+    b_k1, b_k2, b_k4 = 28, 8 + wire, 20 + wire
+    k4_ms = max_over_ranks(ph_ms[3] / max(ph_n[3], 1))
+    k2_ms = max_over_ranks(ph_ms[1] / max(ph_n[1], 1))
+    coll_ms = max_over_ranks(ph_ms[2] / max(ph_n[2], 1)) if ph_n[2] else 0.0
+    k1_ms = max_over_ranks(ph2_ms[0] / max(ph2_n[0], 1))
+
+    def roof(bpp, ms):
+        ach = bpp * n / (ms * 1e-3) / 1e9
+        return {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                "peak_source": peak_kind, "bytes_per_param": bpp, "kernel_ms": ms}
+
+    line = {"metric": METRIC, "value": k * n / (ms_step * 1e-3), "unit": "params/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": workload_config(args, k)}
+    rl = roof(b_k4, k4_ms)
+    rl["kernel"] = "nesterov_outer_kernel (K4)"
+    rl["traffic"] = None
+    line["roofline"] = rl
+    line["phases_ms"] = {"pseudo_grad_K2": k2_ms, "collective_C1_K3": coll_ms, "nesterov_K4": k4_ms}
+    line["phase_roofline"] = {"pseudo_grad_K2": roof(b_k2, k2_ms)["frac"], "nesterov_K4": rl["frac"]}
+    if k > 1:
+        wire_bytes = 2 * (k - 1) * (-(-n // k)) * wire
+        line["nccl_bus_gbs"] = wire_bytes / (coll_ms * 1e-3) / 1e9 if coll_ms else None
+    ir = roof(b_k1, k1_ms)
+    ir["kernel"] = "adamw_kernel (K1, %s)" % args.inner_mode
+    line["inner_adamw"] = {"ms_per_step": inner_ms, "kernel_ms": k1_ms, "roofline": ir,
+                           "vs_8TBs_spec": ir["achieved"] / 8000.0}
+    line["gpu_launches"] = args.steps * (3 if k > 1 and mode == D.MODE_ORDERED else 2) + args.steps
+    line["clocks"] = clk
+
+    # e2e through the public C ABI with host buffers: H2D theta_local, outer step, D2H theta_t.
+    if not args.no_e2e:
+        e2e_steps = args.e2e_steps or max(3, min(args.steps, 5))
+        hx = torch.empty(n, dtype=torch.float32, pin_memory=True)
+        ht = torch.empty(n, dtype=torch.float32, pin_memory=True)
+        hx.copy_(xs[0])
+        eng.outer_step_host(coll, hx.data_ptr(), ht.data_ptr())  # warm
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            eng.outer_step_host(coll, hx.data_ptr(), ht.data_ptr())
+        dt = max_over_ranks(time.perf_counter() - t0)
+        line["e2e"] = {"value": k * n * e2e_steps / dt, "unit": "params/s", "h2d_bytes_per_step": 4 * n,
+                       "d2h_bytes_per_step": 4 * n, "ms_per_step": dt * 1e3 / e2e_steps, "steps": e2e_steps}
+        del hx, ht
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        res = cpu_reference_outer(k, 1 if prec == D.FP16 else 0, iters=2)
+        if res is not None:
+            v, secs, desc = res
+            line["cpu_baseline"] = dict(desc, value=v, unit="params/s")
+    if rank == 0:
+        print(json.dumps(line))
+    eng.close()
+    if coll:
+        coll.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    rank, world, _ = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # not launched by torchrun: relaunch one process per GPU
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", os.environ.get("MASTER_PORT", "29533")] + sys.argv
+        return subprocess.call(cmd)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

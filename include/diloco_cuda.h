@@ -1,0 +1,336 @@
+/*
+ * diloco_cuda.h — C ABI of the B200-native DiLoCo optimizer hot path.
+ *
+ * Drop-in boundary for the reference C++ library (diloco-cpp,
+ * /root/reference/proj).  Plain pointers and sizes, `int` status codes, no
+ * C++ or torch types.  Every entry point names the reference interface it
+ * replaces (file:line under proj/).  Implemented by libdiloco_cuda.so
+ * (paper_2407_07852_b200/csrc, sm_100a kernels + NCCL); there is no CPU
+ * fallback: without a CUDA device every compute call fails with DLC_ECUDA.
+ *
+ * Errors.  C cannot throw, so each reference exception maps to a status
+ * (errors.hpp:12-51); dlc_last_error() returns the calling thread's message:
+ *   DLC_ESHAPE      ShapeError       layout / length mismatch
+ *   DLC_ECONFIG     ConfigError      bad hyperparameter / config
+ *   DLC_ENUMERIC    NumericError     non-finite input where finite math is required
+ *   DLC_ECOLLECTIVE CollectiveError  epoch mismatch, no contributions
+ *   DLC_ENCCL       CollectiveError  NCCL failure
+ *   DLC_ECUDA       Error            CUDA failure / no device
+ *   DLC_EINVAL      Error            null pointer or out-of-range argument
+ * Overflow is a signal, not an error (UnscaleResult.overflow,
+ * Fp16Buffer.overflow, OuterStepResult.applied), exactly as in the reference.
+ *
+ * Threading (reduce.hpp:84-85).  One engine per worker thread
+ * and GPU; no internal locking.  Host-buffer calls block the caller; engine
+ * calls are stream-ordered on the engine's stream and return immediately
+ * unless a result struct is requested.
+ */
+#ifndef DILOCO_CUDA_H_
+#define DILOCO_CUDA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DLC_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define DLC_API __attribute__((visibility("default")))
+#else
+#define DLC_API
+#endif
+
+enum dlc_status {
+  DLC_OK = 0,
+  DLC_ESHAPE = 1,
+  DLC_ECONFIG = 2,
+  DLC_ENUMERIC = 3,
+  DLC_ECOLLECTIVE = 4,
+  DLC_ECUDA = 5,
+  DLC_ENCCL = 6,
+  DLC_EINVAL = 7
+};
+
+/* Precision, reduce.hpp:22 */
+enum dlc_precision { DLC_FP32 = 0, DLC_FP16 = 1 };
+/* LrDecay, optim.hpp:38 */
+enum dlc_lr_decay { DLC_LR_NONE = 0, DLC_LR_COSINE = 1 };
+
+DLC_API int dlc_abi_version(void);
+/* Message of the last failing call on this thread ("" if none). */
+DLC_API const char* dlc_last_error(void);
+DLC_API int dlc_device_count(int* count);
+/* Selects the calling thread's device for the host-buffer math below. */
+DLC_API int dlc_set_device(int device);
+
+/* =========================================================================
+ * 1. Reference math over HOST buffers.  Same argument meaning, ownership and
+ *    error behaviour as the reference free functions; each call stages
+ *    through the calling thread's current device and synchronises.
+ * ========================================================================= */
+
+/* AdamWState, optim.hpp:17-28 (m, v: host arrays of n, updated in place). */
+typedef struct {
+  float* m;
+  float* v;
+  uint64_t step_count;
+  float beta1, beta2, eps, weight_decay;
+} dlc_adamw_state;
+
+/* NesterovState, optim.hpp:30-36 (momentum_buf: host array of n). */
+typedef struct {
+  float* momentum_buf;
+  float lr;
+  float momentum;
+} dlc_nesterov_state;
+
+/* LrSchedule, optim.hpp:40-45 */
+typedef struct {
+  uint64_t warmup_steps;
+  uint64_t total_steps;
+  float base_lr;
+  int decay; /* dlc_lr_decay */
+} dlc_lr_schedule;
+
+/* LossScaler, optim.hpp:52-56 */
+typedef struct {
+  float scale;
+  uint64_t growth_interval;
+  uint64_t consecutive_good;
+} dlc_loss_scaler;
+
+/* axpy, tensor.hpp:108 / tensor.cpp:118-129: out = y + alpha * x. */
+DLC_API int dlc_axpy(float alpha, const float* x, const float* y, size_t n, float* out);
+/* encode_fp16, tensor.hpp:111 / tensor.cpp:131-140 (RNE, overflow -> inf). */
+DLC_API int dlc_encode_fp16(const float* v, size_t n, uint16_t* out, int* overflow);
+/* decode_fp16, tensor.hpp:115 / tensor.cpp:142-154 (exact). */
+DLC_API int dlc_decode_fp16(const uint16_t* bits, size_t n, float* out);
+/* ParamVector::all_finite, tensor.hpp:86 / tensor.cpp:97-104. */
+DLC_API int dlc_all_finite(const float* v, size_t n, int* all_finite);
+/* lr_at, optim.hpp:49 / optim.cpp:37-56 (host scalar). */
+DLC_API float dlc_lr_at(const dlc_lr_schedule* schedule, uint64_t step);
+/* adamw_step, optim.hpp:61-62 / optim.cpp:58-93: out = new params; state m, v,
+ * step_count updated.  DLC_ECONFIG on lr < 0, DLC_ENUMERIC on a non-finite
+ * gradient (state untouched). */
+DLC_API int dlc_adamw_step(dlc_adamw_state* state, const float* params, const float* grad, size_t n,
+                   float lr, float* out);
+/* nesterov_step, optim.hpp:65-66 / optim.cpp:95-115. */
+DLC_API int dlc_nesterov_step(dlc_nesterov_state* state, const float* params, const float* pseudo_grad,
+                      size_t n, float* out);
+/* scaler_scale_loss, optim.hpp:68 / optim.cpp:117-119. */
+DLC_API float dlc_scaler_scale_loss(const dlc_loss_scaler* scaler, float loss);
+/* scaler_unscale_and_check, optim.hpp:76-77 / optim.cpp:121-135. */
+DLC_API int dlc_scaler_unscale_and_check(const dlc_loss_scaler* scaler, const float* grad, size_t n,
+                                 float* out, int* overflow);
+/* scaler_update, optim.hpp:80 / optim.cpp:137-148 (host scalar). */
+DLC_API void dlc_scaler_update(dlc_loss_scaler* scaler, int overflow);
+/* reduce_average, reduce.hpp:65-66 / reduce.cpp:46-89: mean of k host vectors
+ * folded in index order; DLC_FP16 reproduces the wire path (one encode per
+ * contribution, one of the mean).  DLC_ECOLLECTIVE when k == 0. */
+DLC_API int dlc_reduce_average(const float* const* contributions, size_t k, size_t n, int precision,
+                       float* out);
+/* partition_ranges / per_peer_reduce_bytes / fleet_reduce_bytes,
+ * reduce.hpp:55,78-82 / reduce.cpp:20-31,91-111 (host integers). */
+DLC_API void dlc_partition_ranges(size_t n, size_t k, size_t* offsets, size_t* lengths);
+DLC_API uint64_t dlc_per_peer_reduce_bytes(size_t n, size_t k, size_t rank, int precision);
+DLC_API uint64_t dlc_fleet_reduce_bytes(size_t n, size_t k, int precision);
+
+/* =========================================================================
+ * 2. Collective plugin, class Collective (reduce.hpp:86-97).
+ * ========================================================================= */
+
+typedef struct dlc_collective dlc_collective;
+
+/* ReduceReport, reduce.hpp:37-46 */
+typedef struct {
+  uint64_t outer_epoch;
+  size_t contributors;
+  uint64_t data_bytes_sent;
+  uint64_t data_bytes_received;
+  uint64_t wire_bytes_sent;
+  uint64_t wire_bytes_received;
+  double wall_ms;
+  uint32_t attempts;
+} dlc_reduce_report;
+
+/* DLC_MODE_ORDERED: NCCL grouped send/recv scatter -> owner fold in rank order
+ *   (K3) -> NCCL all-gather; bit-identical to reduce_average in rank order.
+ * DLC_MODE_ALLREDUCE: ncclAllReduce(ncclAvg) on the flat buffer; NCCL's
+ *   reduction order, within the tolerance stated in DESIGN.md. */
+enum dlc_reduce_mode { DLC_MODE_ORDERED = 0, DLC_MODE_ALLREDUCE = 1 };
+
+/* 128-byte ncclUniqueId, created on rank 0 and shipped to every rank. */
+DLC_API int dlc_nccl_unique_id(uint8_t id[128]);
+/* SocketCollective replacement: one rank per process and GPU. */
+DLC_API int dlc_collective_create_nccl(int rank, int world, const uint8_t id[128], int device, int mode,
+                               dlc_collective** out);
+/* SoloCollective, reduce.hpp:101-106. */
+DLC_API int dlc_collective_create_solo(int device, dlc_collective** out);
+DLC_API int dlc_collective_destroy(dlc_collective* c);
+DLC_API size_t dlc_collective_world_size(const dlc_collective* c);
+DLC_API int dlc_collective_rank(const dlc_collective* c);
+/* Collective::all_reduce_avg on a HOST pseudo-gradient (reduce.hpp:95-96). */
+DLC_API int dlc_collective_all_reduce_avg(dlc_collective* c, const float* local_delta, size_t n,
+                                  int precision, uint64_t outer_epoch, float* out,
+                                  dlc_reduce_report* report);
+
+/* =========================================================================
+ * 3. Device-resident engine: DilocoEngine (engine.hpp:76-116) with theta_t,
+ *    theta_local, AdamW m/v, Nesterov buffer, loss scaler and counters all in
+ *    HBM.  The inner step, pseudo-gradient, collective and outer step never
+ *    leave the GPU.
+ * ========================================================================= */
+
+/* DilocoConfig, engine.hpp:22-32 (batch_size belongs to the out-of-scope
+ * gradient producer). */
+typedef struct {
+  uint64_t local_steps_h;
+  size_t num_workers_k;
+  int reduce_precision; /* dlc_precision */
+  uint64_t total_inner_steps;
+} dlc_config;
+
+/* OptimHyperparams, engine.hpp:34-46 */
+typedef struct {
+  float inner_lr;
+  uint64_t warmup_steps;
+  int lr_decay;
+  float weight_decay, beta1, beta2, adam_eps;
+  float outer_lr, outer_momentum;
+  float scaler_init_scale;
+  uint64_t scaler_growth_interval;
+} dlc_hyperparams;
+
+/* Engine scalars (EngineState engine.hpp:48-56 minus the vectors). */
+typedef struct {
+  uint64_t step_count;      /* AdamWState::step_count */
+  uint64_t inner_step;      /* data cursor */
+  uint64_t outer_epoch;
+  float scale;              /* LossScaler::scale */
+  uint64_t consecutive_good;
+  uint64_t overflow_skips;
+  uint64_t outer_skips;
+  float last_lr;            /* InnerStepResult::lr */
+  int last_overflow;        /* InnerStepResult::overflow_skipped */
+  int last_applied;         /* OuterStepResult::applied */
+} dlc_engine_scalars;
+
+/* K1 variants.  PINGPONG: one HBM pass (28 B/param), p/m/v alternate between
+ * two buffers and the live one is picked on the device.  INPLACE: fixed
+ * addresses, an overflow pre-pass over the gradient then a gated in-place
+ * update (32 B/param). */
+enum dlc_inner_mode { DLC_INNER_PINGPONG = 0, DLC_INNER_INPLACE = 1 };
+
+/* Buffers of one engine. */
+enum dlc_buffer {
+  DLC_THETA_T = 0,
+  DLC_THETA_LOCAL = 1,
+  DLC_ADAM_M = 2,
+  DLC_ADAM_V = 3,
+  DLC_MOMENTUM = 4,
+  DLC_GRAD = 5 /* gradient staging buffer owned by the engine */
+};
+
+typedef struct dlc_engine dlc_engine;
+
+DLC_API void dlc_hyperparams_default(dlc_hyperparams* h);
+/* Allocates every buffer on `device` (theta zero-initialised; load weights with
+ * dlc_engine_upload(DLC_THETA_T) and (DLC_THETA_LOCAL)).  DLC_ECONFIG per
+ * DilocoConfig::validate (engine.cpp:31-48). */
+DLC_API int dlc_engine_create(const dlc_config* cfg, const dlc_hyperparams* hyper, size_t n_params,
+                      int device, int inner_mode, dlc_engine** out);
+DLC_API int dlc_engine_destroy(dlc_engine* e);
+DLC_API size_t dlc_engine_size(const dlc_engine* e);
+/* The engine's CUDA stream (cudaStream_t), for producers of gradients. */
+DLC_API int dlc_engine_stream(dlc_engine* e, void** stream);
+/* Host <-> device copies of one buffer (synchronous). */
+DLC_API int dlc_engine_upload(dlc_engine* e, int which, const float* host, size_t n);
+DLC_API int dlc_engine_download(dlc_engine* e, int which, float* host, size_t n);
+/* Current device address of a buffer (synchronises: the live p/m/v buffer is
+ * chosen on the device in PINGPONG mode). */
+DLC_API int dlc_engine_device_ptr(dlc_engine* e, int which, float** dev);
+DLC_API int dlc_engine_get_scalars(dlc_engine* e, dlc_engine_scalars* out);
+DLC_API int dlc_engine_set_scalars(dlc_engine* e, const dlc_engine_scalars* in);
+DLC_API int dlc_engine_synchronize(dlc_engine* e);
+
+/* InnerStepResult, engine.hpp:58-62 (loss belongs to the producer). */
+typedef struct {
+  float lr;
+  int overflow_skipped;
+} dlc_inner_result;
+
+/* apply_inner_step minus the producer (engine.cpp:50-69): unscale + overflow
+ * check + AdamW + scaler update, skip semantics on overflow.  `grad` is a
+ * device pointer on the engine's device; `grad_is_scaled` = 1 when it is
+ * already multiplied by the current loss scale (backward of the scaled loss),
+ * 0 to have the engine apply scale_gradient (engine.cpp:20-27) first.
+ * `result` may be NULL (asynchronous); otherwise the call synchronises. */
+DLC_API int dlc_engine_inner_step(dlc_engine* e, const float* grad, int grad_is_scaled,
+                          dlc_inner_result* result);
+/* Same with a HOST gradient (copied to DLC_GRAD first). */
+DLC_API int dlc_engine_inner_step_host(dlc_engine* e, const float* host_grad, int grad_is_scaled,
+                               dlc_inner_result* result);
+
+/* OuterStepResult, engine.hpp:64-66 */
+typedef struct {
+  int applied;
+  uint64_t outer_epoch; /* epoch after the step */
+} dlc_outer_result;
+
+/* DilocoOptimizer::step's outer part (engine.cpp:165-172): K2 pseudo-gradient
+ * -> Collective::all_reduce_avg on device buffers -> K4 outer Nesterov +
+ * theta_local refresh.  `c` NULL or solo => K = 1.  DLC_ECOLLECTIVE when the
+ * collective's world size differs from num_workers_k or when called
+ * mid-window (engine.cpp:116-120).  `result` / `report` may be NULL. */
+DLC_API int dlc_engine_outer_step(dlc_engine* e, dlc_collective* c, dlc_outer_result* result,
+                          dlc_reduce_report* report);
+/* Outer step whose theta(t+h) comes from a caller-owned DEVICE buffer (a model
+ * trained outside the engine); the engine's theta_local is refreshed as usual. */
+DLC_API int dlc_engine_outer_step_from(dlc_engine* e, dlc_collective* c, const float* theta_local_dev,
+                                       dlc_outer_result* result, dlc_reduce_report* report);
+/* Host-buffer outer round for drop-in callers whose inner loop runs on the
+ * host: theta_local is uploaded, the outer step runs, theta_t is downloaded. */
+DLC_API int dlc_engine_outer_step_host(dlc_engine* e, dlc_collective* c, const float* host_theta_local,
+                               float* host_theta_t, dlc_outer_result* result);
+/* K engines of one process on one device (in-process fleet, the device
+ * analogue of run_simulated's outer round, netsim.cpp:325-357): pseudo-grads,
+ * one fold in index order, K outer steps. */
+DLC_API int dlc_engines_outer_step_local(dlc_engine* const* engines, size_t k, dlc_outer_result* result);
+
+/* DilocoOptimizer::step (engine.cpp:162-174): one inner step, then the outer
+ * step when the window boundary is reached.  `round_completed` may be NULL. */
+DLC_API int dlc_optimizer_step(dlc_engine* e, dlc_collective* c, const float* grad, int grad_is_scaled,
+                       int* round_completed);
+
+/* Per-phase device timing with CUDA events on the engine stream (ncu-free
+ * evidence for the roofline): phase 0 = K1 inner AdamW, 1 = K2 pseudo-grad,
+ * 2 = collective (C1 + K3 fold), 3 = K4 outer Nesterov.  dlc_engine_phase_times
+ * synchronises, returns the summed milliseconds and launch counts since the
+ * previous call, and resets them. */
+enum { DLC_PHASE_INNER = 0, DLC_PHASE_PSEUDO = 1, DLC_PHASE_COLLECTIVE = 2, DLC_PHASE_OUTER = 3 };
+DLC_API int dlc_engine_set_timing(dlc_engine* e, int on);
+DLC_API int dlc_engine_phase_times(dlc_engine* e, double total_ms[4], uint64_t count[4]);
+
+/* =========================================================================
+ * 4. Synthetic inputs and test probes (bench / parity tests).  Counter-based
+ *    streams identical to the reference's CounterRng (rng.hpp:38-74).
+ * ========================================================================= */
+
+/* key of CounterRng(seed, purpose, index) */
+DLC_API uint64_t dlc_rng_key(uint64_t seed, const char* purpose, uint64_t index);
+/* dev[i] = draw (first + i) of the stream `key`, uniform in [lo, hi). */
+DLC_API int dlc_rng_fill_device(dlc_engine* e, int which, uint64_t key, uint64_t first, float lo, float hi);
+/* dst = theta_t - U(lo, hi) drawn from `key` (synthetic end-of-window weights);
+ * dst = NULL writes the engine's own theta_local, else a caller device buffer of n. */
+DLC_API int dlc_rng_perturb(dlc_engine* e, float* dst, uint64_t key, float lo, float hi);
+/* FP16 codes of the 2^32 FP32 bit patterns [start, start + n) (host out). */
+DLC_API int dlc_fp16_encode_bits(uint32_t start, size_t n, uint16_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DILOCO_CUDA_H_ */

@@ -1,0 +1,855 @@
+// engine.cu — sections 2 and 3 of include/diloco_cuda.h: the collective plugin
+// (class Collective, reduce.hpp:86-97) and the device-resident DilocoEngine
+// (engine.hpp:76-157).
+//
+// HBM layout of one engine (one worker, one GPU), every buffer 256-B aligned:
+//   theta_t[N]                     outer weights            FP32
+//   p[2][N], m[2][N], v[2][N]      theta_local + AdamW      FP32 ping-pong pair
+//                                  (one buffer each in INPLACE mode)
+//   buf[N]                         Nesterov momentum        FP32
+//   grad[N]                        gradient staging          FP32
+//   send[K*S]                      pseudo-gradient, padded   FP32 | FP16 codes
+//   recv[K*S], gather[K*S]         scatter / all-gather      (K > 1)
+//   flags[kMaxK], DevState, lr/corr tables
+// S = ceil(N / K) rounded up to 64 elements: rank r owns send[r*S, (r+1)*S).
+// The partition differs from partition_ranges (reduce.cpp:20-31) only by the
+// padding; results are independent of the split because the fold is
+// elementwise, and the scalar bytes on the wire are the same
+// 2(K-1)/K*N*{4,2} per peer.
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.hpp"
+#include "kernels.cuh"
+
+using namespace dlc;
+
+struct dlc_collective {
+  int kind = 0;  // 0 solo, 1 nccl
+  int rank = 0;
+  int world = 1;
+  int device = 0;
+  int mode = DLC_MODE_ORDERED;
+  ncclComm_t comm = nullptr;
+  cudaStream_t stream = nullptr;  // used only by the host-buffer plugin call
+};
+
+struct dlc_engine {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  dlc_config cfg{};
+  dlc_hyperparams hyper{};
+  int inner_mode = DLC_INNER_PINGPONG;
+  size_t n = 0, k = 1, S = 0;
+  int prec = DLC_FP32;
+  float* theta_t = nullptr;
+  float* p[2] = {nullptr, nullptr};
+  float* m[2] = {nullptr, nullptr};
+  float* v[2] = {nullptr, nullptr};
+  float* buf = nullptr;
+  float* grad = nullptr;
+  void* send = nullptr;
+  void* recv = nullptr;
+  void* gather = nullptr;
+  int* flags = nullptr;
+  DevState* st = nullptr;
+  float* tab = nullptr;  // corr1 | corr2 | lr, tab_cap entries each
+  size_t tab_cap = 0;
+  uint64_t issued_inner = 0;  // host mirror of the data cursor (always advances)
+  std::vector<void*> allocs;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // per-phase event timing (dlc_engine_set_timing)
+  struct Mark {
+    int phase;
+    cudaEvent_t a, b;
+  };
+  bool timing = false;
+  std::vector<Mark> pending;
+  std::vector<cudaEvent_t> pool;
+  double phase_ms[4] = {0, 0, 0, 0};
+  uint64_t phase_n[4] = {0, 0, 0, 0};
+  cudaEvent_t open_ev = nullptr;
+};
+
+namespace {
+
+size_t elem_width(int prec) { return prec == DLC_FP16 ? 2 : 4; }
+
+void* dalloc(dlc_engine* e, size_t bytes) {
+  void* p = nullptr;
+  DLC_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 256)));
+  e->allocs.push_back(p);
+  return p;
+}
+
+struct DeviceGuard {
+  int prev = 0;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) DLC_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+void launched(const char* what) { DLC_LAUNCHED(what); }
+
+void harvest(dlc_engine* e) {
+  if (e->pending.empty()) return;
+  DLC_CUDA(cudaStreamSynchronize(e->stream));
+  for (const auto& mk : e->pending) {
+    float ms = 0.0f;
+    DLC_CUDA(cudaEventElapsedTime(&ms, mk.a, mk.b));
+    e->phase_ms[mk.phase] += ms;
+    e->phase_n[mk.phase] += 1;
+    e->pool.push_back(mk.a);
+    e->pool.push_back(mk.b);
+  }
+  e->pending.clear();
+}
+
+cudaEvent_t pooled_event(dlc_engine* e) {
+  if (e->pool.empty()) {
+    cudaEvent_t ev;
+    DLC_CUDA(cudaEventCreate(&ev));
+    return ev;
+  }
+  cudaEvent_t ev = e->pool.back();
+  e->pool.pop_back();
+  return ev;
+}
+
+// Brackets one phase on the engine stream when timing is on.
+void phase_begin(dlc_engine* e) {
+  if (!e->timing) return;
+  if (e->pending.size() > 8192) harvest(e);
+  e->open_ev = pooled_event(e);
+  DLC_CUDA(cudaEventRecord(e->open_ev, e->stream));
+}
+
+void phase_end(dlc_engine* e, int phase) {
+  if (!e->timing) return;
+  cudaEvent_t b = pooled_event(e);
+  DLC_CUDA(cudaEventRecord(b, e->stream));
+  e->pending.push_back({phase, e->open_ev, b});
+}
+
+// Host tables of the per-step scalars the reference computes on the host:
+// corr1/corr2 from std::pow(float, float) (optim.cpp:73-76) and lr_at
+// (optim.cpp:37-56, indexed as engine.cpp:64).  Index = the 1-based step t.
+void ensure_tables(dlc_engine* e, uint64_t t_max) {
+  if (t_max < e->tab_cap) return;
+  size_t cap = std::max<size_t>(e->tab_cap * 2, 4096);
+  while (cap <= t_max) cap *= 2;
+  std::vector<float> h(3 * cap);
+  const float b1 = e->hyper.beta1, b2 = e->hyper.beta2;
+  dlc_lr_schedule sch{e->hyper.warmup_steps, e->cfg.total_inner_steps, e->hyper.inner_lr, e->hyper.lr_decay};
+  for (size_t t = 0; t < cap; ++t) {
+    h[t] = 1.0f - std::pow(b1, static_cast<float>(t));
+    h[cap + t] = 1.0f - std::pow(b2, static_cast<float>(t));
+    h[2 * cap + t] = dlc_lr_at(&sch, t);
+  }
+  float* fresh = nullptr;
+  DLC_CUDA(cudaMalloc(&fresh, 3 * cap * sizeof(float)));
+  DLC_CUDA(cudaMemcpyAsync(fresh, h.data(), 3 * cap * sizeof(float), cudaMemcpyHostToDevice, e->stream));
+  DLC_CUDA(cudaStreamSynchronize(e->stream));  // in-flight K1 launches still read the old table
+  if (e->tab) cudaFree(e->tab);
+  e->tab = fresh;
+  e->tab_cap = cap;
+}
+
+DevState read_state(dlc_engine* e) {
+  DevState s;
+  DLC_CUDA(cudaStreamSynchronize(e->stream));
+  DLC_CUDA(cudaMemcpy(&s, e->st, sizeof(DevState), cudaMemcpyDeviceToHost));
+  return s;
+}
+
+float* live(dlc_engine* e, int which) {
+  const int cur = e->inner_mode == DLC_INNER_PINGPONG ? read_state(e).cur : 0;
+  switch (which) {
+    case DLC_THETA_T: return e->theta_t;
+    case DLC_THETA_LOCAL: return e->p[cur];
+    case DLC_ADAM_M: return e->m[cur];
+    case DLC_ADAM_V: return e->v[cur];
+    case DLC_MOMENTUM: return e->buf;
+    case DLC_GRAD: return e->grad;
+  }
+  fail(DLC_EINVAL, "unknown engine buffer " + std::to_string(which));
+}
+
+void engine_inner(dlc_engine* e, const float* grad, int grad_is_scaled) {
+  if (e->issued_inner >= e->cfg.total_inner_steps) fail(DLC_EINVAL, "inner_step called after total_inner_steps");
+  ensure_tables(e, e->issued_inner + 2);
+  const float* g = grad;
+  if (!grad_is_scaled) {  // engine.cpp:56: closed-form backward of the scaled loss
+    launch_scale_gradient(grad, e->st, e->grad, e->n, e->stream);
+    g = e->grad;
+  }
+  AdamWArgs a{};
+  for (int i = 0; i < 2; ++i) {
+    a.p[i] = e->p[i];
+    a.m[i] = e->m[i];
+    a.v[i] = e->v[i];
+  }
+  a.g = g;
+  a.corr1 = e->tab;
+  a.corr2 = e->tab + e->tab_cap;
+  a.lr = e->tab + 2 * e->tab_cap;
+  a.st = e->st;
+  a.n = e->n;
+  a.b1 = e->hyper.beta1;
+  a.b2 = e->hyper.beta2;
+  a.eps = e->hyper.adam_eps;
+  a.wd = e->hyper.weight_decay;
+  a.omb1 = 1.0f - e->hyper.beta1;
+  a.omb2 = 1.0f - e->hyper.beta2;
+  a.pingpong = e->inner_mode == DLC_INNER_PINGPONG;
+  phase_begin(e);
+  if (!a.pingpong) launch_unscale_check(g, e->st, &e->st->found_inf, e->n, e->stream);
+  launch_adamw(a, e->stream);
+  phase_end(e, DLC_PHASE_INNER);
+  launched("adamw");
+  e->issued_inner += 1;
+}
+
+Pair local_pair(dlc_engine* e) { return Pair{{e->p[0], e->p[1]}}; }
+
+void reset_flags(dlc_engine* e) {
+  DLC_CUDA(cudaMemsetAsync(e->flags, 0, kMaxK * sizeof(int), e->stream));
+  DLC_CUDA(cudaMemsetAsync(&e->st->delta_nonfinite, 0, sizeof(int), e->stream));
+}
+
+// K2 from an explicit theta_local pair (the engine's own, or a staging buffer).
+void pseudo_grad(dlc_engine* e, Pair tl) {
+  phase_begin(e);
+  launch_pseudo_grad(e->theta_t, tl, e->st, e->send, e->prec, &e->st->delta_nonfinite, e->n, e->stream);
+  phase_end(e, DLC_PHASE_PSEUDO);
+  launched("pseudo_grad");
+}
+
+void nesterov(dlc_engine* e, const void* dbar, const int* flags, int nflags) {
+  phase_begin(e);
+  launch_nesterov_outer(e->theta_t, e->buf, local_pair(e), dbar, e->prec, flags, nflags, e->st,
+                        e->hyper.outer_lr, e->hyper.outer_momentum, e->n, e->stream);
+  phase_end(e, DLC_PHASE_OUTER);
+  launched("nesterov_outer");
+}
+
+ncclDataType_t nccl_type(int prec) { return prec == DLC_FP16 ? ncclFloat16 : ncclFloat32; }
+
+// C1 + K3 on the engine's send buffer, then K4.  Everything is enqueued on the
+// engine stream; NCCL calls are stream-ordered with the kernels around them.
+void outer_collective(dlc_engine* e, dlc_collective* c, dlc_reduce_report* rep) {
+  const size_t K = e->k, S = e->S, w = elem_width(e->prec);
+  char* send = static_cast<char*>(e->send);
+  if (K == 1) {  // SoloCollective: the mean of one contribution is itself (reduce.cpp:113-126)
+    nesterov(e, e->send, &e->st->delta_nonfinite, 1);
+    return;
+  }
+  const int r = c->rank;
+  if (rep) DLC_CUDA(cudaEventRecord(e->ev0, e->stream));
+  phase_begin(e);
+  if (c->mode == DLC_MODE_ORDERED) {
+    char* recv = static_cast<char*>(e->recv);
+    char* gather = static_cast<char*>(e->gather);
+    // scatter: partition j of my delta goes to its owner j (collective.cpp:1400-1426)
+    DLC_NCCL(ncclGroupStart());
+    for (size_t j = 0; j < K; ++j) {
+      if ((int)j == r) continue;
+      DLC_NCCL(ncclSend(send + j * S * w, S, nccl_type(e->prec), (int)j, c->comm, e->stream));
+      DLC_NCCL(ncclRecv(recv + j * S * w, S, nccl_type(e->prec), (int)j, c->comm, e->stream));
+    }
+    DLC_NCCL(ncclGroupEnd());
+    // owner fold in rank order (collective.cpp:1444-1489)
+    PtrList in{};
+    for (size_t j = 0; j < K; ++j) in.ptr[j] = ((int)j == r) ? send + r * S * w : recv + j * S * w;
+    launch_fold(in, (int)K, e->prec, gather + r * S * w, e->prec, e->flags + r, S, e->stream);
+    launched("fold");
+    // all-gather of the owner means and their non-finite flags (collective.cpp:1491-1531)
+    DLC_NCCL(ncclGroupStart());
+    DLC_NCCL(ncclAllGather(gather + r * S * w, gather, S, nccl_type(e->prec), c->comm, e->stream));
+    DLC_NCCL(ncclAllGather(e->flags + r, e->flags, 1, ncclInt32, c->comm, e->stream));
+    DLC_NCCL(ncclGroupEnd());
+    phase_end(e, DLC_PHASE_COLLECTIVE);
+    if (rep) DLC_CUDA(cudaEventRecord(e->ev1, e->stream));
+    nesterov(e, e->gather, e->flags, (int)K);
+  } else {
+    DLC_NCCL(ncclAllReduce(send, send, K * S, nccl_type(e->prec), ncclAvg, c->comm, e->stream));
+    if (e->prec == DLC_FP16)
+      launch_nonfinite_codes(static_cast<const uint16_t*>(e->send), e->flags, e->n, e->stream);
+    else
+      launch_nonfinite(static_cast<const float*>(e->send), e->flags, e->n, e->stream);
+    launched("nonfinite");
+    phase_end(e, DLC_PHASE_COLLECTIVE);
+    if (rep) DLC_CUDA(cudaEventRecord(e->ev1, e->stream));
+    nesterov(e, e->send, e->flags, 1);
+  }
+}
+
+void fill_report(dlc_engine* e, dlc_collective* c, dlc_reduce_report* rep, uint64_t epoch) {
+  if (!rep) return;
+  *rep = dlc_reduce_report{};
+  rep->outer_epoch = epoch;
+  rep->contributors = e->k;
+  rep->attempts = 1;
+  if (e->k > 1) {
+    const uint64_t bytes = 2ull * (e->k - 1) * e->S * elem_width(e->prec);
+    rep->data_bytes_sent = rep->data_bytes_received = bytes;
+    rep->wire_bytes_sent = rep->wire_bytes_received = bytes;
+    DLC_CUDA(cudaEventSynchronize(e->ev1));
+    float ms = 0;
+    DLC_CUDA(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
+    rep->wall_ms = ms;
+  }
+  (void)c;
+}
+
+void check_collective(dlc_engine* e, dlc_collective* c) {
+  const size_t world = c ? (size_t)c->world : 1;
+  if (world != e->k)
+    fail(DLC_ECOLLECTIVE, "collective world size " + std::to_string(world) + " != num_workers_k " +
+                              std::to_string(e->k));
+  if (c && c->kind == 1 && c->device != e->device) fail(DLC_ECOLLECTIVE, "collective and engine devices differ");
+  if (e->issued_inner % e->cfg.local_steps_h != 0)  // engine.cpp:116-120
+    fail(DLC_EINVAL, "pseudo-gradient requested mid-window (inner_step " + std::to_string(e->issued_inner) +
+                         ", H " + std::to_string(e->cfg.local_steps_h) + ")");
+}
+
+void outer_result(dlc_engine* e, dlc_outer_result* res) {
+  if (!res) return;
+  const DevState s = read_state(e);
+  res->applied = s.last_applied;
+  res->outer_epoch = s.outer_epoch;
+}
+
+}  // namespace
+
+extern "C" {
+
+void dlc_hyperparams_default(dlc_hyperparams* h) {
+  // OptimHyperparams defaults, engine.hpp:34-46
+  h->inner_lr = 4e-4f;
+  h->warmup_steps = 1000;
+  h->lr_decay = DLC_LR_NONE;
+  h->weight_decay = 0.1f;
+  h->beta1 = 0.9f;
+  h->beta2 = 0.95f;
+  h->adam_eps = 1e-8f;
+  h->outer_lr = 0.7f;
+  h->outer_momentum = 0.9f;
+  h->scaler_init_scale = 65536.0f;
+  h->scaler_growth_interval = 2000;
+}
+
+int dlc_engine_create(const dlc_config* cfg, const dlc_hyperparams* hyper, size_t n, int device, int inner_mode,
+                      dlc_engine** out) {
+  dlc_engine* e = nullptr;
+  const int st = guard([&] {
+    if (!cfg || !hyper || !out) fail(DLC_EINVAL, "dlc_engine_create: null argument");
+    *out = nullptr;
+    // DilocoConfig::validate, engine.cpp:31-48
+    if (cfg->local_steps_h < 1) fail(DLC_ECONFIG, "local_steps must be >= 1");
+    if (cfg->num_workers_k < 1) fail(DLC_ECONFIG, "num_workers must be >= 1");
+    if (cfg->total_inner_steps == 0 || cfg->total_inner_steps % cfg->local_steps_h != 0)
+      fail(DLC_ECONFIG, "total_inner_steps (" + std::to_string(cfg->total_inner_steps) +
+                            ") must be a positive multiple of local_steps (" + std::to_string(cfg->local_steps_h) +
+                            ")");
+    if (cfg->num_workers_k > (size_t)kMaxK) fail(DLC_ECONFIG, "num_workers_k exceeds 32");
+    if (cfg->reduce_precision != DLC_FP32 && cfg->reduce_precision != DLC_FP16)
+      fail(DLC_ECONFIG, "unknown reduce precision");
+    if (inner_mode != DLC_INNER_PINGPONG && inner_mode != DLC_INNER_INPLACE) fail(DLC_ECONFIG, "unknown inner mode");
+    DeviceGuard dg(device);
+    e = new dlc_engine();
+    e->device = device;
+    e->cfg = *cfg;
+    e->hyper = *hyper;
+    e->inner_mode = inner_mode;
+    e->n = n;
+    e->k = cfg->num_workers_k;
+    e->prec = cfg->reduce_precision;
+    e->S = (((n + e->k - 1) / e->k) + 63) / 64 * 64;
+    DLC_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+    DLC_CUDA(cudaEventCreate(&e->ev0));
+    DLC_CUDA(cudaEventCreate(&e->ev1));
+    const size_t vb = n * sizeof(float);
+    e->theta_t = (float*)dalloc(e, vb);
+    const int pairs = inner_mode == DLC_INNER_PINGPONG ? 2 : 1;
+    for (int i = 0; i < pairs; ++i) {
+      e->p[i] = (float*)dalloc(e, vb);
+      e->m[i] = (float*)dalloc(e, vb);
+      e->v[i] = (float*)dalloc(e, vb);
+    }
+    if (pairs == 1) {
+      e->p[1] = e->p[0];
+      e->m[1] = e->m[0];
+      e->v[1] = e->v[0];
+    }
+    e->buf = (float*)dalloc(e, vb);
+    e->grad = (float*)dalloc(e, vb);
+    const size_t pb = e->k * e->S * elem_width(e->prec);
+    e->send = dalloc(e, pb);
+    DLC_CUDA(cudaMemsetAsync(e->send, 0, pb, e->stream));  // padding stays zero
+    if (e->k > 1) {
+      e->recv = dalloc(e, pb);
+      e->gather = dalloc(e, pb);
+      DLC_CUDA(cudaMemsetAsync(e->gather, 0, pb, e->stream));
+    }
+    e->flags = (int*)dalloc(e, kMaxK * sizeof(int));
+    e->st = (DevState*)dalloc(e, sizeof(DevState));
+    for (int i = 0; i < pairs; ++i) {
+      DLC_CUDA(cudaMemsetAsync(e->p[i], 0, vb, e->stream));
+      DLC_CUDA(cudaMemsetAsync(e->m[i], 0, vb, e->stream));  // AdamWState::init zeros, optim.cpp:17-27
+      DLC_CUDA(cudaMemsetAsync(e->v[i], 0, vb, e->stream));
+    }
+    DLC_CUDA(cudaMemsetAsync(e->theta_t, 0, vb, e->stream));
+    DLC_CUDA(cudaMemsetAsync(e->buf, 0, vb, e->stream));  // NesterovState::init, optim.cpp:29-35
+    DLC_CUDA(cudaMemsetAsync(e->flags, 0, kMaxK * sizeof(int), e->stream));
+    DevState s{};
+    s.scale = hyper->scaler_init_scale;
+    s.growth = hyper->scaler_growth_interval;
+    DLC_CUDA(cudaMemcpyAsync(e->st, &s, sizeof(s), cudaMemcpyHostToDevice, e->stream));
+    ensure_tables(e, std::min<uint64_t>(cfg->total_inner_steps + 2, 1u << 16));
+    DLC_CUDA(cudaStreamSynchronize(e->stream));
+    *out = e;
+  });
+  if (st != DLC_OK && e) dlc_engine_destroy(e);
+  return st;
+}
+
+int dlc_engine_destroy(dlc_engine* e) {
+  if (!e) return DLC_OK;
+  return guard([&] {
+    DeviceGuard dg(e->device);
+    if (e->stream) cudaStreamSynchronize(e->stream);
+    for (void* p : e->allocs) cudaFree(p);
+    for (const auto& mk : e->pending) {
+      cudaEventDestroy(mk.a);
+      cudaEventDestroy(mk.b);
+    }
+    for (cudaEvent_t ev : e->pool) cudaEventDestroy(ev);
+    if (e->tab) cudaFree(e->tab);
+    if (e->ev0) cudaEventDestroy(e->ev0);
+    if (e->ev1) cudaEventDestroy(e->ev1);
+    if (e->stream) cudaStreamDestroy(e->stream);
+    delete e;
+  });
+}
+
+size_t dlc_engine_size(const dlc_engine* e) { return e ? e->n : 0; }
+
+int dlc_engine_stream(dlc_engine* e, void** stream) {
+  return guard([&] {
+    if (!e || !stream) fail(DLC_EINVAL, "dlc_engine_stream: null argument");
+    *stream = (void*)e->stream;
+  });
+}
+
+int dlc_engine_upload(dlc_engine* e, int which, const float* host, size_t n) {
+  return guard([&] {
+    if (!e || (n && !host)) fail(DLC_EINVAL, "dlc_engine_upload: null argument");
+    if (n != e->n) fail(DLC_ESHAPE, "upload length " + std::to_string(n) + " != engine size " + std::to_string(e->n));
+    DeviceGuard dg(e->device);
+    float* d = live(e, which);
+    DLC_CUDA(cudaMemcpyAsync(d, host, n * sizeof(float), cudaMemcpyHostToDevice, e->stream));
+    DLC_CUDA(cudaStreamSynchronize(e->stream));
+  });
+}
+
+int dlc_engine_download(dlc_engine* e, int which, float* host, size_t n) {
+  return guard([&] {
+    if (!e || (n && !host)) fail(DLC_EINVAL, "dlc_engine_download: null argument");
+    if (n != e->n) fail(DLC_ESHAPE, "download length " + std::to_string(n) + " != engine size " + std::to_string(e->n));
+    DeviceGuard dg(e->device);
+    float* d = live(e, which);
+    DLC_CUDA(cudaMemcpyAsync(host, d, n * sizeof(float), cudaMemcpyDeviceToHost, e->stream));
+    DLC_CUDA(cudaStreamSynchronize(e->stream));
+  });
+}
+
+int dlc_engine_device_ptr(dlc_engine* e, int which, float** dev) {
+  return guard([&] {
+    if (!e || !dev) fail(DLC_EINVAL, "dlc_engine_device_ptr: null argument");
+    DeviceGuard dg(e->device);
+    *dev = live(e, which);
+  });
+}
+
+int dlc_engine_get_scalars(dlc_engine* e, dlc_engine_scalars* out) {
+  return guard([&] {
+    if (!e || !out) fail(DLC_EINVAL, "dlc_engine_get_scalars: null argument");
+    DeviceGuard dg(e->device);
+    const DevState s = read_state(e);
+    out->step_count = s.step_count;
+    out->inner_step = s.inner_step;
+    out->outer_epoch = s.outer_epoch;
+    out->scale = s.scale;
+    out->consecutive_good = s.good;
+    out->overflow_skips = s.overflow_skips;
+    out->outer_skips = s.outer_skips;
+    out->last_lr = s.last_lr;
+    out->last_overflow = s.last_overflow;
+    out->last_applied = s.last_applied;
+  });
+}
+
+int dlc_engine_set_scalars(dlc_engine* e, const dlc_engine_scalars* in) {
+  return guard([&] {
+    if (!e || !in) fail(DLC_EINVAL, "dlc_engine_set_scalars: null argument");
+    if (in->inner_step > e->cfg.total_inner_steps) fail(DLC_ECONFIG, "inner_step beyond total_inner_steps");
+    DeviceGuard dg(e->device);
+    DevState s = read_state(e);
+    s.step_count = in->step_count;
+    s.inner_step = in->inner_step;
+    s.outer_epoch = in->outer_epoch;
+    s.scale = in->scale;
+    s.good = in->consecutive_good;
+    s.overflow_skips = in->overflow_skips;
+    s.outer_skips = in->outer_skips;
+    s.last_lr = in->last_lr;
+    s.last_overflow = in->last_overflow;
+    s.last_applied = in->last_applied;
+    ensure_tables(e, in->step_count + 2);
+    DLC_CUDA(cudaMemcpy(e->st, &s, sizeof(s), cudaMemcpyHostToDevice));
+    e->issued_inner = in->inner_step;
+  });
+}
+
+int dlc_engine_synchronize(dlc_engine* e) {
+  return guard([&] {
+    if (!e) fail(DLC_EINVAL, "dlc_engine_synchronize: null engine");
+    DeviceGuard dg(e->device);
+    DLC_CUDA(cudaStreamSynchronize(e->stream));
+  });
+}
+
+int dlc_engine_inner_step(dlc_engine* e, const float* grad, int grad_is_scaled, dlc_inner_result* result) {
+  return guard([&] {
+    if (!e || (e->n && !grad)) fail(DLC_EINVAL, "dlc_engine_inner_step: null argument");
+    DeviceGuard dg(e->device);
+    engine_inner(e, grad, grad_is_scaled);
+    if (result) {
+      const DevState s = read_state(e);
+      result->lr = s.last_lr;
+      result->overflow_skipped = s.last_overflow;
+    }
+  });
+}
+
+int dlc_engine_inner_step_host(dlc_engine* e, const float* host_grad, int grad_is_scaled,
+                               dlc_inner_result* result) {
+  return guard([&] {
+    if (!e || (e->n && !host_grad)) fail(DLC_EINVAL, "dlc_engine_inner_step_host: null argument");
+    DeviceGuard dg(e->device);
+    DLC_CUDA(cudaMemcpyAsync(e->grad, host_grad, e->n * sizeof(float), cudaMemcpyHostToDevice, e->stream));
+    engine_inner(e, e->grad, grad_is_scaled);
+    if (result) {
+      const DevState s = read_state(e);
+      result->lr = s.last_lr;
+      result->overflow_skipped = s.last_overflow;
+    }
+  });
+}
+
+int dlc_engine_outer_step(dlc_engine* e, dlc_collective* c, dlc_outer_result* result, dlc_reduce_report* report) {
+  return guard([&] {
+    if (!e) fail(DLC_EINVAL, "dlc_engine_outer_step: null engine");
+    if (c && c->kind == 0) c = nullptr;
+    check_collective(e, c);
+    DeviceGuard dg(e->device);
+    const uint64_t epoch = report ? read_state(e).outer_epoch : 0;
+    reset_flags(e);
+    pseudo_grad(e, local_pair(e));
+    outer_collective(e, c, report);
+    fill_report(e, c, report, epoch);
+    outer_result(e, result);
+  });
+}
+
+int dlc_engine_outer_step_from(dlc_engine* e, dlc_collective* c, const float* theta_local_dev,
+                               dlc_outer_result* result, dlc_reduce_report* report) {
+  return guard([&] {
+    if (!e || (e->n && !theta_local_dev)) fail(DLC_EINVAL, "dlc_engine_outer_step_from: null argument");
+    if (c && c->kind == 0) c = nullptr;
+    check_collective(e, c);
+    DeviceGuard dg(e->device);
+    const uint64_t epoch = report ? read_state(e).outer_epoch : 0;
+    float* src = const_cast<float*>(theta_local_dev);
+    reset_flags(e);
+    pseudo_grad(e, Pair{{src, src}});
+    outer_collective(e, c, report);
+    fill_report(e, c, report, epoch);
+    outer_result(e, result);
+  });
+}
+
+int dlc_engine_set_timing(dlc_engine* e, int on) {
+  return guard([&] {
+    if (!e) fail(DLC_EINVAL, "dlc_engine_set_timing: null engine");
+    DeviceGuard dg(e->device);
+    harvest(e);
+    e->timing = on != 0;
+  });
+}
+
+int dlc_engine_phase_times(dlc_engine* e, double total_ms[4], uint64_t count[4]) {
+  return guard([&] {
+    if (!e || !total_ms || !count) fail(DLC_EINVAL, "dlc_engine_phase_times: null argument");
+    DeviceGuard dg(e->device);
+    harvest(e);
+    for (int i = 0; i < 4; ++i) {
+      total_ms[i] = e->phase_ms[i];
+      count[i] = e->phase_n[i];
+      e->phase_ms[i] = 0.0;
+      e->phase_n[i] = 0;
+    }
+  });
+}
+
+int dlc_engine_outer_step_host(dlc_engine* e, dlc_collective* c, const float* host_theta_local, float* host_theta_t,
+                               dlc_outer_result* result) {
+  return guard([&] {
+    if (!e || (e->n && (!host_theta_local || !host_theta_t))) fail(DLC_EINVAL, "dlc_engine_outer_step_host: null argument");
+    if (c && c->kind == 0) c = nullptr;
+    check_collective(e, c);
+    DeviceGuard dg(e->device);
+    // theta_local arrives in the staging buffer; K4 then refreshes the engine's
+    // own theta_local from the new theta_t.
+    DLC_CUDA(cudaMemcpyAsync(e->grad, host_theta_local, e->n * sizeof(float), cudaMemcpyHostToDevice, e->stream));
+    reset_flags(e);
+    pseudo_grad(e, Pair{{e->grad, e->grad}});
+    outer_collective(e, c, nullptr);
+    DLC_CUDA(cudaMemcpyAsync(host_theta_t, e->theta_t, e->n * sizeof(float), cudaMemcpyDeviceToHost, e->stream));
+    DLC_CUDA(cudaStreamSynchronize(e->stream));
+    outer_result(e, result);
+  });
+}
+
+int dlc_engines_outer_step_local(dlc_engine* const* engines, size_t k, dlc_outer_result* result) {
+  return guard([&] {
+    if (!engines || k == 0) fail(DLC_ECOLLECTIVE, "outer_step_local: no engines");
+    if (k > (size_t)kMaxK) fail(DLC_ECONFIG, "outer_step_local: more than 32 engines");
+    dlc_engine* e0 = engines[0];
+    for (size_t j = 0; j < k; ++j) {
+      dlc_engine* e = engines[j];
+      if (!e) fail(DLC_EINVAL, "outer_step_local: null engine");
+      if (e->n != e0->n || e->prec != e0->prec || e->device != e0->device)
+        fail(DLC_ESHAPE, "outer_step_local: engines differ in size, precision or device");  // reduce.cpp:52-56
+      if (e->k != k) fail(DLC_ECOLLECTIVE, "outer_step_local: num_workers_k != fleet size");
+      if (e->issued_inner % e->cfg.local_steps_h != 0) fail(DLC_EINVAL, "pseudo-gradient requested mid-window");
+    }
+    DeviceGuard dg(e0->device);
+    cudaEvent_t ev;
+    DLC_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    for (size_t j = 1; j < k; ++j) {  // everything below runs on engine 0's stream
+      DLC_CUDA(cudaEventRecord(ev, engines[j]->stream));
+      DLC_CUDA(cudaStreamWaitEvent(e0->stream, ev, 0));
+    }
+    cudaStream_t s = e0->stream;
+    for (size_t j = 0; j < k; ++j)
+      DLC_CUDA(cudaMemsetAsync(&engines[j]->st->delta_nonfinite, 0, sizeof(int), s));
+    PtrList in{};
+    for (size_t j = 0; j < k; ++j) {
+      dlc_engine* e = engines[j];
+      launch_pseudo_grad(e->theta_t, local_pair(e), e->st, e->send, e->prec, &e->st->delta_nonfinite, e->n, s);
+      in.ptr[j] = e->send;
+    }
+    DLC_CUDA(cudaMemsetAsync(e0->flags, 0, kMaxK * sizeof(int), s));
+    void* dbar = k > 1 ? e0->gather : e0->send;
+    if (k > 1) {
+      launch_fold(in, (int)k, e0->prec, e0->gather, e0->prec, e0->flags, e0->n, s);
+    } else {
+      DLC_CUDA(cudaMemcpyAsync(e0->flags, &e0->st->delta_nonfinite, sizeof(int), cudaMemcpyDeviceToDevice, s));
+    }
+    for (size_t j = 0; j < k; ++j) {
+      dlc_engine* e = engines[j];
+      launch_nesterov_outer(e->theta_t, e->buf, local_pair(e), dbar, e->prec, e0->flags, 1, e->st,
+                            e->hyper.outer_lr, e->hyper.outer_momentum, e->n, s);
+    }
+    launched("outer_step_local");
+    DLC_CUDA(cudaEventRecord(ev, s));
+    for (size_t j = 1; j < k; ++j) DLC_CUDA(cudaStreamWaitEvent(engines[j]->stream, ev, 0));
+    DLC_CUDA(cudaEventDestroy(ev));
+    outer_result(e0, result);
+  });
+}
+
+int dlc_optimizer_step(dlc_engine* e, dlc_collective* c, const float* grad, int grad_is_scaled, int* round_completed) {
+  return guard([&] {
+    if (!e || (e->n && !grad)) fail(DLC_EINVAL, "dlc_optimizer_step: null argument");
+    if (c && c->kind == 0) c = nullptr;
+    DeviceGuard dg(e->device);
+    engine_inner(e, grad, grad_is_scaled);  // engine.cpp:163
+    const bool boundary = e->issued_inner % e->cfg.local_steps_h == 0;
+    if (round_completed) *round_completed = boundary ? 1 : 0;
+    if (boundary) {  // engine.cpp:165-172
+      check_collective(e, c);
+      reset_flags(e);
+      pseudo_grad(e, local_pair(e));
+      outer_collective(e, c, nullptr);
+    }
+  });
+}
+
+int dlc_rng_fill_device(dlc_engine* e, int which, uint64_t key, uint64_t first, float lo, float hi) {
+  return guard([&] {
+    if (!e) fail(DLC_EINVAL, "dlc_rng_fill_device: null engine");
+    DeviceGuard dg(e->device);
+    float* d = live(e, which);
+    launch_rng_fill(key, first, lo, hi, d, e->n, e->stream);
+    launched("rng_fill");
+  });
+}
+
+int dlc_rng_perturb(dlc_engine* e, float* dst, uint64_t key, float lo, float hi) {
+  return guard([&] {
+    if (!e) fail(DLC_EINVAL, "dlc_rng_perturb: null engine");
+    DeviceGuard dg(e->device);
+    float* d = dst ? dst : live(e, DLC_THETA_LOCAL);
+    launch_rng_perturb(e->theta_t, key, lo, hi, d, e->n, e->stream);
+    launched("rng_perturb");
+  });
+}
+
+// ---- collectives ---------------------------------------------------------------
+
+int dlc_nccl_unique_id(uint8_t id[128]) {
+  return guard([&] {
+    if (!id) fail(DLC_EINVAL, "dlc_nccl_unique_id: null id");
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    ncclUniqueId u;
+    DLC_NCCL(ncclGetUniqueId(&u));
+    std::memcpy(id, &u, 128);
+  });
+}
+
+int dlc_collective_create_nccl(int rank, int world, const uint8_t id[128], int device, int mode,
+                               dlc_collective** out) {
+  return guard([&] {
+    if (!id || !out) fail(DLC_EINVAL, "dlc_collective_create_nccl: null argument");
+    if (world < 1 || rank < 0 || rank >= world) fail(DLC_ECONFIG, "bad rank/world");
+    if (mode != DLC_MODE_ORDERED && mode != DLC_MODE_ALLREDUCE) fail(DLC_ECONFIG, "unknown reduce mode");
+    DeviceGuard dg(device);
+    auto* c = new dlc_collective();
+    c->kind = 1;
+    c->rank = rank;
+    c->world = world;
+    c->device = device;
+    c->mode = mode;
+    ncclUniqueId u;
+    std::memcpy(&u, id, 128);
+    const ncclResult_t r = ncclCommInitRank(&c->comm, world, u, rank);
+    if (r != ncclSuccess) {
+      delete c;
+      fail(DLC_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    }
+    cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    *out = c;
+  });
+}
+
+int dlc_collective_create_solo(int device, dlc_collective** out) {
+  return guard([&] {
+    if (!out) fail(DLC_EINVAL, "dlc_collective_create_solo: null out");
+    auto* c = new dlc_collective();
+    c->device = device;
+    *out = c;
+  });
+}
+
+int dlc_collective_destroy(dlc_collective* c) {
+  if (!c) return DLC_OK;
+  return guard([&] {
+    if (c->kind == 1) {
+      DeviceGuard dg(c->device);
+      if (c->stream) cudaStreamDestroy(c->stream);
+      ncclCommDestroy(c->comm);
+    }
+    delete c;
+  });
+}
+
+size_t dlc_collective_world_size(const dlc_collective* c) { return c ? (size_t)c->world : 1; }
+int dlc_collective_rank(const dlc_collective* c) { return c ? c->rank : 0; }
+
+int dlc_collective_all_reduce_avg(dlc_collective* c, const float* local, size_t n, int precision,
+                                  uint64_t outer_epoch, float* out, dlc_reduce_report* report) {
+  return guard([&] {
+    if (!c || (n && (!local || !out))) fail(DLC_EINVAL, "all_reduce_avg: null argument");
+    if (precision != DLC_FP32 && precision != DLC_FP16) fail(DLC_ECONFIG, "unknown precision");
+    const auto t0 = std::chrono::steady_clock::now();
+    if (c->kind == 0 || c->world == 1) {  // SoloCollective, reduce.cpp:113-126
+      const float* one[1] = {local};
+      const int st = dlc_reduce_average(one, 1, n, precision, out);
+      if (st != DLC_OK) fail(st, dlc_last_error());
+    } else {
+      // Host pseudo-gradient through a transient device engine-less pipeline:
+      // encode -> scatter -> ordered fold -> all-gather -> decode.
+      DeviceGuard dg(c->device);
+      const size_t K = c->world, w = precision == DLC_FP16 ? 2 : 4;
+      const size_t S = (((n + K - 1) / K) + 63) / 64 * 64;
+      std::vector<void*> allocs;
+      auto take = [&](size_t b) {
+        void* p = nullptr;
+        DLC_CUDA(cudaMalloc(&p, std::max<size_t>(b, 256)));
+        allocs.push_back(p);
+        return (char*)p;
+      };
+      try {
+        char* src = take(n * 4);
+        char* send = take(K * S * w);
+        char* recv = take(K * S * w);
+        char* gather = take(K * S * w);
+        float* res = (float*)take(K * S * 4);
+        cudaStream_t s = c->stream;
+        DLC_CUDA(cudaMemsetAsync(send, 0, K * S * w, s));
+        DLC_CUDA(cudaMemcpyAsync(src, local, n * 4, cudaMemcpyHostToDevice, s));
+        if (precision == DLC_FP16)
+          launch_encode((const float*)src, (uint16_t*)send, nullptr, n, s);  // collective.cpp:1356-1366
+        else
+          DLC_CUDA(cudaMemcpyAsync(send, src, n * 4, cudaMemcpyDeviceToDevice, s));
+        const int r = c->rank;
+        if (c->mode == DLC_MODE_ORDERED) {
+          DLC_NCCL(ncclGroupStart());
+          for (size_t j = 0; j < K; ++j) {
+            if ((int)j == r) continue;
+            DLC_NCCL(ncclSend(send + j * S * w, S, nccl_type(precision), (int)j, c->comm, s));
+            DLC_NCCL(ncclRecv(recv + j * S * w, S, nccl_type(precision), (int)j, c->comm, s));
+          }
+          DLC_NCCL(ncclGroupEnd());
+          PtrList in{};
+          for (size_t j = 0; j < K; ++j) in.ptr[j] = ((int)j == r) ? send + r * S * w : recv + j * S * w;
+          launch_fold(in, (int)K, precision, gather + r * S * w, precision, nullptr, S, s);
+          DLC_NCCL(ncclAllGather(gather + r * S * w, gather, S, nccl_type(precision), c->comm, s));
+        } else {
+          DLC_NCCL(ncclAllReduce(send, gather, K * S, nccl_type(precision), ncclAvg, c->comm, s));
+        }
+        if (precision == DLC_FP16)
+          launch_decode((const uint16_t*)gather, res, n, s);
+        else
+          DLC_CUDA(cudaMemcpyAsync(res, gather, n * 4, cudaMemcpyDeviceToDevice, s));
+        DLC_CUDA(cudaMemcpyAsync(out, res, n * 4, cudaMemcpyDeviceToHost, s));
+        DLC_LAUNCHED("all_reduce_avg");
+        DLC_CUDA(cudaStreamSynchronize(s));
+      } catch (...) {
+        for (void* p : allocs) cudaFree(p);
+        throw;
+      }
+      for (void* p : allocs) cudaFree(p);
+    }
+    if (report) {
+      *report = dlc_reduce_report{};
+      report->outer_epoch = outer_epoch;
+      report->contributors = (size_t)c->world;
+      report->attempts = 1;
+      const uint64_t b = c->world > 1 ? dlc_per_peer_reduce_bytes(n, c->world, c->rank, precision) : 0;
+      report->data_bytes_sent = report->data_bytes_received = b;
+      report->wire_bytes_sent = report->wire_bytes_received = b;
+      report->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    }
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,131 @@
+// kernels.cuh — launch interface of the DiLoCo hot-path kernels (sm_100a).
+//
+//   K1  adamw       fused grad-scaler unscale + overflow OR + AdamW
+//                   (proj/src/optim.cpp:58-93,121-148; engine.cpp:50-69)
+//   K2  pseudo_grad delta = theta_t - theta_local, FP32 or FP16-encoded
+//                   (engine.cpp:115-126 -> tensor.cpp:118-140)
+//   K3  fold        owner fold of K contributions in rank order, / K, encode
+//                   once (reduce.cpp:33-89; collective.cpp:1444-1489)
+//   K4  nesterov    finite-gated outer Nesterov + theta_local refresh
+//                   (engine.cpp:128-146 -> optim.cpp:95-115)
+//
+// All kernels are persistent grid-stride loops over 128-bit vectors with a
+// scalar tail; grids are sized to (#SM x resident CTAs) once per kernel.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace dlc {
+
+constexpr int kMaxK = 32;  // largest worker count a single fold launch takes
+
+// Device-resident engine scalars (EngineState, engine.hpp:48-56; AdamWState
+// step_count, optim.hpp:20; LossScaler, optim.hpp:52-56).  Kept on the GPU so
+// the inner loop never waits on the host: the overflow decision, step counter
+// and loss scale are all updated by the last CTA of K1.
+struct DevState {
+  uint64_t step_count;      // applied AdamW steps
+  uint64_t inner_step;      // batches consumed (data cursor, always advances)
+  uint64_t good;            // scaler consecutive_good
+  uint64_t growth;          // scaler growth_interval
+  uint64_t outer_epoch;
+  uint64_t overflow_skips;  // inner steps skipped on overflow
+  uint64_t outer_skips;     // outer steps skipped on a non-finite reduction
+  float scale;              // loss scale (power of two)
+  float last_lr;            // lr of the last inner step (0 when skipped)
+  int cur;                  // live buffer of the p/m/v ping-pong pair
+  int found_inf;            // K1 scratch: OR of !isfinite(g / scale)
+  unsigned done_blocks;     // K1 last-CTA counter
+  int last_overflow;        // InnerStepResult::overflow_skipped
+  int delta_nonfinite;      // K2: non-finite delta (or FP16 encode overflow)
+  int last_applied;         // OuterStepResult::applied
+  int pad[2];
+};
+
+struct AdamWArgs {
+  float* p[2];
+  float* m[2];
+  float* v[2];
+  const float* g;      // scaled gradient (loss-scaled backward output)
+  const float* corr1;  // host tables indexed by the 1-based step t
+  const float* corr2;
+  const float* lr;
+  DevState* st;
+  size_t n;
+  float b1, b2, eps, wd, omb1, omb2;  // omb = 1.0f - b, rounded as optim.cpp:84-85
+  int pingpong;                       // 1: read [cur], write [cur^1]; 0: in place, gated
+};
+
+// Scalars of one out-of-place AdamW call whose gradient is already unscaled
+// and checked (host-staged drop-in of adamw_step, optim.hpp:61-62).
+struct AdamWPlain {
+  float b1, b2, eps, wd, omb1, omb2, corr1, corr2, lr;
+};
+
+struct PtrList {
+  const void* ptr[kMaxK];
+};
+
+// The two buffers of a ping-pong pair; DevState::cur selects the live one.
+struct Pair {
+  float* ptr[2];
+};
+
+int num_sms();
+
+// K1 --------------------------------------------------------------------------
+void launch_adamw(const AdamWArgs& a, cudaStream_t s);
+// In-place mode's first pass: found_inf = OR !isfinite(g * (1/scale)).
+void launch_unscale_check(const float* g, const DevState* st_scale, int* flag, size_t n,
+                          cudaStream_t s);
+void launch_adamw_plain(const float* p, const float* g, float* m, float* v, float* out,
+                        size_t n, const AdamWPlain& a, cudaStream_t s);
+
+// K2 --------------------------------------------------------------------------
+// precision 0: out is float*, 1: out is uint16_t* (binary16 codes).
+void launch_pseudo_grad(const float* theta_t, Pair theta_local,
+                        const DevState* st, void* out, int precision, int* flag, size_t n,
+                        cudaStream_t s);
+
+// K3 --------------------------------------------------------------------------
+// in_kind 0: FP32 contributions, 1: FP16 codes, 2: FP32 contributions that go
+// through one encode/decode each (reduce_average's FP16 path on FP32 inputs).
+// out_kind 0: FP32 mean, 1: FP16 code of the mean, 2: FP32 decode(encode(mean)).
+void launch_fold(const PtrList& in, int k, int in_kind, void* out, int out_kind, int* flag,
+                 size_t n, cudaStream_t s);
+
+// K4 --------------------------------------------------------------------------
+void launch_nesterov_outer(float* theta_t, float* buf, Pair theta_local,
+                           const void* dbar, int precision, const int* flags, int nflags,
+                           DevState* st, float lr, float mu, size_t n, cudaStream_t s);
+void launch_nesterov_plain(const float* p, const float* g, float* buf, float* out, size_t n,
+                           float lr, float mu, cudaStream_t s);
+
+// elementwise helpers -----------------------------------------------------------
+void launch_axpy(float alpha, const float* x, const float* y, float* out, size_t n,
+                 cudaStream_t s);
+void launch_encode(const float* x, uint16_t* out, int* flag, size_t n, cudaStream_t s);
+void launch_decode(const uint16_t* b, float* out, size_t n, cudaStream_t s);
+void launch_nonfinite(const float* x, int* flag, size_t n, cudaStream_t s);
+void launch_nonfinite_codes(const uint16_t* b, int* flag, size_t n, cudaStream_t s);
+// Ordered fold over an arbitrary number of FP32 contributions whose pointers
+// live in device memory (host-staged reduce_average for any k).
+void launch_fold_many(const float* const* ptrs, size_t k, int fp16, float* out, size_t n,
+                      cudaStream_t s);
+void launch_unscale(const float* g, float inv, float* out, int* flag, size_t n, cudaStream_t s);
+// g_scaled = g * scale where scale is read from the device state (engine.cpp:20-27).
+void launch_scale_gradient(const float* g, const DevState* st, float* out, size_t n,
+                           cudaStream_t s);
+// out[i] = CounterRng(key) draw first+i, uniform in [lo, hi) (rng.hpp:43-56).
+void launch_rng_fill(uint64_t key, uint64_t first, float lo, float hi, float* out, size_t n,
+                     cudaStream_t s);
+// theta_local = theta_t - U(lo, hi) keyed draw (synthetic end-of-window weights).
+void launch_rng_perturb(const float* theta_t, uint64_t key, float lo, float hi, float* out,
+                        size_t n, cudaStream_t s);
+// codes for the consecutive FP32 bit patterns [start, start + n)
+void launch_encode_bits_range(uint32_t start, uint16_t* out, size_t n, cudaStream_t s);
+void launch_copy(const float* src, float* dst, size_t n, cudaStream_t s);
+
+}  // namespace dlc

@@ -1,0 +1,403 @@
+"""Parity of the CUDA path (through the C ABI) with the oracle — run on a B200.
+
+Bar: FP32 path and the FP16 ordered path are bit-exact against
+the reference CPU functions on identical inputs; NaNs compare by class.  The
+oracle is the C restatement (pinned to the reference build by
+tests/test_oracle.py) and the committed golden fixtures produced by the
+reference itself.
+"""
+import numpy as np
+import pytest
+
+import paper_2407_07852_b200 as D
+from paper_2407_07852_b200 import _capi as A
+from oracle import driver as DR
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def bits(a):
+    return np.ascontiguousarray(a, np.float32).view(np.uint32)
+
+
+def same(a, b):
+    a = np.asarray(a, np.float32)
+    b = np.asarray(b, np.float32)
+    nan = np.isnan(a) & np.isnan(b)
+    return np.array_equal(np.isnan(a), np.isnan(b)) and np.array_equal(bits(a)[~nan], bits(b)[~nan])
+
+
+@pytest.fixture(scope="module", autouse=True)
+def gpu():
+    try:
+        n = D.device_count()
+    except D.Error:
+        n = 0
+    if n < 1:
+        pytest.skip("no CUDA device")
+    D.lib.dlc_set_device(0)
+
+
+# ---- FP16 codec (fp16.cpp:25-85; test_tensor.cpp:28-99) ---------------------------------
+
+def test_fp16_encode_exhaustive(port):
+    """Every one of the 2^32 FP32 bit patterns encodes to the reference's code."""
+    chunk = 1 << 26
+    for start in range(0, 1 << 32, chunk):
+        got = D.fp16_encode_bits(start, chunk)
+        x = np.arange(start, start + chunk, dtype=np.uint64).astype(np.uint32).view(np.float32)
+        want, _ = port.encode_fp16(x)
+        if not np.array_equal(got, want):
+            bad = np.nonzero(got != want)[0][:5]
+            raise AssertionError(f"mismatch at bit patterns {[hex(start + int(i)) for i in bad]}: "
+                                 f"got {got[bad]}, want {want[bad]}")
+
+
+def test_fp16_decode_every_code(port, golden):
+    codes = np.arange(65536, dtype=np.uint32).astype(np.uint16)
+    got = D.decode_fp16(codes)
+    assert same(got, port.decode_fp16(codes))
+    assert same(got, golden("fp16_codec.npz")["decoded_all"])
+    # exact round trip for every finite code (test_tensor.cpp:68-76)
+    fin = codes[(codes & 0x7C00) != 0x7C00]
+    back, ov = D.encode_fp16(D.decode_fp16(fin))
+    assert not ov and np.array_equal(back, fin)
+
+
+def test_fp16_codec_golden(golden):
+    z = golden("fp16_codec.npz")
+    got, ov = D.encode_fp16(z["x"])
+    assert np.array_equal(got, z["codes"])
+    assert ov  # the fixture holds inf / overflow values
+
+
+def test_fp16_scalar_goldens():
+    enc = lambda x: int(D.encode_fp16([x])[0][0])  # noqa: E731
+    assert enc(1.0) == 0x3C00 and enc(-0.0) == 0x8000 and enc(0.0) == 0
+    assert enc(65520.0) == 0x7C00 and enc(-65520.0) == 0xFC00 and enc(65519.0) == 0x7BFF
+    assert enc(1e30) == 0x7C00 and enc(float("nan")) == 0x7E00 and enc(1e-9) == 0
+    assert D.decode_fp16([enc(2049.0)])[0] == 2048.0
+    assert D.decode_fp16([0x7BFF])[0] == 65504.0
+    _, ov = D.encode_fp16([1.5, -2.0, 0.25])
+    assert not ov
+    codes, ov = D.encode_fp16([1e9, 1.0])
+    assert ov and codes[0] == 0x7C00
+    codes, ov = D.encode_fp16(np.zeros(0, np.float32))
+    assert codes.size == 0 and not ov
+
+
+# ---- host-buffer reference functions ------------------------------------------------------
+
+def test_adamw_golden_trajectory(golden):
+    z = golden("adamw.npz")
+    st = D.AdamWState.init(z["p0"].size)
+    p = z["p0"].copy()
+    for t in range(5):
+        p = D.adamw_step(st, p, z["grads"][t], float(z["lrs"][t]))
+        assert np.array_equal(bits(p), bits(z["traj"][t])), t
+    assert np.array_equal(bits(st.m), bits(z["m"])) and np.array_equal(bits(st.v), bits(z["v"]))
+    assert st.step_count == int(z["step_count"])
+
+
+def test_adamw_goldens_and_errors():
+    st = D.AdamWState.init(1, weight_decay=0.1)
+    p = D.adamw_step(st, [1.0], [0.1], 4e-4)
+    assert abs(float(p[0]) - 0.99956) <= 1e-6 * 0.99956 and st.step_count == 1
+    st = D.AdamWState.init(3, weight_decay=0.0)
+    assert np.array_equal(D.adamw_step(st, [1, -2, 0.5], [0, 0, 0], 4e-4), np.float32([1, -2, 0.5]))
+    st = D.AdamWState.init(1, weight_decay=0.0)
+    with pytest.raises(D.NumericError):
+        D.adamw_step(st, [1.0], [np.inf], 1e-3)
+    assert st.step_count == 0 and st.m[0] == 0 and st.v[0] == 0
+    with pytest.raises(D.ConfigError):
+        D.adamw_step(st, [1.0], [0.1], -1e-3)
+    with pytest.raises(D.ShapeError):
+        D.adamw_step(st, [1.0, 2.0], [0.1], 1e-3)
+
+
+def test_adamw_random_vs_oracle(port):
+    rng = np.random.default_rng(5)
+    n = 100_003  # ragged: exercises the scalar tail
+    for trial in range(3):
+        p = rng.uniform(-2, 2, n).astype(np.float32)
+        st = D.AdamWState.init(n, weight_decay=0.05 * trial)
+        m, v, sc = np.zeros(n, np.float32), np.zeros(n, np.float32), 0
+        for s in range(4):
+            g = (rng.uniform(-1, 1, n) * 10.0 ** (trial - 2)).astype(np.float32)
+            g[:3] = [0.0, 1e-40, -3e-39]
+            out = D.adamw_step(st, p, g, 1e-3 * (s + 1))
+            _, want, sc = port.adamw_step(p, g, m, v, sc, 1e-3 * (s + 1), wd=0.05 * trial)
+            assert np.array_equal(bits(out), bits(want))
+            assert np.array_equal(bits(st.m), bits(m)) and np.array_equal(bits(st.v), bits(v))
+            p = out
+
+
+def test_nesterov_golden(golden):
+    z = golden("nesterov.npz")
+    st = D.NesterovState.init(z["theta0"].size, 0.7, 0.9)
+    th = z["theta0"].copy()
+    for t in range(4):
+        th = D.nesterov_step(st, th, z["grads"][t])
+        assert np.array_equal(bits(th), bits(z["traj"][t]))
+    assert np.array_equal(bits(st.momentum_buf), bits(z["buf"]))
+    st = D.NesterovState.init(1, 0.7, 0.9)
+    out = D.nesterov_step(st, [10.0], [1.0])
+    assert st.momentum_buf[0] == 1.0 and abs(float(out[0]) - 8.67) <= 1e-6 * 8.67
+    st = D.NesterovState.init(2, 1.0, 0.0)
+    assert np.array_equal(D.nesterov_step(st, [1.25, -3.5], [0.25, 0.5]), np.float32([1.0, -4.0]))
+    with pytest.raises(D.NumericError):
+        D.nesterov_step(D.NesterovState.init(1), [1.0], [np.nan])
+
+
+def test_reduce_average_golden(golden):
+    z = golden("reduce.npz")
+    for k in (1, 2, 3, 5, 8):
+        for prec in (0, 1):
+            got = D.reduce_average(list(z[f"in_k{k}"]), prec)
+            assert same(got, z[f"out_k{k}_p{prec}"]), (k, prec)
+    assert np.array_equal(D.reduce_average([[2, 4], [4, 8]], 0), np.float32([3, 6]))
+    with pytest.raises(D.CollectiveError):
+        D.reduce_average([], 0)
+    with pytest.raises(D.ShapeError):
+        D.reduce_average([[1.0], [1.0, 2.0]], 0)
+
+
+def test_reduce_average_many_contributors(port):
+    rng = np.random.default_rng(3)
+    cs = [rng.uniform(-1, 1, 999).astype(np.float32) * np.float32(2.0 ** (j % 7)) for j in range(40)]
+    for prec in (0, 1):
+        assert same(D.reduce_average(cs, prec), port.reduce_average(cs, prec)[1])
+
+
+def test_unscale_axpy_all_finite(port):
+    rng = np.random.default_rng(9)
+    x = np.ldexp(rng.uniform(-2, 2, 50001), rng.integers(-40, 40, 50001)).astype(np.float32)
+    x[7] = np.inf
+    for scale in (65536.0, 2.0 ** -20, 1.0):
+        u, ov = D.scaler_unscale_and_check(D.LossScaler(scale), x)
+        u2, ov2 = port.scaler_unscale_and_check(scale, x)
+        assert ov == ov2 and same(u, u2)
+    y = rng.uniform(-1, 1, 50001).astype(np.float32)
+    assert np.array_equal(bits(D.axpy(-1.0, x, y)), bits(port.axpy(-1.0, x, y)))
+    assert np.array_equal(D.axpy(-1.0, [0.5, 2.5], [1.0, 2.0]), np.float32([0.5, -0.5]))
+    assert not D.all_finite(x) and D.all_finite(y) and D.all_finite(np.zeros(0, np.float32))
+
+
+# ---- device-resident engine: full DiLoCo trajectories -------------------------------------
+
+def run_engines(k, h, rounds, prec, n, hyper, grad_fn, theta0, inner_mode=A.INNER_PINGPONG):
+    cfg = D.DilocoConfig(h, k, prec, h * rounds)
+    hp = D.OptimHyperparams(inner_lr=hyper.inner_lr, warmup_steps=hyper.warmup_steps,
+                            weight_decay=hyper.weight_decay, outer_lr=hyper.outer_lr,
+                            outer_momentum=hyper.outer_momentum, scaler_init_scale=hyper.scale,
+                            scaler_growth_interval=hyper.growth_interval)
+    engines = [D.DilocoEngine(cfg, hp, n, 0, inner_mode) for _ in range(k)]
+    for e in engines:
+        e.upload(A.THETA_T, theta0)
+        e.upload(A.THETA_LOCAL, theta0)
+    step = 0
+    results = []
+    for _ in range(rounds):
+        for _t in range(h):
+            for wi, e in enumerate(engines):
+                e.inner_step_host(grad_fn(wi, step), grad_is_scaled=False)
+            step += 1
+        results.append(D.outer_step_local(engines))
+    return engines
+
+
+@pytest.mark.parametrize("inner_mode", [A.INNER_PINGPONG, A.INNER_INPLACE])
+@pytest.mark.parametrize("prec", [0, 1])
+def test_engine_matches_reference_golden_trajectory(golden, prec, inner_mode):
+    """K=2, H=5, 2 rounds, injected overflow at (worker 1, step 3) — bitwise vs the reference."""
+    z = golden("diloco_k2_h5.npz")
+    theta0 = z["theta0"]
+    n = theta0.size
+
+    def grad_fn(w, t):
+        g = O.rng_fill(4242, "grad", w * 1000 + t, n, -1e-2, 1e-2)
+        if (w, t) == (1, 3):
+            g[17] = np.inf
+        return g
+
+    hyper = DR.Hyper(inner_lr=4e-4, warmup_steps=5)
+    engines = run_engines(2, 5, 2, prec, n, hyper, grad_fn, theta0, inner_mode)
+    for wi, e in enumerate(engines):
+        for which, name in ((A.THETA_T, "theta_t"), (A.THETA_LOCAL, "theta_local"), (A.ADAM_M, "m"),
+                            (A.ADAM_V, "v"), (A.MOMENTUM, "buf")):
+            assert np.array_equal(bits(e.download(which)), bits(z[f"p{prec}_w{wi}_{name}"])), (wi, name)
+        s = e.scalars()
+        assert s.step_count == int(z[f"p{prec}_w{wi}_step_count"])
+        assert s.scale == float(z[f"p{prec}_w{wi}_scale"])
+        assert s.outer_epoch == 2 and s.inner_step == 10
+        assert s.overflow_skips == (1 if wi == 1 else 0)
+        e.close()
+
+
+@pytest.mark.parametrize("k,prec", [(2, 0), (3, 1), (8, 1), (8, 0)])
+def test_engine_config1_shape_vs_oracle(port, k, prec):
+    """Config-1 shape (N = 2^20 ragged to 2^20 + 5, H = 50, 1 outer step) at K = 2, and K up to 8."""
+    n = (1 << 20) + 5 if k == 2 else 40_000 + 3
+    h = 50 if k == 2 else 4
+    hyper = DR.Hyper(inner_lr=4e-4, warmup_steps=20)
+    theta0 = O.rng_fill(4242, "theta", 0, n, -0.05, 0.05)
+    grads = {}
+
+    def grad_fn(w, t):
+        key = (w, t)
+        if key not in grads:
+            grads[key] = O.rng_fill(4242, "grad", w * 100_000 + t, n, -1e-2, 1e-2)
+        return grads[key]
+
+    workers, hist = DR.simulate(port, theta0, grad_fn, k, h, 1, prec, hyper)
+    engines = run_engines(k, h, 1, prec, n, hyper, grad_fn, theta0)
+    for wi, e in enumerate(engines):
+        assert np.array_equal(bits(e.download(A.THETA_T)), bits(workers[wi].theta_t))
+        assert np.array_equal(bits(e.download(A.THETA_LOCAL)), bits(workers[wi].theta_local))
+        assert np.array_equal(bits(e.download(A.MOMENTUM)), bits(workers[wi].buf))
+        assert np.array_equal(bits(e.download(A.ADAM_M)), bits(workers[wi].m))
+        assert np.array_equal(bits(e.download(A.ADAM_V)), bits(workers[wi].v))
+        e.close()
+
+
+def test_outer_nonfinite_skip_and_resnapshot():
+    """engine.cpp:136-144 / test_engine.cpp:179-191: a non-finite mean skips Nesterov, resets local."""
+    n = 1000
+    theta0 = O.rng_fill(1, "theta", 0, n, -1, 1)
+    cfg = D.DilocoConfig(1, 2, A.FP16, 2)
+    engines = [D.DilocoEngine(cfg, D.OptimHyperparams(), n) for _ in range(2)]
+    for wi, e in enumerate(engines):
+        e.upload(A.THETA_T, theta0)
+        local = theta0 - np.float32(0.01)
+        if wi == 1:
+            local[5] = -7e4  # delta = 7e4 encodes to +inf in FP16
+        e.upload(A.THETA_LOCAL, local)
+    res = D.outer_step_local(engines)
+    assert not res.applied and res.outer_epoch == 1
+    for e in engines:
+        assert np.array_equal(e.download(A.THETA_T), theta0)
+        assert np.array_equal(e.download(A.THETA_LOCAL), theta0)
+        assert not e.download(A.MOMENTUM).any()
+        assert e.scalars().outer_skips == 1
+    # solo engine, FP32: NaN in theta_local skips too
+    e = D.DilocoEngine(D.DilocoConfig(1, 1, A.FP32, 1), D.OptimHyperparams(), n)
+    e.upload(A.THETA_T, theta0)
+    bad = theta0.copy()
+    bad[999] = np.nan
+    e.upload(A.THETA_LOCAL, bad)
+    r = e.outer_step(None, wait=True)
+    assert not r.applied
+    assert np.array_equal(e.download(A.THETA_LOCAL), theta0)
+
+
+def test_outer_identity_transport():
+    """test_engine.cpp:156-169: K=1, lr=1, mu=0 transports theta_local exactly (FP32)."""
+    n = 4099
+    theta0 = O.rng_fill(2, "theta", 0, n, -1, 1)
+    local = O.rng_fill(2, "local", 0, n, -1, 1)
+    hp = D.OptimHyperparams(outer_lr=1.0, outer_momentum=0.0)
+    e = D.DilocoEngine(D.DilocoConfig(3, 1, A.FP32, 3), hp, n)
+    e.upload(A.THETA_T, theta0)
+    e.upload(A.THETA_LOCAL, local)
+    r = e.outer_step(None, wait=True)
+    assert r.applied
+    # theta - 1*(delta + 0) with delta = theta - local is local up to one rounding; the
+    # reference's arithmetic is reproduced bit for bit:
+    port = O.port()
+    tt, tl, buf = theta0.copy(), local.copy(), np.zeros(n, np.float32)
+    d = port.axpy(-1.0, tl, tt)
+    _, want = port.nesterov_step(tt, d, buf, 1.0, 0.0)
+    assert np.array_equal(bits(e.download(A.THETA_T)), bits(want))
+
+
+def test_engine_errors():
+    e = D.DilocoEngine(D.DilocoConfig(5, 1, A.FP32, 5), D.OptimHyperparams(), 64)
+    g = np.zeros(64, np.float32)
+    e.inner_step_host(g)
+    with pytest.raises(D.Error):  # engine.cpp:116-120, mid-window
+        e.outer_step(None)
+    for _ in range(4):
+        e.inner_step_host(g)
+    e.outer_step(None)
+    with pytest.raises(D.Error):  # engine.cpp:98-100, past total_inner_steps
+        e.inner_step_host(g)
+    with pytest.raises(D.CollectiveError):  # K mismatch
+        D.DilocoEngine(D.DilocoConfig(1, 2, A.FP32, 1), D.OptimHyperparams(), 64).outer_step(None)
+    with pytest.raises(D.ShapeError):
+        e.upload(A.THETA_T, np.zeros(63, np.float32))
+
+
+def test_inner_overflow_skip_semantics():
+    """engine.cpp:50-69: overflow leaves p/m/v/step_count, halves the scale, cursor advances."""
+    n = 513
+    for mode in (A.INNER_PINGPONG, A.INNER_INPLACE):
+        e = D.DilocoEngine(D.DilocoConfig(10, 1, A.FP32, 10), D.OptimHyperparams(warmup_steps=2), n, 0, mode)
+        th = O.rng_fill(3, "theta", 0, n, -1, 1)
+        e.upload(A.THETA_LOCAL, th)
+        g = O.rng_fill(3, "grad", 0, n, -1e-2, 1e-2)
+        r = e.inner_step_host(g)
+        assert not r.overflow_skipped and r.lr == np.float32(2e-4)
+        before = {w: e.download(w) for w in (A.THETA_LOCAL, A.ADAM_M, A.ADAM_V)}
+        bad = g.copy()
+        bad[512] = np.inf  # lands in the scalar tail
+        r = e.inner_step_host(bad)
+        assert r.overflow_skipped and r.lr == 0.0
+        for w, arr in before.items():
+            assert np.array_equal(bits(e.download(w)), bits(arr))
+        s = e.scalars()
+        assert s.step_count == 1 and s.inner_step == 2 and s.scale == 32768.0 and s.overflow_skips == 1
+        r = e.inner_step_host(g)  # lr index continues from the applied-step count (engine.cpp:64)
+        assert not r.overflow_skipped and r.lr == np.float32(4e-4)
+
+
+def test_large_n_slices_vs_oracle(port):
+    """150M-parameter buffers (configs 2-3): elementwise path, so oracle slices are exact."""
+    n = 150_000_000
+    hyper = DR.Hyper(inner_lr=4e-4, warmup_steps=5)
+    hp = D.OptimHyperparams(inner_lr=4e-4, warmup_steps=5)
+    e = D.DilocoEngine(D.DilocoConfig(2, 1, A.FP16, 2), hp, n)
+    e.rng_fill(A.THETA_T, 4242, "theta", 0, -0.05, 0.05)
+    e.rng_fill(A.THETA_LOCAL, 4242, "theta", 0, -0.05, 0.05)
+    for t in range(2):
+        e.rng_fill(A.GRAD, 4242, "grad", t, -1e-2, 1e-2)
+        e.inner_step(e.device_ptr(A.GRAD), grad_is_scaled=False)
+    r = e.outer_step(None, wait=True)
+    assert r.applied
+    out = {w: e.download(w) for w in (A.THETA_T, A.THETA_LOCAL, A.ADAM_M, A.ADAM_V, A.MOMENTUM)}
+    for lo in (0, n // 2 - 777, n - 4096):
+        sl = slice(lo, lo + 4096)
+        th0 = O.rng_fill(4242, "theta", 0, 4096, -0.05, 0.05, first=lo)
+        w = DR.make_workers(th0, 1, hyper)[0]
+        for t in range(2):
+            DR.inner_step(port, w, O.rng_fill(4242, "grad", t, 4096, -1e-2, 1e-2, first=lo), hyper)
+        DR.outer_round(port, [w], 1, hyper)
+        for which, arr in ((A.THETA_T, w.theta_t), (A.THETA_LOCAL, w.theta_local), (A.ADAM_M, w.m),
+                           (A.ADAM_V, w.v), (A.MOMENTUM, w.buf)):
+            assert np.array_equal(bits(out[which][sl]), bits(arr)), (lo, which)
+    e.close()
+
+
+def test_optimizer_facade_rounds():
+    """DilocoOptimizer::step (engine.cpp:162-174): outer round after every H-th inner step."""
+    n = 1024
+    e = D.DilocoEngine(D.DilocoConfig(3, 1, A.FP32, 9), D.OptimHyperparams(), n)
+    opt = D.DilocoOptimizer(e, D.SoloCollective(0))
+    e.rng_fill(A.GRAD, 1, "g", 0, -1e-2, 1e-2)
+    g = e.device_ptr(A.GRAD)
+    flags = []
+    for _ in range(9):
+        opt.step(g, grad_is_scaled=False)
+        flags.append(opt.round_just_completed)
+    assert flags == [False, False, True] * 3
+    assert e.scalars().outer_epoch == 3
+
+
+def test_solo_collective_host_plugin(golden):
+    z = golden("reduce.npz")
+    c = D.SoloCollective(0)
+    assert c.world_size() == 1
+    for prec in (0, 1):
+        out, rep = c.all_reduce_avg(z["in_k1"][0], prec, outer_epoch=4)
+        assert same(out, z[f"out_k1_p{prec}"])
+        assert rep.contributors == 1 and rep.outer_epoch == 4 and rep.data_bytes_sent == 0
