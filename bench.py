@@ -70,34 +70,62 @@ def measured_peak():
 # ---- clocks sampler (B200_PROFILING.md "clocks DURING the timed region") -----------------
 
 class Clocks:
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """Samples SM clock, power and clock-event reasons through NVML every 2 ms
+    (the same counters `nvidia-smi --query-gpu=clocks.sm,clocks_event_reasons.*`
+    reads) on a background thread for the duration of the timed region."""
+
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
 
     def __init__(self, device: int, enabled: bool = True):
-        self.proc = None
-        self.device = device
-        if enabled:
+        import threading
+        self.samples = []
+        self.err = None
+        self.stop_evt = threading.Event()
+        self.thread = None
+        if not enabled:
+            self.err = "disabled"
+            return
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            phys = int(vis.split(",")[device]) if vis and vis.split(",")[device].isdigit() else device
+            self.N, self.h = N, N.nvmlDeviceGetHandleByIndex(phys)
+            self.max_sm = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+        except Exception as e:  # NVML missing: report, do not guess
+            self.err = f"nvml unavailable: {e}"
+            return
+        self.thread = threading.Thread(target=self._run, daemon=True)
+        self.thread.start()
+
+    def _run(self):
+        N = self.N
+        while not self.stop_evt.is_set():
             try:
-                self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                              "-i", str(device), "-lms", "100"], stdout=subprocess.PIPE,
-                                             stderr=subprocess.DEVNULL, text=True)
-            except FileNotFoundError:
-                self.proc = None
+                self.samples.append((N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM),
+                                     N.nvmlDeviceGetPowerUsage(self.h) / 1000.0,
+                                     N.nvmlDeviceGetCurrentClocksEventReasons(self.h)))
+            except Exception as e:
+                self.err = str(e)
+                return
+            time.sleep(0.002)
 
     def stop(self):
-        if not self.proc:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        out, _ = self.proc.communicate(timeout=10)
-        rows = [r.split(", ") for r in out.strip().splitlines() if r.count(",") >= 8]
-        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].strip() == "Active"})
-        pw = [float(r[3]) for r in rows if r[3].replace(".", "").isdigit()]
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(rows), "power_w_max": max(pw) if pw else None}
+        if self.thread is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [self.err or "unavailable"]}
+        self.stop_evt.set()
+        self.thread.join(timeout=5)
+        N = self.N
+        reasons = sorted({name for _, _, mask in self.samples for name, attr in self.REASONS
+                          if mask & getattr(N, attr, 0)})
+        sm = [s[0] for s in self.samples]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_sm,
+                "sm_mhz_min": min(sm) if sm else None, "reasons": reasons, "samples": len(sm),
+                "power_w_max": max(s[1] for s in self.samples) if sm else None, "source": "nvml"}
 
 
 # ---- CPU baseline: the reference's own functions on host threads --------------------------

@@ -1,0 +1,118 @@
+"""One rank of the multi-GPU parity test (launched by tests/test_multigpu.py via torchrun).
+
+Every rank drives one GPU as one DiLoCo worker; the collective is the NCCL
+communicator inside libdiloco_cuda.so.  Each rank replays the whole K-worker
+run on the CPU oracle and checks its own worker:
+  * ordered mode: bit-exact (theta_t, theta_local, m, v, momentum);
+  * allreduce mode (NCCL's own reduction order): theta_t within
+    lr*(1+mu)*tol(dbar) + 2 ulp, tol(dbar) = K*2^-24*max|delta| (FP32) or
+    2^-10*max|delta| + 2^-24 (FP16), SPEC.md:325 / test_engine.cpp:311-323.
+"""
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_2407_07852_b200 as D  # noqa: E402
+from paper_2407_07852_b200 import dist as PD  # noqa: E402
+from oracle import driver as DR  # noqa: E402
+from oracle import oracle as O  # noqa: E402
+
+
+def bits(a):
+    return np.ascontiguousarray(a, np.float32).view(np.uint32)
+
+
+def main():
+    r = PD.init("gloo")
+    D.lib.dlc_set_device(r.local)
+    k = r.world
+    out = {"rank": r.rank, "checks": []}
+    port = O.port()
+    n, h, rounds = 50_021, 3, 2
+    hyper = DR.Hyper(inner_lr=1e-3, warmup_steps=2)
+    theta0 = O.rng_fill(4242, "theta", 0, n, -0.05, 0.05)
+
+    def grad_fn(w, t):
+        g = O.rng_fill(4242, "grad", w * 1000 + t, n, -1e-2, 1e-2)
+        if (w, t) == (k - 1, 1):
+            g[3] = np.inf  # one overflowed inner step on the last worker
+        return g
+
+    for mode_name, mode in (("ordered", D.MODE_ORDERED), ("allreduce", D.MODE_ALLREDUCE)):
+        coll = PD.make_nccl_collective(r, mode)
+        assert coll.world_size() == k and coll.rank() == r.rank
+        for prec in (D.FP32, D.FP16):
+            workers, hist = DR.simulate(port, theta0, grad_fn, k, h, rounds, prec, hyper)
+            cfg = D.DilocoConfig(h, k, prec, h * rounds)
+            hp = D.OptimHyperparams(inner_lr=1e-3, warmup_steps=2)
+            e = D.DilocoEngine(cfg, hp, n, r.local)
+            e.upload(D.THETA_T, theta0)
+            e.upload(D.THETA_LOCAL, theta0)
+            step = 0
+            for _ in range(rounds):
+                for _t in range(h):
+                    e.inner_step_host(grad_fn(r.rank, step), grad_is_scaled=False)
+                    step += 1
+                res = e.outer_step(coll, wait=True, report=True)
+                assert res.applied
+                rep = res.report
+                assert rep.contributors == k and rep.data_bytes_sent == 2 * (k - 1) * PD.slot_elems(n, k) * (
+                    2 if prec == D.FP16 else 4)
+            me = workers[r.rank]
+            got = {w: e.download(w) for w in (D.THETA_T, D.THETA_LOCAL, D.ADAM_M, D.ADAM_V, D.MOMENTUM)}
+            if mode == D.MODE_ORDERED:
+                for w, want in ((D.THETA_T, me.theta_t), (D.THETA_LOCAL, me.theta_local), (D.ADAM_M, me.m),
+                                (D.ADAM_V, me.v), (D.MOMENTUM, me.buf)):
+                    assert np.array_equal(bits(got[w]), bits(want)), (mode_name, prec, w)
+                out["checks"].append(f"{mode_name}/{'fp16' if prec else 'fp32'}: bitwise")
+            else:
+                # first round only: later rounds compound through AdamW's nonlinearity
+                deltas = hist[0][2]
+                mx = np.max(np.abs(np.stack(deltas)), axis=0).astype(np.float64)
+                tol_d = (k * 2.0 ** -24 * mx) if prec == D.FP32 else (2.0 ** -10 * mx + 2.0 ** -24)
+                e1 = D.DilocoEngine(D.DilocoConfig(1, k, prec, 1), hp, n, r.local)
+                e1.upload(D.THETA_T, theta0)
+                loc = workers_round0_local(port, theta0, grad_fn, k, h, hyper, r.rank)
+                e1.upload(D.THETA_LOCAL, loc)
+                e1.outer_step(coll, wait=True)
+                got_t = e1.download(D.THETA_T).astype(np.float64)
+                w0, _ = DR.simulate(port, theta0, grad_fn, k, h, 1, prec, hyper)
+                want_t = w0[r.rank].theta_t.astype(np.float64)
+                tol = 0.7 * 1.9 * tol_d + 2 * np.spacing(np.abs(want_t).astype(np.float32)).astype(np.float64)
+                err = np.abs(got_t - want_t)
+                assert np.all(err <= tol), (mode_name, prec, float(np.max(err / tol)))
+                out["checks"].append(f"{mode_name}/{'fp16' if prec else 'fp32'}: max err/tol "
+                                     f"{float(np.max(err / tol)):.3f}")
+                e1.close()
+            e.close()
+        # host-buffer plugin call (Collective::all_reduce_avg) vs reduce_average in rank order
+        for prec in (D.FP32, D.FP16):
+            deltas = [O.rng_fill(9, "delta", j, 10_007, -1, 1) for j in range(k)]
+            got, rep = coll.all_reduce_avg(deltas[r.rank], prec, outer_epoch=3)
+            _, want = port.reduce_average(deltas, prec)
+            if mode == D.MODE_ORDERED:
+                assert np.array_equal(bits(got), bits(want))
+            else:
+                assert np.max(np.abs(got - want)) <= (2.0 ** -10 if prec else k * 2.0 ** -23)
+            assert rep.contributors == k and rep.outer_epoch == 3
+            assert rep.data_bytes_sent == D.per_peer_reduce_bytes(10_007, k, r.rank, prec)
+        coll.close()
+    PD.barrier(r.world)
+    print("MPRESULT " + json.dumps(out), flush=True)
+
+
+def workers_round0_local(port, theta0, grad_fn, k, h, hyper, rank):
+    ws = DR.make_workers(theta0, k, hyper)
+    for t in range(h):
+        for wi, w in enumerate(ws):
+            DR.inner_step(port, w, grad_fn(wi, t), hyper)
+    return ws[rank].theta_local
+
+
+if __name__ == "__main__":
+    main()

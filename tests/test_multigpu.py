@@ -1,0 +1,33 @@
+"""Multi-GPU parity (NCCL over NVLink): one process per GPU via torchrun.
+
+Runs tests/mp_gpu_worker.py on min(4, #GPUs) ranks; skipped on a 1-GPU box.
+"""
+import os
+import subprocess
+import sys
+
+import pytest
+
+import paper_2407_07852_b200 as D
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def gpus():
+    try:
+        return D.device_count()
+    except D.Error:
+        return 0
+
+
+@pytest.mark.parametrize("nproc", [2, 4])
+def test_multigpu_parity(nproc):
+    if gpus() < nproc:
+        pytest.skip(f"needs {nproc} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29600 + nproc),
+           os.path.join(ROOT, "tests", "mp_gpu_worker.py")]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("MPRESULT")]
+    assert p.returncode == 0 and len(lines) == nproc, p.stdout[-3000:] + p.stderr[-3000:]
