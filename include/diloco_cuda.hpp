@@ -1,0 +1,221 @@
+// diloco_cuda.hpp — C++ drop-in layer over the C ABI (include/diloco_cuda.h).
+//
+// Header-only.  Include it in the reference code base (diloco-cpp) after its
+// own headers; it provides the reference's signatures backed by the B200
+// kernels, so call sites swap `diloco::adamw_step` for
+// `diloco::cuda::adamw_step` (or bring the names in with a using-declaration):
+//
+//   adamw_step / nesterov_step / scaler_unscale_and_check   (optim.hpp:61-77)
+//   axpy / encode_fp16 / decode_fp16                         (tensor.hpp:108-115)
+//   reduce_average                                           (reduce.hpp:65-66)
+//   NcclCollective final : Collective                        (reduce.hpp:86-97)
+//   DeviceEngine: DilocoEngine's state and steps resident in HBM (engine.hpp:76-116)
+//
+// Status codes from the C ABI are rethrown as the reference's exception
+// classes (errors.hpp:12-51), so error behaviour is unchanged for callers.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "diloco/errors.hpp"
+#include "diloco/optim.hpp"
+#include "diloco/reduce.hpp"
+#include "diloco/tensor.hpp"
+#include "diloco_cuda.h"
+
+namespace diloco::cuda {
+
+inline void throw_status(int st) {
+  if (st == DLC_OK) return;
+  const std::string msg = dlc_last_error();
+  switch (st) {
+    case DLC_ESHAPE: throw ShapeError(msg);
+    case DLC_ECONFIG: throw ConfigError(msg);
+    case DLC_ENUMERIC: throw NumericError(msg);
+    case DLC_ECOLLECTIVE:
+    case DLC_ENCCL: throw CollectiveError(msg);
+    default: throw Error(msg);
+  }
+}
+
+inline int to_c(Precision p) { return p == Precision::fp16 ? DLC_FP16 : DLC_FP32; }
+
+/// adamw_step (optim.hpp:61-62): new params; state.m, state.v, step_count in place.
+inline ParamVector adamw_step(AdamWState& state, const ParamVector& params, const ParamVector& grad, float lr) {
+  if (!params.same_layout(grad) || !params.same_layout(state.m)) throw ShapeError("adamw_step: layout mismatch");
+  dlc_adamw_state s{state.m.mutable_values().data(), state.v.mutable_values().data(), state.step_count,
+                    state.beta1, state.beta2, state.eps, state.weight_decay};
+  std::vector<float> out(params.size());
+  throw_status(dlc_adamw_step(&s, params.values().data(), grad.values().data(), params.size(), lr, out.data()));
+  state.step_count = s.step_count;
+  return ParamVector(params.layout(), std::move(out));
+}
+
+/// nesterov_step (optim.hpp:65-66).
+inline ParamVector nesterov_step(NesterovState& state, const ParamVector& params, const ParamVector& pseudo_grad) {
+  if (!params.same_layout(pseudo_grad) || !params.same_layout(state.momentum_buf))
+    throw ShapeError("nesterov_step: layout mismatch");
+  dlc_nesterov_state s{state.momentum_buf.mutable_values().data(), state.lr, state.momentum};
+  std::vector<float> out(params.size());
+  throw_status(dlc_nesterov_step(&s, params.values().data(), pseudo_grad.values().data(), params.size(), out.data()));
+  return ParamVector(params.layout(), std::move(out));
+}
+
+/// scaler_unscale_and_check (optim.hpp:76-77).
+inline UnscaleResult scaler_unscale_and_check(const LossScaler& scaler, const ParamVector& grad) {
+  dlc_loss_scaler s{scaler.scale, scaler.growth_interval, scaler.consecutive_good};
+  std::vector<float> out(grad.size());
+  int overflow = 0;
+  throw_status(dlc_scaler_unscale_and_check(&s, grad.values().data(), grad.size(), out.data(), &overflow));
+  UnscaleResult r;
+  r.grad = ParamVector(grad.layout(), std::move(out));
+  r.overflow = overflow != 0;
+  return r;
+}
+
+/// axpy (tensor.hpp:108).
+inline ParamVector axpy(float alpha, const ParamVector& x, const ParamVector& y) {
+  if (!x.same_layout(y)) throw ShapeError("axpy: layout mismatch");
+  std::vector<float> out(x.size());
+  throw_status(dlc_axpy(alpha, x.values().data(), y.values().data(), x.size(), out.data()));
+  return ParamVector(x.layout(), std::move(out));
+}
+
+/// encode_fp16 (tensor.hpp:111).
+inline Fp16Buffer encode_fp16(const ParamVector& v) {
+  Fp16Buffer b;
+  b.bits.resize(v.size());
+  int overflow = 0;
+  throw_status(dlc_encode_fp16(v.values().data(), v.size(), b.bits.data(), &overflow));
+  b.overflow = overflow != 0;
+  return b;
+}
+
+/// decode_fp16 (tensor.hpp:115).
+inline ParamVector decode_fp16(const Fp16Buffer& buffer, LayoutPtr layout) {
+  if (buffer.bits.size() != layout->total_length()) throw ShapeError("decode_fp16: length mismatch");
+  std::vector<float> out(buffer.bits.size());
+  throw_status(dlc_decode_fp16(buffer.bits.data(), buffer.bits.size(), out.data()));
+  return ParamVector(std::move(layout), std::move(out));
+}
+
+/// reduce_average (reduce.hpp:65-66).
+inline ParamVector reduce_average(std::span<const ParamVector* const> contributions, Precision precision) {
+  if (contributions.empty()) throw CollectiveError("reduce_average: no contributions");
+  const ParamVector& first = *contributions.front();
+  std::vector<const float*> ptrs;
+  for (const ParamVector* c : contributions) {
+    if (!c->same_layout(first)) throw ShapeError("reduce_average: contribution layout mismatch");
+    ptrs.push_back(c->values().data());
+  }
+  std::vector<float> out(first.size());
+  throw_status(dlc_reduce_average(ptrs.data(), ptrs.size(), first.size(), to_c(precision), out.data()));
+  return ParamVector(first.layout(), std::move(out));
+}
+
+/// Collective plugin over NCCL: one rank per process and GPU (replaces
+/// SocketCollective, collective.hpp:160-178).  Rank 0 creates the id with
+/// make_unique_id() and ships it to the other ranks out of band.
+class NcclCollective final : public Collective {
+ public:
+  static std::vector<uint8_t> make_unique_id() {
+    std::vector<uint8_t> id(128);
+    throw_status(dlc_nccl_unique_id(id.data()));
+    return id;
+  }
+
+  NcclCollective(int rank, int world, const std::vector<uint8_t>& id, int device,
+                 dlc_reduce_mode mode = DLC_MODE_ORDERED) {
+    if (id.size() != 128) throw ConfigError("NcclCollective: unique id must be 128 bytes");
+    throw_status(dlc_collective_create_nccl(rank, world, id.data(), device, mode, &c_));
+  }
+  ~NcclCollective() override { dlc_collective_destroy(c_); }
+  NcclCollective(const NcclCollective&) = delete;
+  NcclCollective& operator=(const NcclCollective&) = delete;
+
+  size_t world_size() const override { return dlc_collective_world_size(c_); }
+
+  PseudoGradient all_reduce_avg(const PseudoGradient& local, ReduceReport* report) override {
+    PseudoGradient out;
+    std::vector<float> mean(local.delta.size());
+    dlc_reduce_report rep{};
+    throw_status(dlc_collective_all_reduce_avg(c_, local.delta.values().data(), local.delta.size(),
+                                               to_c(local.precision), local.outer_epoch, mean.data(), &rep));
+    out.delta = ParamVector(local.delta.layout(), std::move(mean));
+    out.precision = local.precision;
+    out.outer_epoch = local.outer_epoch;
+    if (report) {
+      *report = ReduceReport{};
+      report->outer_epoch = rep.outer_epoch;
+      report->contributors = rep.contributors;
+      report->data_bytes_sent = rep.data_bytes_sent;
+      report->data_bytes_received = rep.data_bytes_received;
+      report->wire_bytes_sent = rep.wire_bytes_sent;
+      report->wire_bytes_received = rep.wire_bytes_received;
+      report->wall_ms = rep.wall_ms;
+      report->attempts = rep.attempts;
+    }
+    return out;
+  }
+
+  dlc_collective* handle() const { return c_; }
+
+ private:
+  dlc_collective* c_ = nullptr;
+};
+
+/// DilocoEngine's optimizer state resident in HBM (engine.hpp:76-116).  The
+/// gradient producer (task/model) stays with the caller: inner_step takes the
+/// gradient of one batch; outer_step runs pseudo-gradient -> all-reduce ->
+/// Nesterov on the device.
+class DeviceEngine {
+ public:
+  DeviceEngine(const dlc_config& cfg, const dlc_hyperparams& hyper, const ParamVector& theta0, int device,
+               dlc_inner_mode mode = DLC_INNER_PINGPONG)
+      : layout_(theta0.layout()) {
+    throw_status(dlc_engine_create(&cfg, &hyper, theta0.size(), device, mode, &e_));
+    throw_status(dlc_engine_upload(e_, DLC_THETA_T, theta0.values().data(), theta0.size()));
+    throw_status(dlc_engine_upload(e_, DLC_THETA_LOCAL, theta0.values().data(), theta0.size()));
+  }
+  ~DeviceEngine() { dlc_engine_destroy(e_); }
+  DeviceEngine(const DeviceEngine&) = delete;
+  DeviceEngine& operator=(const DeviceEngine&) = delete;
+
+  /// apply_inner_step with the gradient of one batch (engine.cpp:50-69).
+  dlc_inner_result inner_step(const ParamVector& grad) {
+    if (!grad.layout() || !(*grad.layout() == *layout_)) throw ShapeError("inner_step: layout mismatch");
+    dlc_inner_result r{};
+    throw_status(dlc_engine_inner_step_host(e_, grad.values().data(), 0, &r));
+    return r;
+  }
+
+  /// compute_pseudo_gradient -> all_reduce_avg -> outer_step (engine.cpp:165-172).
+  dlc_outer_result outer_step(NcclCollective* collective = nullptr) {
+    dlc_outer_result r{};
+    throw_status(dlc_engine_outer_step(e_, collective ? collective->handle() : nullptr, &r, nullptr));
+    return r;
+  }
+
+  ParamVector download(dlc_buffer which) const {
+    std::vector<float> h(layout_->total_length());
+    throw_status(dlc_engine_download(e_, which, h.data(), h.size()));
+    return ParamVector(layout_, std::move(h));
+  }
+
+  dlc_engine_scalars scalars() const {
+    dlc_engine_scalars s{};
+    throw_status(dlc_engine_get_scalars(e_, &s));
+    return s;
+  }
+
+  dlc_engine* handle() const { return e_; }
+
+ private:
+  LayoutPtr layout_;
+  dlc_engine* e_ = nullptr;
+};
+
+}  // namespace diloco::cuda

@@ -40,6 +40,9 @@ def build(ref: bool | None = None) -> None:
         ref = os.path.isdir("/root/reference/proj/src")
     if ref:
         targets.append("ref")
+        lib = os.path.join(os.path.dirname(HERE), "paper_2407_07852_b200", "libdiloco_cuda.so")
+        if os.path.exists(lib):
+            targets.append("dropin")  # C++ drop-in layer vs the reference (tests/cpp)
     subprocess.run(["make", "-s", "-C", HERE] + targets, check=True)
 
 
