@@ -45,11 +45,13 @@ struct dlc_engine {
   int inner_mode = DLC_INNER_PINGPONG;
   size_t n = 0, k = 1, S = 0;
   int prec = DLC_FP32;
-  float* theta_t = nullptr;
+  // theta_t / momentum: a ping-pong pair for a single worker (fused solo outer
+  // step, DevState::ocur selects the live one); both entries alias for K > 1.
+  float* theta_t[2] = {nullptr, nullptr};
   float* p[2] = {nullptr, nullptr};
   float* m[2] = {nullptr, nullptr};
   float* v[2] = {nullptr, nullptr};
-  float* buf = nullptr;
+  float* buf[2] = {nullptr, nullptr};
   float* grad = nullptr;
   void* send = nullptr;
   void* recv = nullptr;
@@ -168,13 +170,14 @@ DevState read_state(dlc_engine* e) {
 }
 
 float* live(dlc_engine* e, int which) {
-  const int cur = e->inner_mode == DLC_INNER_PINGPONG ? read_state(e).cur : 0;
+  const DevState s = read_state(e);
+  const int cur = s.cur, oc = s.ocur;
   switch (which) {
-    case DLC_THETA_T: return e->theta_t;
+    case DLC_THETA_T: return e->theta_t[oc];
     case DLC_THETA_LOCAL: return e->p[cur];
     case DLC_ADAM_M: return e->m[cur];
     case DLC_ADAM_V: return e->v[cur];
-    case DLC_MOMENTUM: return e->buf;
+    case DLC_MOMENTUM: return e->buf[oc];
     case DLC_GRAD: return e->grad;
   }
   fail(DLC_EINVAL, "unknown engine buffer " + std::to_string(which));
@@ -217,6 +220,9 @@ void engine_inner(dlc_engine* e, const float* grad, int grad_is_scaled) {
 
 Pair local_pair(dlc_engine* e) { return Pair{{e->p[0], e->p[1]}}; }
 
+Pair tt_pair(dlc_engine* e) { return Pair{{e->theta_t[0], e->theta_t[1]}}; }
+Pair buf_pair(dlc_engine* e) { return Pair{{e->buf[0], e->buf[1]}}; }
+
 void reset_flags(dlc_engine* e) {
   DLC_CUDA(cudaMemsetAsync(e->flags, 0, kMaxK * sizeof(int), e->stream));
   DLC_CUDA(cudaMemsetAsync(&e->st->delta_nonfinite, 0, sizeof(int), e->stream));
@@ -225,18 +231,22 @@ void reset_flags(dlc_engine* e) {
 // K2 from an explicit theta_local pair (the engine's own, or a staging buffer).
 void pseudo_grad(dlc_engine* e, Pair tl) {
   phase_begin(e);
-  launch_pseudo_grad(e->theta_t, tl, e->st, e->send, e->prec, &e->st->delta_nonfinite, e->n, e->stream);
+  launch_pseudo_grad(tt_pair(e), tl, e->st, e->send, e->prec, &e->st->delta_nonfinite, e->n, e->stream);
   phase_end(e, DLC_PHASE_PSEUDO);
   launched("pseudo_grad");
 }
 
 void nesterov(dlc_engine* e, const void* dbar, const int* flags, int nflags) {
   phase_begin(e);
-  launch_nesterov_outer(e->theta_t, e->buf, local_pair(e), dbar, e->prec, flags, nflags, e->st,
+  launch_nesterov_outer(tt_pair(e), buf_pair(e), local_pair(e), dbar, e->prec, flags, nflags, e->st,
                         e->hyper.outer_lr, e->hyper.outer_momentum, e->n, e->stream);
   phase_end(e, DLC_PHASE_OUTER);
   launched("nesterov_outer");
 }
+
+// The whole outer step: fused K2+K4 for one worker, else K2 -> C1/K3 -> K4.
+// `src` (nullable) supplies theta(t+h) from a caller buffer.
+void outer_round(dlc_engine* e, dlc_collective* c, const float* src, dlc_reduce_report* rep);
 
 ncclDataType_t nccl_type(int prec) { return prec == DLC_FP16 ? ncclFloat16 : ncclFloat32; }
 
@@ -287,6 +297,21 @@ void outer_collective(dlc_engine* e, dlc_collective* c, dlc_reduce_report* rep) 
     if (rep) DLC_CUDA(cudaEventRecord(e->ev1, e->stream));
     nesterov(e, e->send, e->flags, 1);
   }
+}
+
+void outer_round(dlc_engine* e, dlc_collective* c, const float* src, dlc_reduce_report* rep) {
+  reset_flags(e);
+  if (e->k == 1) {
+    phase_begin(e);
+    launch_outer_solo_fused(tt_pair(e), buf_pair(e), local_pair(e), src, e->prec, e->st, e->hyper.outer_lr,
+                            e->hyper.outer_momentum, e->n, e->stream);
+    phase_end(e, DLC_PHASE_OUTER);
+    launched("outer_solo");
+    return;
+  }
+  float* s = const_cast<float*>(src);
+  pseudo_grad(e, s ? Pair{{s, s}} : local_pair(e));
+  outer_collective(e, c, rep);
 }
 
 void fill_report(dlc_engine* e, dlc_collective* c, dlc_reduce_report* rep, uint64_t epoch) {
@@ -375,7 +400,15 @@ int dlc_engine_create(const dlc_config* cfg, const dlc_hyperparams* hyper, size_
     DLC_CUDA(cudaEventCreate(&e->ev0));
     DLC_CUDA(cudaEventCreate(&e->ev1));
     const size_t vb = n * sizeof(float);
-    e->theta_t = (float*)dalloc(e, vb);
+    e->theta_t[0] = (float*)dalloc(e, vb);
+    e->buf[0] = (float*)dalloc(e, vb);
+    if (e->k == 1) {  // fused solo outer step: theta_t / momentum ping-pong
+      e->theta_t[1] = (float*)dalloc(e, vb);
+      e->buf[1] = (float*)dalloc(e, vb);
+    } else {
+      e->theta_t[1] = e->theta_t[0];
+      e->buf[1] = e->buf[0];
+    }
     const int pairs = inner_mode == DLC_INNER_PINGPONG ? 2 : 1;
     for (int i = 0; i < pairs; ++i) {
       e->p[i] = (float*)dalloc(e, vb);
@@ -387,7 +420,6 @@ int dlc_engine_create(const dlc_config* cfg, const dlc_hyperparams* hyper, size_
       e->m[1] = e->m[0];
       e->v[1] = e->v[0];
     }
-    e->buf = (float*)dalloc(e, vb);
     e->grad = (float*)dalloc(e, vb);
     const size_t pb = e->k * e->S * elem_width(e->prec);
     e->send = dalloc(e, pb);
@@ -404,8 +436,10 @@ int dlc_engine_create(const dlc_config* cfg, const dlc_hyperparams* hyper, size_
       DLC_CUDA(cudaMemsetAsync(e->m[i], 0, vb, e->stream));  // AdamWState::init zeros, optim.cpp:17-27
       DLC_CUDA(cudaMemsetAsync(e->v[i], 0, vb, e->stream));
     }
-    DLC_CUDA(cudaMemsetAsync(e->theta_t, 0, vb, e->stream));
-    DLC_CUDA(cudaMemsetAsync(e->buf, 0, vb, e->stream));  // NesterovState::init, optim.cpp:29-35
+    for (int i = 0; i < 2; ++i) {
+      DLC_CUDA(cudaMemsetAsync(e->theta_t[i], 0, vb, e->stream));
+      DLC_CUDA(cudaMemsetAsync(e->buf[i], 0, vb, e->stream));  // NesterovState::init, optim.cpp:29-35
+    }
     DLC_CUDA(cudaMemsetAsync(e->flags, 0, kMaxK * sizeof(int), e->stream));
     DevState s{};
     s.scale = hyper->scaler_init_scale;
@@ -560,9 +594,7 @@ int dlc_engine_outer_step(dlc_engine* e, dlc_collective* c, dlc_outer_result* re
     check_collective(e, c);
     DeviceGuard dg(e->device);
     const uint64_t epoch = report ? read_state(e).outer_epoch : 0;
-    reset_flags(e);
-    pseudo_grad(e, local_pair(e));
-    outer_collective(e, c, report);
+    outer_round(e, c, nullptr, report);
     fill_report(e, c, report, epoch);
     outer_result(e, result);
   });
@@ -577,9 +609,7 @@ int dlc_engine_outer_step_from(dlc_engine* e, dlc_collective* c, const float* th
     DeviceGuard dg(e->device);
     const uint64_t epoch = report ? read_state(e).outer_epoch : 0;
     float* src = const_cast<float*>(theta_local_dev);
-    reset_flags(e);
-    pseudo_grad(e, Pair{{src, src}});
-    outer_collective(e, c, report);
+    outer_round(e, c, src, report);
     fill_report(e, c, report, epoch);
     outer_result(e, result);
   });
@@ -618,10 +648,10 @@ int dlc_engine_outer_step_host(dlc_engine* e, dlc_collective* c, const float* ho
     // theta_local arrives in the staging buffer; K4 then refreshes the engine's
     // own theta_local from the new theta_t.
     DLC_CUDA(cudaMemcpyAsync(e->grad, host_theta_local, e->n * sizeof(float), cudaMemcpyHostToDevice, e->stream));
-    reset_flags(e);
-    pseudo_grad(e, Pair{{e->grad, e->grad}});
-    outer_collective(e, c, nullptr);
-    DLC_CUDA(cudaMemcpyAsync(host_theta_t, e->theta_t, e->n * sizeof(float), cudaMemcpyDeviceToHost, e->stream));
+    outer_round(e, c, e->grad, nullptr);
+    const DevState s = read_state(e);  // which theta_t buffer is live after the step
+    DLC_CUDA(cudaMemcpyAsync(host_theta_t, e->theta_t[s.ocur], e->n * sizeof(float), cudaMemcpyDeviceToHost,
+                             e->stream));
     DLC_CUDA(cudaStreamSynchronize(e->stream));
     outer_result(e, result);
   });
@@ -653,7 +683,7 @@ int dlc_engines_outer_step_local(dlc_engine* const* engines, size_t k, dlc_outer
     PtrList in{};
     for (size_t j = 0; j < k; ++j) {
       dlc_engine* e = engines[j];
-      launch_pseudo_grad(e->theta_t, local_pair(e), e->st, e->send, e->prec, &e->st->delta_nonfinite, e->n, s);
+      launch_pseudo_grad(tt_pair(e), local_pair(e), e->st, e->send, e->prec, &e->st->delta_nonfinite, e->n, s);
       in.ptr[j] = e->send;
     }
     DLC_CUDA(cudaMemsetAsync(e0->flags, 0, kMaxK * sizeof(int), s));
@@ -665,7 +695,7 @@ int dlc_engines_outer_step_local(dlc_engine* const* engines, size_t k, dlc_outer
     }
     for (size_t j = 0; j < k; ++j) {
       dlc_engine* e = engines[j];
-      launch_nesterov_outer(e->theta_t, e->buf, local_pair(e), dbar, e->prec, e0->flags, 1, e->st,
+      launch_nesterov_outer(tt_pair(e), buf_pair(e), local_pair(e), dbar, e->prec, e0->flags, 1, e->st,
                             e->hyper.outer_lr, e->hyper.outer_momentum, e->n, s);
     }
     launched("outer_step_local");
@@ -686,9 +716,7 @@ int dlc_optimizer_step(dlc_engine* e, dlc_collective* c, const float* grad, int 
     if (round_completed) *round_completed = boundary ? 1 : 0;
     if (boundary) {  // engine.cpp:165-172
       check_collective(e, c);
-      reset_flags(e);
-      pseudo_grad(e, local_pair(e));
-      outer_collective(e, c, nullptr);
+      outer_round(e, c, nullptr, nullptr);
     }
   });
 }
@@ -708,7 +736,7 @@ int dlc_rng_perturb(dlc_engine* e, float* dst, uint64_t key, float lo, float hi)
     if (!e) fail(DLC_EINVAL, "dlc_rng_perturb: null engine");
     DeviceGuard dg(e->device);
     float* d = dst ? dst : live(e, DLC_THETA_LOCAL);
-    launch_rng_perturb(e->theta_t, key, lo, hi, d, e->n, e->stream);
+    launch_rng_perturb(live(e, DLC_THETA_T), key, lo, hi, d, e->n, e->stream);
     launched("rng_perturb");
   });
 }

@@ -240,8 +240,9 @@ __global__ void __launch_bounds__(kThreads) adamw_plain_kernel(const float* p, c
 // =============================================================================
 
 template <int PREC>
-__global__ void __launch_bounds__(kThreads) pseudo_grad_kernel(const float* tt, Pair tl, const DevState* st,
+__global__ void __launch_bounds__(kThreads) pseudo_grad_kernel(Pair ttp, Pair tl, const DevState* st,
                                                                void* out, int* flag, size_t n) {
+  const float* tt = st->ocur ? ttp.ptr[1] : ttp.ptr[0];
   const float* L = st->cur ? tl.ptr[1] : tl.ptr[0];
   const float4* T4 = reinterpret_cast<const float4*>(tt);
   const float4* L4 = reinterpret_cast<const float4*>(L);
@@ -386,9 +387,11 @@ __global__ void __launch_bounds__(kThreads) fold_kernel(const __grid_constant__ 
 // =============================================================================
 
 template <int PREC>
-__global__ void __launch_bounds__(kThreads) nesterov_outer_kernel(float* tt, float* buf, Pair tl,
+__global__ void __launch_bounds__(kThreads) nesterov_outer_kernel(Pair ttp, Pair bufp, Pair tl,
                                                                   const void* dbar, const int* flags, int nflags,
                                                                   DevState* st, float lr, float mu, size_t n) {
+  float* tt = st->ocur ? ttp.ptr[1] : ttp.ptr[0];
+  float* buf = st->ocur ? bufp.ptr[1] : bufp.ptr[0];
   int nonfinite = 0;
   for (int j = 0; j < nflags; ++j) nonfinite |= flags[j];
   const bool applied = nonfinite == 0;
@@ -461,6 +464,98 @@ __global__ void __launch_bounds__(kThreads) nesterov_outer_kernel(float* tt, flo
     st->outer_skips += applied ? 0 : 1;
     st->outer_epoch += 1;  // engine.cpp:144
   }
+}
+
+// K2 + K4 fused for K = 1 (see kernels.cuh).  Speculative: the new theta_t and
+// momentum go to the idle buffers of their ping-pong pairs, so a skip only has
+// to leave `ocur` unflipped.
+template <int PREC>
+__device__ __forceinline__ float solo_delta(float tt, float tl, bool& bad) {
+  const float d = delta_elem(tt, tl);  // engine.cpp:122
+  if (PREC == 0) {
+    bad |= !finite_f(d);
+    return d;
+  }
+  const uint16_t h = fp16_encode(d);  // encode once at the source; the mean of one
+  bad |= fp16_nonfinite(h);           // contribution re-encodes to the same code
+  return fp16_decode(h);
+}
+
+template <int PREC>
+__global__ void __launch_bounds__(kThreads) outer_solo_kernel(Pair ttp, Pair bufp, Pair tl, const float* src,
+                                                              DevState* st, float lr, float mu, size_t n) {
+  const int oc = st->ocur;
+  const float4* T = reinterpret_cast<const float4*>(oc ? ttp.ptr[1] : ttp.ptr[0]);
+  const float4* B = reinterpret_cast<const float4*>(oc ? bufp.ptr[1] : bufp.ptr[0]);
+  float4* To = reinterpret_cast<float4*>(oc ? ttp.ptr[0] : ttp.ptr[1]);
+  float4* Bo = reinterpret_cast<float4*>(oc ? bufp.ptr[0] : bufp.ptr[1]);
+  float* Ld = st->cur ? tl.ptr[1] : tl.ptr[0];
+  const float4* Ls = reinterpret_cast<const float4*>(src ? src : Ld);
+  float4* L4 = reinterpret_cast<float4*>(Ld);
+  bool bad = false;
+  const size_t n4 = n / 4, stride = gstride();
+  for (size_t i = gtid(); i < n4; i += stride * kU) {
+    float4 t[kU], b[kU], l[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const size_t j = i + u * stride;
+      if (j < n4) {
+        t[u] = ld_stream(T + j);
+        l[u] = ld_stream(Ls + j);
+        b[u] = ld_stream(B + j);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const size_t j = i + u * stride;
+      if (j < n4) {
+        float4 o;
+        o.x = nesterov_elem(t[u].x, solo_delta<PREC>(t[u].x, l[u].x, bad), b[u].x, lr, mu);
+        o.y = nesterov_elem(t[u].y, solo_delta<PREC>(t[u].y, l[u].y, bad), b[u].y, lr, mu);
+        o.z = nesterov_elem(t[u].z, solo_delta<PREC>(t[u].z, l[u].z, bad), b[u].z, lr, mu);
+        o.w = nesterov_elem(t[u].w, solo_delta<PREC>(t[u].w, l[u].w, bad), b[u].w, lr, mu);
+        st_stream(To + j, o);
+        st_stream(Bo + j, b[u]);
+        st_stream(L4 + j, o);
+      }
+    }
+  }
+  const size_t i = gtid();
+  if (i < n - n4 * 4) {
+    const size_t e = n4 * 4 + i;
+    const float* Tf = reinterpret_cast<const float*>(T);
+    float bb = reinterpret_cast<const float*>(B)[e];
+    const float t0 = Tf[e];
+    const float o = nesterov_elem(t0, solo_delta<PREC>(t0, reinterpret_cast<const float*>(Ls)[e], bad), bb, lr, mu);
+    reinterpret_cast<float*>(To)[e] = o;
+    reinterpret_cast<float*>(Bo)[e] = bb;
+    Ld[e] = o;
+  }
+  block_or_flag(bad, &st->delta_nonfinite);
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(&st->done_blocks, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    const int skip = atomicAdd(&st->delta_nonfinite, 0);
+    if (!skip) st->ocur ^= 1;  // engine.cpp:136-139: apply only a finite reduction
+    st->last_applied = skip ? 0 : 1;
+    st->outer_skips += skip ? 1 : 0;
+    st->outer_epoch += 1;  // engine.cpp:144
+    st->done_blocks = 0;
+  }
+}
+
+// After a skipped solo step: theta_local := theta_t (engine.cpp:143).
+__global__ void __launch_bounds__(kThreads) outer_solo_recover_kernel(Pair ttp, Pair tl, const DevState* st,
+                                                                      size_t n) {
+  if (st->last_applied) return;
+  const float* T = st->ocur ? ttp.ptr[1] : ttp.ptr[0];
+  float* L = st->cur ? tl.ptr[1] : tl.ptr[0];
+  for (size_t e = gtid(); e < n; e += gstride()) L[e] = T[e];
 }
 
 __global__ void __launch_bounds__(kThreads) nesterov_plain_kernel(const float* p, const float* g, float* buf,
@@ -600,7 +695,7 @@ void launch_adamw_plain(const float* p, const float* g, float* m, float* v, floa
   adamw_plain_kernel<<<grid_for(adamw_plain_kernel, n), kThreads, 0, s>>>(p, g, m, v, out, n, a);
 }
 
-void launch_pseudo_grad(const float* tt, Pair tl, const DevState* st, void* out, int precision, int* flag,
+void launch_pseudo_grad(Pair tt, Pair tl, const DevState* st, void* out, int precision, int* flag,
                         size_t n, cudaStream_t s) {
   if (precision == 0)
     pseudo_grad_kernel<0><<<grid_for(pseudo_grad_kernel<0>, n / 4 / kU + 1), kThreads, 0, s>>>(tt, tl, st, out,
@@ -623,7 +718,7 @@ void launch_fold(const PtrList& in, int k, int in_kind, void* out, int out_kind,
 #undef DLC_FOLD
 }
 
-void launch_nesterov_outer(float* tt, float* buf, Pair tl, const void* dbar, int precision, const int* flags,
+void launch_nesterov_outer(Pair tt, Pair buf, Pair tl, const void* dbar, int precision, const int* flags,
                            int nflags, DevState* st, float lr, float mu, size_t n, cudaStream_t s) {
   const size_t work = n / 4 / kU + 1;
   if (precision == 0)
@@ -632,6 +727,16 @@ void launch_nesterov_outer(float* tt, float* buf, Pair tl, const void* dbar, int
   else
     nesterov_outer_kernel<1><<<grid_for(nesterov_outer_kernel<1>, work), kThreads, 0, s>>>(
         tt, buf, tl, dbar, flags, nflags, st, lr, mu, n);
+}
+
+void launch_outer_solo_fused(Pair tt, Pair buf, Pair tl, const float* src, int precision, DevState* st, float lr,
+                             float mu, size_t n, cudaStream_t s) {
+  const size_t work = n / 4 / kU + 1;
+  if (precision == 0)
+    outer_solo_kernel<0><<<grid_for(outer_solo_kernel<0>, work), kThreads, 0, s>>>(tt, buf, tl, src, st, lr, mu, n);
+  else
+    outer_solo_kernel<1><<<grid_for(outer_solo_kernel<1>, work), kThreads, 0, s>>>(tt, buf, tl, src, st, lr, mu, n);
+  outer_solo_recover_kernel<<<grid_for(outer_solo_recover_kernel, n), kThreads, 0, s>>>(tt, tl, st, n);
 }
 
 void launch_nesterov_plain(const float* p, const float* g, float* buf, float* out, size_t n, float lr, float mu,

@@ -41,7 +41,8 @@ struct DevState {
   int last_overflow;        // InnerStepResult::overflow_skipped
   int delta_nonfinite;      // K2: non-finite delta (or FP16 encode overflow)
   int last_applied;         // OuterStepResult::applied
-  int pad[2];
+  int ocur;                 // live buffer of the theta_t / momentum pair (solo fused outer step)
+  int pad;
 };
 
 struct AdamWArgs {
@@ -85,7 +86,7 @@ void launch_adamw_plain(const float* p, const float* g, float* m, float* v, floa
 
 // K2 --------------------------------------------------------------------------
 // precision 0: out is float*, 1: out is uint16_t* (binary16 codes).
-void launch_pseudo_grad(const float* theta_t, Pair theta_local,
+void launch_pseudo_grad(Pair theta_t, Pair theta_local,
                         const DevState* st, void* out, int precision, int* flag, size_t n,
                         cudaStream_t s);
 
@@ -97,9 +98,18 @@ void launch_fold(const PtrList& in, int k, int in_kind, void* out, int out_kind,
                  size_t n, cudaStream_t s);
 
 // K4 --------------------------------------------------------------------------
-void launch_nesterov_outer(float* theta_t, float* buf, Pair theta_local,
+void launch_nesterov_outer(Pair theta_t, Pair buf, Pair theta_local,
                            const void* dbar, int precision, const int* flags, int nflags,
                            DevState* st, float lr, float mu, size_t n, cudaStream_t s);
+// K2+K4 fused for a single worker (SoloCollective, reduce.cpp:113-126): one
+// HBM pass reading theta_t[ocur], buf[ocur], theta_local and writing
+// theta_t[ocur^1], buf[ocur^1], theta_local (24 B/param).  The non-finite gate
+// is decided by the last CTA (ocur flips only when applied); a following
+// recovery kernel restores theta_local := theta_t when the step was skipped
+// (engine.cpp:136-144).  `src` (nullable) overrides the theta_local input.
+void launch_outer_solo_fused(Pair theta_t, Pair buf, Pair theta_local, const float* src,
+                             int precision, DevState* st, float lr, float mu, size_t n,
+                             cudaStream_t s);
 void launch_nesterov_plain(const float* p, const float* g, float* buf, float* out, size_t n,
                            float lr, float mu, cudaStream_t s);
 
