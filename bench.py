@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--params", type=int, default=1_100_000_000)
     ap.add_argument("--precision", choices=["fp16", "fp32"], default="fp16")
-    ap.add_argument("--mode", choices=["ordered", "allreduce"], default="ordered")
+    ap.add_argument("--mode", choices=["p2p", "ordered", "allreduce"], default="p2p")
     ap.add_argument("--inner-mode", choices=["pingpong", "inplace"], default="pingpong")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
@@ -197,7 +197,7 @@ def run_ours(args):
     k = world
     n = args.params
     prec = D.FP16 if args.precision == "fp16" else D.FP32
-    mode = D.MODE_ORDERED if args.mode == "ordered" else D.MODE_ALLREDUCE
+    mode = {"p2p": D.MODE_P2P, "ordered": D.MODE_ORDERED, "allreduce": D.MODE_ALLREDUCE}[args.mode]
 
     def barrier():
         if world > 1:
@@ -280,12 +280,20 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": workload_config(args, k)}
-    rl = roof(b_k4, k4_ms)
-    rl["kernel"] = "nesterov_outer_kernel (K4)"
+    if k == 1:
+        # one worker: K2 and K4 fused into one pass (theta_t, theta_local, momentum in;
+        # theta_t', momentum', theta_local' out) = 24 B/param in either precision
+        rl = roof(24, k4_ms)
+        rl["kernel"] = "outer_solo_kernel (K2+K4 fused)"
+        line["phases_ms"] = {"outer_solo_K2K4": k4_ms}
+        line["phase_roofline"] = {"outer_solo_K2K4": rl["frac"]}
+    else:
+        rl = roof(b_k4, k4_ms)
+        rl["kernel"] = "nesterov_outer%s_kernel (K4)" % ("_p2p" if mode == D.MODE_P2P else "")
+        line["phases_ms"] = {"pseudo_grad_K2": k2_ms, "collective_C1_K3": coll_ms, "nesterov_K4": k4_ms}
+        line["phase_roofline"] = {"pseudo_grad_K2": roof(b_k2, k2_ms)["frac"], "nesterov_K4": rl["frac"]}
     rl["traffic"] = None
     line["roofline"] = rl
-    line["phases_ms"] = {"pseudo_grad_K2": k2_ms, "collective_C1_K3": coll_ms, "nesterov_K4": k4_ms}
-    line["phase_roofline"] = {"pseudo_grad_K2": roof(b_k2, k2_ms)["frac"], "nesterov_K4": rl["frac"]}
     if k > 1:
         wire_bytes = 2 * (k - 1) * (-(-n // k)) * wire
         line["nccl_bus_gbs"] = wire_bytes / (coll_ms * 1e-3) / 1e9 if coll_ms else None
@@ -293,7 +301,8 @@ def run_ours(args):
     ir["kernel"] = "adamw_kernel (K1, %s)" % args.inner_mode
     line["inner_adamw"] = {"ms_per_step": inner_ms, "kernel_ms": k1_ms, "roofline": ir,
                            "vs_8TBs_spec": ir["achieved"] / 8000.0}
-    line["gpu_launches"] = args.steps * (3 if k > 1 and mode == D.MODE_ORDERED else 2) + args.steps
+    # outer: fused solo + recovery (K=1) or K2 + fold/check + K4; inner: K1 (+ pre-pass in place)
+    line["gpu_launches"] = args.steps * (3 if k > 1 else 2) + args.steps * (1 if args.inner_mode == "pingpong" else 2)
     line["clocks"] = clk
 
     # e2e through the public C ABI with host buffers: H2D theta_local, outer step, D2H theta_t.

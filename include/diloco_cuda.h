@@ -160,7 +160,14 @@ typedef struct {
  *   (K3) -> NCCL all-gather; bit-identical to reduce_average in rank order.
  * DLC_MODE_ALLREDUCE: ncclAllReduce(ncclAvg) on the flat buffer; NCCL's
  *   reduction order, within the tolerance stated in DESIGN.md. */
-enum dlc_reduce_mode { DLC_MODE_ORDERED = 0, DLC_MODE_ALLREDUCE = 1 };
+enum dlc_reduce_mode { DLC_MODE_ORDERED = 0, DLC_MODE_ALLREDUCE = 1, DLC_MODE_P2P = 2 };
+/* DLC_MODE_P2P: the same rank-ordered fold as ORDERED, fused with the data
+ *   movement over NVLink peer memory (CUDA IPC): each owner folds its slot
+ *   straight out of the peers' send buffers, and the outer Nesterov kernel
+ *   reads every owner's mean slot in place, so there are no recv / gather
+ *   copies in HBM.  Two 4-byte NCCL all-reduces order the phases.  Bitwise
+ *   equal to ORDERED.  Engine path only; the host-buffer plugin call uses
+ *   ORDERED semantics. */
 
 /* 128-byte ncclUniqueId, created on rank 0 and shipped to every rank. */
 DLC_API int dlc_nccl_unique_id(uint8_t id[128]);

@@ -19,4 +19,4 @@ def build_library() -> str:
 from . import _capi  # noqa: E402  (raises ImportError when the .so is missing)
 from .diloco import *  # noqa: E402,F401,F403
 from ._capi import (FP16, FP32, INNER_INPLACE, INNER_PINGPONG, MODE_ALLREDUCE,  # noqa: E402,F401
-                    MODE_ORDERED, THETA_T, THETA_LOCAL, ADAM_M, ADAM_V, MOMENTUM, GRAD, LR_NONE, LR_COSINE)
+                    MODE_ORDERED, MODE_P2P, THETA_T, THETA_LOCAL, ADAM_M, ADAM_V, MOMENTUM, GRAD, LR_NONE, LR_COSINE)

@@ -17,7 +17,7 @@ HEADER = os.path.join(os.path.dirname(HERE), "include", "diloco_cuda.h")
 OK, ESHAPE, ECONFIG, ENUMERIC, ECOLLECTIVE, ECUDA, ENCCL, EINVAL = range(8)
 FP32, FP16 = 0, 1
 LR_NONE, LR_COSINE = 0, 1
-MODE_ORDERED, MODE_ALLREDUCE = 0, 1
+MODE_ORDERED, MODE_ALLREDUCE, MODE_P2P = 0, 1, 2
 INNER_PINGPONG, INNER_INPLACE = 0, 1
 THETA_T, THETA_LOCAL, ADAM_M, ADAM_V, MOMENTUM, GRAD = range(6)
 

@@ -74,6 +74,16 @@ struct dlc_engine {
   double phase_ms[4] = {0, 0, 0, 0};
   uint64_t phase_n[4] = {0, 0, 0, 0};
   cudaEvent_t open_ev = nullptr;
+  // DLC_MODE_P2P: my owner slot / flag, and every rank's send, slot and flag
+  // mapped into this process through CUDA IPC (own entries are local).
+  void* dbar = nullptr;
+  int* pflag = nullptr;
+  int* barrier_buf = nullptr;
+  const dlc_collective* p2p_bound = nullptr;
+  void* peer_send[kMaxK] = {};
+  void* peer_dbar[kMaxK] = {};
+  int* peer_flag[kMaxK] = {};
+  std::vector<void*> ipc_opened;
 };
 
 namespace {
@@ -250,6 +260,68 @@ void outer_round(dlc_engine* e, dlc_collective* c, const float* src, dlc_reduce_
 
 ncclDataType_t nccl_type(int prec) { return prec == DLC_FP16 ? ncclFloat16 : ncclFloat32; }
 
+void p2p_unbind(dlc_engine* e) {
+  for (void* p : e->ipc_opened) cudaIpcCloseMemHandle(p);
+  e->ipc_opened.clear();
+  e->p2p_bound = nullptr;
+}
+
+// Maps every rank's send buffer, owner slot and owner flag into this process:
+// IPC handles are all-gathered over the collective's own NCCL communicator.
+void p2p_bind(dlc_engine* e, dlc_collective* c) {
+  if (e->p2p_bound == c) return;
+  p2p_unbind(e);
+  const int K = (int)e->k, r = c->rank;
+  struct Handles {
+    cudaIpcMemHandle_t send, dbar, flag;
+  };
+  Handles mine;
+  DLC_CUDA(cudaIpcGetMemHandle(&mine.send, e->send));
+  DLC_CUDA(cudaIpcGetMemHandle(&mine.dbar, e->dbar));
+  DLC_CUDA(cudaIpcGetMemHandle(&mine.flag, e->pflag));
+  const size_t sz = sizeof(Handles);
+  char* dbuf = nullptr;
+  DLC_CUDA(cudaMalloc(&dbuf, K * sz));
+  std::vector<Handles> all(K);
+  try {
+    DLC_CUDA(cudaMemcpyAsync(dbuf + r * sz, &mine, sz, cudaMemcpyHostToDevice, e->stream));
+    DLC_NCCL(ncclAllGather(dbuf + r * sz, dbuf, sz, ncclUint8, c->comm, e->stream));
+    DLC_CUDA(cudaMemcpyAsync(all.data(), dbuf, K * sz, cudaMemcpyDeviceToHost, e->stream));
+    DLC_CUDA(cudaStreamSynchronize(e->stream));
+  } catch (...) {
+    cudaFree(dbuf);
+    throw;
+  }
+  cudaFree(dbuf);
+  for (int j = 0; j < K; ++j) {
+    if (j == r) {
+      e->peer_send[j] = e->send;
+      e->peer_dbar[j] = e->dbar;
+      e->peer_flag[j] = e->pflag;
+      continue;
+    }
+    void* ps = nullptr;
+    void* pd = nullptr;
+    void* pf = nullptr;
+    const char* what = "cudaIpcOpenMemHandle (DLC_MODE_P2P needs one process per GPU with NVLink peer access)";
+    check_cuda(cudaIpcOpenMemHandle(&ps, all[j].send, cudaIpcMemLazyEnablePeerAccess), what);
+    e->ipc_opened.push_back(ps);
+    check_cuda(cudaIpcOpenMemHandle(&pd, all[j].dbar, cudaIpcMemLazyEnablePeerAccess), what);
+    e->ipc_opened.push_back(pd);
+    check_cuda(cudaIpcOpenMemHandle(&pf, all[j].flag, cudaIpcMemLazyEnablePeerAccess), what);
+    e->ipc_opened.push_back(pf);
+    e->peer_send[j] = ps;
+    e->peer_dbar[j] = pd;
+    e->peer_flag[j] = (int*)pf;
+  }
+  e->p2p_bound = c;
+}
+
+// Stream-ordered fleet barrier: a 4-byte NCCL all-reduce.
+void fleet_barrier(dlc_engine* e, dlc_collective* c) {
+  DLC_NCCL(ncclAllReduce(e->barrier_buf, e->barrier_buf, 1, ncclInt32, ncclSum, c->comm, e->stream));
+}
+
 // C1 + K3 on the engine's send buffer, then K4.  Everything is enqueued on the
 // engine stream; NCCL calls are stream-ordered with the kernels around them.
 void outer_collective(dlc_engine* e, dlc_collective* c, dlc_reduce_report* rep) {
@@ -262,6 +334,33 @@ void outer_collective(dlc_engine* e, dlc_collective* c, dlc_reduce_report* rep) 
   const int r = c->rank;
   if (rep) DLC_CUDA(cudaEventRecord(e->ev0, e->stream));
   phase_begin(e);
+  if (c->mode == DLC_MODE_P2P) {
+    p2p_bind(e, c);
+    // (1) every rank's K2 is done, and every peer has finished reading my slot
+    // and flag in its previous K4, so both may be rewritten.
+    fleet_barrier(e, c);
+    DLC_CUDA(cudaMemsetAsync(e->pflag, 0, sizeof(int), e->stream));
+    // owner fold of slot r straight out of every rank's send buffer, rank order
+    PtrList in{};
+    for (size_t j = 0; j < K; ++j) in.ptr[j] = static_cast<char*>(e->peer_send[j]) + r * S * w;
+    launch_fold(in, (int)K, e->prec, e->dbar, e->prec, e->pflag, S, e->stream);
+    launched("fold_p2p");
+    // (2) every owner slot and flag is final.
+    fleet_barrier(e, c);
+    phase_end(e, DLC_PHASE_COLLECTIVE);
+    if (rep) DLC_CUDA(cudaEventRecord(e->ev1, e->stream));
+    PtrList slots{}, fl{};
+    for (size_t q = 0; q < K; ++q) {
+      slots.ptr[q] = e->peer_dbar[q];
+      fl.ptr[q] = e->peer_flag[q];
+    }
+    phase_begin(e);
+    launch_nesterov_outer_p2p(tt_pair(e), buf_pair(e), local_pair(e), slots, fl, (int)K, S, e->prec, e->st,
+                              e->hyper.outer_lr, e->hyper.outer_momentum, e->n, e->stream);
+    phase_end(e, DLC_PHASE_OUTER);
+    launched("nesterov_outer_p2p");
+    return;
+  }
   if (c->mode == DLC_MODE_ORDERED) {
     char* recv = static_cast<char*>(e->recv);
     char* gather = static_cast<char*>(e->gather);
@@ -428,6 +527,10 @@ int dlc_engine_create(const dlc_config* cfg, const dlc_hyperparams* hyper, size_
       e->recv = dalloc(e, pb);
       e->gather = dalloc(e, pb);
       DLC_CUDA(cudaMemsetAsync(e->gather, 0, pb, e->stream));
+      e->dbar = dalloc(e, e->S * elem_width(e->prec));
+      e->pflag = (int*)dalloc(e, 256);
+      e->barrier_buf = (int*)dalloc(e, 256);
+      DLC_CUDA(cudaMemsetAsync(e->pflag, 0, 256, e->stream));
     }
     e->flags = (int*)dalloc(e, kMaxK * sizeof(int));
     e->st = (DevState*)dalloc(e, sizeof(DevState));
@@ -458,6 +561,7 @@ int dlc_engine_destroy(dlc_engine* e) {
   return guard([&] {
     DeviceGuard dg(e->device);
     if (e->stream) cudaStreamSynchronize(e->stream);
+    p2p_unbind(e);
     for (void* p : e->allocs) cudaFree(p);
     for (const auto& mk : e->pending) {
       cudaEventDestroy(mk.a);
@@ -758,7 +862,7 @@ int dlc_collective_create_nccl(int rank, int world, const uint8_t id[128], int d
   return guard([&] {
     if (!id || !out) fail(DLC_EINVAL, "dlc_collective_create_nccl: null argument");
     if (world < 1 || rank < 0 || rank >= world) fail(DLC_ECONFIG, "bad rank/world");
-    if (mode != DLC_MODE_ORDERED && mode != DLC_MODE_ALLREDUCE) fail(DLC_ECONFIG, "unknown reduce mode");
+    if (mode != DLC_MODE_ORDERED && mode != DLC_MODE_ALLREDUCE && mode != DLC_MODE_P2P) fail(DLC_ECONFIG, "unknown reduce mode");
     DeviceGuard dg(device);
     auto* c = new dlc_collective();
     c->kind = 1;
@@ -839,7 +943,7 @@ int dlc_collective_all_reduce_avg(dlc_collective* c, const float* local, size_t 
         else
           DLC_CUDA(cudaMemcpyAsync(send, src, n * 4, cudaMemcpyDeviceToDevice, s));
         const int r = c->rank;
-        if (c->mode == DLC_MODE_ORDERED) {
+        if (c->mode != DLC_MODE_ALLREDUCE) {  // ORDERED and P2P: rank-order fold
           DLC_NCCL(ncclGroupStart());
           for (size_t j = 0; j < K; ++j) {
             if ((int)j == r) continue;

@@ -558,6 +558,95 @@ __global__ void __launch_bounds__(kThreads) outer_solo_recover_kernel(Pair ttp, 
   for (size_t e = gtid(); e < n; e += gstride()) L[e] = T[e];
 }
 
+// K4 over NVLink peer memory (DLC_MODE_P2P): the mean slot of owner q is read
+// in place from q's HBM; the K owner flags are read once per CTA.
+template <int PREC>
+__global__ void __launch_bounds__(kThreads) nesterov_outer_p2p_kernel(Pair ttp, Pair bufp, Pair tl,
+                                                                      const __grid_constant__ PtrList slots,
+                                                                      const __grid_constant__ PtrList flags, int k,
+                                                                      size_t S, DevState* st, float lr, float mu,
+                                                                      size_t n) {
+  __shared__ int s_nonfinite;
+  if (threadIdx.x == 0) {
+    int nf = 0;
+    for (int j = 0; j < k; ++j) nf |= *reinterpret_cast<const volatile int*>(flags.ptr[j]);
+    s_nonfinite = nf;
+  }
+  __syncthreads();
+  const bool applied = s_nonfinite == 0;
+  float* tt = st->ocur ? ttp.ptr[1] : ttp.ptr[0];
+  float* buf = st->ocur ? bufp.ptr[1] : bufp.ptr[0];
+  float* L = st->cur ? tl.ptr[1] : tl.ptr[0];
+  const size_t stride = gstride();
+  for (int q = 0; q < k; ++q) {
+    const size_t base = (size_t)q * S;
+    if (base >= n) break;
+    const size_t len = n - base < S ? n - base : S;
+    const size_t len4 = len / 4;
+    float4* T4 = reinterpret_cast<float4*>(tt + base);
+    float4* B4 = reinterpret_cast<float4*>(buf + base);
+    float4* L4 = reinterpret_cast<float4*>(L + base);
+    const void* dbar = slots.ptr[q];
+    if (applied) {
+      for (size_t i = gtid(); i < len4; i += stride * kU) {
+        float4 t[kU], b[kU], d[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const size_t j = i + u * stride;
+          if (j < len4) {
+            if (PREC == 0) {
+              d[u] = ld_stream(reinterpret_cast<const float4*>(dbar) + j);
+            } else {
+              const uint2 w = ld_stream(reinterpret_cast<const uint2*>(dbar) + j);
+              F4_APPLY(d[u], fp16_decode(lo16(w.x)), fp16_decode(hi16(w.x)), fp16_decode(lo16(w.y)),
+                       fp16_decode(hi16(w.y)));
+            }
+            t[u] = ld_stream(T4 + j);
+            b[u] = ld_stream(B4 + j);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const size_t j = i + u * stride;
+          if (j < len4) {
+            float4 o;
+            o.x = nesterov_elem(t[u].x, d[u].x, b[u].x, lr, mu);
+            o.y = nesterov_elem(t[u].y, d[u].y, b[u].y, lr, mu);
+            o.z = nesterov_elem(t[u].z, d[u].z, b[u].z, lr, mu);
+            o.w = nesterov_elem(t[u].w, d[u].w, b[u].w, lr, mu);
+            st_stream(T4 + j, o);
+            st_stream(B4 + j, b[u]);
+            st_stream(L4 + j, o);
+          }
+        }
+      }
+    } else {
+      for (size_t i = gtid(); i < len4; i += stride) st_stream(L4 + i, ld_stream(T4 + i));
+    }
+    const size_t i = gtid();
+    if (i < len - len4 * 4) {
+      const size_t e = len4 * 4 + i;
+      float* te = tt + base;
+      if (applied) {
+        const float d = PREC == 0 ? reinterpret_cast<const float*>(dbar)[e]
+                                  : fp16_decode(reinterpret_cast<const uint16_t*>(dbar)[e]);
+        float b = buf[base + e];
+        const float o = nesterov_elem(te[e], d, b, lr, mu);
+        te[e] = o;
+        buf[base + e] = b;
+        L[base + e] = o;
+      } else {
+        L[base + e] = te[e];
+      }
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->last_applied = applied ? 1 : 0;
+    st->outer_skips += applied ? 0 : 1;
+    st->outer_epoch += 1;  // engine.cpp:144
+  }
+}
+
 __global__ void __launch_bounds__(kThreads) nesterov_plain_kernel(const float* p, const float* g, float* buf,
                                                                   float* out, size_t n, float lr, float mu) {
   for (size_t e = gtid(); e < n; e += gstride()) {
@@ -737,6 +826,18 @@ void launch_outer_solo_fused(Pair tt, Pair buf, Pair tl, const float* src, int p
   else
     outer_solo_kernel<1><<<grid_for(outer_solo_kernel<1>, work), kThreads, 0, s>>>(tt, buf, tl, src, st, lr, mu, n);
   outer_solo_recover_kernel<<<grid_for(outer_solo_recover_kernel, n), kThreads, 0, s>>>(tt, tl, st, n);
+}
+
+void launch_nesterov_outer_p2p(Pair tt, Pair buf, Pair tl, const PtrList& slots, const PtrList& flags, int k,
+                               size_t S, int precision, DevState* st, float lr, float mu, size_t n,
+                               cudaStream_t s) {
+  const size_t work = n / 4 / kU + 1;
+  if (precision == 0)
+    nesterov_outer_p2p_kernel<0><<<grid_for(nesterov_outer_p2p_kernel<0>, work), kThreads, 0, s>>>(
+        tt, buf, tl, slots, flags, k, S, st, lr, mu, n);
+  else
+    nesterov_outer_p2p_kernel<1><<<grid_for(nesterov_outer_p2p_kernel<1>, work), kThreads, 0, s>>>(
+        tt, buf, tl, slots, flags, k, S, st, lr, mu, n);
 }
 
 void launch_nesterov_plain(const float* p, const float* g, float* buf, float* out, size_t n, float lr, float mu,

@@ -112,6 +112,12 @@ void launch_outer_solo_fused(Pair theta_t, Pair buf, Pair theta_local, const flo
                              cudaStream_t s);
 void launch_nesterov_plain(const float* p, const float* g, float* buf, float* out, size_t n,
                            float lr, float mu, cudaStream_t s);
+// K4 reading the mean in place from its K owners over NVLink (DLC_MODE_P2P):
+// element i lives in slots.ptr[i / S][i % S]; owner q's non-finite flag at
+// flags.ptr[q].  Same arithmetic and skip gate as launch_nesterov_outer.
+void launch_nesterov_outer_p2p(Pair theta_t, Pair buf, Pair theta_local, const PtrList& slots,
+                               const PtrList& flags, int k, size_t S, int precision, DevState* st,
+                               float lr, float mu, size_t n, cudaStream_t s);
 
 // elementwise helpers -----------------------------------------------------------
 void launch_axpy(float alpha, const float* x, const float* y, float* out, size_t n,

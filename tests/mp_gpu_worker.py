@@ -43,7 +43,7 @@ def main():
             g[3] = np.inf  # one overflowed inner step on the last worker
         return g
 
-    for mode_name, mode in (("ordered", D.MODE_ORDERED), ("allreduce", D.MODE_ALLREDUCE)):
+    for mode_name, mode in (("ordered", D.MODE_ORDERED), ("p2p", D.MODE_P2P), ("allreduce", D.MODE_ALLREDUCE)):
         coll = PD.make_nccl_collective(r, mode)
         assert coll.world_size() == k and coll.rank() == r.rank
         for prec in (D.FP32, D.FP16):
@@ -65,7 +65,7 @@ def main():
                     2 if prec == D.FP16 else 4)
             me = workers[r.rank]
             got = {w: e.download(w) for w in (D.THETA_T, D.THETA_LOCAL, D.ADAM_M, D.ADAM_V, D.MOMENTUM)}
-            if mode == D.MODE_ORDERED:
+            if mode != D.MODE_ALLREDUCE:
                 for w, want in ((D.THETA_T, me.theta_t), (D.THETA_LOCAL, me.theta_local), (D.ADAM_M, me.m),
                                 (D.ADAM_V, me.v), (D.MOMENTUM, me.buf)):
                     assert np.array_equal(bits(got[w]), bits(want)), (mode_name, prec, w)
@@ -95,7 +95,7 @@ def main():
             deltas = [O.rng_fill(9, "delta", j, 10_007, -1, 1) for j in range(k)]
             got, rep = coll.all_reduce_avg(deltas[r.rank], prec, outer_epoch=3)
             _, want = port.reduce_average(deltas, prec)
-            if mode == D.MODE_ORDERED:
+            if mode != D.MODE_ALLREDUCE:
                 assert np.array_equal(bits(got), bits(want))
             else:
                 assert np.max(np.abs(got - want)) <= (2.0 ** -10 if prec else k * 2.0 ** -23)

@@ -29,5 +29,5 @@ def test_multigpu_parity(nproc):
            "--master-addr", "127.0.0.1", "--master-port", str(29600 + nproc),
            os.path.join(ROOT, "tests", "mp_gpu_worker.py")]
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
-    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("MPRESULT")]
-    assert p.returncode == 0 and len(lines) == nproc, p.stdout[-3000:] + p.stderr[-3000:]
+    # ranks share stdout, so their result lines may interleave: count markers
+    assert p.returncode == 0 and p.stdout.count("MPRESULT") == nproc, p.stdout[-3000:] + p.stderr[-3000:]
