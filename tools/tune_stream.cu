@@ -1,124 +1,116 @@
-// tune_stream.cu — HBM streaming micro-benchmark used to pick the K1/K4 access
-// pattern (development tool, not part of the product).
-//
-// Measures, over N = 1.1e9 FP32 elements (every stream >> L2):
-//   copy 1R1W with several access variants, and the AdamW traffic shape (4R3W)
-//   with the real AdamW arithmetic, under different load/store cache hints,
-//   vectors-in-flight U, CTA size and grid policy.
+// tune_stream.cu — HBM streaming micro-benchmark used to pick the grid /
+// work-distribution policy of the hot-path kernels (development tool, not part
+// of the product).  Random-initialised buffers of N = 1.1e9 FP32 (every stream
+// >> L2); patterns with the hot-path traffic shapes and the real arithmetic:
+//   copy  1R1W    adam 4R3W (K1)    nest 3R3W (K4/solo)    pg 2R + half W (K2)
+// Work-distribution policies:
+//   gs  : persistent grid-stride (grid = #SM x occupancy), U vectors per trip
+//   full: one CTA per 256*U vectors, every thread U vectors (non-persistent)
+//   blk : persistent, each CTA owns one contiguous range
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -fmad=false -o tune_stream tune_stream.cu
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
 
-#define CK(x)                                                                   \
-  do {                                                                          \
-    cudaError_t e = (x);                                                        \
-    if (e != cudaSuccess) {                                                     \
-      std::printf("CUDA error %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__); \
-      std::exit(1);                                                             \
-    }                                                                           \
+#define CK(x)                                                                                \
+  do {                                                                                       \
+    cudaError_t e = (x);                                                                     \
+    if (e != cudaSuccess) {                                                                  \
+      std::printf("CUDA error %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__);    \
+      std::exit(1);                                                                          \
+    }                                                                                        \
   } while (0)
 
-enum { LD_DEF = 0, LD_CS = 1, LD_NC_NA = 2, LD_LU = 3 };
-enum { ST_DEF = 0, ST_CS = 1, ST_NA = 2 };
+enum { GS = 0, FULL = 1, BLK = 2 };
 
-template <int LD>
-__device__ __forceinline__ float4 ld4(const float4* p) {
-  if (LD == LD_CS) return __ldcs(p);
-  if (LD == LD_LU) return __ldlu(p);
-  if (LD == LD_NC_NA) {
-    float4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
-                 : "l"(p));
-    return r;
-  }
-  return *p;
-}
-
-template <int ST>
-__device__ __forceinline__ void st4(float4* p, float4 v) {
-  if (ST == ST_CS) {
-    __stcs(p, v);
-  } else if (ST == ST_NA) {
-    asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
-                 "f"(v.w));
-  } else {
-    *p = v;
+__global__ void fill(float* p, size_t n, unsigned seed, float lo, float hi) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    unsigned x = (unsigned)i * 2654435761u ^ seed;
+    x ^= x >> 13;
+    x *= 0x5bd1e995;
+    x ^= x >> 15;
+    p[i] = lo + (hi - lo) * (x & 0xFFFFFF) * (1.0f / 16777216.0f);
   }
 }
 
-template <int LD, int ST, int U>
-__global__ void copy_k(const float4* __restrict__ a, float4* __restrict__ b, size_t n4) {
-  const size_t stride = (size_t)gridDim.x * blockDim.x;
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride * U) {
-    float4 x[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (i + u * stride < n4) x[u] = ld4<LD>(a + i + u * stride);
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (i + u * stride < n4) st4<ST>(b + i + u * stride, x[u]);
-  }
-}
-
-struct S {
-  float b1, b2, eps, wd, omb1, omb2, c1, c2, lr, inv;
+struct Ar {
+  const float4* in[4];
+  float4* out[3];
+  size_t n4;
 };
 
-__device__ __forceinline__ float adam1(float p, float g, float& m, float& v, const S& s) {
-  g = __fmul_rn(g, s.inv);
-  m = __fadd_rn(__fmul_rn(s.b1, m), __fmul_rn(s.omb1, g));
-  v = __fadd_rn(__fmul_rn(s.b2, v), __fmul_rn(__fmul_rn(s.omb2, g), g));
-  const float mh = __fdiv_rn(m, s.c1), vh = __fdiv_rn(v, s.c2);
-  return __fsub_rn(p, __fmul_rn(s.lr, __fadd_rn(__fdiv_rn(mh, __fadd_rn(__fsqrt_rn(vh), s.eps)), __fmul_rn(s.wd, p))));
+__device__ __forceinline__ float adam1(float p, float g, float& m, float& v) {
+  g = __fmul_rn(g, 1.0f / 65536.0f);
+  m = __fadd_rn(__fmul_rn(0.9f, m), __fmul_rn(0.1f, g));
+  v = __fadd_rn(__fmul_rn(0.95f, v), __fmul_rn(__fmul_rn(0.05f, g), g));
+  const float mh = __fdiv_rn(m, 0.1f), vh = __fdiv_rn(v, 0.05f);
+  return __fsub_rn(p, __fmul_rn(4e-4f, __fadd_rn(__fdiv_rn(mh, __fadd_rn(__fsqrt_rn(vh), 1e-8f)), __fmul_rn(0.1f, p))));
+}
+__device__ __forceinline__ float nest1(float t, float d, float& b) {
+  b = __fadd_rn(__fmul_rn(0.9f, b), d);
+  return __fsub_rn(t, __fmul_rn(0.7f, __fadd_rn(d, __fmul_rn(0.9f, b))));
 }
 
-// AdamW traffic: read p,g,m,v ; write p2,m2,v2 (ping-pong)
-template <int LD, int ST, int U, bool MATH>
-__global__ void adam_k(const float4* __restrict__ P, const float4* __restrict__ G, const float4* __restrict__ M,
-                       const float4* __restrict__ V, float4* __restrict__ Po, float4* __restrict__ Mo,
-                       float4* __restrict__ Vo, size_t n4, S s, int* flag) {
-  const size_t stride = (size_t)gridDim.x * blockDim.x;
+// one vector of work for pattern PAT at vector index j
+template <int PAT>
+__device__ __forceinline__ void work(const Ar& a, size_t j, bool& bad) {
+  if (PAT == 0) {  // copy
+    __stcs(a.out[0] + j, __ldcs(a.in[0] + j));
+  } else if (PAT == 1) {  // adam
+    float4 p = __ldcs(a.in[0] + j), g = __ldcs(a.in[1] + j), m = __ldcs(a.in[2] + j), v = __ldcs(a.in[3] + j), o;
+    o.x = adam1(p.x, g.x, m.x, v.x);
+    o.y = adam1(p.y, g.y, m.y, v.y);
+    o.z = adam1(p.z, g.z, m.z, v.z);
+    o.w = adam1(p.w, g.w, m.w, v.w);
+    bad |= !isfinite(o.x + o.y + o.z + o.w);
+    __stcs(a.out[0] + j, o);
+    __stcs(a.out[1] + j, m);
+    __stcs(a.out[2] + j, v);
+  } else if (PAT == 2) {  // nesterov solo: t, l, b -> t', b', l'
+    float4 t = __ldcs(a.in[0] + j), l = __ldcs(a.in[1] + j), b = __ldcs(a.in[2] + j), o;
+    o.x = nest1(t.x, __fsub_rn(t.x, l.x), b.x);
+    o.y = nest1(t.y, __fsub_rn(t.y, l.y), b.y);
+    o.z = nest1(t.z, __fsub_rn(t.z, l.z), b.z);
+    o.w = nest1(t.w, __fsub_rn(t.w, l.w), b.w);
+    __stcs(a.out[0] + j, o);
+    __stcs(a.out[1] + j, b);
+    __stcs(a.out[2] + j, o);
+  } else {  // pseudo-grad fp16: t, l -> 4 codes
+    float4 t = __ldcs(a.in[0] + j), l = __ldcs(a.in[1] + j);
+    __half2 h0 = __floats2half2_rn(t.x - l.x, t.y - l.y), h1 = __floats2half2_rn(t.z - l.z, t.w - l.w);
+    uint2 w = make_uint2(*reinterpret_cast<unsigned*>(&h0), *reinterpret_cast<unsigned*>(&h1));
+    __stcs(reinterpret_cast<uint2*>(a.out[0]) + j, w);
+  }
+}
+
+template <int PAT, int POL, int U>
+__global__ void __launch_bounds__(256) kern(Ar a, int* flag) {
   bool bad = false;
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride * U) {
-    float4 p[U], g[U], m[U], v[U];
+  if (POL == GS) {
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n4; i += stride * U) {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (i + u * stride < a.n4) work<PAT>(a, i + u * stride, bad);
+    }
+  } else if (POL == FULL) {
+    const size_t base = (size_t)blockIdx.x * blockDim.x * U + threadIdx.x;
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if (i + u * stride < n4) {
-        g[u] = ld4<LD>(G + i + u * stride);
-        p[u] = ld4<LD>(P + i + u * stride);
-        m[u] = ld4<LD>(M + i + u * stride);
-        v[u] = ld4<LD>(V + i + u * stride);
-      }
+      if (base + u * blockDim.x < a.n4) work<PAT>(a, base + u * blockDim.x, bad);
+  } else {
+    const size_t per = (a.n4 + gridDim.x - 1) / gridDim.x;
+    const size_t lo = blockIdx.x * per, hi = lo + per < a.n4 ? lo + per : a.n4;
+    for (size_t i = lo + threadIdx.x; i < hi; i += (size_t)blockDim.x * U) {
 #pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (i + u * stride < n4) {
-        float4 o;
-        if (MATH) {
-          o.x = adam1(p[u].x, g[u].x, m[u].x, v[u].x, s);
-          o.y = adam1(p[u].y, g[u].y, m[u].y, v[u].y, s);
-          o.z = adam1(p[u].z, g[u].z, m[u].z, v[u].z, s);
-          o.w = adam1(p[u].w, g[u].w, m[u].w, v[u].w, s);
-          bad |= !isfinite(o.x);
-        } else {
-          o = make_float4(p[u].x + g[u].x, p[u].y + g[u].y, p[u].z + g[u].z, p[u].w + g[u].w);
-        }
-        st4<ST>(Po + i + u * stride, o);
-        st4<ST>(Mo + i + u * stride, m[u]);
-        st4<ST>(Vo + i + u * stride, v[u]);
-      }
+      for (int u = 0; u < U; ++u)
+        if (i + u * blockDim.x < hi) work<PAT>(a, i + u * blockDim.x, bad);
+    }
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
-}
-
-template <typename K>
-int occ(K k, int threads) {
-  int b = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k, threads, 0));
-  return b;
 }
 
 int main(int argc, char** argv) {
@@ -127,71 +119,56 @@ int main(int argc, char** argv) {
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
   std::vector<float*> buf(7);
-  for (auto& b : buf) {
-    CK(cudaMalloc(&b, n * 4));
-    CK(cudaMemset(b, 0, n * 4));
+  for (int i = 0; i < 7; ++i) {
+    CK(cudaMalloc(&buf[i], n * 4));
+    fill<<<4096, 256>>>(buf[i], n, 1234u + i, i == 3 ? 0.0f : -1.0f, 1.0f);
   }
+  CK(cudaDeviceSynchronize());
   int* flag;
   CK(cudaMalloc(&flag, 4));
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
-  S s{0.9f, 0.95f, 1e-8f, 0.1f, 0.1f, 0.05f, 0.1f, 0.05f, 4e-4f, 1.0f / 65536.0f};
+  const double bytes[4] = {8.0, 28.0, 24.0, 10.0};
+  const char* pn[4] = {"copy", "adam", "nest", "pg16"};
 
-  auto timeit = [&](const char* name, double bytes, auto launch) {
-    for (int w = 0; w < 2; ++w) launch();
-    CK(cudaDeviceSynchronize());
-    const int reps = 8;
-    CK(cudaEventRecord(e0));
-    for (int r = 0; r < reps; ++r) launch();
-    CK(cudaEventRecord(e1));
-    CK(cudaEventSynchronize(e1));
-    float ms = 0;
-    CK(cudaEventElapsedTime(&ms, e0, e1));
-    ms /= reps;
-    std::printf("%-48s %8.3f ms  %8.1f GB/s\n", name, ms, bytes / (ms * 1e-3) / 1e9);
-  };
-
-#define COPY(LD, ST, U, T, PERSIST)                                                                   \
-  {                                                                                                   \
-    auto k = copy_k<LD, ST, U>;                                                                       \
-    const int grid = PERSIST ? sms * occ(k, T) : (int)((n4 / U + T - 1) / T);                         \
-    char nm[96];                                                                                      \
-    std::snprintf(nm, sizeof nm, "copy ld%d st%d U%d T%d %s", LD, ST, U, T, PERSIST ? "persist" : "full"); \
-    timeit(nm, 8.0 * n, [&] { k<<<grid, T>>>((const float4*)buf[0], (float4*)buf[1], n4); });      \
+#define RUN(PAT, POL, U, MULT)                                                                         \
+  {                                                                                                    \
+    auto k = kern<PAT, POL, U>;                                                                        \
+    int occ = 0;                                                                                       \
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 256, 0));                                \
+    int grid = POL == FULL ? (int)((n4 + 256 * U - 1) / (256 * U)) : sms * occ * MULT;                 \
+    Ar a;                                                                                              \
+    for (int i = 0; i < 4; ++i) a.in[i] = (const float4*)buf[i];                                       \
+    for (int i = 0; i < 3; ++i) a.out[i] = (float4*)buf[4 + i];                                        \
+    a.n4 = n4;                                                                                         \
+    for (int w = 0; w < 2; ++w) k<<<grid, 256>>>(a, flag);                                              \
+    CK(cudaDeviceSynchronize());                                                                       \
+    CK(cudaEventRecord(e0));                                                                           \
+    for (int r = 0; r < 8; ++r) k<<<grid, 256>>>(a, flag);                                              \
+    CK(cudaEventRecord(e1));                                                                           \
+    CK(cudaEventSynchronize(e1));                                                                      \
+    float ms = 0;                                                                                      \
+    CK(cudaEventElapsedTime(&ms, e0, e1));                                                             \
+    ms /= 8;                                                                                           \
+    std::printf("%-5s %-4s U%d x%d occ%d grid%-8d %8.3f ms %8.1f GB/s\n", pn[PAT],                     \
+                POL == GS ? "gs" : POL == FULL ? "full" : "blk", U, MULT, occ, grid, ms,               \
+                bytes[PAT] * n / (ms * 1e-3) / 1e9);                                                   \
   }
-  COPY(LD_DEF, ST_DEF, 1, 256, false)
-  COPY(LD_DEF, ST_DEF, 2, 256, true)
-  COPY(LD_CS, ST_CS, 2, 256, true)
-  COPY(LD_NC_NA, ST_DEF, 2, 256, true)
-  COPY(LD_CS, ST_CS, 4, 256, true)
-  COPY(LD_CS, ST_CS, 4, 512, true)
-  COPY(LD_NC_NA, ST_NA, 4, 256, true)
-
-#define ADAM(LD, ST, U, T, PERSIST, MATH)                                                               \
-  {                                                                                                     \
-    auto k = adam_k<LD, ST, U, MATH>;                                                                   \
-    const int grid = PERSIST ? sms * occ(k, T) : (int)((n4 / U + T - 1) / T);                          \
-    char nm[96];                                                                                        \
-    std::snprintf(nm, sizeof nm, "adam%s ld%d st%d U%d T%d %s", MATH ? "" : "-nomath", LD, ST, U, T,   \
-                  PERSIST ? "persist" : "full");                                                        \
-    timeit(nm, 28.0 * n, [&] {                                                                          \
-      k<<<grid, T>>>((const float4*)buf[0], (const float4*)buf[1], (const float4*)buf[2],               \
-                     (const float4*)buf[3], (float4*)buf[4], (float4*)buf[5], (float4*)buf[6], n4, s, flag); \
-    });                                                                                                 \
-  }
-  ADAM(LD_CS, ST_CS, 2, 256, true, true)
-  ADAM(LD_CS, ST_CS, 2, 256, true, false)
-  ADAM(LD_DEF, ST_DEF, 2, 256, true, true)
-  ADAM(LD_NC_NA, ST_DEF, 2, 256, true, true)
-  ADAM(LD_NC_NA, ST_NA, 2, 256, true, true)
-  ADAM(LD_CS, ST_CS, 1, 256, true, true)
-  ADAM(LD_CS, ST_CS, 4, 256, true, true)
-  ADAM(LD_CS, ST_CS, 2, 512, true, true)
-  ADAM(LD_CS, ST_CS, 2, 128, true, true)
-  ADAM(LD_CS, ST_CS, 2, 256, false, true)
-  ADAM(LD_CS, ST_DEF, 2, 256, true, true)
-  ADAM(LD_DEF, ST_CS, 2, 256, true, true)
-  ADAM(LD_LU, ST_CS, 2, 256, true, true)
+#define PATSET(P)    \
+  RUN(P, GS, 1, 1)   \
+  RUN(P, GS, 2, 1)   \
+  RUN(P, GS, 2, 2)   \
+  RUN(P, GS, 4, 1)   \
+  RUN(P, FULL, 1, 1) \
+  RUN(P, FULL, 2, 1) \
+  RUN(P, FULL, 4, 1) \
+  RUN(P, BLK, 1, 1)  \
+  RUN(P, BLK, 2, 1)  \
+  RUN(P, BLK, 2, 4)
+  PATSET(0)
+  PATSET(1)
+  PATSET(2)
+  PATSET(3)
   return 0;
 }
