@@ -84,6 +84,9 @@ struct dlc_engine {
   void* peer_dbar[kMaxK] = {};
   int* peer_flag[kMaxK] = {};
   std::vector<void*> ipc_opened;
+  // host-buffer path: copy streams and per-chunk events
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  std::vector<cudaEvent_t> chunk_ev;
 };
 
 namespace {
@@ -107,6 +110,22 @@ struct DeviceGuard {
 };
 
 void launched(const char* what) { DLC_LAUNCHED(what); }
+
+// Host <-> device chunk of the host-buffer outer step (64 MB of FP32).
+constexpr size_t kHostChunk = size_t(16) << 20;
+
+void ensure_copy_streams(dlc_engine* e) {
+  if (!e->h2d) DLC_CUDA(cudaStreamCreateWithFlags(&e->h2d, cudaStreamNonBlocking));
+  if (!e->d2h) DLC_CUDA(cudaStreamCreateWithFlags(&e->d2h, cudaStreamNonBlocking));
+}
+
+void ensure_chunk_events(dlc_engine* e, size_t count) {
+  while (e->chunk_ev.size() < count) {
+    cudaEvent_t ev;
+    DLC_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    e->chunk_ev.push_back(ev);
+  }
+}
 
 void harvest(dlc_engine* e) {
   if (e->pending.empty()) return;
@@ -221,7 +240,6 @@ void engine_inner(dlc_engine* e, const float* grad, int grad_is_scaled) {
   a.omb2 = 1.0f - e->hyper.beta2;
   a.pingpong = e->inner_mode == DLC_INNER_PINGPONG;
   phase_begin(e);
-  if (!a.pingpong) launch_unscale_check(g, e->st, &e->st->found_inf, e->n, e->stream);
   launch_adamw(a, e->stream);
   phase_end(e, DLC_PHASE_INNER);
   launched("adamw");
@@ -241,7 +259,7 @@ void reset_flags(dlc_engine* e) {
 // K2 from an explicit theta_local pair (the engine's own, or a staging buffer).
 void pseudo_grad(dlc_engine* e, Pair tl) {
   phase_begin(e);
-  launch_pseudo_grad(tt_pair(e), tl, e->st, e->send, e->prec, &e->st->delta_nonfinite, e->n, e->stream);
+  launch_pseudo_grad(tt_pair(e), tl, e->st, e->send, e->prec, &e->st->delta_nonfinite, 0, e->n, e->stream);
   phase_end(e, DLC_PHASE_PSEUDO);
   launched("pseudo_grad");
 }
@@ -561,6 +579,12 @@ int dlc_engine_destroy(dlc_engine* e) {
   return guard([&] {
     DeviceGuard dg(e->device);
     if (e->stream) cudaStreamSynchronize(e->stream);
+    if (e->p2p_bound) {
+      // peers may still be reading this engine's slot / send buffer: wait for
+      // the whole fleet (engines are destroyed collectively, before their collective)
+      fleet_barrier(e, const_cast<dlc_collective*>(e->p2p_bound));
+      cudaStreamSynchronize(e->stream);
+    }
     p2p_unbind(e);
     for (void* p : e->allocs) cudaFree(p);
     for (const auto& mk : e->pending) {
@@ -571,6 +595,9 @@ int dlc_engine_destroy(dlc_engine* e) {
     if (e->tab) cudaFree(e->tab);
     if (e->ev0) cudaEventDestroy(e->ev0);
     if (e->ev1) cudaEventDestroy(e->ev1);
+    for (cudaEvent_t ev : e->chunk_ev) cudaEventDestroy(ev);
+    if (e->h2d) cudaStreamDestroy(e->h2d);
+    if (e->d2h) cudaStreamDestroy(e->d2h);
     if (e->stream) cudaStreamDestroy(e->stream);
     delete e;
   });
@@ -749,14 +776,52 @@ int dlc_engine_outer_step_host(dlc_engine* e, dlc_collective* c, const float* ho
     if (c && c->kind == 0) c = nullptr;
     check_collective(e, c);
     DeviceGuard dg(e->device);
-    // theta_local arrives in the staging buffer; K4 then refreshes the engine's
+    // theta_local arrives chunk by chunk in the staging buffer (copy stream);
+    // each chunk's kernel starts as soon as its bytes land, and for a single
+    // worker each finished chunk of the new theta_t streams back on a second
+    // copy stream, so H2D, compute and D2H overlap.  K4 refreshes the engine's
     // own theta_local from the new theta_t.
-    DLC_CUDA(cudaMemcpyAsync(e->grad, host_theta_local, e->n * sizeof(float), cudaMemcpyHostToDevice, e->stream));
-    outer_round(e, c, e->grad, nullptr);
-    const DevState s = read_state(e);  // which theta_t buffer is live after the step
-    DLC_CUDA(cudaMemcpyAsync(host_theta_t, e->theta_t[s.ocur], e->n * sizeof(float), cudaMemcpyDeviceToHost,
-                             e->stream));
-    DLC_CUDA(cudaStreamSynchronize(e->stream));
+    ensure_copy_streams(e);
+    const DevState s0 = read_state(e);
+    const size_t n = e->n, C = kHostChunk, nch = (n + C - 1) / C;
+    ensure_chunk_events(e, 2 * nch + 1);
+    reset_flags(e);
+    DLC_CUDA(cudaEventRecord(e->chunk_ev[2 * nch], e->stream));  // staging buffer free to overwrite
+    DLC_CUDA(cudaStreamWaitEvent(e->h2d, e->chunk_ev[2 * nch], 0));
+    float* staged = e->grad;
+    for (size_t ci = 0; ci < nch; ++ci) {
+      const size_t off = ci * C, len = std::min(C, n - off);
+      DLC_CUDA(cudaMemcpyAsync(staged + off, host_theta_local + off, len * sizeof(float), cudaMemcpyHostToDevice,
+                               e->h2d));
+      DLC_CUDA(cudaEventRecord(e->chunk_ev[2 * ci], e->h2d));
+      DLC_CUDA(cudaStreamWaitEvent(e->stream, e->chunk_ev[2 * ci], 0));
+      if (e->k == 1) {
+        launch_outer_solo_chunk(tt_pair(e), buf_pair(e), local_pair(e), staged, e->prec, e->st, e->hyper.outer_lr,
+                                e->hyper.outer_momentum, off, len, e->stream);
+        launched("outer_solo_chunk");
+        DLC_CUDA(cudaEventRecord(e->chunk_ev[2 * ci + 1], e->stream));
+        DLC_CUDA(cudaStreamWaitEvent(e->d2h, e->chunk_ev[2 * ci + 1], 0));
+        // speculative: the idle theta_t buffer holds the new weights if the step applies
+        DLC_CUDA(cudaMemcpyAsync(host_theta_t + off, e->theta_t[s0.ocur ^ 1] + off, len * sizeof(float),
+                                 cudaMemcpyDeviceToHost, e->d2h));
+      } else {
+        launch_pseudo_grad(tt_pair(e), Pair{{staged, staged}}, e->st, e->send, e->prec, &e->st->delta_nonfinite,
+                           off, len, e->stream);
+        launched("pseudo_grad_chunk");
+      }
+    }
+    if (e->k == 1) {
+      launch_outer_solo_finish(tt_pair(e), local_pair(e), e->st, n, e->stream);
+      launched("outer_solo_finish");
+    } else {
+      outer_collective(e, c, nullptr);
+      DLC_CUDA(cudaMemcpyAsync(host_theta_t, e->theta_t[0], n * sizeof(float), cudaMemcpyDeviceToHost, e->stream));
+    }
+    DLC_CUDA(cudaStreamSynchronize(e->h2d));
+    DLC_CUDA(cudaStreamSynchronize(e->d2h));
+    const DevState s1 = read_state(e);
+    if (e->k == 1 && !s1.last_applied)  // skipped: theta_t did not move
+      DLC_CUDA(cudaMemcpy(host_theta_t, e->theta_t[s1.ocur], n * sizeof(float), cudaMemcpyDeviceToHost));
     outer_result(e, result);
   });
 }
@@ -787,7 +852,8 @@ int dlc_engines_outer_step_local(dlc_engine* const* engines, size_t k, dlc_outer
     PtrList in{};
     for (size_t j = 0; j < k; ++j) {
       dlc_engine* e = engines[j];
-      launch_pseudo_grad(tt_pair(e), local_pair(e), e->st, e->send, e->prec, &e->st->delta_nonfinite, e->n, s);
+      launch_pseudo_grad(tt_pair(e), local_pair(e), e->st, e->send, e->prec, &e->st->delta_nonfinite, 0, e->n,
+                         s);
       in.ptr[j] = e->send;
     }
     DLC_CUDA(cudaMemsetAsync(e0->flags, 0, kMaxK * sizeof(int), s));

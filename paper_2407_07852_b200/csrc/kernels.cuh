@@ -9,8 +9,12 @@
 //   K4  nesterov    finite-gated outer Nesterov + theta_local refresh
 //                   (engine.cpp:128-146 -> optim.cpp:95-115)
 //
-// All kernels are persistent grid-stride loops over 128-bit vectors with a
-// scalar tail; grids are sized to (#SM x resident CTAs) once per kernel.
+// Work distribution (measured, profiles/r1_tune_stream_v2.log): one CTA per
+// 256*U consecutive 128-bit vectors, launched in address order, so the CTAs
+// resident at any instant stream through one compact window of every buffer.
+// That beats a persistent grid-stride loop by 12-18% on these shapes (K1
+// 7.0 vs 5.9 TB/s).  Global decisions that need every element (overflow skip,
+// non-finite outer step) are taken by a one-CTA finalize kernel that follows.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -24,7 +28,7 @@ constexpr int kMaxK = 32;  // largest worker count a single fold launch takes
 // Device-resident engine scalars (EngineState, engine.hpp:48-56; AdamWState
 // step_count, optim.hpp:20; LossScaler, optim.hpp:52-56).  Kept on the GPU so
 // the inner loop never waits on the host: the overflow decision, step counter
-// and loss scale are all updated by the last CTA of K1.
+// and loss scale are all updated by the K1 finalize kernel.
 struct DevState {
   uint64_t step_count;      // applied AdamW steps
   uint64_t inner_step;      // batches consumed (data cursor, always advances)
@@ -37,9 +41,9 @@ struct DevState {
   float last_lr;            // lr of the last inner step (0 when skipped)
   int cur;                  // live buffer of the p/m/v ping-pong pair
   int found_inf;            // K1 scratch: OR of !isfinite(g / scale)
-  unsigned done_blocks;     // K1 last-CTA counter
+  unsigned reserved;
   int last_overflow;        // InnerStepResult::overflow_skipped
-  int delta_nonfinite;      // K2: non-finite delta (or FP16 encode overflow)
+  int delta_nonfinite;      // K2 / solo: non-finite delta (or FP16 encode overflow)
   int last_applied;         // OuterStepResult::applied
   int ocur;                 // live buffer of the theta_t / momentum pair (solo fused outer step)
   int pad;
@@ -69,7 +73,7 @@ struct PtrList {
   const void* ptr[kMaxK];
 };
 
-// The two buffers of a ping-pong pair; DevState::cur selects the live one.
+// The two buffers of a ping-pong pair; DevState::cur / ocur selects the live one.
 struct Pair {
   float* ptr[2];
 };
@@ -77,18 +81,17 @@ struct Pair {
 int num_sms();
 
 // K1 --------------------------------------------------------------------------
+// PINGPONG: one pass (reads [cur], writes [cur^1]) + finalize.  INPLACE: an
+// overflow pre-pass over g, the gated in-place update, finalize.
 void launch_adamw(const AdamWArgs& a, cudaStream_t s);
-// In-place mode's first pass: found_inf = OR !isfinite(g * (1/scale)).
-void launch_unscale_check(const float* g, const DevState* st_scale, int* flag, size_t n,
-                          cudaStream_t s);
 void launch_adamw_plain(const float* p, const float* g, float* m, float* v, float* out,
                         size_t n, const AdamWPlain& a, cudaStream_t s);
 
 // K2 --------------------------------------------------------------------------
-// precision 0: out is float*, 1: out is uint16_t* (binary16 codes).
-void launch_pseudo_grad(Pair theta_t, Pair theta_local,
-                        const DevState* st, void* out, int precision, int* flag, size_t n,
-                        cudaStream_t s);
+// Elements [off, off + len) of delta = theta_t - theta_local into `out`
+// (float* for precision 0, binary16 codes for 1); non-finite OR into *flag.
+void launch_pseudo_grad(Pair theta_t, Pair theta_local, const DevState* st, void* out,
+                        int precision, int* flag, size_t off, size_t len, cudaStream_t s);
 
 // K3 --------------------------------------------------------------------------
 // in_kind 0: FP32 contributions, 1: FP16 codes, 2: FP32 contributions that go
@@ -101,23 +104,29 @@ void launch_fold(const PtrList& in, int k, int in_kind, void* out, int out_kind,
 void launch_nesterov_outer(Pair theta_t, Pair buf, Pair theta_local,
                            const void* dbar, int precision, const int* flags, int nflags,
                            DevState* st, float lr, float mu, size_t n, cudaStream_t s);
-// K2+K4 fused for a single worker (SoloCollective, reduce.cpp:113-126): one
-// HBM pass reading theta_t[ocur], buf[ocur], theta_local and writing
-// theta_t[ocur^1], buf[ocur^1], theta_local (24 B/param).  The non-finite gate
-// is decided by the last CTA (ocur flips only when applied); a following
-// recovery kernel restores theta_local := theta_t when the step was skipped
-// (engine.cpp:136-144).  `src` (nullable) overrides the theta_local input.
-void launch_outer_solo_fused(Pair theta_t, Pair buf, Pair theta_local, const float* src,
-                             int precision, DevState* st, float lr, float mu, size_t n,
-                             cudaStream_t s);
-void launch_nesterov_plain(const float* p, const float* g, float* buf, float* out, size_t n,
-                           float lr, float mu, cudaStream_t s);
 // K4 reading the mean in place from its K owners over NVLink (DLC_MODE_P2P):
 // element i lives in slots.ptr[i / S][i % S]; owner q's non-finite flag at
-// flags.ptr[q].  Same arithmetic and skip gate as launch_nesterov_outer.
+// flags.ptr[q].  Consecutive CTAs cycle through the owners so NVLink reads and
+// local HBM traffic overlap.  Same arithmetic and skip gate as above.
 void launch_nesterov_outer_p2p(Pair theta_t, Pair buf, Pair theta_local, const PtrList& slots,
                                const PtrList& flags, int k, size_t S, int precision, DevState* st,
                                float lr, float mu, size_t n, cudaStream_t s);
+// K2+K4 fused for a single worker (SoloCollective, reduce.cpp:113-126): one
+// HBM pass reading theta_t[ocur], buf[ocur], theta_local and writing
+// theta_t[ocur^1], buf[ocur^1], theta_local (24 B/param), then a finish kernel
+// that flips `ocur` only when every delta was finite and otherwise restores
+// theta_local := theta_t (engine.cpp:136-144).  `src` (nullable) overrides the
+// theta_local input.  The chunk / finish split lets host copies overlap.
+void launch_outer_solo_fused(Pair theta_t, Pair buf, Pair theta_local, const float* src,
+                             int precision, DevState* st, float lr, float mu, size_t n,
+                             cudaStream_t s);
+void launch_outer_solo_chunk(Pair theta_t, Pair buf, Pair theta_local, const float* src,
+                             int precision, DevState* st, float lr, float mu, size_t off,
+                             size_t len, cudaStream_t s);
+void launch_outer_solo_finish(Pair theta_t, Pair theta_local, DevState* st, size_t n,
+                              cudaStream_t s);
+void launch_nesterov_plain(const float* p, const float* g, float* buf, float* out, size_t n,
+                           float lr, float mu, cudaStream_t s);
 
 // elementwise helpers -----------------------------------------------------------
 void launch_axpy(float alpha, const float* x, const float* y, float* out, size_t n,

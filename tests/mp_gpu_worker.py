@@ -90,6 +90,25 @@ def main():
                                      f"{float(np.max(err / tol)):.3f}")
                 e1.close()
             e.close()
+        # e2e host-buffer outer step (dlc_engine_outer_step_host) vs the oracle's outer round
+        for prec in (D.FP32, D.FP16):
+            n2 = 20_011
+            th = O.rng_fill(5, "theta", 0, n2, -1, 1)
+            locs = [(th - O.rng_fill(5, "local", j, n2, -1e-3, 1e-3)).astype(np.float32) for j in range(k)]
+            e2 = D.DilocoEngine(D.DilocoConfig(1, k, prec, 1), D.OptimHyperparams(), n2, r.local)
+            e2.upload(D.THETA_T, th)
+            out_t = np.empty(n2, np.float32)
+            res = e2.outer_step_host(coll, locs[r.rank], out_t)
+            assert res.applied
+            ws = DR.make_workers(th, k, hyper)
+            for j, w in enumerate(ws):
+                w.theta_local = locs[j].copy()
+            DR.outer_round(port, ws, prec, hyper)
+            if mode != D.MODE_ALLREDUCE:
+                assert np.array_equal(bits(out_t), bits(ws[r.rank].theta_t)), (mode_name, prec)
+            else:
+                assert np.max(np.abs(out_t - ws[r.rank].theta_t)) <= 1e-3
+            e2.close()
         # host-buffer plugin call (Collective::all_reduce_avg) vs reduce_average in rank order
         for prec in (D.FP32, D.FP16):
             deltas = [O.rng_fill(9, "delta", j, 10_007, -1, 1) for j in range(k)]

@@ -401,3 +401,33 @@ def test_solo_collective_host_plugin(golden):
         out, rep = c.all_reduce_avg(z["in_k1"][0], prec, outer_epoch=4)
         assert same(out, z[f"out_k1_p{prec}"])
         assert rep.contributors == 1 and rep.outer_epoch == 4 and rep.data_bytes_sent == 0
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+def test_outer_step_host_buffers_chunked(port, prec):
+    """dlc_engine_outer_step_host (the e2e path): chunked H2D / fused solo step / D2H,
+    bitwise vs the oracle's outer round, including a skipped (non-finite) step."""
+    n = 3 * (16 << 20) + 1001  # several 64 MB chunks plus a ragged tail
+    hyper = DR.Hyper()
+    e = D.DilocoEngine(D.DilocoConfig(1, 1, prec, 1), D.OptimHyperparams(), n)
+    e.rng_fill(A.THETA_T, 4242, "theta", 0, -0.05, 0.05)
+    theta0 = e.download(A.THETA_T)
+    loc = (theta0 - O.rng_fill(4242, "local", 0, n, -1e-3, 1e-3)).astype(np.float32)
+    out = np.empty(n, np.float32)
+    r = e.outer_step_host(None, loc, out)
+    assert r.applied
+    w = DR.make_workers(theta0, 1, hyper)[0]
+    w.theta_local = loc.copy()
+    DR.outer_round(port, [w], prec, hyper)
+    assert np.array_equal(bits(out), bits(w.theta_t))
+    assert np.array_equal(bits(e.download(A.THETA_LOCAL)), bits(w.theta_t))
+    assert np.array_equal(bits(e.download(A.MOMENTUM)), bits(w.buf))
+    # second step, non-finite in the last chunk: skipped, theta_t returned unchanged
+    bad = loc.copy()
+    bad[n - 7] = np.nan
+    r = e.outer_step_host(None, bad, out)
+    assert not r.applied and r.outer_epoch == 2
+    assert np.array_equal(bits(out), bits(w.theta_t))
+    assert np.array_equal(bits(e.download(A.THETA_LOCAL)), bits(w.theta_t))
+    assert np.array_equal(bits(e.download(A.THETA_T)), bits(w.theta_t))
+    e.close()
