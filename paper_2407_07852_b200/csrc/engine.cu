@@ -74,19 +74,20 @@ struct dlc_engine {
   double phase_ms[4] = {0, 0, 0, 0};
   uint64_t phase_n[4] = {0, 0, 0, 0};
   cudaEvent_t open_ev = nullptr;
-  // DLC_MODE_P2P: my owner slot / flag, and every rank's send, slot and flag
-  // mapped into this process through CUDA IPC (own entries are local).
-  void* dbar = nullptr;
-  int* pflag = nullptr;
+  // DLC_MODE_P2P: every rank's send buffer, gather buffer and flag array mapped
+  // into this process through CUDA IPC (own entries are local).
   int* barrier_buf = nullptr;
   const dlc_collective* p2p_bound = nullptr;
   void* peer_send[kMaxK] = {};
-  void* peer_dbar[kMaxK] = {};
-  int* peer_flag[kMaxK] = {};
+  void* peer_gather[kMaxK] = {};
+  int* peer_flags[kMaxK] = {};
   std::vector<void*> ipc_opened;
   // host-buffer path: copy streams and per-chunk events
   cudaStream_t h2d = nullptr, d2h = nullptr;
   std::vector<cudaEvent_t> chunk_ev;
+  // pipelined P2P: high-priority stream for barriers + owner folds, per-piece events
+  cudaStream_t cstream = nullptr;
+  std::vector<cudaEvent_t> piece_ev;
 };
 
 namespace {
@@ -113,6 +114,8 @@ void launched(const char* what) { DLC_LAUNCHED(what); }
 
 // Host <-> device chunk of the host-buffer outer step (64 MB of FP32).
 constexpr size_t kHostChunk = size_t(16) << 20;
+// Pieces of the pipelined P2P outer step (DLC_MODE_P2P).
+constexpr size_t kP2PPieces = 4;
 
 void ensure_copy_streams(dlc_engine* e) {
   if (!e->h2d) DLC_CUDA(cudaStreamCreateWithFlags(&e->h2d, cudaStreamNonBlocking));
@@ -291,12 +294,12 @@ void p2p_bind(dlc_engine* e, dlc_collective* c) {
   p2p_unbind(e);
   const int K = (int)e->k, r = c->rank;
   struct Handles {
-    cudaIpcMemHandle_t send, dbar, flag;
+    cudaIpcMemHandle_t send, gather, flags;
   };
   Handles mine;
   DLC_CUDA(cudaIpcGetMemHandle(&mine.send, e->send));
-  DLC_CUDA(cudaIpcGetMemHandle(&mine.dbar, e->dbar));
-  DLC_CUDA(cudaIpcGetMemHandle(&mine.flag, e->pflag));
+  DLC_CUDA(cudaIpcGetMemHandle(&mine.gather, e->gather));
+  DLC_CUDA(cudaIpcGetMemHandle(&mine.flags, e->flags));
   const size_t sz = sizeof(Handles);
   char* dbuf = nullptr;
   DLC_CUDA(cudaMalloc(&dbuf, K * sz));
@@ -314,23 +317,23 @@ void p2p_bind(dlc_engine* e, dlc_collective* c) {
   for (int j = 0; j < K; ++j) {
     if (j == r) {
       e->peer_send[j] = e->send;
-      e->peer_dbar[j] = e->dbar;
-      e->peer_flag[j] = e->pflag;
+      e->peer_gather[j] = e->gather;
+      e->peer_flags[j] = e->flags;
       continue;
     }
     void* ps = nullptr;
-    void* pd = nullptr;
+    void* pg = nullptr;
     void* pf = nullptr;
     const char* what = "cudaIpcOpenMemHandle (DLC_MODE_P2P needs one process per GPU with NVLink peer access)";
     check_cuda(cudaIpcOpenMemHandle(&ps, all[j].send, cudaIpcMemLazyEnablePeerAccess), what);
     e->ipc_opened.push_back(ps);
-    check_cuda(cudaIpcOpenMemHandle(&pd, all[j].dbar, cudaIpcMemLazyEnablePeerAccess), what);
-    e->ipc_opened.push_back(pd);
-    check_cuda(cudaIpcOpenMemHandle(&pf, all[j].flag, cudaIpcMemLazyEnablePeerAccess), what);
+    check_cuda(cudaIpcOpenMemHandle(&pg, all[j].gather, cudaIpcMemLazyEnablePeerAccess), what);
+    e->ipc_opened.push_back(pg);
+    check_cuda(cudaIpcOpenMemHandle(&pf, all[j].flags, cudaIpcMemLazyEnablePeerAccess), what);
     e->ipc_opened.push_back(pf);
     e->peer_send[j] = ps;
-    e->peer_dbar[j] = pd;
-    e->peer_flag[j] = (int*)pf;
+    e->peer_gather[j] = pg;
+    e->peer_flags[j] = (int*)pf;
   }
   e->p2p_bound = c;
 }
@@ -352,33 +355,6 @@ void outer_collective(dlc_engine* e, dlc_collective* c, dlc_reduce_report* rep) 
   const int r = c->rank;
   if (rep) DLC_CUDA(cudaEventRecord(e->ev0, e->stream));
   phase_begin(e);
-  if (c->mode == DLC_MODE_P2P) {
-    p2p_bind(e, c);
-    // (1) every rank's K2 is done, and every peer has finished reading my slot
-    // and flag in its previous K4, so both may be rewritten.
-    fleet_barrier(e, c);
-    DLC_CUDA(cudaMemsetAsync(e->pflag, 0, sizeof(int), e->stream));
-    // owner fold of slot r straight out of every rank's send buffer, rank order
-    PtrList in{};
-    for (size_t j = 0; j < K; ++j) in.ptr[j] = static_cast<char*>(e->peer_send[j]) + r * S * w;
-    launch_fold(in, (int)K, e->prec, e->dbar, e->prec, e->pflag, S, e->stream);
-    launched("fold_p2p");
-    // (2) every owner slot and flag is final.
-    fleet_barrier(e, c);
-    phase_end(e, DLC_PHASE_COLLECTIVE);
-    if (rep) DLC_CUDA(cudaEventRecord(e->ev1, e->stream));
-    PtrList slots{}, fl{};
-    for (size_t q = 0; q < K; ++q) {
-      slots.ptr[q] = e->peer_dbar[q];
-      fl.ptr[q] = e->peer_flag[q];
-    }
-    phase_begin(e);
-    launch_nesterov_outer_p2p(tt_pair(e), buf_pair(e), local_pair(e), slots, fl, (int)K, S, e->prec, e->st,
-                              e->hyper.outer_lr, e->hyper.outer_momentum, e->n, e->stream);
-    phase_end(e, DLC_PHASE_OUTER);
-    launched("nesterov_outer_p2p");
-    return;
-  }
   if (c->mode == DLC_MODE_ORDERED) {
     char* recv = static_cast<char*>(e->recv);
     char* gather = static_cast<char*>(e->gather);
@@ -416,6 +392,118 @@ void outer_collective(dlc_engine* e, dlc_collective* c, dlc_reduce_report* rep) 
   }
 }
 
+// DLC_MODE_P2P, software-pipelined over kP2PPieces pieces (kernels.cuh):
+//   main stream : K2(0..P-1), then K4(p) as soon as fold(p) is final, finish
+//   cstream     : B0, fold(0), B1, fold(1), ..., fold(P-1), B_P   (high priority)
+// where B_p is a 4-byte NCCL all-reduce: B_0 orders every rank's K2(0) (and
+// its previous step's finish) before any fold; B_{p+1} orders every fold(p)
+// and every K2(p+1) before the K4(p) that reads the owners' slots.  NVLink
+// traffic of fold(p) overlaps the HBM traffic of K2(p+1) and K4(p-1).
+// With host buffers (`hsrc`/`hdst`), piece p is also copied in before K2(p) and
+// its new theta_t copied out after K4(p), overlapping PCIe both ways.
+void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc_reduce_report* rep,
+                         const float* hsrc, float* hdst, int oc_host) {
+  p2p_bind(e, c);
+  if (!e->cstream) {
+    int lo = 0, hi = 0;
+    DLC_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    DLC_CUDA(cudaStreamCreateWithPriority(&e->cstream, cudaStreamNonBlocking, hi));
+  }
+  const size_t P = kP2PPieces;
+  while (e->piece_ev.size() < 4 * P + 2) {
+    cudaEvent_t ev;
+    DLC_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    e->piece_ev.push_back(ev);
+  }
+  cudaEvent_t* evK2 = e->piece_ev.data();
+  cudaEvent_t* evF = evK2 + P;
+  cudaEvent_t* evH = evF + P;
+  cudaEvent_t* evK4 = evH + P;
+  cudaEvent_t evStart = evK4[P];
+  const size_t K = e->k, S = e->S, Sp = S / P, w = elem_width(e->prec), n = e->n;
+  const int r = c->rank;
+  float* s = const_cast<float*>(src);
+  const Pair tl = s ? Pair{{s, s}} : local_pair(e);
+  const float lr = e->hyper.outer_lr, mu = e->hyper.outer_momentum;
+  auto rows = [&](size_t p, auto&& fn) {  // piece p of every owner slot, clipped to n
+    for (size_t q = 0; q < K; ++q) {
+      const size_t lo = q * S + p * Sp;
+      if (lo >= n) break;
+      fn(lo, std::min(Sp, n - lo));
+    }
+  };
+  if (rep) DLC_CUDA(cudaEventRecord(e->ev0, e->stream));
+  DLC_CUDA(cudaEventRecord(evStart, e->stream));
+  if (hsrc) {
+    ensure_copy_streams(e);
+    DLC_CUDA(cudaStreamWaitEvent(e->h2d, evStart, 0));  // staging buffer free
+  }
+  phase_begin(e);
+  for (size_t p = 0; p < P; ++p) {
+    if (hsrc) {
+      rows(p, [&](size_t lo, size_t len) {
+        DLC_CUDA(cudaMemcpyAsync(s + lo, hsrc + lo, len * sizeof(float), cudaMemcpyHostToDevice, e->h2d));
+      });
+      DLC_CUDA(cudaEventRecord(evH[p], e->h2d));
+      DLC_CUDA(cudaStreamWaitEvent(e->stream, evH[p], 0));
+    }
+    launch_pseudo_grad_piece(tt_pair(e), tl, e->st, e->send, e->prec, (int)K, S, p * Sp, Sp, n, e->stream);
+    DLC_CUDA(cudaEventRecord(evK2[p], e->stream));
+  }
+  launched("pseudo_grad_piece");
+  phase_end(e, DLC_PHASE_PSEUDO);
+  // collective stream: barriers + owner folds straight out of every rank's send buffer
+  DLC_CUDA(cudaStreamWaitEvent(e->cstream, evStart, 0));
+  cudaEvent_t c0 = pooled_event(e), c1 = pooled_event(e);
+  DLC_CUDA(cudaEventRecord(c0, e->cstream));
+  DLC_CUDA(cudaStreamWaitEvent(e->cstream, evK2[0], 0));
+  DLC_NCCL(ncclAllReduce(e->barrier_buf, e->barrier_buf, 1, ncclInt32, ncclSum, c->comm, e->cstream));
+  PtrList pflags{};  // my flag slot r in every rank's flag array (reset by each rank before its K2)
+  for (size_t q = 0; q < K; ++q) pflags.ptr[q] = e->peer_flags[q] + r;
+  for (size_t p = 0; p < P; ++p) {
+    // pull piece p of slot r from every rank (rank order), push the mean into
+    // slot r of every rank's gather buffer
+    PtrList in{}, outs{};
+    for (size_t j = 0; j < K; ++j) in.ptr[j] = static_cast<char*>(e->peer_send[j]) + (r * S + p * Sp) * w;
+    for (size_t q = 0; q < K; ++q) outs.ptr[q] = static_cast<char*>(e->peer_gather[q]) + (r * S + p * Sp) * w;
+    launch_fold_push(in, (int)K, e->prec, outs, (int)K, pflags, Sp, e->cstream);
+    if (p + 1 < P) DLC_CUDA(cudaStreamWaitEvent(e->cstream, evK2[p + 1], 0));
+    DLC_NCCL(ncclAllReduce(e->barrier_buf, e->barrier_buf, 1, ncclInt32, ncclSum, c->comm, e->cstream));
+    DLC_CUDA(cudaEventRecord(evF[p], e->cstream));
+  }
+  launched("fold_p2p");
+  DLC_CUDA(cudaEventRecord(c1, e->cstream));
+  if (e->timing) e->pending.push_back({DLC_PHASE_COLLECTIVE, c0, c1});
+  else {
+    e->pool.push_back(c0);
+    e->pool.push_back(c1);
+  }
+  if (rep) DLC_CUDA(cudaEventRecord(e->ev1, e->cstream));
+  // K4 pieces, speculative into the idle theta_t / momentum buffers
+  PtrList slots{}, fl{};  // every owner's mean and flag, now local
+  for (size_t q = 0; q < K; ++q) {
+    slots.ptr[q] = static_cast<char*>(e->gather) + q * S * w;
+    fl.ptr[q] = e->flags + q;
+  }
+  phase_begin(e);
+  for (size_t p = 0; p < P; ++p) {
+    DLC_CUDA(cudaStreamWaitEvent(e->stream, evF[p], 0));
+    launch_nesterov_p2p_piece(tt_pair(e), buf_pair(e), local_pair(e), slots, (int)K, S, p * Sp, Sp, e->prec, e->st,
+                              lr, mu, n, e->stream);
+    if (hdst) {
+      DLC_CUDA(cudaEventRecord(evK4[p], e->stream));
+      DLC_CUDA(cudaStreamWaitEvent(e->d2h, evK4[p], 0));
+      rows(p, [&](size_t lo, size_t len) {
+        DLC_CUDA(cudaMemcpyAsync(hdst + lo, e->theta_t[oc_host ^ 1] + lo, len * sizeof(float),
+                                 cudaMemcpyDeviceToHost, e->d2h));
+      });
+    }
+  }
+  launch_p2p_finish(tt_pair(e), local_pair(e), fl, (int)K, e->st, n, e->stream);
+  phase_end(e, DLC_PHASE_OUTER);
+  launched("nesterov_p2p_piece");
+}
+
 void outer_round(dlc_engine* e, dlc_collective* c, const float* src, dlc_reduce_report* rep) {
   reset_flags(e);
   if (e->k == 1) {
@@ -424,6 +512,10 @@ void outer_round(dlc_engine* e, dlc_collective* c, const float* src, dlc_reduce_
                             e->hyper.outer_momentum, e->n, e->stream);
     phase_end(e, DLC_PHASE_OUTER);
     launched("outer_solo");
+    return;
+  }
+  if (c->mode == DLC_MODE_P2P) {
+    outer_p2p_pipelined(e, c, src, rep, nullptr, nullptr, 0);
     return;
   }
   float* s = const_cast<float*>(src);
@@ -512,19 +604,18 @@ int dlc_engine_create(const dlc_config* cfg, const dlc_hyperparams* hyper, size_
     e->n = n;
     e->k = cfg->num_workers_k;
     e->prec = cfg->reduce_precision;
-    e->S = (((n + e->k - 1) / e->k) + 63) / 64 * 64;
+    // owner slot: a multiple of 64 elements per P2P piece
+    const size_t quantum = 64 * kP2PPieces;
+    e->S = (((n + e->k - 1) / e->k) + quantum - 1) / quantum * quantum;
     DLC_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
     DLC_CUDA(cudaEventCreate(&e->ev0));
     DLC_CUDA(cudaEventCreate(&e->ev1));
     const size_t vb = n * sizeof(float);
-    e->theta_t[0] = (float*)dalloc(e, vb);
-    e->buf[0] = (float*)dalloc(e, vb);
-    if (e->k == 1) {  // fused solo outer step: theta_t / momentum ping-pong
-      e->theta_t[1] = (float*)dalloc(e, vb);
-      e->buf[1] = (float*)dalloc(e, vb);
-    } else {
-      e->theta_t[1] = e->theta_t[0];
-      e->buf[1] = e->buf[0];
+    // theta_t / momentum ping-pong: the fused solo step (K = 1) and the pipelined
+    // P2P step (K > 1) write the new values speculatively into the idle buffer
+    for (int i = 0; i < 2; ++i) {
+      e->theta_t[i] = (float*)dalloc(e, vb);
+      e->buf[i] = (float*)dalloc(e, vb);
     }
     const int pairs = inner_mode == DLC_INNER_PINGPONG ? 2 : 1;
     for (int i = 0; i < pairs; ++i) {
@@ -545,10 +636,7 @@ int dlc_engine_create(const dlc_config* cfg, const dlc_hyperparams* hyper, size_
       e->recv = dalloc(e, pb);
       e->gather = dalloc(e, pb);
       DLC_CUDA(cudaMemsetAsync(e->gather, 0, pb, e->stream));
-      e->dbar = dalloc(e, e->S * elem_width(e->prec));
-      e->pflag = (int*)dalloc(e, 256);
       e->barrier_buf = (int*)dalloc(e, 256);
-      DLC_CUDA(cudaMemsetAsync(e->pflag, 0, 256, e->stream));
     }
     e->flags = (int*)dalloc(e, kMaxK * sizeof(int));
     e->st = (DevState*)dalloc(e, sizeof(DevState));
@@ -783,6 +871,17 @@ int dlc_engine_outer_step_host(dlc_engine* e, dlc_collective* c, const float* ho
     // own theta_local from the new theta_t.
     ensure_copy_streams(e);
     const DevState s0 = read_state(e);
+    if (e->k > 1 && c->mode == DLC_MODE_P2P) {  // piece-pipelined H2D / step / D2H
+      reset_flags(e);
+      outer_p2p_pipelined(e, c, e->grad, nullptr, host_theta_local, host_theta_t, s0.ocur);
+      DLC_CUDA(cudaStreamSynchronize(e->h2d));
+      DLC_CUDA(cudaStreamSynchronize(e->d2h));
+      const DevState s1 = read_state(e);
+      if (!s1.last_applied)  // skipped: theta_t did not move
+        DLC_CUDA(cudaMemcpy(host_theta_t, e->theta_t[s1.ocur], e->n * sizeof(float), cudaMemcpyDeviceToHost));
+      outer_result(e, result);
+      return;
+    }
     const size_t n = e->n, C = kHostChunk, nch = (n + C - 1) / C;
     ensure_chunk_events(e, 2 * nch + 1);
     reset_flags(e);
@@ -814,8 +913,9 @@ int dlc_engine_outer_step_host(dlc_engine* e, dlc_collective* c, const float* ho
       launch_outer_solo_finish(tt_pair(e), local_pair(e), e->st, n, e->stream);
       launched("outer_solo_finish");
     } else {
-      outer_collective(e, c, nullptr);
-      DLC_CUDA(cudaMemcpyAsync(host_theta_t, e->theta_t[0], n * sizeof(float), cudaMemcpyDeviceToHost, e->stream));
+      outer_collective(e, c, nullptr);  // ORDERED / ALLREDUCE: K4 in place on theta_t[ocur]
+      DLC_CUDA(cudaMemcpyAsync(host_theta_t, e->theta_t[s0.ocur], n * sizeof(float), cudaMemcpyDeviceToHost,
+                               e->stream));
     }
     DLC_CUDA(cudaStreamSynchronize(e->h2d));
     DLC_CUDA(cudaStreamSynchronize(e->d2h));

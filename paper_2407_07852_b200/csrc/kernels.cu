@@ -368,6 +368,57 @@ __global__ void __launch_bounds__(kThreads) fold_kernel(const __grid_constant__ 
   if (flag) block_or_flag(bad, flag);
 }
 
+// K3 fused with the all-gather: the owner pushes its mean to every rank.
+template <int PREC>
+__global__ void __launch_bounds__(kThreads) fold_push_kernel(const __grid_constant__ PtrList in, int k,
+                                                             const __grid_constant__ PtrList outs, int nout,
+                                                             const __grid_constant__ PtrList flags, size_t n) {
+  const float divisor = (float)k;  // reduce.cpp:36
+  bool bad = false;
+  const size_t n8 = n / 8, i = gtid();
+  if (i < n8) {
+    float acc[8], x[8];
+    load8<PREC>(in.ptr[0], i, acc);
+    for (int j = 1; j < k; ++j) {
+      load8<PREC>(in.ptr[j], i, x);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[q] = __fadd_rn(acc[q], x[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = __fdiv_rn(acc[q], divisor);
+    if (PREC == 1) {
+      uint16_t h[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        h[q] = fp16_encode(acc[q]);
+        bad |= fp16_nonfinite(h[q]);
+      }
+      const uint4 w = make_uint4(pack2(h[0], h[1]), pack2(h[2], h[3]), pack2(h[4], h[5]), pack2(h[6], h[7]));
+      for (int o = 0; o < nout; ++o) st_stream(reinterpret_cast<uint4*>(const_cast<void*>(outs.ptr[o])) + i, w);
+    } else {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) bad |= !finite_f(acc[q]);
+      const float4 a = make_float4(acc[0], acc[1], acc[2], acc[3]), b = make_float4(acc[4], acc[5], acc[6], acc[7]);
+      for (int o = 0; o < nout; ++o) {
+        float4* d = reinterpret_cast<float4*>(const_cast<void*>(outs.ptr[o])) + 2 * i;
+        st_stream(d, a);
+        st_stream(d + 1, b);
+      }
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x < n - n8 * 8) {
+    const size_t e = n8 * 8 + threadIdx.x;
+    float acc = load1<PREC>(in.ptr[0], e);
+    for (int j = 1; j < k; ++j) acc = __fadd_rn(acc, load1<PREC>(in.ptr[j], e));
+    const float mean = __fdiv_rn(acc, divisor);
+    for (int o = 0; o < nout; ++o) bad |= store1<PREC>(const_cast<void*>(outs.ptr[o]), e, mean);
+  }
+  if (__syncthreads_or(bad ? 1 : 0) && threadIdx.x == 0) {
+    for (int o = 0; o < nout; ++o) *reinterpret_cast<volatile int*>(const_cast<void*>(flags.ptr[o])) = 1;
+  }
+  __threadfence_system();  // the pushed slots are visible to the peers before the barrier that follows
+}
+
 // =============================================================================
 // K4: finite-gated Nesterov on theta_t + theta_local refresh (engine.cpp:136-144).
 // =============================================================================
@@ -442,49 +493,106 @@ __global__ void __launch_bounds__(kThreads) nesterov_outer_kernel(Pair ttp, Pair
   if (blockIdx.x == 0 && threadIdx.x == 0) k4_finalize(st, applied);
 }
 
-// CTA b works on owner q = b % K, vectors [(b / K) * 256, ...) of that slot:
-// CTAs resident together read every owner's slot, spreading the NVLink reads
-// across all links while the local theta_t / momentum traffic streams.
+// ---- pipelined P2P pieces ----------------------------------------------------
+// CTA b covers owner q = b % K, vectors [(b / K) * 256, ...) of that owner's
+// piece, so every piece launch spreads over all slots.
+
 template <int PREC>
-__global__ void __launch_bounds__(kThreads) nesterov_outer_p2p_kernel(Pair ttp, Pair bufp, Pair tl,
-                                                                      const __grid_constant__ PtrList slots,
-                                                                      const __grid_constant__ PtrList flags, int k,
-                                                                      size_t S, DevState* st, float lr, float mu,
-                                                                      size_t n) {
-  __shared__ int s_nonfinite;
+__global__ void __launch_bounds__(kThreads) pseudo_grad_piece_kernel(Pair ttp, Pair tl, const DevState* st,
+                                                                     void* send, int k, size_t S, size_t po,
+                                                                     size_t plen, size_t n) {
+  const int q = (int)(blockIdx.x % (unsigned)k);
+  const size_t j = (size_t)(blockIdx.x / (unsigned)k) * kThreads + threadIdx.x;
+  const size_t e0 = (size_t)q * S + po + 4 * j;
+  if (4 * j >= plen || e0 >= n) return;
+  const float* T = sel(ttp, st->ocur);
+  const float* L = sel(tl, st->cur);
+  if (e0 + 3 < n) {
+    const float4 x = ld_stream(reinterpret_cast<const float4*>(T + e0));
+    const float4 y = ld_stream(reinterpret_cast<const float4*>(L + e0));
+    const float4 d = make_float4(delta_elem(x.x, y.x), delta_elem(x.y, y.y), delta_elem(x.z, y.z),
+                                 delta_elem(x.w, y.w));
+    if (PREC == 0) {
+      st_stream(reinterpret_cast<float4*>(static_cast<float*>(send) + e0), d);
+    } else {
+      st_stream(reinterpret_cast<uint2*>(static_cast<uint16_t*>(send) + e0),
+                make_uint2(pack2(fp16_encode(d.x), fp16_encode(d.y)), pack2(fp16_encode(d.z), fp16_encode(d.w))));
+    }
+  } else {
+    for (size_t e = e0; e < n; ++e) {
+      const float d = delta_elem(T[e], L[e]);
+      if (PREC == 0)
+        static_cast<float*>(send)[e] = d;
+      else
+        static_cast<uint16_t*>(send)[e] = fp16_encode(d);
+    }
+  }
+}
+
+template <int PREC>
+__global__ void __launch_bounds__(kThreads) nesterov_p2p_piece_kernel(Pair ttp, Pair bufp, Pair tl,
+                                                                      const __grid_constant__ PtrList slots, int k,
+                                                                      size_t S, size_t po, size_t plen,
+                                                                      DevState* st, float lr, float mu, size_t n) {
+  const int q = (int)(blockIdx.x % (unsigned)k);
+  const size_t j = (size_t)(blockIdx.x / (unsigned)k) * kThreads + threadIdx.x;
+  const size_t e0 = (size_t)q * S + po + 4 * j;
+  if (4 * j >= plen || e0 >= n) return;
+  const int oc = st->ocur;
+  const float* T = sel(ttp, oc);
+  const float* B = sel(bufp, oc);
+  float* To = sel(ttp, oc ^ 1);
+  float* Bo = sel(bufp, oc ^ 1);
+  float* L = sel(tl, st->cur);
+  const void* dbar = slots.ptr[q];
+  const size_t o0 = po + 4 * j;  // offset inside owner q's mean slot
+  if (e0 + 3 < n) {
+    const float4 d = PREC == 0 ? ld_stream(reinterpret_cast<const float4*>(static_cast<const float*>(dbar) + o0))
+                               : decode4(ld_stream(reinterpret_cast<const uint2*>(
+                                     static_cast<const uint16_t*>(dbar) + o0)));
+    const float4 t = ld_stream(reinterpret_cast<const float4*>(T + e0));
+    float4 b = ld_stream(reinterpret_cast<const float4*>(B + e0)), o;
+    o.x = nesterov_elem(t.x, d.x, b.x, lr, mu);
+    o.y = nesterov_elem(t.y, d.y, b.y, lr, mu);
+    o.z = nesterov_elem(t.z, d.z, b.z, lr, mu);
+    o.w = nesterov_elem(t.w, d.w, b.w, lr, mu);
+    st_stream(reinterpret_cast<float4*>(To + e0), o);
+    st_stream(reinterpret_cast<float4*>(Bo + e0), b);
+    st_stream(reinterpret_cast<float4*>(L + e0), o);
+  } else {
+    for (size_t e = e0; e < n; ++e) {
+      const size_t o = o0 + (e - e0);
+      const float d = PREC == 0 ? static_cast<const float*>(dbar)[o]
+                                : fp16_decode(static_cast<const uint16_t*>(dbar)[o]);
+      float b = B[e];
+      const float v = nesterov_elem(T[e], d, b, lr, mu);
+      To[e] = v;
+      Bo[e] = b;
+      L[e] = v;
+    }
+  }
+}
+
+// Gate of the pipelined P2P step: flip `ocur` when all K owner flags are clean
+// (engine.cpp:136-139), else theta_local := theta_t (engine.cpp:143).
+__global__ void __launch_bounds__(kThreads) p2p_finish_kernel(Pair ttp, Pair tl, const __grid_constant__ PtrList flags,
+                                                              int k, DevState* st, size_t n) {
+  __shared__ int s_skip;
   if (threadIdx.x == 0) {
     int nf = 0;
     for (int j = 0; j < k; ++j) nf |= *reinterpret_cast<const volatile int*>(flags.ptr[j]);
-    s_nonfinite = nf;
+    s_skip = nf;
   }
   __syncthreads();
-  const bool applied = s_nonfinite == 0;
-  float* tt = sel(ttp, st->ocur);
-  float* buf = sel(bufp, st->ocur);
-  float* L = sel(tl, st->cur);
-  const int q = (int)(blockIdx.x % (unsigned)k);
-  const size_t j = (size_t)(blockIdx.x / (unsigned)k) * kThreads + threadIdx.x;  // vector index in the slot
-  const size_t e0 = (size_t)q * S + 4 * j;
-  const void* dbar = slots.ptr[q];
-  if (4 * j < S && e0 < n) {
-    if (e0 + 3 < n) {
-      float4 d = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (applied) {
-        d = PREC == 0 ? ld_stream(reinterpret_cast<const float4*>(dbar) + j)
-                      : decode4(ld_stream(reinterpret_cast<const uint2*>(dbar) + j));
-      }
-      k4_vec(applied, reinterpret_cast<float4*>(tt + e0), reinterpret_cast<float4*>(buf + e0),
-             reinterpret_cast<float4*>(L + e0), d, lr, mu);
-    } else {  // the ragged end of the last owner's slot
-      for (size_t e = e0; e < n; ++e) {
-        const size_t o = 4 * j + (e - e0);
-        const float d = PREC == 0 ? reinterpret_cast<const float*>(dbar)[o]
-                                  : fp16_decode(reinterpret_cast<const uint16_t*>(dbar)[o]);
-        k4_scalar(applied, tt + e, buf + e, L + e, d, lr, mu);
-      }
-    }
+  const int skip = s_skip;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (!skip) st->ocur ^= 1;
+    k4_finalize(st, !skip);
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) k4_finalize(st, applied);
+  if (!skip) return;
+  const float* T = sel(ttp, st->ocur);  // unchanged on a skip
+  float* L = sel(tl, st->cur);
+  for (size_t e = gtid(); e < n; e += gstride()) L[e] = T[e];
 }
 
 // ---- K2 + K4 fused for K = 1 -------------------------------------------------
@@ -714,15 +822,36 @@ void launch_nesterov_outer(Pair tt, Pair buf, Pair tl, const void* dbar, int pre
     nesterov_outer_kernel<1><<<grid, kThreads, 0, s>>>(tt, buf, tl, dbar, flags, nflags, st, lr, mu, n);
 }
 
-void launch_nesterov_outer_p2p(Pair tt, Pair buf, Pair tl, const PtrList& slots, const PtrList& flags, int k,
-                               size_t S, int precision, DevState* st, float lr, float mu, size_t n,
-                               cudaStream_t s) {
-  const size_t per_slot = std::max<size_t>(1, (S / 4 + kThreads - 1) / kThreads);
-  const int grid = (int)(per_slot * (size_t)k);
+void launch_fold_push(const PtrList& in, int k, int precision, const PtrList& outs, int nout, const PtrList& flags,
+                      size_t n, cudaStream_t s) {
+  const int grid = grid_window<1>(n / 8);
   if (precision == 0)
-    nesterov_outer_p2p_kernel<0><<<grid, kThreads, 0, s>>>(tt, buf, tl, slots, flags, k, S, st, lr, mu, n);
+    fold_push_kernel<0><<<grid, kThreads, 0, s>>>(in, k, outs, nout, flags, n);
   else
-    nesterov_outer_p2p_kernel<1><<<grid, kThreads, 0, s>>>(tt, buf, tl, slots, flags, k, S, st, lr, mu, n);
+    fold_push_kernel<1><<<grid, kThreads, 0, s>>>(in, k, outs, nout, flags, n);
+}
+
+void launch_pseudo_grad_piece(Pair tt, Pair tl, const DevState* st, void* send, int precision, int k, size_t S,
+                              size_t po, size_t plen, size_t n, cudaStream_t s) {
+  const int grid = (int)(std::max<size_t>(1, (plen / 4 + kThreads - 1) / kThreads) * (size_t)k);
+  if (precision == 0)
+    pseudo_grad_piece_kernel<0><<<grid, kThreads, 0, s>>>(tt, tl, st, send, k, S, po, plen, n);
+  else
+    pseudo_grad_piece_kernel<1><<<grid, kThreads, 0, s>>>(tt, tl, st, send, k, S, po, plen, n);
+}
+
+void launch_nesterov_p2p_piece(Pair tt, Pair buf, Pair tl, const PtrList& slots, int k, size_t S, size_t po,
+                               size_t plen, int precision, DevState* st, float lr, float mu, size_t n,
+                               cudaStream_t s) {
+  const int grid = (int)(std::max<size_t>(1, (plen / 4 + kThreads - 1) / kThreads) * (size_t)k);
+  if (precision == 0)
+    nesterov_p2p_piece_kernel<0><<<grid, kThreads, 0, s>>>(tt, buf, tl, slots, k, S, po, plen, st, lr, mu, n);
+  else
+    nesterov_p2p_piece_kernel<1><<<grid, kThreads, 0, s>>>(tt, buf, tl, slots, k, S, po, plen, st, lr, mu, n);
+}
+
+void launch_p2p_finish(Pair tt, Pair tl, const PtrList& flags, int k, DevState* st, size_t n, cudaStream_t s) {
+  p2p_finish_kernel<<<num_sms() * 4, kThreads, 0, s>>>(tt, tl, flags, k, st, n);
 }
 
 void launch_outer_solo_chunk(Pair tt, Pair buf, Pair tl, const float* src, int precision, DevState* st, float lr,

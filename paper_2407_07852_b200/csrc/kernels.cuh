@@ -104,13 +104,27 @@ void launch_fold(const PtrList& in, int k, int in_kind, void* out, int out_kind,
 void launch_nesterov_outer(Pair theta_t, Pair buf, Pair theta_local,
                            const void* dbar, int precision, const int* flags, int nflags,
                            DevState* st, float lr, float mu, size_t n, cudaStream_t s);
-// K4 reading the mean in place from its K owners over NVLink (DLC_MODE_P2P):
-// element i lives in slots.ptr[i / S][i % S]; owner q's non-finite flag at
-// flags.ptr[q].  Consecutive CTAs cycle through the owners so NVLink reads and
-// local HBM traffic overlap.  Same arithmetic and skip gate as above.
-void launch_nesterov_outer_p2p(Pair theta_t, Pair buf, Pair theta_local, const PtrList& slots,
-                               const PtrList& flags, int k, size_t S, int precision, DevState* st,
-                               float lr, float mu, size_t n, cudaStream_t s);
+// Pipelined DLC_MODE_P2P pieces.  Piece p of the outer step is the sub-range
+// [q*S + po, q*S + po + plen) of every owner slot q (po = p*plen).  K2 writes a
+// piece of the send buffer; K4 consumes a piece of every owner's mean slot and
+// writes theta_t / momentum speculatively into the idle ping-pong buffers (the
+// non-finite gate is only known after the last piece); p2p_finish then flips
+// `ocur` when every owner flag is clean, else restores theta_local := theta_t.
+// Owner fold fused with the all-gather (DLC_MODE_P2P): contributions `in`
+// (peer send buffers, pulled over NVLink) folded in rank order exactly as
+// launch_fold, the encoded mean stored to all `nout` destinations (this rank's
+// slot in every peer's gather buffer, posted NVLink writes) and a non-finite
+// mean marked by storing 1 to every `flags` entry; ends with a system fence.
+void launch_fold_push(const PtrList& in, int k, int precision, const PtrList& outs, int nout,
+                      const PtrList& flags, size_t n, cudaStream_t s);
+void launch_pseudo_grad_piece(Pair theta_t, Pair theta_local, const DevState* st, void* send,
+                              int precision, int k, size_t S, size_t po, size_t plen, size_t n,
+                              cudaStream_t s);
+void launch_nesterov_p2p_piece(Pair theta_t, Pair buf, Pair theta_local, const PtrList& slots,
+                               int k, size_t S, size_t po, size_t plen, int precision,
+                               DevState* st, float lr, float mu, size_t n, cudaStream_t s);
+void launch_p2p_finish(Pair theta_t, Pair theta_local, const PtrList& flags, int k, DevState* st,
+                       size_t n, cudaStream_t s);
 // K2+K4 fused for a single worker (SoloCollective, reduce.cpp:113-126): one
 // HBM pass reading theta_t[ocur], buf[ocur], theta_local and writing
 // theta_t[ocur^1], buf[ocur^1], theta_local (24 B/param), then a finish kernel
