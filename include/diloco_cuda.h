@@ -312,6 +312,31 @@ DLC_API int dlc_engines_outer_step_local(dlc_engine* const* engines, size_t k, d
 DLC_API int dlc_optimizer_step(dlc_engine* e, dlc_collective* c, const float* grad, int grad_is_scaled,
                        int* round_completed);
 
+/* Checkpoint / resume of device-resident engines in the reference's ODLCKPT1
+ * format (save_checkpoint / load_checkpoint, checkpoint.cpp:17,74-198):
+ * magic, config hash, completed rounds, clock, reduce bytes, utilization
+ * ledger, then per engine the FP64-text scalar header (checkpoint.cpp:74-91)
+ * and serialize_param_vector blocks (tensor.cpp:188-200) of theta_t,
+ * theta_local, m, v and the momentum buffer.  Files are interchangeable with
+ * the reference's.  The Layout is `nseg` named segments of `seg_lengths`
+ * (NULL names: one segment "p" covering the vector).  Vectors stream through
+ * a pinned staging buffer. */
+typedef struct {
+  uint64_t config_hash;
+  uint64_t completed_rounds;
+  double clock_seconds;
+  uint64_t reduce_data_bytes;
+  size_t ledger_workers;  /* entries in `ledger` (compute, comm, idle seconds each) */
+  const double* ledger;   /* save: 3 * ledger_workers doubles, may be NULL when 0 */
+} dlc_checkpoint_meta;
+DLC_API int dlc_checkpoint_save(dlc_engine* const* engines, size_t count, const char* path,
+                                const dlc_checkpoint_meta* meta, const char* const* seg_names,
+                                const uint64_t* seg_lengths, size_t nseg);
+/* Restores `count` engines (sizes must match, ShapeError otherwise);
+ * meta_out (may be NULL) receives the header fields (ledger = NULL). */
+DLC_API int dlc_checkpoint_load(dlc_engine* const* engines, size_t count, const char* path,
+                                dlc_checkpoint_meta* meta_out);
+
 /* Per-phase device timing with CUDA events on the engine stream (ncu-free
  * evidence for the roofline): phase 0 = K1 inner AdamW, 1 = K2 pseudo-grad,
  * 2 = collective (C1 + K3 fold), 3 = K4 outer Nesterov.  dlc_engine_phase_times

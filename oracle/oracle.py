@@ -87,6 +87,38 @@ class _Lib:
             self._bench_outer = fn("bench_outer", C.c_int, C.c_int, _sz, _sz, C.c_int, C.c_int,
                                    C.c_float, C.c_float, C.POINTER(C.c_double))
             self._bench_inner = fn("bench_inner", C.c_int, C.c_int, _sz, C.c_int, C.POINTER(C.c_double))
+            vp = C.c_void_p
+            self._ck_read = fn("checkpoint_read", C.c_int, C.c_char_p, _sz, _sz, vp, vp, vp, vp, vp,
+                               C.POINTER(_u64), C.POINTER(C.c_double), C.POINTER(_u64))
+            self._ck_write = fn("checkpoint_write", C.c_int, C.c_char_p, _sz, vp, vp, vp, vp, vp,
+                                C.POINTER(_u64), C.POINTER(C.c_double), C.POINTER(_u64))
+
+    # -- checkpoints through the reference's save/load_checkpoint (reference only) --------
+    _CK_U = ("step_count", "growth_interval", "consecutive_good", "inner_step", "outer_epoch", "engines")
+    _CK_D = ("beta1", "beta2", "eps", "weight_decay", "outer_lr", "outer_momentum", "scale", "clock_seconds")
+    _CK_H = ("config_hash", "completed_rounds", "reduce_data_bytes")
+    _CK_V = ("theta_t", "theta_local", "m", "v", "buf")
+
+    def checkpoint_read(self, path, idx, n):
+        vec = {k: np.empty(n, np.float32) for k in self._CK_V}
+        u, d, h = (_u64 * 6)(), (C.c_double * 8)(), (_u64 * 3)()
+        st = self._ck_read(path.encode(), idx, n, *[vec[k].ctypes.data for k in self._CK_V], u, d, h)
+        if st:
+            raise RuntimeError(f"ref_checkpoint_read failed with status {st}")
+        out = dict(vec)
+        out.update({k: int(u[i]) for i, k in enumerate(self._CK_U)})
+        out.update({k: float(d[i]) for i, k in enumerate(self._CK_D)})
+        out.update({k: int(h[i]) for i, k in enumerate(self._CK_H)})
+        return out
+
+    def checkpoint_write(self, path, state):
+        vec = [np.ascontiguousarray(state[k], np.float32) for k in self._CK_V]
+        u = (_u64 * 6)(*[int(state.get(k, 0)) for k in self._CK_U])
+        d = (C.c_double * 8)(*[float(state.get(k, 0.0)) for k in self._CK_D])
+        h = (_u64 * 3)(*[int(state.get(k, 0)) for k in self._CK_H])
+        st = self._ck_write(path.encode(), vec[0].size, *[x.ctypes.data for x in vec], u, d, h)
+        if st:
+            raise RuntimeError(f"ref_checkpoint_write failed with status {st}")
 
     # -- codec ---------------------------------------------------------------
     def fp16_encode_scalar(self, x: float) -> int:

@@ -320,3 +320,79 @@ REF_API int ref_bench_inner(int threads, size_t slice, int iters, double* sec_pe
   *sec_per_iter = worst / iters;
   return kOk;
 }
+
+// ---------------------------------------------------------------------------
+// Checkpoint files through the reference's own save/load (checkpoint.cpp).
+// ---------------------------------------------------------------------------
+#include "diloco/checkpoint.hpp"
+
+// Reads engine `idx` of a checkpoint with load_checkpoint (checkpoint.cpp:162-198).
+// u[0..5] = step_count, growth_interval, consecutive_good, inner_step,
+// outer_epoch, engine count; d[0..7] = beta1, beta2, eps, weight_decay,
+// outer_lr, outer_momentum, scale, clock_seconds; h[0..2] = config_hash,
+// completed_rounds, reduce_data_bytes.  Vectors are copied when non-null and n
+// matches.
+REF_API int ref_checkpoint_read(const char* path, size_t idx, size_t n, float* tt, float* tl, float* m, float* v,
+                                float* buf, uint64_t* u, double* d, uint64_t* h) {
+  return guarded([&] {
+    const Checkpoint ck = load_checkpoint(path);
+    h[0] = ck.config_hash;
+    h[1] = ck.completed_rounds;
+    h[2] = ck.reduce_data_bytes;
+    u[5] = ck.engines.size();
+    d[7] = ck.clock_seconds;
+    if (idx >= ck.engines.size()) throw ShapeError("engine index");
+    const EngineState& s = ck.engines[idx];
+    if (s.theta_t.size() != n) throw ShapeError("size");
+    if (tt) put(s.theta_t, tt);
+    if (tl) put(s.theta_local, tl);
+    if (m) put(s.inner.m, m);
+    if (v) put(s.inner.v, v);
+    if (buf) put(s.outer.momentum_buf, buf);
+    u[0] = s.inner.step_count;
+    u[1] = s.scaler.growth_interval;
+    u[2] = s.scaler.consecutive_good;
+    u[3] = s.inner_step;
+    u[4] = s.outer_epoch;
+    d[0] = s.inner.beta1;
+    d[1] = s.inner.beta2;
+    d[2] = s.inner.eps;
+    d[3] = s.inner.weight_decay;
+    d[4] = s.outer.lr;
+    d[5] = s.outer.momentum;
+    d[6] = s.scaler.scale;
+  });
+}
+
+// Writes a one-engine checkpoint with save_checkpoint (checkpoint.cpp:131-160).
+REF_API int ref_checkpoint_write(const char* path, size_t n, const float* tt, const float* tl, const float* m,
+                                 const float* v, const float* buf, const uint64_t* u, const double* d,
+                                 const uint64_t* h) {
+  return guarded([&] {
+    Checkpoint ck;
+    ck.config_hash = h[0];
+    ck.completed_rounds = h[1];
+    ck.reduce_data_bytes = h[2];
+    ck.clock_seconds = d[7];
+    EngineState s;
+    s.theta_t = pv(tt, n);
+    s.theta_local = pv(tl, n);
+    s.inner.m = pv(m, n);
+    s.inner.v = pv(v, n);
+    s.outer.momentum_buf = pv(buf, n);
+    s.inner.step_count = u[0];
+    s.scaler.growth_interval = u[1];
+    s.scaler.consecutive_good = u[2];
+    s.inner_step = u[3];
+    s.outer_epoch = u[4];
+    s.inner.beta1 = (float)d[0];
+    s.inner.beta2 = (float)d[1];
+    s.inner.eps = (float)d[2];
+    s.inner.weight_decay = (float)d[3];
+    s.outer.lr = (float)d[4];
+    s.outer.momentum = (float)d[5];
+    s.scaler.scale = (float)d[6];
+    ck.engines.push_back(std::move(s));
+    save_checkpoint(ck, path);
+  });
+}

@@ -65,6 +65,12 @@ class EngineScalars(C.Structure):
                 ("last_applied", C.c_int)]
 
 
+class CheckpointMeta(C.Structure):
+    _fields_ = [("config_hash", C.c_uint64), ("completed_rounds", C.c_uint64), ("clock_seconds", C.c_double),
+                ("reduce_data_bytes", C.c_uint64), ("ledger_workers", C.c_size_t),
+                ("ledger", C.POINTER(C.c_double))]
+
+
 class InnerResult(C.Structure):
     _fields_ = [("lr", C.c_float), ("overflow_skipped", C.c_int)]
 
@@ -125,6 +131,9 @@ _SIGS = {
     "dlc_engine_set_timing": (I, [P, I]),
     "dlc_engine_phase_times": (I, [P, C.POINTER(C.c_double), C.POINTER(C.c_uint64)]),
     "dlc_engines_outer_step_local": (I, [PP, SZ, C.POINTER(OuterResult)]),
+    "dlc_checkpoint_save": (I, [PP, SZ, C.c_char_p, C.POINTER(CheckpointMeta), C.POINTER(C.c_char_p),
+                                C.POINTER(C.c_uint64), SZ]),
+    "dlc_checkpoint_load": (I, [PP, SZ, C.c_char_p, C.POINTER(CheckpointMeta)]),
     "dlc_optimizer_step": (I, [P, P, P, I, C.POINTER(I)]),
     "dlc_rng_key": (U64, [U64, C.c_char_p, U64]),
     "dlc_rng_fill_device": (I, [P, I, U64, U64, F, F]),

@@ -440,6 +440,35 @@ def outer_step_local(engines) -> OuterStepResult:
     return OuterStepResult(bool(res.applied), int(res.outer_epoch))
 
 
+def checkpoint_save(engines, path: str, config_hash: int = 0, completed_rounds: int = 0,
+                    clock_seconds: float = 0.0, reduce_data_bytes: int = 0, ledger=None, segments=None) -> None:
+    """save_checkpoint (checkpoint.cpp:131-160) of device engines in the ODLCKPT1 format.
+
+    ledger: optional [(compute_s, comm_s, idle_s), ...]; segments: optional
+    [(name, length), ...] Layout (default one segment "p")."""
+    arr = (C.c_void_p * len(engines))(*[e.handle.value for e in engines])
+    led = np.ascontiguousarray(ledger if ledger is not None else np.zeros((0, 3)), np.float64).reshape(-1)
+    meta = A.CheckpointMeta(config_hash, completed_rounds, clock_seconds, reduce_data_bytes, led.size // 3,
+                            led.ctypes.data_as(C.POINTER(C.c_double)) if led.size else None)
+    names = lens = None
+    nseg = 0
+    if segments:
+        nseg = len(segments)
+        names = (C.c_char_p * nseg)(*[s[0].encode() for s in segments])
+        lens = (C.c_uint64 * nseg)(*[int(s[1]) for s in segments])
+    _check(lib.dlc_checkpoint_save(arr, len(engines), path.encode(), C.byref(meta), names, lens, nseg))
+
+
+def checkpoint_load(engines, path: str) -> dict:
+    """load_checkpoint (checkpoint.cpp:162-198) into device engines; returns the header fields."""
+    arr = (C.c_void_p * len(engines))(*[e.handle.value for e in engines])
+    meta = A.CheckpointMeta()
+    _check(lib.dlc_checkpoint_load(arr, len(engines), path.encode(), C.byref(meta)))
+    return {"config_hash": int(meta.config_hash), "completed_rounds": int(meta.completed_rounds),
+            "clock_seconds": float(meta.clock_seconds), "reduce_data_bytes": int(meta.reduce_data_bytes),
+            "ledger_workers": int(meta.ledger_workers)}
+
+
 class DilocoOptimizer:
     """Single-optimizer facade (engine.hpp:122-140; paper Fig. 2)."""
 

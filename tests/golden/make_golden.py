@@ -122,6 +122,16 @@ def main():
     for k, g in ((0, 0), (1, 0), (0, 3), (1, 3)):
         traj[f"grad_w{k}_t{g}"] = grad_fn(k, g)
     np.savez_compressed(os.path.join(OUT, "diloco_k2_h5.npz"), **traj)
+    # --- ODLCKPT1 checkpoint written by the reference's save_checkpoint ---
+    n = 1031
+    ck = {name: rng.uniform(-1, 1, n).astype(np.float32) for name in ("theta_t", "theta_local", "m", "buf")}
+    ck["v"] = rng.uniform(0, 1e-3, n).astype(np.float32)
+    ck.update(step_count=17, growth_interval=2000, consecutive_good=5, inner_step=20, outer_epoch=4,
+              beta1=np.float32(0.9), beta2=np.float32(0.95), eps=np.float32(1e-8), weight_decay=np.float32(0.1),
+              outer_lr=np.float32(0.7), outer_momentum=np.float32(0.9), scale=32768.0, clock_seconds=1.25,
+              config_hash=0xC0FFEE, completed_rounds=3, reduce_data_bytes=123456)
+    R.checkpoint_write(os.path.join(OUT, "engine.ckpt"), ck)
+    np.savez_compressed(os.path.join(OUT, "engine_ckpt.npz"), **{k: np.asarray(v) for k, v in ck.items()})
     print("golden fixtures written to", OUT)
 
 

@@ -1,0 +1,104 @@
+"""Checkpoint / resume in the reference's ODLCKPT1 format.
+
+CPU: the committed fixture tests/golden/engine.ckpt (written by the reference's
+save_checkpoint) reads back through the reference's load_checkpoint.
+GPU: device engines load that file, write byte-identical files, and resume
+bit-for-bit (test_harness.cpp:197-222 style).
+"""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import driver as DR
+from oracle import oracle as O
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def bits(a):
+    return np.ascontiguousarray(a, np.float32).view(np.uint32)
+
+
+def test_reference_reads_golden_checkpoint(ref):
+    z = np.load(os.path.join(GOLD, "engine_ckpt.npz"))
+    got = ref.checkpoint_read(os.path.join(GOLD, "engine.ckpt"), 0, z["theta_t"].size)
+    for k in ("theta_t", "theta_local", "m", "v", "buf"):
+        assert np.array_equal(bits(got[k]), bits(z[k]))
+    for k in ("step_count", "inner_step", "outer_epoch", "consecutive_good", "config_hash", "completed_rounds"):
+        assert got[k] == int(z[k])
+    assert got["scale"] == float(z["scale"]) and got["engines"] == 1
+
+
+@pytest.fixture
+def gpu():
+    import paper_2407_07852_b200 as D
+    try:
+        n = D.device_count()
+    except D.Error:
+        n = 0
+    if n < 1:
+        pytest.skip("no CUDA device")
+    D.lib.dlc_set_device(0)
+    return D
+
+
+@pytest.mark.gpu
+def test_engine_loads_and_rewrites_reference_checkpoint(gpu, tmp_path):
+    D = gpu
+    z = np.load(os.path.join(GOLD, "engine_ckpt.npz"))
+    n = z["theta_t"].size
+    e = D.DilocoEngine(D.DilocoConfig(10, 1, D.FP16, 100), D.OptimHyperparams(), n)
+    meta = D.checkpoint_load([e], os.path.join(GOLD, "engine.ckpt"))
+    assert meta["config_hash"] == 0xC0FFEE and meta["completed_rounds"] == 3
+    for which, k in ((D.THETA_T, "theta_t"), (D.THETA_LOCAL, "theta_local"), (D.ADAM_M, "m"), (D.ADAM_V, "v"),
+                     (D.MOMENTUM, "buf")):
+        assert np.array_equal(bits(e.download(which)), bits(z[k]))
+    s = e.scalars()
+    assert (s.step_count, s.inner_step, s.outer_epoch, s.consecutive_good) == (17, 20, 4, 5)
+    assert s.scale == 32768.0
+    out = str(tmp_path / "rewrite.ckpt")
+    D.checkpoint_save([e], out, config_hash=0xC0FFEE, completed_rounds=3, clock_seconds=1.25,
+                      reduce_data_bytes=123456)
+    with open(out, "rb") as a, open(os.path.join(GOLD, "engine.ckpt"), "rb") as b:
+        assert a.read() == b.read()  # byte-identical to the reference's writer
+    e.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("segments", [None, [("w", 60_000), ("b", 5_011)]])
+def test_resume_is_bitwise(gpu, tmp_path, segments):
+    """Save mid-run, restore into a fresh engine, continue both: identical trajectories,
+    and the reference's load_checkpoint reads the engine's file."""
+    D = gpu
+    n = 65_011
+    hyper = D.OptimHyperparams(inner_lr=1e-3, warmup_steps=3)
+    cfg = D.DilocoConfig(2, 1, D.FP16, 12)
+    a = D.DilocoEngine(cfg, hyper, n)
+    th = O.rng_fill(1, "theta", 0, n, -0.1, 0.1)
+    a.upload(D.THETA_T, th)
+    a.upload(D.THETA_LOCAL, th)
+    grads = [O.rng_fill(1, "grad", t, n, -1e-2, 1e-2) for t in range(12)]
+    for t in range(6):
+        a.inner_step_host(grads[t])
+        if (t + 1) % 2 == 0:
+            a.outer_step(None)
+    path = str(tmp_path / "mid.ckpt")
+    D.checkpoint_save([a], path, completed_rounds=3, segments=segments)
+    b = D.DilocoEngine(cfg, hyper, n)
+    D.checkpoint_load([b], path)
+    for t in range(6, 12):
+        for e in (a, b):
+            e.inner_step_host(grads[t])
+            if (t + 1) % 2 == 0:
+                e.outer_step(None)
+    for w in (D.THETA_T, D.THETA_LOCAL, D.ADAM_M, D.ADAM_V, D.MOMENTUM):
+        assert np.array_equal(bits(a.download(w)), bits(b.download(w)))
+    r = O.reference()
+    if r is not None:
+        got = r.checkpoint_read(path, 0, n)
+        assert got["step_count"] == 6 and got["outer_epoch"] == 3 and got["inner_step"] == 6
+    with pytest.raises(D.ShapeError):
+        D.checkpoint_load([D.DilocoEngine(cfg, hyper, n + 1)], path)
+    a.close()
+    b.close()
