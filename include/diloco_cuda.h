@@ -302,6 +302,19 @@ DLC_API int dlc_engine_outer_step_from(dlc_engine* e, dlc_collective* c, const f
  * host: theta_local is uploaded, the outer step runs, theta_t is downloaded. */
 DLC_API int dlc_engine_outer_step_host(dlc_engine* e, dlc_collective* c, const float* host_theta_local,
                                float* host_theta_t, dlc_outer_result* result);
+/* The outer step split around a collective that runs outside this library
+ * (e.g. the reference's SocketCollective between boxes,
+ * fed from D2H-staged buffers):
+ *   dlc_engine_compute_pseudo_gradient = DilocoEngine::compute_pseudo_gradient
+ *     (engine.cpp:115-126): the raw FP32 delta = theta_t - theta_local into a
+ *     host buffer of n, plus the engine's outer epoch (the PseudoGradient tag);
+ *     Error when mid-window.
+ *   dlc_engine_apply_outer_step = DilocoEngine::outer_step (engine.cpp:128-146)
+ *     on a host FP32 mean: CollectiveError on an epoch mismatch, Nesterov only
+ *     when every element is finite, theta_local := theta_t always. */
+DLC_API int dlc_engine_compute_pseudo_gradient(dlc_engine* e, float* host_delta, uint64_t* outer_epoch);
+DLC_API int dlc_engine_apply_outer_step(dlc_engine* e, const float* host_mean, uint64_t outer_epoch,
+                                        dlc_outer_result* result);
 /* K engines of one process on one device (in-process fleet, the device
  * analogue of run_simulated's outer round, netsim.cpp:325-357): pseudo-grads,
  * one fold in index order, K outer steps. */

@@ -20,6 +20,7 @@
 #include <cinttypes>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -118,7 +119,19 @@ void launched(const char* what) { DLC_LAUNCHED(what); }
 // Host <-> device chunk of the host-buffer outer step (64 MB of FP32).
 constexpr size_t kHostChunk = size_t(16) << 20;
 // Pieces of the pipelined P2P outer step (DLC_MODE_P2P).
-constexpr size_t kP2PPieces = 4;
+// Owner slots are a multiple of 64 * kMaxPieces elements; the number actually
+// used comes from DLC_P2P_PIECES (default 1: K2 -> fold+push -> K4, no
+// cross-stream overlap), a tuning knob measured in profiles/.
+constexpr size_t kMaxPieces = 8;
+
+size_t p2p_pieces() {
+  static const size_t p = [] {
+    const char* s = std::getenv("DLC_P2P_PIECES");
+    const long v = s ? std::strtol(s, nullptr, 10) : 1;
+    return (size_t)std::min<long>(std::max<long>(v, 1), (long)kMaxPieces);
+  }();
+  return p;
+}
 
 void ensure_copy_streams(dlc_engine* e) {
   if (!e->h2d) DLC_CUDA(cudaStreamCreateWithFlags(&e->h2d, cudaStreamNonBlocking));
@@ -395,7 +408,7 @@ void outer_collective(dlc_engine* e, dlc_collective* c, dlc_reduce_report* rep) 
   }
 }
 
-// DLC_MODE_P2P, software-pipelined over kP2PPieces pieces (kernels.cuh):
+// DLC_MODE_P2P, software-pipelined over P = p2p_pieces() pieces (kernels.cuh):
 //   main stream : K2(0..P-1), then K4(p) as soon as fold(p) is final, finish
 //   cstream     : B0, fold(0), B1, fold(1), ..., fold(P-1), B_P   (high priority)
 // where B_p is a 4-byte NCCL all-reduce: B_0 orders every rank's K2(0) (and
@@ -412,7 +425,7 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
     DLC_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     DLC_CUDA(cudaStreamCreateWithPriority(&e->cstream, cudaStreamNonBlocking, hi));
   }
-  const size_t P = kP2PPieces;
+  const size_t P = p2p_pieces();
   while (e->piece_ev.size() < 4 * P + 2) {
     cudaEvent_t ev;
     DLC_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -608,7 +621,7 @@ int dlc_engine_create(const dlc_config* cfg, const dlc_hyperparams* hyper, size_
     e->k = cfg->num_workers_k;
     e->prec = cfg->reduce_precision;
     // owner slot: a multiple of 64 elements per P2P piece
-    const size_t quantum = 64 * kP2PPieces;
+    const size_t quantum = 64 * kMaxPieces;
     e->S = (((n + e->k - 1) / e->k) + quantum - 1) / quantum * quantum;
     DLC_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
     DLC_CUDA(cudaEventCreate(&e->ev0));
@@ -925,6 +938,42 @@ int dlc_engine_outer_step_host(dlc_engine* e, dlc_collective* c, const float* ho
     const DevState s1 = read_state(e);
     if (e->k == 1 && !s1.last_applied)  // skipped: theta_t did not move
       DLC_CUDA(cudaMemcpy(host_theta_t, e->theta_t[s1.ocur], n * sizeof(float), cudaMemcpyDeviceToHost));
+    outer_result(e, result);
+  });
+}
+
+int dlc_engine_compute_pseudo_gradient(dlc_engine* e, float* host_delta, uint64_t* outer_epoch) {
+  return guard([&] {
+    if (!e || (e->n && !host_delta)) fail(DLC_EINVAL, "dlc_engine_compute_pseudo_gradient: null argument");
+    if (e->issued_inner % e->cfg.local_steps_h != 0)  // engine.cpp:116-120
+      fail(DLC_EINVAL, "pseudo-gradient requested mid-window (inner_step " + std::to_string(e->issued_inner) +
+                           ", H " + std::to_string(e->cfg.local_steps_h) + ")");
+    DeviceGuard dg(e->device);
+    // raw FP32 delta (axpy(-1, theta_local, theta_t), engine.cpp:122) into the staging buffer
+    launch_pseudo_grad(tt_pair(e), local_pair(e), e->st, e->grad, DLC_FP32, &e->st->delta_nonfinite, 0, e->n,
+                       e->stream);
+    launched("pseudo_grad");
+    DLC_CUDA(cudaMemcpyAsync(host_delta, e->grad, e->n * sizeof(float), cudaMemcpyDeviceToHost, e->stream));
+    const DevState s = read_state(e);
+    if (outer_epoch) *outer_epoch = s.outer_epoch;
+  });
+}
+
+int dlc_engine_apply_outer_step(dlc_engine* e, const float* host_mean, uint64_t outer_epoch,
+                                dlc_outer_result* result) {
+  return guard([&] {
+    if (!e || (e->n && !host_mean)) fail(DLC_EINVAL, "dlc_engine_apply_outer_step: null argument");
+    DeviceGuard dg(e->device);
+    const DevState s = read_state(e);
+    if (outer_epoch != s.outer_epoch)  // engine.cpp:129-134
+      fail(DLC_ECOLLECTIVE, "outer_step: reduced pseudo-gradient from epoch " + std::to_string(outer_epoch) +
+                                " applied at epoch " + std::to_string(s.outer_epoch));
+    DLC_CUDA(cudaMemcpyAsync(e->grad, host_mean, e->n * sizeof(float), cudaMemcpyHostToDevice, e->stream));
+    DLC_CUDA(cudaMemsetAsync(e->flags, 0, sizeof(int), e->stream));
+    launch_nonfinite(e->grad, e->flags, e->n, e->stream);  // engine.cpp:136
+    launch_nesterov_outer(tt_pair(e), buf_pair(e), local_pair(e), e->grad, DLC_FP32, e->flags, 1, e->st,
+                          e->hyper.outer_lr, e->hyper.outer_momentum, e->n, e->stream);
+    launched("apply_outer_step");
     outer_result(e, result);
   });
 }

@@ -416,7 +416,10 @@ __global__ void __launch_bounds__(kThreads) fold_push_kernel(const __grid_consta
   if (__syncthreads_or(bad ? 1 : 0) && threadIdx.x == 0) {
     for (int o = 0; o < nout; ++o) *reinterpret_cast<volatile int*>(const_cast<void*>(flags.ptr[o])) = 1;
   }
-  __threadfence_system();  // the pushed slots are visible to the peers before the barrier that follows
+  // The CTA's pushed slots are visible system-wide before the barrier that
+  // follows: the __syncthreads_or above orders every thread's stores before
+  // this (cumulative) system-scope fence of one thread.
+  if (threadIdx.x == 0) __threadfence_system();
 }
 
 // =============================================================================

@@ -61,9 +61,12 @@ def max_over_ranks(x: float, world: int) -> float:
     return float(t.item())
 
 
+SLOT_QUANTUM = 64 * 8  # engine.cu: 64 elements x kMaxPieces
+
+
 def slot_elems(n: int, k: int) -> int:
-    """Owner slot size S used by the engine (engine.cu): ceil(n / k) rounded up to 64."""
-    return ((-(-n // k)) + 63) // 64 * 64
+    """Owner slot size S used by the engine (engine.cu): ceil(n / k) rounded up to SLOT_QUANTUM."""
+    return ((-(-n // k)) + SLOT_QUANTUM - 1) // SLOT_QUANTUM * SLOT_QUANTUM
 
 
 def make_nccl_collective(rank: Rank, mode: int):
