@@ -199,6 +199,25 @@ class DeviceEngine {
     return r;
   }
 
+  /// The same outer round through ANY reference Collective, e.g. a
+  /// SocketCollective between boxes: the pseudo-gradient
+  /// is staged to the host, averaged by `collective`, and applied on the device.
+  /// Returns OuterStepResult::applied (engine.hpp:64-66).
+  bool outer_step(Collective& collective, Precision precision, ReduceReport* report = nullptr) {
+    std::vector<float> d(layout_->total_length());
+    uint64_t epoch = 0;
+    throw_status(dlc_engine_compute_pseudo_gradient(e_, d.data(), &epoch));
+    PseudoGradient pg;
+    pg.delta = ParamVector(layout_, std::move(d));
+    pg.precision = precision;
+    pg.outer_epoch = epoch;
+    const PseudoGradient reduced = collective.all_reduce_avg(pg, report);
+    if (!reduced.delta.same_layout(pg.delta)) throw ShapeError("outer_step: reduced layout mismatch");
+    dlc_outer_result r{};
+    throw_status(dlc_engine_apply_outer_step(e_, reduced.delta.values().data(), reduced.outer_epoch, &r));
+    return r.applied != 0;
+  }
+
   ParamVector download(dlc_buffer which) const {
     std::vector<float> h(layout_->total_length());
     throw_status(dlc_engine_download(e_, which, h.data(), h.size()));

@@ -128,6 +128,8 @@ _SIGS = {
     "dlc_engine_outer_step": (I, [P, P, C.POINTER(OuterResult), C.POINTER(ReduceReport)]),
     "dlc_engine_outer_step_host": (I, [P, P, P, P, C.POINTER(OuterResult)]),
     "dlc_engine_outer_step_from": (I, [P, P, P, C.POINTER(OuterResult), C.POINTER(ReduceReport)]),
+    "dlc_engine_compute_pseudo_gradient": (I, [P, P, C.POINTER(C.c_uint64)]),
+    "dlc_engine_apply_outer_step": (I, [P, P, C.c_uint64, C.POINTER(OuterResult)]),
     "dlc_engine_set_timing": (I, [P, I]),
     "dlc_engine_phase_times": (I, [P, C.POINTER(C.c_double), C.POINTER(C.c_uint64)]),
     "dlc_engines_outer_step_local": (I, [PP, SZ, C.POINTER(OuterResult)]),

@@ -402,6 +402,22 @@ class DilocoEngine:
                                               None))
         return OuterStepResult(bool(res.applied), int(res.outer_epoch)) if wait else None
 
+    def compute_pseudo_gradient(self):
+        """DilocoEngine::compute_pseudo_gradient (engine.cpp:115-126): (FP32 delta on the host, outer epoch)."""
+        out = np.empty(self.n, np.float32)
+        ep = C.c_uint64(0)
+        _check(lib.dlc_engine_compute_pseudo_gradient(self.handle, _ptr(out), C.byref(ep)))
+        return out, int(ep.value)
+
+    def apply_outer_step(self, mean, outer_epoch: int) -> OuterStepResult:
+        """DilocoEngine::outer_step (engine.cpp:128-146) on a host FP32 mean from any collective."""
+        m = _f32(mean)
+        if m.size != self.n:
+            raise ShapeError(A.ESHAPE, "apply_outer_step: length mismatch")
+        res = A.OuterResult()
+        _check(lib.dlc_engine_apply_outer_step(self.handle, _ptr(m), outer_epoch, C.byref(res)))
+        return OuterStepResult(bool(res.applied), int(res.outer_epoch))
+
     def set_timing(self, on: bool) -> None:
         _check(lib.dlc_engine_set_timing(self.handle, int(on)))
 

@@ -176,6 +176,55 @@ int main() {
     const dlc_engine_scalars s = eng.scalars();
     CHECK(s.step_count == adam.step_count && s.scale == scaler.scale && s.overflow_skips == 1);
   }
+  // DeviceEngine's outer round through the reference's own Collective class
+  // (SoloCollective here; SocketCollective plugs in the same way across boxes),
+  // with an epoch-guard violation and a non-finite skip.
+  for (Precision prec : {Precision::fp32, Precision::fp16}) {
+    const ParamVector theta0 = random_vec(layout, 31, "theta", -0.05f, 0.05f);
+    dlc_config cfg{2, 1, cuda::to_c(prec), 6};
+    dlc_hyperparams hp;
+    dlc_hyperparams_default(&hp);
+    cuda::DeviceEngine eng(cfg, hp, theta0, 0);
+    ParamVector theta_t = theta0, theta_local = theta0;
+    AdamWState adam = AdamWState::init(layout, hp.beta1, hp.beta2, hp.adam_eps, hp.weight_decay);
+    NesterovState outer = NesterovState::init(layout, hp.outer_lr, hp.outer_momentum);
+    LossScaler scaler;
+    LrSchedule sched;
+    sched.warmup_steps = hp.warmup_steps;
+    sched.total_steps = cfg.total_inner_steps;
+    sched.base_lr = hp.inner_lr;
+    SoloCollective solo;
+    for (int round = 0; round < 3; ++round) {
+      for (int t = 0; t < 2; ++t) {
+        const ParamVector g = random_vec(layout, 2000 + round * 10 + t, "grad", -1e-2f, 1e-2f);
+        std::vector<float> scaled(n);
+        for (size_t i = 0; i < n; ++i) scaled[i] = g.values()[i] * scaler.scale;
+        const UnscaleResult un = scaler_unscale_and_check(scaler, ParamVector(layout, scaled));
+        if (!un.overflow) theta_local = adamw_step(adam, theta_local, un.grad, lr_at(sched, adam.step_count + 1));
+        scaler_update(scaler, un.overflow);
+        eng.inner_step(g);
+      }
+      PseudoGradient pg;
+      pg.delta = axpy(-1.0f, theta_local, theta_t);
+      pg.precision = prec;
+      PseudoGradient red = solo.all_reduce_avg(pg, nullptr);
+      bool applied = red.delta.all_finite();
+      if (applied) theta_t = nesterov_step(outer, theta_t, red.delta);
+      theta_local = theta_t;
+      CHECK(eng.outer_step(solo, prec) == applied);
+    }
+    CHECK(eng.download(DLC_THETA_T) == theta_t && eng.download(DLC_THETA_LOCAL) == theta_local);
+    CHECK(eng.download(DLC_MOMENTUM) == outer.momentum_buf);
+    // a reduction tagged with the wrong epoch is a CollectiveError (engine.cpp:129-134)
+    std::vector<float> zeros(n, 0.0f);
+    dlc_outer_result r{};
+    CHECK(dlc_engine_apply_outer_step(eng.handle(), zeros.data(), 99, &r) == DLC_ECOLLECTIVE);
+    // a non-finite mean skips Nesterov but re-snapshots theta_local (engine.cpp:136-144)
+    std::vector<float> bad(n, 0.0f);
+    bad[3] = NAN;
+    CHECK(dlc_engine_apply_outer_step(eng.handle(), bad.data(), eng.scalars().outer_epoch, &r) == DLC_OK);
+    CHECK(r.applied == 0 && eng.download(DLC_THETA_T) == theta_t && eng.download(DLC_THETA_LOCAL) == theta_t);
+  }
   std::printf("test_dropin: %d passed, %d failed\n", g_pass, g_fail);
   return g_fail == 0 ? 0 : 1;
 }
