@@ -59,6 +59,22 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
+def ncu_traffic(kernel_prefix: str, n: int, launches: int = 1):
+    """DRAM read+write bytes of the kernel per step from the committed ncu capture
+    (profiles/ncu_traffic.json, tools/ncu_summary.py), when it was taken at the same size."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            d = json.load(f)
+    except Exception:
+        return None
+    if int(d.get("params", -1)) != n:
+        return None
+    for k, v in d.get("bytes_per_launch", {}).items():
+        if k.startswith(kernel_prefix):
+            return v * launches
+    return None
+
+
 def measured_peak():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -292,13 +308,16 @@ def run_ours(args):
         rl["kernel"] = "nesterov_outer%s_kernel (K4)" % ("_p2p" if mode == D.MODE_P2P else "")
         line["phases_ms"] = {"pseudo_grad_K2": k2_ms, "collective_C1_K3": coll_ms, "nesterov_K4": k4_ms}
         line["phase_roofline"] = {"pseudo_grad_K2": roof(b_k2, k2_ms)["frac"], "nesterov_K4": rl["frac"]}
-    rl["traffic"] = None
+    rl["traffic"] = ncu_traffic("outer_solo_kernel" if k == 1 else "nesterov_", n)
+    if k > 1 and rl["traffic"] is not None:
+        rl["traffic"] = None  # the committed capture is single-GPU; multi-rank ncu is not run
     line["roofline"] = rl
     if k > 1:
         wire_bytes = 2 * (k - 1) * (-(-n // k)) * wire
         line["nccl_bus_gbs"] = wire_bytes / (coll_ms * 1e-3) / 1e9 if coll_ms else None
     ir = roof(b_k1, k1_ms)
     ir["kernel"] = "adamw_kernel (K1, %s)" % args.inner_mode
+    ir["traffic"] = ncu_traffic("adamw_kernel", n)
     line["inner_adamw"] = {"ms_per_step": inner_ms, "kernel_ms": k1_ms, "roofline": ir,
                            "vs_8TBs_spec": ir["achieved"] / 8000.0}
     # outer: fused solo + recovery (K=1) or K2 + fold/check + K4; inner: K1 (+ pre-pass in place)

@@ -91,6 +91,8 @@ struct dlc_engine {
   std::vector<cudaEvent_t> chunk_ev;
   // pipelined P2P: high-priority stream for barriers + owner folds, per-piece events
   cudaStream_t cstream = nullptr;
+  cudaStream_t pull[kMaxK] = {};  // copy-engine pulls of peers' delta slices
+  cudaStream_t gath[kMaxK] = {};  // copy-engine pulls of owners' mean slices
   std::vector<cudaEvent_t> piece_ev;
 };
 
@@ -408,39 +410,56 @@ void outer_collective(dlc_engine* e, dlc_collective* c, dlc_reduce_report* rep) 
   }
 }
 
-// DLC_MODE_P2P, software-pipelined over P = p2p_pieces() pieces (kernels.cuh):
-//   main stream : K2(0..P-1), then K4(p) as soon as fold(p) is final, finish
-//   cstream     : B0, fold(0), B1, fold(1), ..., fold(P-1), B_P   (high priority)
-// where B_p is a 4-byte NCCL all-reduce: B_0 orders every rank's K2(0) (and
-// its previous step's finish) before any fold; B_{p+1} orders every fold(p)
-// and every K2(p+1) before the K4(p) that reads the owners' slots.  NVLink
-// traffic of fold(p) overlaps the HBM traffic of K2(p+1) and K4(p-1).
-// With host buffers (`hsrc`/`hdst`), piece p is also copied in before K2(p) and
-// its new theta_t copied out after K4(p), overlapping PCIe both ways.
+// DLC_MODE_P2P: the rank-ordered owner fold with the bytes moved by the DMA
+// copy engines over NVLink (pulls from CUDA-IPC peer pointers), pipelined over
+// P = p2p_pieces() pieces, piece p being a sub-range of every owner slot:
+//   main       K2(p)                                              -> evK2[p]
+//   cstream    wait evK2[p]; A_p (4-byte NCCL all-reduce)         -> evA[p]
+//   pull[j]    wait evA[p];  recv row j <- rank j's send (slot r, piece p)
+//   cstream    wait pulls;   fold(p) -> my gather slot + my flag; B_p -> evB[p]
+//   gath[q]    wait evB[p];  gather slot q <- owner q's gather slot (piece p)
+//   main       wait gathers; K4(p) speculative;  ...;  finish (all owner flags)
+// Copy engines need no SMs, so the NVLink time of piece p overlaps the HBM
+// kernels of pieces p-1 / p+1.  A_p orders every rank's K2(p) (and, for p = 0,
+// every rank's previous finish) before anyone pulls; B_p orders every fold(p)
+// before anyone gathers.  flags[r] (read remotely by every finish) is only
+// cleared after A_0.  With host buffers (`hsrc` / `hdst`) piece p is also
+// copied in before K2(p) and its new theta_t copied out after K4(p).
 void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc_reduce_report* rep,
                          const float* hsrc, float* hdst, int oc_host) {
   p2p_bind(e, c);
+  const size_t K = e->k, S = e->S, w = elem_width(e->prec), n = e->n;
+  const int r = c->rank;
   if (!e->cstream) {
     int lo = 0, hi = 0;
     DLC_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     DLC_CUDA(cudaStreamCreateWithPriority(&e->cstream, cudaStreamNonBlocking, hi));
+    for (size_t j = 0; j < K; ++j) {
+      DLC_CUDA(cudaStreamCreateWithFlags(&e->pull[j], cudaStreamNonBlocking));
+      DLC_CUDA(cudaStreamCreateWithFlags(&e->gath[j], cudaStreamNonBlocking));
+    }
   }
-  const size_t P = p2p_pieces();
-  while (e->piece_ev.size() < 4 * P + 2) {
+  const size_t P = p2p_pieces(), Sp = S / P;
+  const size_t nev = 5 * P + 2 * K * P + 1;
+  while (e->piece_ev.size() < nev) {
     cudaEvent_t ev;
     DLC_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     e->piece_ev.push_back(ev);
   }
   cudaEvent_t* evK2 = e->piece_ev.data();
-  cudaEvent_t* evF = evK2 + P;
-  cudaEvent_t* evH = evF + P;
+  cudaEvent_t* evA = evK2 + P;
+  cudaEvent_t* evB = evA + P;
+  cudaEvent_t* evH = evB + P;
   cudaEvent_t* evK4 = evH + P;
-  cudaEvent_t evStart = evK4[P];
-  const size_t K = e->k, S = e->S, Sp = S / P, w = elem_width(e->prec), n = e->n;
-  const int r = c->rank;
+  cudaEvent_t* evPull = evK4 + P;       // [j * P + p]
+  cudaEvent_t* evGath = evPull + K * P;  // [q * P + p]
+  cudaEvent_t evStart = evGath[K * P];
   float* s = const_cast<float*>(src);
   const Pair tl = s ? Pair{{s, s}} : local_pair(e);
   const float lr = e->hyper.outer_lr, mu = e->hyper.outer_momentum;
+  char* send = static_cast<char*>(e->send);
+  char* recv = static_cast<char*>(e->recv);
+  char* gather = static_cast<char*>(e->gather);
   auto rows = [&](size_t p, auto&& fn) {  // piece p of every owner slot, clipped to n
     for (size_t q = 0; q < K; ++q) {
       const size_t lo = q * S + p * Sp;
@@ -468,42 +487,57 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
   }
   launched("pseudo_grad_piece");
   phase_end(e, DLC_PHASE_PSEUDO);
-  // collective stream: barriers + owner folds straight out of every rank's send buffer
   DLC_CUDA(cudaStreamWaitEvent(e->cstream, evStart, 0));
   cudaEvent_t c0 = pooled_event(e), c1 = pooled_event(e);
   DLC_CUDA(cudaEventRecord(c0, e->cstream));
-  DLC_CUDA(cudaStreamWaitEvent(e->cstream, evK2[0], 0));
-  DLC_NCCL(ncclAllReduce(e->barrier_buf, e->barrier_buf, 1, ncclInt32, ncclSum, c->comm, e->cstream));
-  PtrList pflags{};  // my flag slot r in every rank's flag array (reset by each rank before its K2)
-  for (size_t q = 0; q < K; ++q) pflags.ptr[q] = e->peer_flags[q] + r;
   for (size_t p = 0; p < P; ++p) {
-    // pull piece p of slot r from every rank (rank order), push the mean into
-    // slot r of every rank's gather buffer
-    PtrList in{}, outs{};
-    for (size_t j = 0; j < K; ++j) in.ptr[j] = static_cast<char*>(e->peer_send[j]) + (r * S + p * Sp) * w;
-    for (size_t q = 0; q < K; ++q) outs.ptr[q] = static_cast<char*>(e->peer_gather[q]) + (r * S + p * Sp) * w;
-    launch_fold_push(in, (int)K, e->prec, outs, (int)K, pflags, Sp, e->cstream);
-    if (p + 1 < P) DLC_CUDA(cudaStreamWaitEvent(e->cstream, evK2[p + 1], 0));
-    DLC_NCCL(ncclAllReduce(e->barrier_buf, e->barrier_buf, 1, ncclInt32, ncclSum, c->comm, e->cstream));
-    DLC_CUDA(cudaEventRecord(evF[p], e->cstream));
+    DLC_CUDA(cudaStreamWaitEvent(e->cstream, evK2[p], 0));
+    DLC_NCCL(ncclAllReduce(e->barrier_buf, e->barrier_buf, 1, ncclInt32, ncclSum, c->comm, e->cstream));  // A_p
+    if (p == 0) DLC_CUDA(cudaMemsetAsync(e->flags + r, 0, sizeof(int), e->cstream));
+    DLC_CUDA(cudaEventRecord(evA[p], e->cstream));
+    for (size_t j = 0; j < K; ++j) {  // scatter: pull slot r, piece p of every peer's delta
+      if ((int)j == r) continue;
+      DLC_CUDA(cudaStreamWaitEvent(e->pull[j], evA[p], 0));
+      DLC_CUDA(cudaMemcpyAsync(recv + (j * S + p * Sp) * w, static_cast<char*>(e->peer_send[j]) + (r * S + p * Sp) * w,
+                               Sp * w, cudaMemcpyDefault, e->pull[j]));
+      DLC_CUDA(cudaEventRecord(evPull[j * P + p], e->pull[j]));
+      DLC_CUDA(cudaStreamWaitEvent(e->cstream, evPull[j * P + p], 0));
+    }
+    PtrList in{};  // owner fold in rank order (collective.cpp:1444-1489)
+    for (size_t j = 0; j < K; ++j)  // my own contribution straight from my send buffer
+      in.ptr[j] = ((int)j == r ? send + (r * S + p * Sp) * w : recv + (j * S + p * Sp) * w);
+    launch_fold(in, (int)K, e->prec, gather + (r * S + p * Sp) * w, e->prec, e->flags + r, Sp, e->cstream);
+    DLC_NCCL(ncclAllReduce(e->barrier_buf, e->barrier_buf, 1, ncclInt32, ncclSum, c->comm, e->cstream));  // B_p
+    DLC_CUDA(cudaEventRecord(evB[p], e->cstream));
+    for (size_t q = 0; q < K; ++q) {  // all-gather: pull piece p of every owner's mean slot
+      if ((int)q == r) continue;
+      DLC_CUDA(cudaStreamWaitEvent(e->gath[q], evB[p], 0));
+      DLC_CUDA(cudaMemcpyAsync(gather + (q * S + p * Sp) * w,
+                               static_cast<char*>(e->peer_gather[q]) + (q * S + p * Sp) * w, Sp * w,
+                               cudaMemcpyDefault, e->gath[q]));
+      DLC_CUDA(cudaEventRecord(evGath[q * P + p], e->gath[q]));
+    }
   }
   launched("fold_p2p");
   DLC_CUDA(cudaEventRecord(c1, e->cstream));
-  if (e->timing) e->pending.push_back({DLC_PHASE_COLLECTIVE, c0, c1});
-  else {
+  if (e->timing) {
+    e->pending.push_back({DLC_PHASE_COLLECTIVE, c0, c1});
+  } else {
     e->pool.push_back(c0);
     e->pool.push_back(c1);
   }
   if (rep) DLC_CUDA(cudaEventRecord(e->ev1, e->cstream));
-  // K4 pieces, speculative into the idle theta_t / momentum buffers
-  PtrList slots{}, fl{};  // every owner's mean and flag, now local
+  // K4 pieces on the local gather buffer, speculative into the idle theta_t / momentum
+  PtrList slots{}, fl{};
   for (size_t q = 0; q < K; ++q) {
-    slots.ptr[q] = static_cast<char*>(e->gather) + q * S * w;
-    fl.ptr[q] = e->flags + q;
+    slots.ptr[q] = gather + q * S * w;
+    fl.ptr[q] = e->peer_flags[q] + q;  // owner q's flag lives in owner q's memory
   }
   phase_begin(e);
   for (size_t p = 0; p < P; ++p) {
-    DLC_CUDA(cudaStreamWaitEvent(e->stream, evF[p], 0));
+    DLC_CUDA(cudaStreamWaitEvent(e->stream, evB[p], 0));
+    for (size_t q = 0; q < K; ++q)
+      if ((int)q != r) DLC_CUDA(cudaStreamWaitEvent(e->stream, evGath[q * P + p], 0));
     launch_nesterov_p2p_piece(tt_pair(e), buf_pair(e), local_pair(e), slots, (int)K, S, p * Sp, Sp, e->prec, e->st,
                               lr, mu, n, e->stream);
     if (hdst) {
@@ -521,6 +555,10 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
 }
 
 void outer_round(dlc_engine* e, dlc_collective* c, const float* src, dlc_reduce_report* rep) {
+  if (e->k > 1 && c->mode == DLC_MODE_P2P) {  // manages its own flag (read remotely by peers)
+    outer_p2p_pipelined(e, c, src, rep, nullptr, nullptr, 0);
+    return;
+  }
   reset_flags(e);
   if (e->k == 1) {
     phase_begin(e);
@@ -528,10 +566,6 @@ void outer_round(dlc_engine* e, dlc_collective* c, const float* src, dlc_reduce_
                             e->hyper.outer_momentum, e->n, e->stream);
     phase_end(e, DLC_PHASE_OUTER);
     launched("outer_solo");
-    return;
-  }
-  if (c->mode == DLC_MODE_P2P) {
-    outer_p2p_pipelined(e, c, src, rep, nullptr, nullptr, 0);
     return;
   }
   float* s = const_cast<float*>(src);
@@ -700,6 +734,12 @@ int dlc_engine_destroy(dlc_engine* e) {
     if (e->ev0) cudaEventDestroy(e->ev0);
     if (e->ev1) cudaEventDestroy(e->ev1);
     for (cudaEvent_t ev : e->chunk_ev) cudaEventDestroy(ev);
+    for (cudaEvent_t ev : e->piece_ev) cudaEventDestroy(ev);
+    for (size_t j = 0; j < (size_t)kMaxK; ++j) {
+      if (e->pull[j]) cudaStreamDestroy(e->pull[j]);
+      if (e->gath[j]) cudaStreamDestroy(e->gath[j]);
+    }
+    if (e->cstream) cudaStreamDestroy(e->cstream);
     if (e->h2d) cudaStreamDestroy(e->h2d);
     if (e->d2h) cudaStreamDestroy(e->d2h);
     if (e->stream) cudaStreamDestroy(e->stream);
@@ -888,7 +928,6 @@ int dlc_engine_outer_step_host(dlc_engine* e, dlc_collective* c, const float* ho
     ensure_copy_streams(e);
     const DevState s0 = read_state(e);
     if (e->k > 1 && c->mode == DLC_MODE_P2P) {  // piece-pipelined H2D / step / D2H
-      reset_flags(e);
       outer_p2p_pipelined(e, c, e->grad, nullptr, host_theta_local, host_theta_t, s0.ocur);
       DLC_CUDA(cudaStreamSynchronize(e->h2d));
       DLC_CUDA(cudaStreamSynchronize(e->d2h));

@@ -431,3 +431,36 @@ def test_outer_step_host_buffers_chunked(port, prec):
     assert np.array_equal(bits(e.download(A.THETA_LOCAL)), bits(w.theta_t))
     assert np.array_equal(bits(e.download(A.THETA_T)), bits(w.theta_t))
     e.close()
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+def test_external_collective_outer_step(port, prec):
+    """compute_pseudo_gradient -> any host collective (here reduce_average) -> apply_outer_step:
+    the split the reference's SocketCollective needs between boxes."""
+    n, k = 30_011, 3
+    hyper = DR.Hyper()
+    theta0 = O.rng_fill(6, "theta", 0, n, -1, 1)
+    locs = [(theta0 - O.rng_fill(6, "local", j, n, -1e-3, 1e-3)).astype(np.float32) for j in range(k)]
+    engines = [D.DilocoEngine(D.DilocoConfig(1, k, prec, 1), D.OptimHyperparams(), n) for _ in range(k)]
+    deltas = []
+    for e, loc in zip(engines, locs):
+        e.upload(A.THETA_T, theta0)
+        e.upload(A.THETA_LOCAL, loc)
+        d, ep = e.compute_pseudo_gradient()
+        assert ep == 0
+        deltas.append(d)
+    _, mean = port.reduce_average(deltas, prec)
+    ws = DR.make_workers(theta0, k, hyper)
+    for w, loc in zip(ws, locs):
+        w.theta_local = loc.copy()
+    dbar, applied, ref_deltas = DR.outer_round(port, ws, prec, hyper)
+    for d, rd in zip(deltas, ref_deltas):
+        assert np.array_equal(bits(d), bits(rd))
+    for e, w in zip(engines, ws):
+        r = e.apply_outer_step(mean, 0)
+        assert r.applied and r.outer_epoch == 1
+        assert np.array_equal(bits(e.download(A.THETA_T)), bits(w.theta_t))
+        assert np.array_equal(bits(e.download(A.THETA_LOCAL)), bits(w.theta_t))
+        with pytest.raises(D.CollectiveError):
+            e.apply_outer_step(mean, 0)  # stale epoch (engine.cpp:129-134)
+        e.close()
