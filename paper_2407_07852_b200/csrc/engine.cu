@@ -126,13 +126,24 @@ constexpr size_t kHostChunk = size_t(16) << 20;
 // cross-stream overlap), a tuning knob measured in profiles/.
 constexpr size_t kMaxPieces = 8;
 
+// (read on every step so a tuning sweep can change them in-process)
 size_t p2p_pieces() {
-  static const size_t p = [] {
-    const char* s = std::getenv("DLC_P2P_PIECES");
-    const long v = s ? std::strtol(s, nullptr, 10) : 1;
-    return (size_t)std::min<long>(std::max<long>(v, 1), (long)kMaxPieces);
-  }();
-  return p;
+  const char* s = std::getenv("DLC_P2P_PIECES");
+  const long v = s ? std::strtol(s, nullptr, 10) : 1;
+  return (size_t)std::min<long>(std::max<long>(v, 1), (long)kMaxPieces);
+}
+
+// Who moves the bytes in DLC_MODE_P2P: "sm" (default) = a persistent fold
+// kernel pulling deltas and pushing means over NVLink; "ce" = DMA copy engines.
+bool p2p_mover_sm() {
+  const char* s = std::getenv("DLC_P2P_COPY");
+  return !(s && std::string(s) == "ce");
+}
+
+// CTAs of the persistent SM mover (0 = one CTA per window, no SM partitioning).
+int comm_ctas() {
+  const char* s = std::getenv("DLC_COMM_CTAS");
+  return s ? (int)std::strtol(s, nullptr, 10) : 0;
 }
 
 void ensure_copy_streams(dlc_engine* e) {
@@ -468,6 +479,9 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
     }
   };
   if (rep) DLC_CUDA(cudaEventRecord(e->ev0, e->stream));
+  // SM mover: owners push non-finite marks into this array after A_0, which
+  // every rank reaches only after this memset (it precedes our K2(0))
+  if (p2p_mover_sm()) DLC_CUDA(cudaMemsetAsync(e->flags, 0, kMaxK * sizeof(int), e->stream));
   DLC_CUDA(cudaEventRecord(evStart, e->stream));
   if (hsrc) {
     ensure_copy_streams(e);
@@ -490,7 +504,24 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
   DLC_CUDA(cudaStreamWaitEvent(e->cstream, evStart, 0));
   cudaEvent_t c0 = pooled_event(e), c1 = pooled_event(e);
   DLC_CUDA(cudaEventRecord(c0, e->cstream));
-  for (size_t p = 0; p < P; ++p) {
+  const bool sm_mover = p2p_mover_sm();
+  for (size_t p = 0; p < P && sm_mover; ++p) {
+    // SM mover: a persistent fold kernel on a few CTAs pulls slot r / piece p of
+    // every rank's delta and pushes the mean (and a non-finite mark) into slot r
+    // of every rank's gather buffer (flags reset by each rank before its K2(0)).
+    DLC_CUDA(cudaStreamWaitEvent(e->cstream, evK2[p], 0));
+    DLC_NCCL(ncclAllReduce(e->barrier_buf, e->barrier_buf, 1, ncclInt32, ncclSum, c->comm, e->cstream));  // A_p
+    PtrList in{}, outs{}, pfl{};
+    for (size_t j = 0; j < K; ++j) {
+      in.ptr[j] = static_cast<char*>(e->peer_send[j]) + (r * S + p * Sp) * w;
+      outs.ptr[j] = static_cast<char*>(e->peer_gather[j]) + (r * S + p * Sp) * w;
+      pfl.ptr[j] = e->peer_flags[j] + r;
+    }
+    launch_fold_push(in, (int)K, e->prec, outs, (int)K, pfl, Sp, comm_ctas(), e->cstream);
+    DLC_NCCL(ncclAllReduce(e->barrier_buf, e->barrier_buf, 1, ncclInt32, ncclSum, c->comm, e->cstream));  // B_p
+    DLC_CUDA(cudaEventRecord(evB[p], e->cstream));
+  }
+  for (size_t p = 0; p < P && !sm_mover; ++p) {
     DLC_CUDA(cudaStreamWaitEvent(e->cstream, evK2[p], 0));
     DLC_NCCL(ncclAllReduce(e->barrier_buf, e->barrier_buf, 1, ncclInt32, ncclSum, c->comm, e->cstream));  // A_p
     if (p == 0) DLC_CUDA(cudaMemsetAsync(e->flags + r, 0, sizeof(int), e->cstream));
@@ -531,12 +562,14 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
   PtrList slots{}, fl{};
   for (size_t q = 0; q < K; ++q) {
     slots.ptr[q] = gather + q * S * w;
-    fl.ptr[q] = e->peer_flags[q] + q;  // owner q's flag lives in owner q's memory
+    // SM mover: owners pushed their marks into my flag array; CE mover: owner
+    // q's flag lives in owner q's memory
+    fl.ptr[q] = sm_mover ? e->flags + q : e->peer_flags[q] + q;
   }
   phase_begin(e);
   for (size_t p = 0; p < P; ++p) {
     DLC_CUDA(cudaStreamWaitEvent(e->stream, evB[p], 0));
-    for (size_t q = 0; q < K; ++q)
+    for (size_t q = 0; q < K && !sm_mover; ++q)
       if ((int)q != r) DLC_CUDA(cudaStreamWaitEvent(e->stream, evGath[q * P + p], 0));
     launch_nesterov_p2p_piece(tt_pair(e), buf_pair(e), local_pair(e), slots, (int)K, S, p * Sp, Sp, e->prec, e->st,
                               lr, mu, n, e->stream);

@@ -375,8 +375,10 @@ __global__ void __launch_bounds__(kThreads) fold_push_kernel(const __grid_consta
                                                              const __grid_constant__ PtrList flags, size_t n) {
   const float divisor = (float)k;  // reduce.cpp:36
   bool bad = false;
-  const size_t n8 = n / 8, i = gtid();
-  if (i < n8) {
+  const size_t n8 = n / 8;
+  // grid-stride: a persistent grid of a few CTAs leaves the other SMs to the
+  // HBM-bound K2 / K4 pieces running concurrently on the main stream
+  for (size_t i = gtid(); i < n8; i += gstride()) {
     float acc[8], x[8];
     load8<PREC>(in.ptr[0], i, acc);
     for (int j = 1; j < k; ++j) {
@@ -826,8 +828,8 @@ void launch_nesterov_outer(Pair tt, Pair buf, Pair tl, const void* dbar, int pre
 }
 
 void launch_fold_push(const PtrList& in, int k, int precision, const PtrList& outs, int nout, const PtrList& flags,
-                      size_t n, cudaStream_t s) {
-  const int grid = grid_window<1>(n / 8);
+                      size_t n, int ctas, cudaStream_t s) {
+  const int grid = ctas > 0 ? std::min(ctas, grid_window<1>(n / 8)) : grid_window<1>(n / 8);
   if (precision == 0)
     fold_push_kernel<0><<<grid, kThreads, 0, s>>>(in, k, outs, nout, flags, n);
   else

@@ -115,8 +115,9 @@ void launch_nesterov_outer(Pair theta_t, Pair buf, Pair theta_local,
 // launch_fold, the encoded mean stored to all `nout` destinations (this rank's
 // slot in every peer's gather buffer, posted NVLink writes) and a non-finite
 // mean marked by storing 1 to every `flags` entry; ends with a system fence.
+// `ctas` > 0 runs a persistent grid of that many CTAs (0: one CTA per window).
 void launch_fold_push(const PtrList& in, int k, int precision, const PtrList& outs, int nout,
-                      const PtrList& flags, size_t n, cudaStream_t s);
+                      const PtrList& flags, size_t n, int ctas, cudaStream_t s);
 void launch_pseudo_grad_piece(Pair theta_t, Pair theta_local, const DevState* st, void* send,
                               int precision, int k, size_t S, size_t po, size_t plen, size_t n,
                               cudaStream_t s);
