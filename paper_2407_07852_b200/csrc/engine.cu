@@ -122,14 +122,13 @@ void launched(const char* what) { DLC_LAUNCHED(what); }
 constexpr size_t kHostChunk = size_t(16) << 20;
 // Pieces of the pipelined P2P outer step (DLC_MODE_P2P).
 // Owner slots are a multiple of 64 * kMaxPieces elements; the number actually
-// used comes from DLC_P2P_PIECES (default 1: K2 -> fold+push -> K4, no
-// cross-stream overlap), a tuning knob measured in profiles/.
+// used comes from DLC_P2P_PIECES (default 4, profiles/r1_sweep_p2p_*.log).
 constexpr size_t kMaxPieces = 8;
 
 // (read on every step so a tuning sweep can change them in-process)
 size_t p2p_pieces() {
   const char* s = std::getenv("DLC_P2P_PIECES");
-  const long v = s ? std::strtol(s, nullptr, 10) : 1;
+  const long v = s ? std::strtol(s, nullptr, 10) : 4;
   return (size_t)std::min<long>(std::max<long>(v, 1), (long)kMaxPieces);
 }
 
@@ -140,10 +139,11 @@ bool p2p_mover_sm() {
   return !(s && std::string(s) == "ce");
 }
 
-// CTAs of the persistent SM mover (0 = one CTA per window, no SM partitioning).
+// CTAs of the persistent SM mover (0 = one CTA per window, no SM partitioning);
+// default 256 of the 1184 resident CTA slots (profiles/r1_sweep_p2p_*.log).
 int comm_ctas() {
   const char* s = std::getenv("DLC_COMM_CTAS");
-  return s ? (int)std::strtol(s, nullptr, 10) : 0;
+  return s ? (int)std::strtol(s, nullptr, 10) : 256;
 }
 
 void ensure_copy_streams(dlc_engine* e) {

@@ -38,9 +38,12 @@ def main():
         eng.rng_perturb(4242, "local", r.rank * 16 + i, -1e-3, 1e-3, dst_dev_ptr=x.data_ptr())
     stream = torch.cuda.ExternalStream(eng.stream, device=f"cuda:{r.local}")
     configs = [("ordered", None, None, None)]
-    for mover in ("sm", "ce"):
-        for pieces in (1, 2, 4, 8):
-            for ctas in ((0, 32, 64, 128, 256) if mover == "sm" else (0,)):
+    movers = os.environ.get("SWEEP_MOVERS", "sm,ce").split(",")
+    pieces_l = [int(x) for x in os.environ.get("SWEEP_PIECES", "1,2,4,8").split(",")]
+    ctas_l = [int(x) for x in os.environ.get("SWEEP_CTAS", "0,32,64,128,256").split(",")]
+    for mover in movers:
+        for pieces in pieces_l:
+            for ctas in (ctas_l if mover == "sm" else (0,)):
                 configs.append(("p2p", mover, pieces, ctas))
     results = []
     for mode, mover, pieces, ctas in configs:
