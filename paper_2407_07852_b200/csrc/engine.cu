@@ -91,6 +91,12 @@ struct dlc_engine {
   std::vector<cudaEvent_t> chunk_ev;
   // pipelined P2P: high-priority stream for barriers + owner folds, per-piece events
   cudaStream_t cstream = nullptr;
+  struct TraceMark {
+    const char* label;
+    int piece;
+    cudaEvent_t a, b;
+  };
+  std::vector<TraceMark> trace;  // DLC_TRACE=1: per-op timeline of the P2P step
   cudaStream_t pull[kMaxK] = {};  // copy-engine pulls of peers' delta slices
   cudaStream_t gath[kMaxK] = {};  // copy-engine pulls of owners' mean slices
   std::vector<cudaEvent_t> piece_ev;
@@ -140,10 +146,10 @@ bool p2p_mover_sm() {
 }
 
 // CTAs of the persistent SM mover (0 = one CTA per window, no SM partitioning);
-// default 256 of the 1184 resident CTA slots (profiles/r1_sweep_p2p_*.log).
+// default 512 of the 1184 resident CTA slots (profiles/r1_sweep_p2p_4gpu_ctas.log).
 int comm_ctas() {
   const char* s = std::getenv("DLC_COMM_CTAS");
-  return s ? (int)std::strtol(s, nullptr, 10) : 256;
+  return s ? (int)std::strtol(s, nullptr, 10) : 512;
 }
 
 void ensure_copy_streams(dlc_engine* e) {
@@ -197,6 +203,43 @@ void phase_end(dlc_engine* e, int phase) {
   cudaEvent_t b = pooled_event(e);
   DLC_CUDA(cudaEventRecord(b, e->stream));
   e->pending.push_back({phase, e->open_ev, b});
+}
+
+// DLC_TRACE=1: events around every op of the pipelined P2P step, printed to
+// stderr as a timeline (ms from the step start) once the step completes.
+bool tracing() {
+  const char* s = std::getenv("DLC_TRACE");
+  return s && s[0] == '1';
+}
+
+cudaEvent_t trace_begin(dlc_engine* e, cudaStream_t s) {
+  if (!tracing()) return nullptr;
+  cudaEvent_t a = pooled_event(e);
+  DLC_CUDA(cudaEventRecord(a, s));
+  return a;
+}
+
+void trace_end(dlc_engine* e, cudaStream_t s, const char* label, int piece, cudaEvent_t a) {
+  if (!a) return;
+  cudaEvent_t b = pooled_event(e);
+  DLC_CUDA(cudaEventRecord(b, s));
+  e->trace.push_back({label, piece, a, b});
+}
+
+void trace_dump(dlc_engine* e, cudaEvent_t origin) {
+  if (!origin) return;
+  DLC_CUDA(cudaDeviceSynchronize());
+  for (const auto& m : e->trace) {
+    float t0 = 0, t1 = 0;
+    DLC_CUDA(cudaEventElapsedTime(&t0, origin, m.a));
+    DLC_CUDA(cudaEventElapsedTime(&t1, origin, m.b));
+    std::fprintf(stderr, "[dlc trace dev%d] %-10s p%-2d %8.3f -> %8.3f ms (%.3f)\n", e->device, m.label, m.piece, t0,
+                 t1, t1 - t0);
+    e->pool.push_back(m.a);
+    e->pool.push_back(m.b);
+  }
+  e->trace.clear();
+  e->pool.push_back(origin);
 }
 
 // Host tables of the per-step scalars the reference computes on the host:
@@ -482,6 +525,7 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
   // SM mover: owners push non-finite marks into this array after A_0, which
   // every rank reaches only after this memset (it precedes our K2(0))
   if (p2p_mover_sm()) DLC_CUDA(cudaMemsetAsync(e->flags, 0, kMaxK * sizeof(int), e->stream));
+  cudaEvent_t origin = trace_begin(e, e->stream);
   DLC_CUDA(cudaEventRecord(evStart, e->stream));
   if (hsrc) {
     ensure_copy_streams(e);
@@ -496,7 +540,9 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
       DLC_CUDA(cudaEventRecord(evH[p], e->h2d));
       DLC_CUDA(cudaStreamWaitEvent(e->stream, evH[p], 0));
     }
+    cudaEvent_t t0 = trace_begin(e, e->stream);
     launch_pseudo_grad_piece(tt_pair(e), tl, e->st, e->send, e->prec, (int)K, S, p * Sp, Sp, n, e->stream);
+    trace_end(e, e->stream, "K2", (int)p, t0);
     DLC_CUDA(cudaEventRecord(evK2[p], e->stream));
   }
   launched("pseudo_grad_piece");
@@ -510,15 +556,21 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
     // every rank's delta and pushes the mean (and a non-finite mark) into slot r
     // of every rank's gather buffer (flags reset by each rank before its K2(0)).
     DLC_CUDA(cudaStreamWaitEvent(e->cstream, evK2[p], 0));
+    cudaEvent_t ta = trace_begin(e, e->cstream);
     DLC_NCCL(ncclAllReduce(e->barrier_buf, e->barrier_buf, 1, ncclInt32, ncclSum, c->comm, e->cstream));  // A_p
+    trace_end(e, e->cstream, "barrierA", (int)p, ta);
     PtrList in{}, outs{}, pfl{};
     for (size_t j = 0; j < K; ++j) {
       in.ptr[j] = static_cast<char*>(e->peer_send[j]) + (r * S + p * Sp) * w;
       outs.ptr[j] = static_cast<char*>(e->peer_gather[j]) + (r * S + p * Sp) * w;
       pfl.ptr[j] = e->peer_flags[j] + r;
     }
+    cudaEvent_t tf = trace_begin(e, e->cstream);
     launch_fold_push(in, (int)K, e->prec, outs, (int)K, pfl, Sp, comm_ctas(), e->cstream);
+    trace_end(e, e->cstream, "fold_push", (int)p, tf);
+    cudaEvent_t tb = trace_begin(e, e->cstream);
     DLC_NCCL(ncclAllReduce(e->barrier_buf, e->barrier_buf, 1, ncclInt32, ncclSum, c->comm, e->cstream));  // B_p
+    trace_end(e, e->cstream, "barrierB", (int)p, tb);
     DLC_CUDA(cudaEventRecord(evB[p], e->cstream));
   }
   for (size_t p = 0; p < P && !sm_mover; ++p) {
@@ -571,8 +623,10 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
     DLC_CUDA(cudaStreamWaitEvent(e->stream, evB[p], 0));
     for (size_t q = 0; q < K && !sm_mover; ++q)
       if ((int)q != r) DLC_CUDA(cudaStreamWaitEvent(e->stream, evGath[q * P + p], 0));
+    cudaEvent_t t4 = trace_begin(e, e->stream);
     launch_nesterov_p2p_piece(tt_pair(e), buf_pair(e), local_pair(e), slots, (int)K, S, p * Sp, Sp, e->prec, e->st,
                               lr, mu, n, e->stream);
+    trace_end(e, e->stream, "K4", (int)p, t4);
     if (hdst) {
       DLC_CUDA(cudaEventRecord(evK4[p], e->stream));
       DLC_CUDA(cudaStreamWaitEvent(e->d2h, evK4[p], 0));
@@ -585,6 +639,7 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
   launch_p2p_finish(tt_pair(e), local_pair(e), fl, (int)K, e->st, n, e->stream);
   phase_end(e, DLC_PHASE_OUTER);
   launched("nesterov_p2p_piece");
+  trace_dump(e, origin);
 }
 
 void outer_round(dlc_engine* e, dlc_collective* c, const float* src, dlc_reduce_report* rep) {
