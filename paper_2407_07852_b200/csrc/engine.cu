@@ -135,7 +135,9 @@ constexpr size_t kMaxPieces = 8;
 size_t p2p_pieces() {
   const char* s = std::getenv("DLC_P2P_PIECES");
   const long v = s ? std::strtol(s, nullptr, 10) : 4;
-  return (size_t)std::min<long>(std::max<long>(v, 1), (long)kMaxPieces);
+  size_t p = 1;  // a power of two <= kMaxPieces, so every piece is a whole number of 64-element vectors
+  while (p * 2 <= (size_t)std::min<long>(std::max<long>(v, 1), (long)kMaxPieces)) p *= 2;
+  return p;
 }
 
 // Who moves the bytes in DLC_MODE_P2P: "sm" (default) = a persistent fold
