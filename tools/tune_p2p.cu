@@ -14,9 +14,9 @@
 
 #define CK(x)                                                                             \
   do {                                                                                    \
-    cudaError_t e = (x);                                                                  \
-    if (e != cudaSuccess) {                                                               \
-      std::printf("CUDA error %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__); \
+    cudaError_t err_ = (x);                                                                  \
+    if (err_ != cudaSuccess) {                                                               \
+      std::printf("CUDA error %s at %s:%d\n", cudaGetErrorString(err_), __FILE__, __LINE__); \
       std::exit(1);                                                                       \
     }                                                                                     \
   } while (0)
@@ -78,6 +78,10 @@ int main(int argc, char** argv) {
   std::vector<uint4*> src(g), dst(g);
   std::vector<cudaStream_t> st(g);
   std::vector<std::vector<cudaStream_t>> ps(g, std::vector<cudaStream_t>(g));
+  for (int d = 0; d < g; ++d) {  // every primary context exists before peers are enabled
+    CK(cudaSetDevice(d));
+    CK(cudaFree(nullptr));
+  }
   for (int d = 0; d < g; ++d) {
     CK(cudaSetDevice(d));
     for (int e = 0; e < g; ++e)
