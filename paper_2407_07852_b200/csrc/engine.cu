@@ -85,6 +85,10 @@ struct dlc_engine {
   void* peer_send[kMaxK] = {};
   void* peer_gather[kMaxK] = {};
   int* peer_flags[kMaxK] = {};
+  uint64_t* sig = nullptr;  // flag-barrier signal slots, one per rank
+  uint64_t* peer_sig[kMaxK] = {};
+  uint64_t sig_epoch = 0;
+  int* sig_err = nullptr;
   std::vector<void*> ipc_opened;
   // host-buffer path: copy streams and per-chunk events
   cudaStream_t h2d = nullptr, d2h = nullptr;
@@ -368,12 +372,13 @@ void p2p_bind(dlc_engine* e, dlc_collective* c) {
   p2p_unbind(e);
   const int K = (int)e->k, r = c->rank;
   struct Handles {
-    cudaIpcMemHandle_t send, gather, flags;
+    cudaIpcMemHandle_t send, gather, flags, sig;
   };
   Handles mine;
   DLC_CUDA(cudaIpcGetMemHandle(&mine.send, e->send));
   DLC_CUDA(cudaIpcGetMemHandle(&mine.gather, e->gather));
   DLC_CUDA(cudaIpcGetMemHandle(&mine.flags, e->flags));
+  DLC_CUDA(cudaIpcGetMemHandle(&mine.sig, e->sig));
   const size_t sz = sizeof(Handles);
   char* dbuf = nullptr;
   DLC_CUDA(cudaMalloc(&dbuf, K * sz));
@@ -393,8 +398,14 @@ void p2p_bind(dlc_engine* e, dlc_collective* c) {
       e->peer_send[j] = e->send;
       e->peer_gather[j] = e->gather;
       e->peer_flags[j] = e->flags;
+      e->peer_sig[j] = e->sig;
       continue;
     }
+    void* psig = nullptr;
+    check_cuda(cudaIpcOpenMemHandle(&psig, all[j].sig, cudaIpcMemLazyEnablePeerAccess),
+               "cudaIpcOpenMemHandle (signal slots)");
+    e->ipc_opened.push_back(psig);
+    e->peer_sig[j] = (uint64_t*)psig;
     void* ps = nullptr;
     void* pg = nullptr;
     void* pf = nullptr;
@@ -415,6 +426,21 @@ void p2p_bind(dlc_engine* e, dlc_collective* c) {
 // Stream-ordered fleet barrier: a 4-byte NCCL all-reduce.
 void fleet_barrier(dlc_engine* e, dlc_collective* c) {
   DLC_NCCL(ncclAllReduce(e->barrier_buf, e->barrier_buf, 1, ncclInt32, ncclSum, c->comm, e->stream));
+}
+
+// Phase barrier of the P2P step on stream `s`: NVLink flags by default
+// (one CTA, a few microseconds), DLC_P2P_BARRIER=nccl for the NCCL all-reduce.
+void p2p_barrier(dlc_engine* e, dlc_collective* c, cudaStream_t s) {
+  const char* b = std::getenv("DLC_P2P_BARRIER");
+  if (b && std::string(b) == "nccl") {
+    DLC_NCCL(ncclAllReduce(e->barrier_buf, e->barrier_buf, 1, ncclInt32, ncclSum, c->comm, s));
+    return;
+  }
+  PtrList remote{};
+  for (size_t j = 0; j < e->k; ++j) remote.ptr[j] = e->peer_sig[j] + c->rank;
+  e->sig_epoch += 1;
+  launch_flag_barrier(remote, e->sig, (int)e->k, c->rank, e->sig_epoch, e->sig_err, s);
+  launched("flag_barrier");
 }
 
 // C1 + K3 on the engine's send buffer, then K4.  Everything is enqueued on the
@@ -559,7 +585,7 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
     // of every rank's gather buffer (flags reset by each rank before its K2(0)).
     DLC_CUDA(cudaStreamWaitEvent(e->cstream, evK2[p], 0));
     cudaEvent_t ta = trace_begin(e, e->cstream);
-    DLC_NCCL(ncclAllReduce(e->barrier_buf, e->barrier_buf, 1, ncclInt32, ncclSum, c->comm, e->cstream));  // A_p
+    p2p_barrier(e, c, e->cstream);  // A_p
     trace_end(e, e->cstream, "barrierA", (int)p, ta);
     PtrList in{}, outs{}, pfl{};
     for (size_t j = 0; j < K; ++j) {
@@ -571,13 +597,13 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
     launch_fold_push(in, (int)K, e->prec, outs, (int)K, pfl, Sp, comm_ctas(), e->cstream);
     trace_end(e, e->cstream, "fold_push", (int)p, tf);
     cudaEvent_t tb = trace_begin(e, e->cstream);
-    DLC_NCCL(ncclAllReduce(e->barrier_buf, e->barrier_buf, 1, ncclInt32, ncclSum, c->comm, e->cstream));  // B_p
+    p2p_barrier(e, c, e->cstream);  // B_p
     trace_end(e, e->cstream, "barrierB", (int)p, tb);
     DLC_CUDA(cudaEventRecord(evB[p], e->cstream));
   }
   for (size_t p = 0; p < P && !sm_mover; ++p) {
     DLC_CUDA(cudaStreamWaitEvent(e->cstream, evK2[p], 0));
-    DLC_NCCL(ncclAllReduce(e->barrier_buf, e->barrier_buf, 1, ncclInt32, ncclSum, c->comm, e->cstream));  // A_p
+    p2p_barrier(e, c, e->cstream);  // A_p
     if (p == 0) DLC_CUDA(cudaMemsetAsync(e->flags + r, 0, sizeof(int), e->cstream));
     DLC_CUDA(cudaEventRecord(evA[p], e->cstream));
     for (size_t j = 0; j < K; ++j) {  // scatter: pull slot r, piece p of every peer's delta
@@ -592,7 +618,7 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
     for (size_t j = 0; j < K; ++j)  // my own contribution straight from my send buffer
       in.ptr[j] = ((int)j == r ? send + (r * S + p * Sp) * w : recv + (j * S + p * Sp) * w);
     launch_fold(in, (int)K, e->prec, gather + (r * S + p * Sp) * w, e->prec, e->flags + r, Sp, e->cstream);
-    DLC_NCCL(ncclAllReduce(e->barrier_buf, e->barrier_buf, 1, ncclInt32, ncclSum, c->comm, e->cstream));  // B_p
+    p2p_barrier(e, c, e->cstream);  // B_p
     DLC_CUDA(cudaEventRecord(evB[p], e->cstream));
     for (size_t q = 0; q < K; ++q) {  // all-gather: pull piece p of every owner's mean slot
       if ((int)q == r) continue;
@@ -692,8 +718,19 @@ void check_collective(dlc_engine* e, dlc_collective* c) {
                          ", H " + std::to_string(e->cfg.local_steps_h) + ")");
 }
 
+// A flag barrier that timed out (a peer never arrived) surfaces as CollectiveError.
+void check_barrier(dlc_engine* e) {
+  if (!e->sig_err) return;
+  int err = 0;
+  DLC_CUDA(cudaStreamSynchronize(e->stream));
+  if (e->cstream) DLC_CUDA(cudaStreamSynchronize(e->cstream));
+  DLC_CUDA(cudaMemcpy(&err, e->sig_err, sizeof(int), cudaMemcpyDeviceToHost));
+  if (err) fail(DLC_ECOLLECTIVE, "P2P barrier timed out: a peer rank stopped participating");
+}
+
 void outer_result(dlc_engine* e, dlc_outer_result* res) {
-  if (!res) return;
+  if (!res) return;  // asynchronous call: nothing is synchronised here
+  check_barrier(e);
   const DevState s = read_state(e);
   res->applied = s.last_applied;
   res->outer_epoch = s.outer_epoch;
@@ -777,6 +814,10 @@ int dlc_engine_create(const dlc_config* cfg, const dlc_hyperparams* hyper, size_
       e->gather = dalloc(e, pb);
       DLC_CUDA(cudaMemsetAsync(e->gather, 0, pb, e->stream));
       e->barrier_buf = (int*)dalloc(e, 256);
+      e->sig = (uint64_t*)dalloc(e, kMaxK * sizeof(uint64_t));
+      e->sig_err = (int*)dalloc(e, 256);
+      DLC_CUDA(cudaMemsetAsync(e->sig, 0, kMaxK * sizeof(uint64_t), e->stream));
+      DLC_CUDA(cudaMemsetAsync(e->sig_err, 0, 256, e->stream));
     }
     e->flags = (int*)dalloc(e, kMaxK * sizeof(int));
     e->st = (DevState*)dalloc(e, sizeof(DevState));
@@ -921,6 +962,7 @@ int dlc_engine_synchronize(dlc_engine* e) {
     if (!e) fail(DLC_EINVAL, "dlc_engine_synchronize: null engine");
     DeviceGuard dg(e->device);
     DLC_CUDA(cudaStreamSynchronize(e->stream));
+    check_barrier(e);
   });
 }
 

@@ -498,6 +498,26 @@ __global__ void __launch_bounds__(kThreads) nesterov_outer_kernel(Pair ttp, Pair
   if (blockIdx.x == 0 && threadIdx.x == 0) k4_finalize(st, applied);
 }
 
+// ---- NVLink flag barrier ----------------------------------------------------
+__global__ void flag_barrier_kernel(const __grid_constant__ PtrList remote, const uint64_t* local, int k, int me,
+                                    uint64_t epoch, int* err) {
+  const int j = threadIdx.x;
+  if (j < k && j != me) {
+    __threadfence_system();  // everything this GPU wrote before the barrier is visible first
+    *reinterpret_cast<volatile unsigned long long*>(const_cast<void*>(remote.ptr[j])) = epoch;
+    const long long start = clock64();
+    const volatile unsigned long long* mine = reinterpret_cast<const volatile unsigned long long*>(local + j);
+    while (*mine < epoch) {
+      if (clock64() - start > (1ll << 35)) {  // ~17 s at 2 GHz: a peer is gone
+        atomicExch(err, 1);
+        break;
+      }
+    }
+    __threadfence_system();
+  }
+  __syncthreads();
+}
+
 // ---- pipelined P2P pieces ----------------------------------------------------
 // CTA b covers owner q = b % K, vectors [(b / K) * 256, ...) of that owner's
 // piece, so every piece launch spreads over all slots.
@@ -834,6 +854,11 @@ void launch_fold_push(const PtrList& in, int k, int precision, const PtrList& ou
     fold_push_kernel<0><<<grid, kThreads, 0, s>>>(in, k, outs, nout, flags, n);
   else
     fold_push_kernel<1><<<grid, kThreads, 0, s>>>(in, k, outs, nout, flags, n);
+}
+
+void launch_flag_barrier(const PtrList& remote, const uint64_t* local, int k, int me, uint64_t epoch, int* err,
+                         cudaStream_t s) {
+  flag_barrier_kernel<<<1, 32, 0, s>>>(remote, local, k, me, epoch, err);
 }
 
 void launch_pseudo_grad_piece(Pair tt, Pair tl, const DevState* st, void* send, int precision, int k, size_t S,

@@ -118,6 +118,12 @@ void launch_nesterov_outer(Pair theta_t, Pair buf, Pair theta_local,
 // `ctas` > 0 runs a persistent grid of that many CTAs (0: one CTA per window).
 void launch_fold_push(const PtrList& in, int k, int precision, const PtrList& outs, int nout,
                       const PtrList& flags, size_t n, int ctas, cudaStream_t s);
+// Fleet barrier over NVLink flags (DLC_MODE_P2P): one CTA stores `epoch` into
+// slot `me` of every peer's signal array (`remote`, after a system fence), then
+// waits until every peer's store has landed in `local`.  A peer silent for
+// ~10 s sets *err and the kernel exits instead of hanging the GPU.
+void launch_flag_barrier(const PtrList& remote, const uint64_t* local, int k, int me, uint64_t epoch,
+                         int* err, cudaStream_t s);
 void launch_pseudo_grad_piece(Pair theta_t, Pair theta_local, const DevState* st, void* send,
                               int precision, int k, size_t S, size_t po, size_t plen, size_t n,
                               cudaStream_t s);

@@ -1,6 +1,7 @@
 """Multi-GPU parity (NCCL over NVLink): one process per GPU via torchrun.
 
-Runs tests/mp_gpu_worker.py on min(4, #GPUs) ranks; skipped on a 1-GPU box.
+Runs tests/mp_gpu_worker.py on 2, 3 and 4 ranks (3 = a non-power-of-two fleet
+with ragged owner slots); each case is skipped when the box has fewer GPUs.
 """
 import os
 import subprocess
@@ -21,7 +22,7 @@ def gpus():
         return 0
 
 
-@pytest.mark.parametrize("nproc", [2, 4])
+@pytest.mark.parametrize("nproc", [2, 3, 4])
 def test_multigpu_parity(nproc):
     if gpus() < nproc:
         pytest.skip(f"needs {nproc} GPUs")
