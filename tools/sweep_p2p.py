@@ -37,20 +37,23 @@ def main():
     for i, x in enumerate(xs):
         eng.rng_perturb(4242, "local", r.rank * 16 + i, -1e-3, 1e-3, dst_dev_ptr=x.data_ptr())
     stream = torch.cuda.ExternalStream(eng.stream, device=f"cuda:{r.local}")
-    configs = [("ordered", None, None, None)]
+    configs = [("ordered", None, None, None, None)]
     movers = os.environ.get("SWEEP_MOVERS", "sm,ce").split(",")
     pieces_l = [int(x) for x in os.environ.get("SWEEP_PIECES", "1,2,4,8").split(",")]
     ctas_l = [int(x) for x in os.environ.get("SWEEP_CTAS", "0,32,64,128,256").split(",")]
-    for mover in movers:
-        for pieces in pieces_l:
-            for ctas in (ctas_l if mover == "sm" else (0,)):
-                configs.append(("p2p", mover, pieces, ctas))
+    barriers = os.environ.get("SWEEP_BARRIERS", "flag").split(",")
+    for barrier in barriers:
+        for mover in movers:
+            for pieces in pieces_l:
+                for ctas in (ctas_l if mover == "sm" else (0,)):
+                    configs.append(("p2p", mover, pieces, ctas, barrier))
     results = []
-    for mode, mover, pieces, ctas in configs:
+    for mode, mover, pieces, ctas, barrier in configs:
         if mover:
             os.environ["DLC_P2P_COPY"] = mover
             os.environ["DLC_P2P_PIECES"] = str(pieces)
             os.environ["DLC_COMM_CTAS"] = str(ctas)
+            os.environ["DLC_P2P_BARRIER"] = barrier
         c = colls[mode]
         for s in range(2):
             eng.outer_step_from(c, xs[s % 2].data_ptr())
@@ -63,7 +66,7 @@ def main():
         e1.record(stream)
         e1.synchronize()
         ms = PD.max_over_ranks(e0.elapsed_time(e1) / a.steps, r.world)
-        results.append({"mode": mode, "mover": mover, "pieces": pieces, "ctas": ctas, "ms": ms})
+        results.append({"mode": mode, "mover": mover, "pieces": pieces, "ctas": ctas, "barrier": barrier, "ms": ms})
         if r.rank == 0:
             print(json.dumps(results[-1]), flush=True)
     eng.close()
