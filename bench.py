@@ -321,7 +321,18 @@ def run_ours(args):
     line["inner_adamw"] = {"ms_per_step": inner_ms, "kernel_ms": k1_ms, "roofline": ir,
                            "vs_8TBs_spec": ir["achieved"] / 8000.0}
     # outer: fused solo + recovery (K=1) or K2 + fold/check + K4; inner: K1 (+ pre-pass in place)
-    line["gpu_launches"] = args.steps * (3 if k > 1 else 2) + args.steps * (1 if args.inner_mode == "pingpong" else 2)
+    if k == 1:
+        per_outer = 2  # outer_solo + finish
+    elif mode == D.MODE_P2P:
+        pieces = 1
+        while pieces * 2 <= min(max(int(os.environ.get("DLC_P2P_PIECES", "4")), 1), 8):
+            pieces *= 2
+        flag = os.environ.get("DLC_P2P_BARRIER", "flag") != "nccl"
+        per_outer = 3 * pieces + 1 + (2 * pieces if flag else 0)  # K2, fold_push, K4 pieces, finish, barriers
+    else:
+        per_outer = 3  # K2, fold / non-finite check, K4
+    per_inner = 2 if args.inner_mode == "pingpong" else 3  # (pre-pass,) AdamW, finalize
+    line["gpu_launches"] = args.steps * (per_outer + per_inner)
     line["clocks"] = clk
 
     # e2e through the public C ABI with host buffers: H2D theta_local, outer step, D2H theta_t.
