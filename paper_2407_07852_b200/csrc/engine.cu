@@ -152,10 +152,10 @@ bool p2p_mover_sm() {
 }
 
 // CTAs of the persistent SM mover (0 = one CTA per window, no SM partitioning);
-// default 512 of the 1184 resident CTA slots (profiles/r1_sweep_p2p_4gpu_ctas.log).
+// default 384 of the 1184 resident CTA slots (profiles/r1_sweep_p2p_*_barrier.log).
 int comm_ctas() {
   const char* s = std::getenv("DLC_COMM_CTAS");
-  return s ? (int)std::strtol(s, nullptr, 10) : 512;
+  return s ? (int)std::strtol(s, nullptr, 10) : 384;
 }
 
 void ensure_copy_streams(dlc_engine* e) {
