@@ -312,8 +312,21 @@ def run_ours(args):
     if k > 1 and rl["traffic"] is not None:
         rl["traffic"] = None  # the committed capture is single-GPU; multi-rank ncu is not run
     line["roofline"] = rl
+    # whole-step roofline: HBM bytes at the measured copy peak and
+    # NVLink bytes per direction at the pool's measured 770 GB/s peer copy
+    # (B200_PROFILING.md); serial = sum, bound = max (perfect overlap).
+    nvlink_peak = 770.0
+    hbm_bpp = 24 if k == 1 else (b_k2 + b_k4)
+    wire_bytes = 2 * (k - 1) * (-(-n // k)) * wire if k > 1 else 0
+    hbm_ms = hbm_bpp * n / (peak * 1e9) * 1e3
+    nvl_ms = wire_bytes / (nvlink_peak * 1e9) * 1e3
+    line["step_roofline"] = {"hbm_bytes": hbm_bpp * n, "nvlink_bytes_per_direction": wire_bytes,
+                             "hbm_ms": hbm_ms, "nvlink_ms": nvl_ms, "serial_ms": hbm_ms + nvl_ms,
+                             "bound_ms": max(hbm_ms, nvl_ms), "frac_of_serial": (hbm_ms + nvl_ms) / ms_step,
+                             "frac_of_bound": max(hbm_ms, nvl_ms) / ms_step, "nvlink_peak_gbs": nvlink_peak,
+                             "hbm_peak_gbs": peak}
     if k > 1:
-        wire_bytes = 2 * (k - 1) * (-(-n // k)) * wire
+        line["nvlink_gbs_over_step"] = wire_bytes / (ms_step * 1e-3) / 1e9
         line["nccl_bus_gbs"] = wire_bytes / (coll_ms * 1e-3) / 1e9 if coll_ms else None
     ir = roof(b_k1, k1_ms)
     ir["kernel"] = "adamw_kernel (K1, %s)" % args.inner_mode
@@ -324,9 +337,12 @@ def run_ours(args):
     if k == 1:
         per_outer = 2  # outer_solo + finish
     elif mode == D.MODE_P2P:
-        pieces = 1
-        while pieces * 2 <= min(max(int(os.environ.get("DLC_P2P_PIECES", "4")), 1), 8):
-            pieces *= 2
+        if "DLC_P2P_PIECES" in os.environ and "DLC_P2P_PLAN" not in os.environ:
+            pieces = 1
+            while pieces * 2 <= min(max(int(os.environ["DLC_P2P_PIECES"]), 1), 8):
+                pieces *= 2
+        else:
+            pieces = len(os.environ.get("DLC_P2P_PLAN", "1,2,2,2,1").split(","))
         flag = os.environ.get("DLC_P2P_BARRIER", "flag") != "nccl"
         per_outer = 3 * pieces + 1 + (2 * pieces if flag else 0)  # K2, fold_push, K4 pieces, finish, barriers
     else:

@@ -144,6 +144,38 @@ size_t p2p_pieces() {
   return p;
 }
 
+// Piece boundaries inside an owner slot of S elements (S a multiple of
+// 64 * kMaxPieces): DLC_P2P_PLAN lists piece weights in eighths of a slot
+// (default "1,2,2,2,1": short first and last pieces shrink the pipeline's
+// fill (K2 of piece 0) and drain (K4 of the last piece)); DLC_P2P_PIECES asks
+// for equal pieces instead.
+std::vector<size_t> piece_plan(size_t S) {
+  std::vector<size_t> w;
+  const char* plan = std::getenv("DLC_P2P_PLAN");
+  if (plan || !std::getenv("DLC_P2P_PIECES")) {
+    std::string str = plan ? plan : "1,2,2,2,1";
+    size_t pos = 0, sum = 0;
+    while (pos <= str.size()) {
+      const size_t comma = str.find(',', pos);
+      const std::string tok = str.substr(pos, comma == std::string::npos ? std::string::npos : comma - pos);
+      const long v = std::strtol(tok.c_str(), nullptr, 10);
+      if (v <= 0) {
+        w.clear();
+        break;
+      }
+      w.push_back((size_t)v);
+      sum += (size_t)v;
+      if (comma == std::string::npos) break;
+      pos = comma + 1;
+    }
+    if (sum != kMaxPieces) w.clear();
+  }
+  if (w.empty()) w.assign(p2p_pieces(), kMaxPieces / p2p_pieces());
+  std::vector<size_t> b{0};
+  for (size_t x : w) b.push_back(b.back() + x * (S / kMaxPieces));
+  return b;
+}
+
 // Who moves the bytes in DLC_MODE_P2P: "sm" (default) = a persistent fold
 // kernel pulling deltas and pushing means over NVLink; "ce" = DMA copy engines.
 bool p2p_mover_sm() {
@@ -521,7 +553,10 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
       DLC_CUDA(cudaStreamCreateWithFlags(&e->gath[j], cudaStreamNonBlocking));
     }
   }
-  const size_t P = p2p_pieces(), Sp = S / P;
+  const std::vector<size_t> pb = piece_plan(S);  // piece boundaries inside a slot
+  const size_t P = pb.size() - 1;
+  auto po = [&](size_t p) { return pb[p]; };
+  auto pl = [&](size_t p) { return pb[p + 1] - pb[p]; };
   const size_t nev = 5 * P + 2 * K * P + 1;
   while (e->piece_ev.size() < nev) {
     cudaEvent_t ev;
@@ -544,9 +579,9 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
   char* gather = static_cast<char*>(e->gather);
   auto rows = [&](size_t p, auto&& fn) {  // piece p of every owner slot, clipped to n
     for (size_t q = 0; q < K; ++q) {
-      const size_t lo = q * S + p * Sp;
+      const size_t lo = q * S + po(p);
       if (lo >= n) break;
-      fn(lo, std::min(Sp, n - lo));
+      fn(lo, std::min(pl(p), n - lo));
     }
   };
   if (rep) DLC_CUDA(cudaEventRecord(e->ev0, e->stream));
@@ -569,7 +604,7 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
       DLC_CUDA(cudaStreamWaitEvent(e->stream, evH[p], 0));
     }
     cudaEvent_t t0 = trace_begin(e, e->stream);
-    launch_pseudo_grad_piece(tt_pair(e), tl, e->st, e->send, e->prec, (int)K, S, p * Sp, Sp, n, e->stream);
+    launch_pseudo_grad_piece(tt_pair(e), tl, e->st, e->send, e->prec, (int)K, S, po(p), pl(p), n, e->stream);
     trace_end(e, e->stream, "K2", (int)p, t0);
     DLC_CUDA(cudaEventRecord(evK2[p], e->stream));
   }
@@ -589,12 +624,12 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
     trace_end(e, e->cstream, "barrierA", (int)p, ta);
     PtrList in{}, outs{}, pfl{};
     for (size_t j = 0; j < K; ++j) {
-      in.ptr[j] = static_cast<char*>(e->peer_send[j]) + (r * S + p * Sp) * w;
-      outs.ptr[j] = static_cast<char*>(e->peer_gather[j]) + (r * S + p * Sp) * w;
+      in.ptr[j] = static_cast<char*>(e->peer_send[j]) + (r * S + po(p)) * w;
+      outs.ptr[j] = static_cast<char*>(e->peer_gather[j]) + (r * S + po(p)) * w;
       pfl.ptr[j] = e->peer_flags[j] + r;
     }
     cudaEvent_t tf = trace_begin(e, e->cstream);
-    launch_fold_push(in, (int)K, e->prec, outs, (int)K, pfl, Sp, comm_ctas(), e->cstream);
+    launch_fold_push(in, (int)K, e->prec, outs, (int)K, pfl, pl(p), comm_ctas(), e->cstream);
     trace_end(e, e->cstream, "fold_push", (int)p, tf);
     cudaEvent_t tb = trace_begin(e, e->cstream);
     p2p_barrier(e, c, e->cstream);  // B_p
@@ -609,22 +644,22 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
     for (size_t j = 0; j < K; ++j) {  // scatter: pull slot r, piece p of every peer's delta
       if ((int)j == r) continue;
       DLC_CUDA(cudaStreamWaitEvent(e->pull[j], evA[p], 0));
-      DLC_CUDA(cudaMemcpyAsync(recv + (j * S + p * Sp) * w, static_cast<char*>(e->peer_send[j]) + (r * S + p * Sp) * w,
-                               Sp * w, cudaMemcpyDefault, e->pull[j]));
+      DLC_CUDA(cudaMemcpyAsync(recv + (j * S + po(p)) * w, static_cast<char*>(e->peer_send[j]) + (r * S + po(p)) * w,
+                               pl(p) * w, cudaMemcpyDefault, e->pull[j]));
       DLC_CUDA(cudaEventRecord(evPull[j * P + p], e->pull[j]));
       DLC_CUDA(cudaStreamWaitEvent(e->cstream, evPull[j * P + p], 0));
     }
     PtrList in{};  // owner fold in rank order (collective.cpp:1444-1489)
     for (size_t j = 0; j < K; ++j)  // my own contribution straight from my send buffer
-      in.ptr[j] = ((int)j == r ? send + (r * S + p * Sp) * w : recv + (j * S + p * Sp) * w);
-    launch_fold(in, (int)K, e->prec, gather + (r * S + p * Sp) * w, e->prec, e->flags + r, Sp, e->cstream);
+      in.ptr[j] = ((int)j == r ? send + (r * S + po(p)) * w : recv + (j * S + po(p)) * w);
+    launch_fold(in, (int)K, e->prec, gather + (r * S + po(p)) * w, e->prec, e->flags + r, pl(p), e->cstream);
     p2p_barrier(e, c, e->cstream);  // B_p
     DLC_CUDA(cudaEventRecord(evB[p], e->cstream));
     for (size_t q = 0; q < K; ++q) {  // all-gather: pull piece p of every owner's mean slot
       if ((int)q == r) continue;
       DLC_CUDA(cudaStreamWaitEvent(e->gath[q], evB[p], 0));
-      DLC_CUDA(cudaMemcpyAsync(gather + (q * S + p * Sp) * w,
-                               static_cast<char*>(e->peer_gather[q]) + (q * S + p * Sp) * w, Sp * w,
+      DLC_CUDA(cudaMemcpyAsync(gather + (q * S + po(p)) * w,
+                               static_cast<char*>(e->peer_gather[q]) + (q * S + po(p)) * w, pl(p) * w,
                                cudaMemcpyDefault, e->gath[q]));
       DLC_CUDA(cudaEventRecord(evGath[q * P + p], e->gath[q]));
     }
@@ -652,7 +687,7 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
     for (size_t q = 0; q < K && !sm_mover; ++q)
       if ((int)q != r) DLC_CUDA(cudaStreamWaitEvent(e->stream, evGath[q * P + p], 0));
     cudaEvent_t t4 = trace_begin(e, e->stream);
-    launch_nesterov_p2p_piece(tt_pair(e), buf_pair(e), local_pair(e), slots, (int)K, S, p * Sp, Sp, e->prec, e->st,
+    launch_nesterov_p2p_piece(tt_pair(e), buf_pair(e), local_pair(e), slots, (int)K, S, po(p), pl(p), e->prec, e->st,
                               lr, mu, n, e->stream);
     trace_end(e, e->stream, "K4", (int)p, t4);
     if (hdst) {

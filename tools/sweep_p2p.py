@@ -42,16 +42,21 @@ def main():
     pieces_l = [int(x) for x in os.environ.get("SWEEP_PIECES", "1,2,4,8").split(",")]
     ctas_l = [int(x) for x in os.environ.get("SWEEP_CTAS", "0,32,64,128,256").split(",")]
     barriers = os.environ.get("SWEEP_BARRIERS", "flag").split(",")
+    plans = os.environ.get("SWEEP_PLANS", "").split(";") if os.environ.get("SWEEP_PLANS") else None
     for barrier in barriers:
         for mover in movers:
-            for pieces in pieces_l:
+            for pieces in (plans or pieces_l):
                 for ctas in (ctas_l if mover == "sm" else (0,)):
                     configs.append(("p2p", mover, pieces, ctas, barrier))
     results = []
     for mode, mover, pieces, ctas, barrier in configs:
         if mover:
             os.environ["DLC_P2P_COPY"] = mover
-            os.environ["DLC_P2P_PIECES"] = str(pieces)
+            if isinstance(pieces, str):
+                os.environ["DLC_P2P_PLAN"] = pieces
+            else:
+                os.environ.pop("DLC_P2P_PLAN", None)
+                os.environ["DLC_P2P_PIECES"] = str(pieces)
             os.environ["DLC_COMM_CTAS"] = str(ctas)
             os.environ["DLC_P2P_BARRIER"] = barrier
         c = colls[mode]
