@@ -464,3 +464,70 @@ def test_external_collective_outer_step(port, prec):
         with pytest.raises(D.CollectiveError):
             e.apply_outer_step(mean, 0)  # stale epoch (engine.cpp:129-134)
         e.close()
+
+
+# ---- engine properties mirrored from the reference's own tests ----------------------------
+
+def test_identity_transport_equals_bare_adamw(port):
+    """test_engine.cpp:213-241: K=1, H=1, outer lr=1, mu=0 DiLoCo == bare AdamW, bitwise, 60 steps."""
+    n = 4099
+    hyper = DR.Hyper(inner_lr=0.01, warmup_steps=5, weight_decay=0.0)
+    hp = D.OptimHyperparams(inner_lr=0.01, warmup_steps=5, weight_decay=0.0, outer_lr=1.0, outer_momentum=0.0)
+    e = D.DilocoEngine(D.DilocoConfig(1, 1, A.FP32, 60), hp, n)
+    theta0 = O.rng_fill(11, "theta", 0, n, -1, 1)
+    e.upload(A.THETA_T, theta0)
+    e.upload(A.THETA_LOCAL, theta0)
+    bare = DR.make_workers(theta0, 1, hyper)[0]
+    opt = D.DilocoOptimizer(e, None)
+    for t in range(60):
+        g = O.rng_fill(11, "grad", t, n, -1e-1, 1e-1)
+        e.upload(A.GRAD, g)
+        opt.step(e.device_ptr(A.GRAD), grad_is_scaled=False)
+        assert opt.round_just_completed
+        DR.inner_step(port, bare, g, hyper)
+        assert np.array_equal(bits(e.download(A.THETA_T)), bits(bare.theta_local)), t
+    e.close()
+
+
+def test_averaging_equivalence_local_fleet():
+    """test_engine.cpp:243-294: outer lr=1, mu=0 makes theta_t the mean of the workers' theta_local
+    (<= 1e-6 relative), identical on every worker."""
+    n, k = 20_011, 3
+    hp = D.OptimHyperparams(outer_lr=1.0, outer_momentum=0.0)
+    theta0 = O.rng_fill(12, "theta", 0, n, -1, 1)
+    engines = [D.DilocoEngine(D.DilocoConfig(1, k, A.FP32, 1), hp, n) for _ in range(k)]
+    locs = []
+    for j, e in enumerate(engines):
+        e.upload(A.THETA_T, theta0)
+        loc = (theta0 + O.rng_fill(12, "move", j, n, -1e-2, 1e-2)).astype(np.float32)
+        e.upload(A.THETA_LOCAL, loc)
+        locs.append(loc.astype(np.float64))
+    assert D.outer_step_local(engines).applied
+    mean = np.mean(np.stack(locs), axis=0)
+    t0 = engines[0].download(A.THETA_T)
+    assert np.all(np.abs(t0 - mean) / np.maximum(np.abs(mean), 1e-12) <= 1e-6)
+    for e in engines[1:]:
+        assert np.array_equal(bits(e.download(A.THETA_T)), bits(t0))
+    for e in engines:
+        e.close()
+
+
+def test_reruns_are_bitwise_deterministic():
+    """test_harness.cpp:135-146: identical inputs, identical bits on a second run."""
+    n = 1 << 18
+
+    def run():
+        e = D.DilocoEngine(D.DilocoConfig(3, 1, A.FP16, 9), D.OptimHyperparams(warmup_steps=2), n)
+        e.rng_fill(A.THETA_T, 13, "theta", 0, -1, 1)
+        e.rng_fill(A.THETA_LOCAL, 13, "theta", 0, -1, 1)
+        opt = D.DilocoOptimizer(e, None)
+        for t in range(9):
+            e.rng_fill(A.GRAD, 13, "grad", t, -1e-2, 1e-2)
+            opt.step(e.device_ptr(A.GRAD), grad_is_scaled=False)
+        out = [e.download(w) for w in (A.THETA_T, A.THETA_LOCAL, A.ADAM_M, A.ADAM_V, A.MOMENTUM)]
+        e.close()
+        return out
+
+    a, b = run(), run()
+    for x, y in zip(a, b):
+        assert np.array_equal(bits(x), bits(y))
