@@ -471,10 +471,12 @@ def test_external_collective_outer_step(port, prec):
 def test_identity_transport_equals_bare_adamw(port):
     """test_engine.cpp:213-241: K=1, H=1, outer lr=1, mu=0 DiLoCo == bare AdamW, bitwise, 60 steps."""
     n = 4099
-    hyper = DR.Hyper(inner_lr=0.01, warmup_steps=5, weight_decay=0.0)
-    hp = D.OptimHyperparams(inner_lr=0.01, warmup_steps=5, weight_decay=0.0, outer_lr=1.0, outer_momentum=0.0)
+    # weights in [0.5, 1] and small steps keep theta_t and theta_local within a factor of
+    # two, so theta_t - (theta_t - theta_local) is exact (Sterbenz) as in the reference test
+    hyper = DR.Hyper(inner_lr=1e-3, warmup_steps=5, weight_decay=0.0)
+    hp = D.OptimHyperparams(inner_lr=1e-3, warmup_steps=5, weight_decay=0.0, outer_lr=1.0, outer_momentum=0.0)
     e = D.DilocoEngine(D.DilocoConfig(1, 1, A.FP32, 60), hp, n)
-    theta0 = O.rng_fill(11, "theta", 0, n, -1, 1)
+    theta0 = O.rng_fill(11, "theta", 0, n, 0.5, 1.0)
     e.upload(A.THETA_T, theta0)
     e.upload(A.THETA_LOCAL, theta0)
     bare = DR.make_workers(theta0, 1, hyper)[0]
