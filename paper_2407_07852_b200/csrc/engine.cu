@@ -85,6 +85,7 @@ struct dlc_engine {
   void* peer_send[kMaxK] = {};
   void* peer_gather[kMaxK] = {};
   int* peer_flags[kMaxK] = {};
+  void* peer_recv[kMaxK] = {};  // "push" mover: owners' recv buffers
   uint64_t* sig = nullptr;  // flag-barrier signal slots, one per rank
   uint64_t* peer_sig[kMaxK] = {};
   uint64_t sig_epoch = 0;
@@ -181,6 +182,13 @@ std::vector<size_t> piece_plan(size_t S) {
 bool p2p_mover_sm() {
   const char* s = std::getenv("DLC_P2P_COPY");
   return !(s && std::string(s) == "ce");
+}
+
+// "push": the scatter is fused into K2 (deltas stored straight into the
+// owners' recv rows over NVLink), so every NVLink byte is a posted store.
+bool p2p_mover_push() {
+  const char* s = std::getenv("DLC_P2P_COPY");
+  return s && std::string(s) == "push";
 }
 
 // CTAs of the persistent SM mover (0 = one CTA per window, no SM partitioning);
@@ -404,9 +412,10 @@ void p2p_bind(dlc_engine* e, dlc_collective* c) {
   p2p_unbind(e);
   const int K = (int)e->k, r = c->rank;
   struct Handles {
-    cudaIpcMemHandle_t send, gather, flags, sig;
+    cudaIpcMemHandle_t send, gather, flags, sig, recv;
   };
   Handles mine;
+  DLC_CUDA(cudaIpcGetMemHandle(&mine.recv, e->recv));
   DLC_CUDA(cudaIpcGetMemHandle(&mine.send, e->send));
   DLC_CUDA(cudaIpcGetMemHandle(&mine.gather, e->gather));
   DLC_CUDA(cudaIpcGetMemHandle(&mine.flags, e->flags));
@@ -431,8 +440,14 @@ void p2p_bind(dlc_engine* e, dlc_collective* c) {
       e->peer_gather[j] = e->gather;
       e->peer_flags[j] = e->flags;
       e->peer_sig[j] = e->sig;
+      e->peer_recv[j] = e->recv;
       continue;
     }
+    void* precv = nullptr;
+    check_cuda(cudaIpcOpenMemHandle(&precv, all[j].recv, cudaIpcMemLazyEnablePeerAccess),
+               "cudaIpcOpenMemHandle (recv rows)");
+    e->ipc_opened.push_back(precv);
+    e->peer_recv[j] = precv;
     void* psig = nullptr;
     check_cuda(cudaIpcOpenMemHandle(&psig, all[j].sig, cudaIpcMemLazyEnablePeerAccess),
                "cudaIpcOpenMemHandle (signal slots)");
@@ -577,6 +592,7 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
   char* send = static_cast<char*>(e->send);
   char* recv = static_cast<char*>(e->recv);
   char* gather = static_cast<char*>(e->gather);
+  const bool push_mover = p2p_mover_push();
   auto rows = [&](size_t p, auto&& fn) {  // piece p of every owner slot, clipped to n
     for (size_t q = 0; q < K; ++q) {
       const size_t lo = q * S + po(p);
@@ -604,7 +620,13 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
       DLC_CUDA(cudaStreamWaitEvent(e->stream, evH[p], 0));
     }
     cudaEvent_t t0 = trace_begin(e, e->stream);
-    launch_pseudo_grad_piece(tt_pair(e), tl, e->st, e->send, e->prec, (int)K, S, po(p), pl(p), n, e->stream);
+    if (push_mover) {
+      PtrList rows{};  // my row in every owner's recv buffer
+      for (size_t q = 0; q < K; ++q) rows.ptr[q] = static_cast<char*>(e->peer_recv[q]) + r * S * w;
+      launch_pseudo_grad_push_piece(tt_pair(e), tl, e->st, rows, e->prec, (int)K, S, po(p), pl(p), n, e->stream);
+    } else {
+      launch_pseudo_grad_piece(tt_pair(e), tl, e->st, e->send, e->prec, (int)K, S, po(p), pl(p), n, e->stream);
+    }
     trace_end(e, e->stream, "K2", (int)p, t0);
     DLC_CUDA(cudaEventRecord(evK2[p], e->stream));
   }
@@ -624,7 +646,8 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
     trace_end(e, e->cstream, "barrierA", (int)p, ta);
     PtrList in{}, outs{}, pfl{};
     for (size_t j = 0; j < K; ++j) {
-      in.ptr[j] = static_cast<char*>(e->peer_send[j]) + (r * S + po(p)) * w;
+      in.ptr[j] = push_mover ? recv + (j * S + po(p)) * w  // rows already pushed here by K2
+                             : static_cast<char*>(e->peer_send[j]) + (r * S + po(p)) * w;
       outs.ptr[j] = static_cast<char*>(e->peer_gather[j]) + (r * S + po(p)) * w;
       pfl.ptr[j] = e->peer_flags[j] + r;
     }

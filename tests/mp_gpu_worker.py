@@ -43,7 +43,15 @@ def main():
             g[3] = np.inf  # one overflowed inner step on the last worker
         return g
 
-    for mode_name, mode in (("ordered", D.MODE_ORDERED), ("p2p", D.MODE_P2P), ("allreduce", D.MODE_ALLREDUCE)):
+    # P2P runs once per data mover and barrier flavour (read per step from the environment)
+    cases = [("ordered", D.MODE_ORDERED, {}), ("p2p", D.MODE_P2P, {"DLC_P2P_COPY": "sm"}),
+             ("p2p-push", D.MODE_P2P, {"DLC_P2P_COPY": "push", "DLC_P2P_PLAN": "2,2,2,2"}),
+             ("p2p-ce", D.MODE_P2P, {"DLC_P2P_COPY": "ce", "DLC_P2P_BARRIER": "nccl", "DLC_P2P_PIECES": "2"}),
+             ("allreduce", D.MODE_ALLREDUCE, {})]
+    for mode_name, mode, env in cases:
+        for key in ("DLC_P2P_COPY", "DLC_P2P_PLAN", "DLC_P2P_BARRIER", "DLC_P2P_PIECES"):
+            os.environ.pop(key, None)
+        os.environ.update(env)
         coll = PD.make_nccl_collective(r, mode)
         assert coll.world_size() == k and coll.rank() == r.rank
         for prec in (D.FP32, D.FP16):
