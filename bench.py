@@ -342,7 +342,7 @@ def run_ours(args):
             while pieces * 2 <= min(max(int(os.environ["DLC_P2P_PIECES"]), 1), 8):
                 pieces *= 2
         else:
-            pieces = len(os.environ.get("DLC_P2P_PLAN", "1,2,2,2,1").split(","))
+            pieces = len(os.environ.get("DLC_P2P_PLAN", "1,1,2,2,1,1").split(","))
         flag = os.environ.get("DLC_P2P_BARRIER", "flag") != "nccl"
         per_outer = 3 * pieces + 1 + (2 * pieces if flag else 0)  # K2, fold_push, K4 pieces, finish, barriers
     else:

@@ -147,14 +147,14 @@ size_t p2p_pieces() {
 
 // Piece boundaries inside an owner slot of S elements (S a multiple of
 // 64 * kMaxPieces): DLC_P2P_PLAN lists piece weights in eighths of a slot
-// (default "1,2,2,2,1": short first and last pieces shrink the pipeline's
+// (default "1,1,2,2,1,1": short first and last pieces shrink the pipeline's
 // fill (K2 of piece 0) and drain (K4 of the last piece)); DLC_P2P_PIECES asks
 // for equal pieces instead.
 std::vector<size_t> piece_plan(size_t S) {
   std::vector<size_t> w;
   const char* plan = std::getenv("DLC_P2P_PLAN");
   if (plan || !std::getenv("DLC_P2P_PIECES")) {
-    std::string str = plan ? plan : "1,2,2,2,1";
+    std::string str = plan ? plan : "1,1,2,2,1,1";
     size_t pos = 0, sum = 0;
     while (pos <= str.size()) {
       const size_t comma = str.find(',', pos);

@@ -99,8 +99,7 @@ def main():
                 e1.close()
             e.close()
         # e2e host-buffer outer step (dlc_engine_outer_step_host) vs the oracle's outer round
-        for prec in (D.FP32, D.FP16):
-            n2 = 20_011
+        for prec, n2 in ((D.FP32, 20_011), (D.FP16, 20_011), (D.FP16, 5), (D.FP32, 1)):  # tiny: N < K slots
             th = O.rng_fill(5, "theta", 0, n2, -1, 1)
             locs = [(th - O.rng_fill(5, "local", j, n2, -1e-3, 1e-3)).astype(np.float32) for j in range(k)]
             e2 = D.DilocoEngine(D.DilocoConfig(1, k, prec, 1), D.OptimHyperparams(), n2, r.local)
