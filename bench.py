@@ -194,6 +194,8 @@ def workload_config(args, k):
                         f"({args.mode}), Nesterov lr=0.7 mu=0.9",
             "params_per_worker": args.params, "workers": k, "precision": args.precision, "reduce_mode": args.mode,
             "inner_mode": args.inner_mode, "parallelism": f"diloco-dp{k}",
+            "theta_local_refresh": "follows theta_t until the next applied inner step (no store)"
+            if args.inner_mode == "pingpong" else "stored by K4",
             "l2": "inputs larger than L2 (every vector >= 126 MB)" if args.params * 2 > 126e6 else "L2-resident"}
 
 
@@ -281,7 +283,11 @@ def run_ours(args):
     peak, peak_kind = measured_peak()
     wire = 2 if prec == D.FP16 else 4
     # algorithmic bytes per parameter
-    b_k1, b_k2, b_k4 = 28, 8 + wire, 20 + wire
+    # PINGPONG engines do not store theta_local' (it follows theta_t', Pair::follow
+    # in kernels.cuh): K4 = theta_t, momentum, mean in; theta_t', momentum' out
+    follow = args.inner_mode == "pingpong"
+    b_solo = 20 if follow else 24
+    b_k1, b_k2, b_k4 = 28, 8 + wire, (16 if follow else 20) + wire
     k4_ms = max_over_ranks(ph_ms[3] / max(ph_n[3], 1))
     k2_ms = max_over_ranks(ph_ms[1] / max(ph_n[1], 1))
     coll_ms = max_over_ranks(ph_ms[2] / max(ph_n[2], 1)) if ph_n[2] else 0.0
@@ -298,8 +304,8 @@ def run_ours(args):
             "config": workload_config(args, k)}
     if k == 1:
         # one worker: K2 and K4 fused into one pass (theta_t, theta_local, momentum in;
-        # theta_t', momentum', theta_local' out) = 24 B/param in either precision
-        rl = roof(24, k4_ms)
+        # theta_t', momentum' (+ theta_local' in place mode) out) = 20 (24) B/param
+        rl = roof(b_solo, k4_ms)
         rl["kernel"] = "outer_solo_kernel (K2+K4 fused)"
         line["phases_ms"] = {"outer_solo_K2K4": k4_ms}
         line["phase_roofline"] = {"outer_solo_K2K4": rl["frac"]}
@@ -316,7 +322,7 @@ def run_ours(args):
     # NVLink bytes per direction at the pool's measured 770 GB/s peer copy
     # (B200_PROFILING.md); serial = sum, bound = max (perfect overlap).
     nvlink_peak = 770.0
-    hbm_bpp = 24 if k == 1 else (b_k2 + b_k4)
+    hbm_bpp = b_solo if k == 1 else (b_k2 + b_k4)
     wire_bytes = 2 * (k - 1) * (-(-n // k)) * wire if k > 1 else 0
     hbm_ms = hbm_bpp * n / (peak * 1e9) * 1e3
     nvl_ms = wire_bytes / (nvlink_peak * 1e9) * 1e3

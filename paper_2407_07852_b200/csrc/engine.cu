@@ -324,13 +324,31 @@ float* live(dlc_engine* e, int which) {
   const int cur = s.cur, oc = s.ocur;
   switch (which) {
     case DLC_THETA_T: return e->theta_t[oc];
-    case DLC_THETA_LOCAL: return e->p[cur];
+    case DLC_THETA_LOCAL: return s.lalias ? e->theta_t[oc] : e->p[cur];
     case DLC_ADAM_M: return e->m[cur];
     case DLC_ADAM_V: return e->v[cur];
     case DLC_MOMENTUM: return e->buf[oc];
     case DLC_GRAD: return e->grad;
   }
   fail(DLC_EINVAL, "unknown engine buffer " + std::to_string(which));
+}
+
+// Before a caller writes theta_t or theta_local: give theta_local its own copy
+// again (one D2D copy; every kernel path keeps the follow state consistent).
+void unalias(dlc_engine* e) {
+  DevState s = read_state(e);
+  if (!s.lalias) return;
+  DLC_CUDA(cudaMemcpyAsync(e->p[s.cur], e->theta_t[s.ocur], e->n * sizeof(float), cudaMemcpyDeviceToDevice,
+                           e->stream));
+  const int zero = 0;
+  DLC_CUDA(cudaMemcpyAsync(&e->st->lalias, &zero, sizeof(int), cudaMemcpyHostToDevice, e->stream));
+  DLC_CUDA(cudaStreamSynchronize(e->stream));
+}
+
+// live() for a caller that writes through the pointer
+float* writable(dlc_engine* e, int which) {
+  if (which == DLC_THETA_T || which == DLC_THETA_LOCAL) unalias(e);
+  return live(e, which);
 }
 
 void engine_inner(dlc_engine* e, const float* grad, int grad_is_scaled) {
@@ -346,6 +364,7 @@ void engine_inner(dlc_engine* e, const float* grad, int grad_is_scaled) {
     a.p[i] = e->p[i];
     a.m[i] = e->m[i];
     a.v[i] = e->v[i];
+    a.tt[i] = e->theta_t[i];
   }
   a.g = g;
   a.corr1 = e->tab;
@@ -367,7 +386,8 @@ void engine_inner(dlc_engine* e, const float* grad, int grad_is_scaled) {
   e->issued_inner += 1;
 }
 
-Pair local_pair(dlc_engine* e) { return Pair{{e->p[0], e->p[1]}}; }
+// PINGPONG: theta_local follows theta_t after every outer step (Pair::follow).
+Pair local_pair(dlc_engine* e) { return Pair{{e->p[0], e->p[1]}, e->inner_mode == DLC_INNER_PINGPONG}; }
 
 Pair tt_pair(dlc_engine* e) { return Pair{{e->theta_t[0], e->theta_t[1]}}; }
 Pair buf_pair(dlc_engine* e) { return Pair{{e->buf[0], e->buf[1]}}; }
@@ -950,7 +970,7 @@ int dlc_engine_upload(dlc_engine* e, int which, const float* host, size_t n) {
     if (!e || (n && !host)) fail(DLC_EINVAL, "dlc_engine_upload: null argument");
     if (n != e->n) fail(DLC_ESHAPE, "upload length " + std::to_string(n) + " != engine size " + std::to_string(e->n));
     DeviceGuard dg(e->device);
-    float* d = live(e, which);
+    float* d = writable(e, which);
     DLC_CUDA(cudaMemcpyAsync(d, host, n * sizeof(float), cudaMemcpyHostToDevice, e->stream));
     DLC_CUDA(cudaStreamSynchronize(e->stream));
   });
@@ -971,7 +991,7 @@ int dlc_engine_device_ptr(dlc_engine* e, int which, float** dev) {
   return guard([&] {
     if (!e || !dev) fail(DLC_EINVAL, "dlc_engine_device_ptr: null argument");
     DeviceGuard dg(e->device);
-    *dev = live(e, which);
+    *dev = writable(e, which);  // the caller may write through it
   });
 }
 
@@ -1276,7 +1296,7 @@ int dlc_rng_fill_device(dlc_engine* e, int which, uint64_t key, uint64_t first, 
   return guard([&] {
     if (!e) fail(DLC_EINVAL, "dlc_rng_fill_device: null engine");
     DeviceGuard dg(e->device);
-    float* d = live(e, which);
+    float* d = writable(e, which);
     launch_rng_fill(key, first, lo, hi, d, e->n, e->stream);
     launched("rng_fill");
   });
@@ -1286,7 +1306,7 @@ int dlc_rng_perturb(dlc_engine* e, float* dst, uint64_t key, float lo, float hi)
   return guard([&] {
     if (!e) fail(DLC_EINVAL, "dlc_rng_perturb: null engine");
     DeviceGuard dg(e->device);
-    float* d = dst ? dst : live(e, DLC_THETA_LOCAL);
+    float* d = dst ? dst : writable(e, DLC_THETA_LOCAL);
     launch_rng_perturb(live(e, DLC_THETA_T), key, lo, hi, d, e->n, e->stream);
     launched("rng_perturb");
   });
@@ -1640,6 +1660,7 @@ int dlc_checkpoint_load(dlc_engine* const* engines, size_t count, const char* pa
         if (it == kv.end()) fail(DLC_ESHAPE, std::string("checkpoint header missing '") + key + "'");
         return it->second;
       };
+      unalias(e);
       DevState s = read_state(e);
       s.step_count = std::stoull(need("step_count"));
       e->hyper.beta1 = (float)std::stod(need("beta1"));

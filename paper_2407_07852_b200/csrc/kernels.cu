@@ -98,6 +98,12 @@ __device__ __forceinline__ float4 decode4(uint2 w) {
 
 __device__ __forceinline__ float* sel(const Pair& p, int i) { return i ? p.ptr[1] : p.ptr[0]; }
 
+// theta_local as held right now: theta_t[ocur] while the two are equal by
+// construction (Pair::follow + DevState::lalias), else the live p buffer.
+__device__ __forceinline__ const float* local_src(const Pair& tl, const Pair& tt, const DevState* st) {
+  return (tl.follow && st->lalias) ? sel(tt, st->ocur) : sel(tl, st->cur);
+}
+
 // =============================================================================
 // K1: fused unscale + overflow OR + AdamW.
 // =============================================================================
@@ -113,7 +119,7 @@ __global__ void __launch_bounds__(kThreads) adamw_kernel(AdamWArgs a) {
   const uint64_t t = st->step_count + 1;
   const AdamScalars s{a.b1, a.b2, a.eps, a.wd, a.omb1, a.omb2, a.corr1[t], a.corr2[t], a.lr[t]};
   const float inv = __fdiv_rn(1.0f, st->scale);  // optim.cpp:124 (exact: power of two)
-  const float* pc = cur ? a.p[1] : a.p[0];
+  const float* pc = (a.pingpong && st->lalias) ? (st->ocur ? a.tt[1] : a.tt[0]) : (cur ? a.p[1] : a.p[0]);
   const float* mc = cur ? a.m[1] : a.m[0];
   const float* vc = cur ? a.v[1] : a.v[0];
   float* pn = nxt ? a.p[1] : a.p[0];
@@ -168,6 +174,7 @@ __global__ void adamw_finalize_kernel(DevState* st, const float* lr_tab, int pin
   const uint64_t t = st->step_count + 1;
   if (!fi) {
     if (pingpong) st->cur ^= 1;  // the freshly written buffers become live
+    st->lalias = 0;              // theta_local now lives in p[cur]
     st->step_count = t;
     st->last_lr = lr_tab[t];
   } else {
@@ -232,7 +239,7 @@ template <int PREC>
 __global__ void __launch_bounds__(kThreads) pseudo_grad_kernel(Pair ttp, Pair tl, const DevState* st, void* out,
                                                                int* flag, size_t off, size_t len) {
   const float* T = sel(ttp, st->ocur) + off;
-  const float* L = sel(tl, st->cur) + off;
+  const float* L = local_src(tl, ttp, st) + off;
   bool bad = false;
   const size_t n4 = len / 4, b = wbase<kU2>();
   float4 x[kU2], y[kU2];
@@ -429,8 +436,10 @@ __global__ void __launch_bounds__(kThreads) fold_push_kernel(const __grid_consta
 // =============================================================================
 
 // one 4-element vector of K4: applied -> Nesterov + three stores, else copy
+// (L4 == nullptr: theta_local follows theta_t, no refresh store)
 __device__ __forceinline__ void k4_vec(bool applied, float4* T4, float4* B4, float4* L4, float4 d, float lr,
                                        float mu) {
+  if (!applied && !L4) return;
   const float4 t = ld_stream(T4);
   if (applied) {
     float4 b = ld_stream(B4), o;
@@ -440,8 +449,8 @@ __device__ __forceinline__ void k4_vec(bool applied, float4* T4, float4* B4, flo
     o.w = nesterov_elem(t.w, d.w, b.w, lr, mu);
     st_stream(T4, o);
     st_stream(B4, b);
-    st_stream(L4, o);
-  } else {
+    if (L4) st_stream(L4, o);
+  } else if (L4) {
     st_stream(L4, t);
   }
 }
@@ -452,13 +461,14 @@ __device__ __forceinline__ void k4_scalar(bool applied, float* T, float* B, floa
     const float o = nesterov_elem(*T, d, b, lr, mu);
     *T = o;
     *B = b;
-    *L = o;
-  } else {
+    if (L) *L = o;
+  } else if (L) {
     *L = *T;
   }
 }
 
-__device__ __forceinline__ void k4_finalize(DevState* st, bool applied) {
+__device__ __forceinline__ void k4_finalize(DevState* st, bool applied, const Pair& tl) {
+  if (tl.follow) st->lalias = 1;  // theta_local := theta_t (engine.cpp:141-143) without the copy
   st->last_applied = applied ? 1 : 0;
   st->outer_skips += applied ? 0 : 1;
   st->outer_epoch += 1;  // engine.cpp:144
@@ -478,7 +488,7 @@ __global__ void __launch_bounds__(kThreads) nesterov_outer_kernel(Pair ttp, Pair
   const bool applied = s_nonfinite == 0;
   float* tt = sel(ttp, st->ocur);
   float* buf = sel(bufp, st->ocur);
-  float* L = sel(tl, st->cur);
+  float* L = tl.follow ? nullptr : sel(tl, st->cur);
   const size_t n4 = n / 4, j = gtid();
   if (j < n4) {
     float4 d = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -487,15 +497,15 @@ __global__ void __launch_bounds__(kThreads) nesterov_outer_kernel(Pair ttp, Pair
                     : decode4(ld_stream(reinterpret_cast<const uint2*>(dbar) + j));
     }
     k4_vec(applied, reinterpret_cast<float4*>(tt) + j, reinterpret_cast<float4*>(buf) + j,
-           reinterpret_cast<float4*>(L) + j, d, lr, mu);
+           L ? reinterpret_cast<float4*>(L) + j : nullptr, d, lr, mu);
   }
   if (blockIdx.x == 0 && threadIdx.x < n - n4 * 4) {
     const size_t e = n4 * 4 + threadIdx.x;
     const float d = PREC == 0 ? reinterpret_cast<const float*>(dbar)[e]
                               : fp16_decode(reinterpret_cast<const uint16_t*>(dbar)[e]);
-    k4_scalar(applied, tt + e, buf + e, L + e, d, lr, mu);
+    k4_scalar(applied, tt + e, buf + e, L ? L + e : nullptr, d, lr, mu);
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) k4_finalize(st, applied);
+  if (blockIdx.x == 0 && threadIdx.x == 0) k4_finalize(st, applied, tl);
 }
 
 // ---- NVLink flag barrier ----------------------------------------------------
@@ -531,7 +541,7 @@ __global__ void __launch_bounds__(kThreads) pseudo_grad_piece_kernel(Pair ttp, P
   const size_t e0 = (size_t)q * S + po + 4 * j;
   if (4 * j >= plen || e0 >= n) return;
   const float* T = sel(ttp, st->ocur);
-  const float* L = sel(tl, st->cur);
+  const float* L = local_src(tl, ttp, st);
   if (e0 + 3 < n) {
     const float4 x = ld_stream(reinterpret_cast<const float4*>(T + e0));
     const float4 y = ld_stream(reinterpret_cast<const float4*>(L + e0));
@@ -566,7 +576,7 @@ __global__ void __launch_bounds__(kThreads) pseudo_grad_push_piece_kernel(Pair t
   void* row = const_cast<void*>(rows.ptr[q]);
   if (4 * j < plen && e0 < n) {
     const float* T = sel(ttp, st->ocur);
-    const float* L = sel(tl, st->cur);
+    const float* L = local_src(tl, ttp, st);
     if (e0 + 3 < n) {
       const float4 x = ld_stream(reinterpret_cast<const float4*>(T + e0));
       const float4 y = ld_stream(reinterpret_cast<const float4*>(L + e0));
@@ -606,7 +616,7 @@ __global__ void __launch_bounds__(kThreads) nesterov_p2p_piece_kernel(Pair ttp, 
   const float* B = sel(bufp, oc);
   float* To = sel(ttp, oc ^ 1);
   float* Bo = sel(bufp, oc ^ 1);
-  float* L = sel(tl, st->cur);
+  float* L = tl.follow ? nullptr : sel(tl, st->cur);
   const void* dbar = slots.ptr[q];
   const size_t o0 = po + 4 * j;  // offset inside owner q's mean slot
   if (e0 + 3 < n) {
@@ -621,7 +631,7 @@ __global__ void __launch_bounds__(kThreads) nesterov_p2p_piece_kernel(Pair ttp, 
     o.w = nesterov_elem(t.w, d.w, b.w, lr, mu);
     st_stream(reinterpret_cast<float4*>(To + e0), o);
     st_stream(reinterpret_cast<float4*>(Bo + e0), b);
-    st_stream(reinterpret_cast<float4*>(L + e0), o);
+    if (L) st_stream(reinterpret_cast<float4*>(L + e0), o);
   } else {
     for (size_t e = e0; e < n; ++e) {
       const size_t o = o0 + (e - e0);
@@ -631,7 +641,7 @@ __global__ void __launch_bounds__(kThreads) nesterov_p2p_piece_kernel(Pair ttp, 
       const float v = nesterov_elem(T[e], d, b, lr, mu);
       To[e] = v;
       Bo[e] = b;
-      L[e] = v;
+      if (L) L[e] = v;
     }
   }
 }
@@ -650,9 +660,9 @@ __global__ void __launch_bounds__(kThreads) p2p_finish_kernel(Pair ttp, Pair tl,
   const int skip = s_skip;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     if (!skip) st->ocur ^= 1;
-    k4_finalize(st, !skip);
+    k4_finalize(st, !skip, tl);
   }
-  if (!skip) return;
+  if (!skip || tl.follow) return;
   const float* T = sel(ttp, st->ocur);  // unchanged on a skip
   float* L = sel(tl, st->cur);
   for (size_t e = gtid(); e < n; e += gstride()) L[e] = T[e];
@@ -682,8 +692,8 @@ __global__ void __launch_bounds__(kThreads) outer_solo_kernel(Pair ttp, Pair buf
   const float* B = sel(bufp, oc) + off;
   float* To = sel(ttp, oc ^ 1) + off;
   float* Bo = sel(bufp, oc ^ 1) + off;
-  float* Ld = sel(tl, st->cur) + off;
-  const float* Ls = src ? src + off : Ld;
+  float* Ld = tl.follow ? nullptr : sel(tl, st->cur) + off;
+  const float* Ls = src ? src + off : local_src(tl, ttp, st) + off;
   bool bad = false;
   const size_t n4 = len / 4, j = gtid();
   if (j < n4) {
@@ -696,7 +706,7 @@ __global__ void __launch_bounds__(kThreads) outer_solo_kernel(Pair ttp, Pair buf
     o.w = nesterov_elem(t.w, solo_delta<PREC>(t.w, l.w, bad), b.w, lr, mu);
     st_stream(reinterpret_cast<float4*>(To) + j, o);
     st_stream(reinterpret_cast<float4*>(Bo) + j, b);
-    st_stream(reinterpret_cast<float4*>(Ld) + j, o);
+    if (Ld) st_stream(reinterpret_cast<float4*>(Ld) + j, o);
   }
   if (blockIdx.x == 0 && threadIdx.x < len - n4 * 4) {
     const size_t e = n4 * 4 + threadIdx.x;
@@ -704,7 +714,7 @@ __global__ void __launch_bounds__(kThreads) outer_solo_kernel(Pair ttp, Pair buf
     const float o = nesterov_elem(T[e], solo_delta<PREC>(T[e], Ls[e], bad), bb, lr, mu);
     To[e] = o;
     Bo[e] = bb;
-    Ld[e] = o;
+    if (Ld) Ld[e] = o;
   }
   block_or_flag(bad, &st->delta_nonfinite);
 }
@@ -716,9 +726,9 @@ __global__ void __launch_bounds__(kThreads) outer_solo_finish_kernel(Pair ttp, P
   const int skip = *reinterpret_cast<volatile int*>(&st->delta_nonfinite);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     if (!skip) st->ocur ^= 1;
-    k4_finalize(st, !skip);
+    k4_finalize(st, !skip, tl);
   }
-  if (!skip) return;
+  if (!skip || tl.follow) return;
   const float* T = sel(ttp, st->ocur);  // unchanged on a skip
   float* L = sel(tl, st->cur);
   for (size_t e = gtid(); e < n; e += gstride()) L[e] = T[e];

@@ -41,7 +41,7 @@ struct DevState {
   float last_lr;            // lr of the last inner step (0 when skipped)
   int cur;                  // live buffer of the p/m/v ping-pong pair
   int found_inf;            // K1 scratch: OR of !isfinite(g / scale)
-  unsigned reserved;
+  int lalias;               // theta_local == theta_t[ocur] by construction (see Pair::follow)
   int last_overflow;        // InnerStepResult::overflow_skipped
   int delta_nonfinite;      // K2 / solo: non-finite delta (or FP16 encode overflow)
   int last_applied;         // OuterStepResult::applied
@@ -61,6 +61,7 @@ struct AdamWArgs {
   size_t n;
   float b1, b2, eps, wd, omb1, omb2;  // omb = 1.0f - b, rounded as optim.cpp:84-85
   int pingpong;                       // 1: read [cur], write [cur^1]; 0: in place, gated
+  float* tt[2];                       // theta_t pair: the source while DevState::lalias (pingpong only)
 };
 
 // Scalars of one out-of-place AdamW call whose gradient is already unscaled
@@ -76,6 +77,11 @@ struct PtrList {
 // The two buffers of a ping-pong pair; DevState::cur / ocur selects the live one.
 struct Pair {
   float* ptr[2];
+  // theta_local pair only (PINGPONG engines): every outer step ends with
+  // theta_local := theta_t (engine.cpp:141-143).  Instead of copying, the engine
+  // records the equality (DevState::lalias) and reads theta_local from
+  // theta_t[ocur] until the next applied inner step writes a fresh p buffer.
+  int follow;
 };
 
 int num_sms();

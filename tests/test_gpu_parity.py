@@ -351,6 +351,54 @@ def test_inner_overflow_skip_semantics():
         assert not r.overflow_skipped and r.lr == np.float32(4e-4)
 
 
+@pytest.mark.parametrize("inner_mode", [A.INNER_PINGPONG, A.INNER_INPLACE])
+@pytest.mark.parametrize("k", [1, 2])
+def test_theta_local_follows_theta_t(port, tmp_path, k, inner_mode):
+    """theta_local := theta_t after every outer step (engine.cpp:141-143) is recorded,
+    not stored, in PINGPONG engines (Pair::follow).  Overflows on the first inner step
+    of a window (the step that would read the followed buffer), writes through
+    upload / device_ptr, and checkpoints taken right after an outer step must all
+    behave as if the copy had been made."""
+    n, h, rounds = 3001, 2, 3
+    hyper = DR.Hyper(inner_lr=1e-3, warmup_steps=1)
+    theta0 = O.rng_fill(11, "theta", 0, n, -0.5, 0.5)
+
+    def grad_fn(w, t):
+        g = O.rng_fill(11, "grad", w * 100 + t, n, -1e-2, 1e-2)
+        if t in (h, 2 * h) and w == k - 1:  # first step of rounds 2 and 3
+            g[n - 1] = np.inf
+        return g
+
+    workers, _ = DR.simulate(port, theta0, grad_fn, k, h, rounds, 0, hyper)
+    engines = run_engines(k, h, rounds, 0, n, hyper, grad_fn, theta0, inner_mode)
+    for wi, e in enumerate(engines):
+        assert np.array_equal(bits(e.download(A.THETA_LOCAL)), bits(workers[wi].theta_t))
+        assert np.array_equal(bits(e.download(A.THETA_T)), bits(workers[wi].theta_t))
+        assert np.array_equal(bits(e.download(A.ADAM_M)), bits(workers[wi].m))
+        assert e.scalars().overflow_skips == (2 if wi == k - 1 else 0)
+    e = engines[0]
+    want_t = workers[0].theta_t
+    # checkpoint right after an outer step round-trips theta_local
+    path = str(tmp_path / "follow.ckpt")
+    D.checkpoint_save(engines, path)
+    fresh = [D.DilocoEngine(e.config, D.OptimHyperparams(), n, 0, inner_mode) for _ in range(k)]
+    D.checkpoint_load(fresh, path)
+    for wi, x in enumerate(fresh):
+        assert np.array_equal(bits(x.download(A.THETA_LOCAL)), bits(workers[wi].theta_t))
+        assert np.array_equal(bits(x.download(A.THETA_T)), bits(workers[wi].theta_t))
+        x.close()
+    # writing theta_t leaves theta_local alone, and vice versa
+    other = O.rng_fill(12, "theta", 0, n, -1, 1)
+    e.upload(A.THETA_T, other)
+    assert np.array_equal(bits(e.download(A.THETA_LOCAL)), bits(want_t))
+    e.upload(A.THETA_T, want_t)
+    e.rng_fill(A.THETA_LOCAL, 12, "theta", 0, -1, 1)  # device-side write through the live pointer
+    assert np.array_equal(bits(e.download(A.THETA_T)), bits(want_t))
+    assert np.array_equal(bits(e.download(A.THETA_LOCAL)), bits(other))
+    for x in engines:
+        x.close()
+
+
 def test_large_n_slices_vs_oracle(port):
     """150M-parameter buffers (configs 2-3): elementwise path, so oracle slices are exact."""
     n = 150_000_000
