@@ -3,15 +3,15 @@
 // (engine.hpp:76-157).
 //
 // HBM layout of one engine (one worker, one GPU), every buffer 256-B aligned:
-//   theta_t[N]                     outer weights            FP32
+//   theta_t[2][N], buf[2][N]       outer weights, momentum  FP32 ping-pong pair
 //   p[2][N], m[2][N], v[2][N]      theta_local + AdamW      FP32 ping-pong pair
-//                                  (one buffer each in INPLACE mode)
-//   buf[N]                         Nesterov momentum        FP32
+//                                  (one buffer each in INPLACE mode; theta_local
+//                                  may follow theta_t[ocur], Pair::follow)
 //   grad[N]                        gradient staging          FP32
 //   send[K*S]                      pseudo-gradient, padded   FP32 | FP16 codes
 //   recv[K*S], gather[K*S]         scatter / all-gather      (K > 1)
 //   flags[kMaxK], DevState, lr/corr tables
-// S = ceil(N / K) rounded up to 64 elements: rank r owns send[r*S, (r+1)*S).
+// S = ceil(N / K) rounded up to 512 elements: rank r owns send[r*S, (r+1)*S).
 // The partition differs from partition_ranges (reduce.cpp:20-31) only by the
 // padding; results are independent of the split because the fold is
 // elementwise, and the scalar bytes on the wire are the same
@@ -132,8 +132,8 @@ void launched(const char* what) { DLC_LAUNCHED(what); }
 // Host <-> device chunk of the host-buffer outer step (64 MB of FP32).
 constexpr size_t kHostChunk = size_t(16) << 20;
 // Pieces of the pipelined P2P outer step (DLC_MODE_P2P).
-// Owner slots are a multiple of 64 * kMaxPieces elements; the number actually
-// used comes from DLC_P2P_PIECES (default 4, profiles/r1_sweep_p2p_*.log).
+// Owner slots are a multiple of 64 * kMaxPieces elements; the split actually
+// used comes from DLC_P2P_PLAN / DLC_P2P_PIECES (profiles/r1_sweep_p2p_*.log).
 constexpr size_t kMaxPieces = 8;
 
 // (read on every step so a tuning sweep can change them in-process)
