@@ -51,7 +51,8 @@ enum dlc_status {
   DLC_ECOLLECTIVE = 4,
   DLC_ECUDA = 5,
   DLC_ENCCL = 6,
-  DLC_EINVAL = 7
+  DLC_EINVAL = 7,
+  DLC_ESERIAL = 8 /* SerializationError, errors.hpp:48 (wire frames) */
 };
 
 /* Precision, reduce.hpp:22 */
@@ -358,6 +359,95 @@ DLC_API int dlc_checkpoint_load(dlc_engine* const* engines, size_t count, const 
 enum { DLC_PHASE_INNER = 0, DLC_PHASE_PSEUDO = 1, DLC_PHASE_COLLECTIVE = 2, DLC_PHASE_OUTER = 3 };
 DLC_API int dlc_engine_set_timing(dlc_engine* e, int on);
 DLC_API int dlc_engine_phase_times(dlc_engine* e, double total_ms[4], uint64_t count[4]);
+
+/* =========================================================================
+ * 5. Wire codec for cross-box transports.
+ *
+ *    The reference's TCP collective moves pseudo-gradient slices as framed
+ *    messages.  These calls produce and consume exactly those bytes straight
+ *    from / into DEVICE buffers, so a transport between boxes (the
+ *    reference's Node, or any socket code) never touches a host copy of the
+ *    vector: frames are assembled in the caller's (ideally pinned) host
+ *    buffer by strided copy-engine transfers, one per run of full chunks.
+ *    Byte-exact with:
+ *      encode_frame            wire.cpp:10-22   "ODLC" | 1 | type | u64 len | payload
+ *      encode_reduce_payload   wire.cpp:74-88   epoch u64 | chunk_index u32 | precision u8 | segment
+ *      encode_chunk_segment    collective.cpp:63-81  u64 1 | u64 name_len | name | u64 offset | u64 length | scalars
+ *      chunk_name              collective.cpp:126-131, PeerId::hex collective.cpp:214-220
+ *      send_chunk_span         collective.cpp:1318-1345 (max(1, chunk_size_bytes / width) elements per frame)
+ *    and, on receipt, FrameParser::next (wire.cpp:38-72), decode_reduce_payload
+ *    (wire.cpp:90-104), decode_chunk_segment (collective.cpp:90-118) and the
+ *    drop rules of handle_reduce_chunk (collective.cpp:1017-1047).
+ * ========================================================================= */
+
+enum dlc_msg_type { DLC_MSG_REDUCE_CHUNK = 5, DLC_MSG_REDUCE_RESULT = 6 }; /* MsgType, wire.hpp:31-41 */
+
+typedef struct {
+  uint8_t msg_type;          /* DLC_MSG_REDUCE_CHUNK (scatter) | DLC_MSG_REDUCE_RESULT (all-gather) */
+  int precision;             /* DLC_FP32 | DLC_FP16: element width 4 | 2 */
+  uint64_t outer_epoch;
+  uint32_t attempt;          /* barrier attempt of the round */
+  uint32_t partition;        /* owner range index */
+  uint64_t from_hi, from_lo; /* PeerId of the producer (the scatter sender, or the owner for results) */
+  uint64_t chunk_size_bytes; /* NodeOptions::chunk_size_bytes (collective.hpp:93, default 1 MiB) */
+} dlc_wire_tags;
+
+typedef struct {
+  uint8_t msg_type;
+  uint8_t precision;
+  int accepted;              /* 1: scalars copied to the device; 0: dropped (see dlc_wire_decode) */
+  uint32_t chunk_index;
+  uint32_t attempt, partition;
+  uint64_t outer_epoch;
+  uint64_t from_hi, from_lo;
+  uint64_t offset, length;   /* global element range of the chunk */
+  uint64_t frame_offset, frame_bytes;
+} dlc_wire_chunk;
+
+/* Bytes and frames send_chunk_span produces for `elems` elements. */
+DLC_API int dlc_wire_frames_size(uint64_t elems, const dlc_wire_tags* tags, size_t* bytes, uint64_t* frames);
+/* Frames for the DEVICE scalars dev[0, elems) (FP16 codes or FP32 values),
+ * element `global_offset` first, into host_out (cap bytes; DLC_ESHAPE when
+ * short).  Synchronous with respect to `stream` (NULL: the legacy stream). */
+DLC_API int dlc_wire_encode(const void* dev_scalars, uint64_t global_offset, uint64_t elems, const dlc_wire_tags* tags,
+                            uint8_t* host_out, size_t cap, size_t* used, void* stream);
+/* Parses the complete frames at the front of host_in and copies each accepted
+ * chunk's scalars to dev_out[offset - base_offset] (capacity elements).
+ * DLC_ESERIAL on a malformed frame (bad magic / version / length / type,
+ * truncated payload or segment, segment count != 1), with *consumed = the
+ * bytes before it.  A trailing incomplete frame is left unconsumed.  Dropped,
+ * not errors: frames of other message types, unparsable chunk names and size
+ * mismatches (collective.cpp:1022-1029), a precision other than `precision`,
+ * ranges outside [base_offset, base_offset + capacity).  `chunks` (may be NULL)
+ * receives up to max_chunks descriptors.  Synchronous. */
+DLC_API int dlc_wire_decode(const uint8_t* host_in, size_t bytes, int precision, uint64_t base_offset,
+                            uint64_t capacity, void* dev_out, dlc_wire_chunk* chunks, size_t max_chunks,
+                            size_t* n_chunks, size_t* consumed, void* stream);
+
+/* Engine side of a wire round (the device data plane of Node::Impl::all_reduce,
+ * collective.cpp:1347-1595; the control plane - barrier, commit, membership -
+ * stays with the transport):
+ *   begin   K2 over the whole vector into the DELTA buffer in the engine's
+ *           precision (encode once at the source, collective.cpp:1356-1366);
+ *           returns the outer epoch that tags the round.  Error when mid-window.
+ *   encode  frames of DELTA or MEAN [offset, offset + length) (scatter a
+ *           partition to its owner / relay an owner's mean).
+ *   decode  frames into fold ROW `row` (contributor index, base = the owned
+ *           range's offset) or into MEAN (base 0).
+ *   fold    owner fold (collective.cpp:1456-1489): contributors 0..k-1 in
+ *           order, row `rank` read from DELTA, mean encoded once into
+ *           MEAN[offset, offset + length).
+ *   finish  DilocoEngine::outer_step on MEAN (engine.cpp:128-146): epoch
+ *           guard, finite gate, Nesterov, theta_local := theta_t. */
+enum dlc_wire_buffer { DLC_WIRE_DELTA = 0, DLC_WIRE_MEAN = 1, DLC_WIRE_ROW = 2 };
+DLC_API int dlc_engine_wire_begin(dlc_engine* e, uint64_t* outer_epoch);
+DLC_API int dlc_engine_wire_encode(dlc_engine* e, int which, uint64_t offset, uint64_t length,
+                                   const dlc_wire_tags* tags, uint8_t* host_out, size_t cap, size_t* used);
+DLC_API int dlc_engine_wire_decode(dlc_engine* e, int which, int row, uint64_t base_offset, uint64_t capacity,
+                                   const uint8_t* host_in, size_t bytes, dlc_wire_chunk* chunks, size_t max_chunks,
+                                   size_t* n_chunks, size_t* consumed);
+DLC_API int dlc_engine_wire_fold(dlc_engine* e, int rank, int k, uint64_t offset, uint64_t length);
+DLC_API int dlc_engine_wire_finish(dlc_engine* e, uint64_t outer_epoch, dlc_outer_result* result);
 
 /* =========================================================================
  * 4. Synthetic inputs and test probes (bench / parity tests).  Counter-based

@@ -318,3 +318,160 @@ int orc_outer_step(float* theta_t, float* theta_local, float* buf, const float* 
   memcpy(theta_local, theta_t, n * sizeof(float));
   return applied;
 }
+
+/* ---- wire codec: proj/src/wire.cpp:10-104, proj/src/collective.cpp:63-152,
+ *      1318-1345 ----------------------------------------- */
+
+#define ORC_ESERIAL 5   /* SerializationError, errors.hpp:48 */
+#define ORC_EAGAIN 6    /* FrameParser::next() == nullopt: frame incomplete */
+
+static size_t put_le(uint8_t* out, uint64_t v, int nbytes) {
+  for (int i = 0; i < nbytes; ++i) out[i] = (uint8_t)(v >> (8 * i));
+  return (size_t)nbytes;
+}
+
+static uint64_t get_le(const uint8_t* in, int nbytes) {
+  uint64_t v = 0;
+  for (int i = 0; i < nbytes; ++i) v |= (uint64_t)in[i] << (8 * i);
+  return v;
+}
+
+/* encode_frame, wire.cpp:10-22: "ODLC" | version 1 | type | u64 LE length | payload.
+ * out == NULL: size only. */
+size_t orc_encode_frame(uint8_t type, const uint8_t* payload, size_t len, uint8_t* out) {
+  if (out) {
+    memcpy(out, "ODLC", 4);
+    out[4] = 1; /* kWireVersion, wire.hpp:27 */
+    out[5] = type;
+    put_le(out + 6, len, 8);
+    if (len) memcpy(out + 14, payload, len);
+  }
+  return 14 + len;
+}
+
+/* encode_reduce_payload, wire.cpp:74-88: epoch u64 | chunk_index u32 | precision u8 | segment. */
+size_t orc_encode_reduce_payload(uint64_t epoch, uint32_t chunk_index, uint8_t precision,
+                                 const uint8_t* seg, size_t seglen, uint8_t* out) {
+  if (out) {
+    put_le(out, epoch, 8);
+    put_le(out + 8, chunk_index, 4);
+    out[12] = precision;
+    if (seglen) memcpy(out + 13, seg, seglen);
+  }
+  return 13 + seglen;
+}
+
+/* encode_chunk_segment, collective.cpp:63-81: u64 1 | u64 name_len | name |
+ * u64 offset | u64 length | scalars (the tensor-core layout header of one segment). */
+size_t orc_encode_chunk_segment(const char* name, size_t name_len, uint64_t offset, uint64_t length,
+                                const uint8_t* scalars, size_t nbytes, uint8_t* out) {
+  if (out) {
+    uint8_t* o = out;
+    o += put_le(o, 1, 8);
+    o += put_le(o, name_len, 8);
+    memcpy(o, name, name_len);
+    o += name_len;
+    o += put_le(o, offset, 8);
+    o += put_le(o, length, 8);
+    if (nbytes) memcpy(o, scalars, nbytes);
+  }
+  return 32 + name_len + nbytes;
+}
+
+/* chunk_name, collective.cpp:126-131 with PeerId::hex, collective.cpp:214-220:
+ * "a<attempt>.p<partition>.f<%016llx%016llx>".  Returns the length (< 80). */
+size_t orc_chunk_name(uint32_t attempt, uint32_t partition, uint64_t hi, uint64_t lo, char* out) {
+  char buf[96];
+  /* snprintf is not in string.h; build the decimal fields by hand */
+  size_t n = 0;
+  char dec[16];
+  int d;
+  buf[n++] = 'a';
+  d = 0;
+  do { dec[d++] = (char)('0' + attempt % 10); attempt /= 10; } while (attempt);
+  while (d) buf[n++] = dec[--d];
+  buf[n++] = '.';
+  buf[n++] = 'p';
+  do { dec[d++] = (char)('0' + partition % 10); partition /= 10; } while (partition);
+  while (d) buf[n++] = dec[--d];
+  buf[n++] = '.';
+  buf[n++] = 'f';
+  static const char* hx = "0123456789abcdef";
+  for (int i = 15; i >= 0; --i) buf[n++] = hx[(hi >> (4 * i)) & 0xF];
+  for (int i = 15; i >= 0; --i) buf[n++] = hx[(lo >> (4 * i)) & 0xF];
+  memcpy(out, buf, n);
+  return n;
+}
+
+/* The byte stream send_chunk_span puts on one connection (collective.cpp:1318-1345):
+ * max_elems = max(1, chunk_size_bytes / width) elements per frame, chunk_index
+ * counting from 0, each chunk's global offset = global_offset + start.
+ * `scalars` holds elems * width bytes.  out == NULL: size only. */
+size_t orc_send_chunk_span(uint8_t type, uint64_t epoch, const char* name, size_t name_len, int precision,
+                           uint64_t global_offset, const uint8_t* scalars, uint64_t elems,
+                           uint64_t chunk_size_bytes, uint8_t* out) {
+  const uint64_t width = precision ? 2 : 4;
+  uint64_t max_elems = chunk_size_bytes / width;
+  if (max_elems < 1) max_elems = 1;
+  size_t used = 0;
+  uint32_t chunk_index = 0;
+  for (uint64_t start = 0; start < elems; start += max_elems) {
+    const uint64_t count = (elems - start < max_elems) ? elems - start : max_elems;
+    const size_t seg = 32 + name_len + count * width;
+    const size_t payload = 13 + seg;
+    if (out) {
+      uint8_t* f = out + used;
+      orc_encode_frame(type, NULL, 0, f);
+      put_le(f + 6, payload, 8);
+      orc_encode_reduce_payload(epoch, chunk_index, (uint8_t)(precision ? 1 : 0), NULL, 0, f + 14);
+      orc_encode_chunk_segment(name, name_len, global_offset + start, count, scalars + start * width,
+                               count * width, f + 27);
+    }
+    chunk_index++;
+    used += 14 + payload;
+  }
+  return used;
+}
+
+/* One frame off the front of a byte stream: FrameParser::next (wire.cpp:38-72),
+ * decode_reduce_payload (wire.cpp:90-104), decode_chunk_segment
+ * (collective.cpp:90-119).  ORC_EAGAIN when the frame is incomplete. */
+int orc_parse_chunk_frame(const uint8_t* in, size_t avail, size_t* frame_bytes, uint8_t* type,
+                          uint64_t* epoch, uint32_t* chunk_index, uint8_t* precision, size_t* name_off,
+                          size_t* name_len, uint64_t* offset, uint64_t* length, size_t* scalars_off,
+                          size_t* scalars_bytes) {
+  if (avail < 14) return ORC_EAGAIN;
+  if (memcmp(in, "ODLC", 4) != 0) return ORC_ESERIAL;           /* bad frame magic */
+  if (in[4] != 1) return ORC_ESERIAL;                           /* unsupported wire version */
+  const uint64_t len = get_le(in + 6, 8);
+  if (len > (1ull << 33)) return ORC_ESERIAL;                   /* implausible frame length */
+  if (avail < 14 + len) return ORC_EAGAIN;
+  if (in[5] < 1 || in[5] > 9) return ORC_ESERIAL;               /* unknown message type */
+  *type = in[5];
+  *frame_bytes = 14 + len;
+  const uint8_t* p = in + 14;
+  if (len < 13) return ORC_ESERIAL;                             /* truncated reduce payload */
+  *epoch = get_le(p, 8);
+  *chunk_index = (uint32_t)get_le(p + 8, 4);
+  *precision = p[12];
+  const uint8_t* s = p + 13;
+  const size_t slen = len - 13;
+  size_t c = 0;
+  if (c + 8 > slen) return ORC_ESERIAL;                         /* truncated chunk segment */
+  if (get_le(s, 8) != 1) return ORC_ESERIAL;                    /* exactly one segment */
+  c += 8;
+  if (c + 8 > slen) return ORC_ESERIAL;
+  const uint64_t nl = get_le(s + c, 8);
+  c += 8;
+  if (nl > slen - c) return ORC_ESERIAL;                        /* truncated chunk segment name */
+  *name_off = (size_t)(s - in) + c;
+  *name_len = nl;
+  c += nl;
+  if (c + 16 > slen) return ORC_ESERIAL;
+  *offset = get_le(s + c, 8);
+  *length = get_le(s + c + 8, 8);
+  c += 16;
+  *scalars_off = (size_t)(s - in) + c;
+  *scalars_bytes = slen - c;
+  return ORC_OK;
+}

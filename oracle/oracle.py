@@ -30,7 +30,8 @@ _u16p = np.ctypeslib.ndpointer(np.uint16, flags="C_CONTIGUOUS")
 _sz = C.c_size_t
 _u64 = C.c_uint64
 
-OK, ESHAPE, ECONFIG, ENUMERIC, ECOLLECTIVE = 0, 1, 2, 3, 4
+OK, ESHAPE, ECONFIG, ENUMERIC, ECOLLECTIVE, ESERIAL, EAGAIN = 0, 1, 2, 3, 4, 5, 6
+_u8p = C.POINTER(C.c_uint8)
 
 
 def build(ref: bool | None = None) -> None:
@@ -82,6 +83,16 @@ class _Lib:
                               C.c_void_p, _f32p)
             self._key = fn("rng_key", _u64, _u64, C.c_char_p, _u64)
             self._fill = fn("rng_fill", None, _u64, _u64, _sz, C.c_float, C.c_float, _f32p)
+            vp = C.c_void_p
+            self._frame = fn("encode_frame", _sz, C.c_uint8, vp, _sz, vp)
+            self._rpayload = fn("encode_reduce_payload", _sz, _u64, C.c_uint32, C.c_uint8, vp, _sz, vp)
+            self._segment = fn("encode_chunk_segment", _sz, C.c_char_p, _sz, _u64, _u64, vp, _sz, vp)
+            self._cname = fn("chunk_name", _sz, C.c_uint32, C.c_uint32, _u64, _u64, C.c_char_p)
+            self._span = fn("send_chunk_span", _sz, C.c_uint8, _u64, C.c_char_p, _sz, C.c_int, _u64, vp, _u64,
+                            _u64, vp)
+            P = C.POINTER
+            self._parse = fn("parse_chunk_frame", C.c_int, vp, _sz, P(_sz), P(C.c_uint8), P(_u64), P(C.c_uint32),
+                             P(C.c_uint8), P(_sz), P(_sz), P(_u64), P(_u64), P(_sz), P(_sz))
         else:
             self._reduce = fn("reduce_average", C.c_int, C.POINTER(C.c_void_p), _sz, _sz, C.c_int, _f32p)
             self._bench_outer = fn("bench_outer", C.c_int, C.c_int, _sz, _sz, C.c_int, C.c_int,
@@ -92,6 +103,10 @@ class _Lib:
                                C.POINTER(_u64), C.POINTER(C.c_double), C.POINTER(_u64))
             self._ck_write = fn("checkpoint_write", C.c_int, C.c_char_p, _sz, vp, vp, vp, vp, vp,
                                 C.POINTER(_u64), C.POINTER(C.c_double), C.POINTER(_u64))
+            P = C.POINTER
+            self._frame = fn("encode_frame", C.c_int, C.c_uint8, vp, _sz, vp, P(_sz))
+            self._rpayload = fn("encode_reduce_payload", C.c_int, _u64, C.c_uint32, C.c_uint8, vp, _sz, vp, P(_sz))
+            self._parse_frames = fn("parse_frames", C.c_int, vp, _sz, _sz, vp, vp, vp, vp, vp, vp, _sz, P(_sz))
 
     # -- checkpoints through the reference's save/load_checkpoint (reference only) --------
     _CK_U = ("step_count", "growth_interval", "consecutive_good", "inner_step", "outer_epoch", "engines")
@@ -208,6 +223,94 @@ class _Lib:
 
     def fleet_reduce_bytes(self, n, k, precision):
         return int(self._fleet(n, k, precision))
+
+    # -- wire codec (wire.cpp:10-104; collective.cpp:63-152, 1318-1345) ----------
+    def encode_frame(self, msg_type: int, payload: bytes) -> bytes:
+        pl = np.frombuffer(bytes(payload), np.uint8) if payload else np.zeros(1, np.uint8)
+        out = np.empty(14 + len(payload), np.uint8)
+        if self.kind == "port":
+            self._frame(msg_type, pl.ctypes.data, len(payload), out.ctypes.data)
+        else:
+            used = _sz(0)
+            st = self._frame(msg_type, pl.ctypes.data, len(payload), out.ctypes.data, C.byref(used))
+            assert st == 0 and used.value == out.size
+        return out.tobytes()
+
+    def encode_reduce_payload(self, epoch: int, chunk_index: int, precision: int, segment: bytes) -> bytes:
+        sg = np.frombuffer(bytes(segment), np.uint8) if segment else np.zeros(1, np.uint8)
+        out = np.empty(13 + len(segment), np.uint8)
+        if self.kind == "port":
+            self._rpayload(epoch, chunk_index, precision, sg.ctypes.data, len(segment), out.ctypes.data)
+        else:
+            used = _sz(0)
+            st = self._rpayload(epoch, chunk_index, precision, sg.ctypes.data, len(segment), out.ctypes.data,
+                                C.byref(used))
+            assert st == 0 and used.value == out.size
+        return out.tobytes()
+
+    # (restatement only: the reference keeps these in collective.cpp's anonymous namespace)
+    def encode_chunk_segment(self, name: str, offset: int, length: int, scalars: bytes) -> bytes:
+        sc = np.frombuffer(bytes(scalars), np.uint8) if scalars else np.zeros(1, np.uint8)
+        out = np.empty(32 + len(name) + len(scalars), np.uint8)
+        self._segment(name.encode(), len(name), offset, length, sc.ctypes.data, len(scalars), out.ctypes.data)
+        return out.tobytes()
+
+    def chunk_name(self, attempt: int, partition: int, hi: int, lo: int) -> str:
+        buf = C.create_string_buffer(96)
+        n = self._cname(attempt, partition, hi, lo, buf)
+        return buf.raw[:n].decode()
+
+    def send_chunk_span(self, msg_type, epoch, name, precision, global_offset, scalars, chunk_size_bytes) -> bytes:
+        """The bytes send_chunk_span writes to one connection; `scalars` is an array of
+        uint16 codes (FP16) or float32 values (FP32)."""
+        sc = np.ascontiguousarray(scalars)
+        elems = sc.size
+        nm = name.encode()
+        size = self._span(msg_type, epoch, nm, len(nm), precision, global_offset, sc.ctypes.data, elems,
+                          chunk_size_bytes, None)
+        out = np.empty(max(size, 1), np.uint8)
+        self._span(msg_type, epoch, nm, len(nm), precision, global_offset, sc.ctypes.data, elems, chunk_size_bytes,
+                   out.ctypes.data)
+        return out[:size].tobytes()
+
+    def parse_chunk_frames(self, data: bytes):
+        """Every complete frame of `data` as a dict; stops at an incomplete tail.
+        Raises ValueError (SerializationError) on a malformed frame."""
+        buf = np.frombuffer(bytes(data), np.uint8) if data else np.zeros(1, np.uint8)
+        out, at = [], 0
+        while True:
+            v = [_sz(0), C.c_uint8(0), _u64(0), C.c_uint32(0), C.c_uint8(0), _sz(0), _sz(0), _u64(0), _u64(0),
+                 _sz(0), _sz(0)]
+            st = self._parse(buf.ctypes.data + at, len(data) - at, *[C.byref(x) for x in v])
+            if st == EAGAIN:
+                return out, at
+            if st != OK:
+                raise ValueError(f"SerializationError at byte {at}")
+            fb, ty, ep, ci, pr, no, nl, off, ln, so, sb = [x.value for x in v]
+            out.append({"type": ty, "epoch": ep, "chunk_index": ci, "precision": pr,
+                        "name": bytes(data[at + no:at + no + nl]).decode(errors="replace"),
+                        "offset": off, "length": ln, "scalars": bytes(data[at + so:at + so + sb]),
+                        "frame_offset": at, "frame_bytes": fb})
+            at += fb
+
+    def parse_frames(self, data: bytes, feed: int = 0, max_frames: int = 1 << 16):
+        """Reference only: FrameParser fed in `feed`-byte pieces + decode_reduce_payload."""
+        buf = np.frombuffer(bytes(data), np.uint8) if data else np.zeros(1, np.uint8)
+        ty = np.zeros(max_frames, np.uint8)
+        pl = np.zeros(max_frames, np.uint64)
+        ep = np.zeros(max_frames, np.uint64)
+        ci = np.zeros(max_frames, np.uint32)
+        pr = np.zeros(max_frames, np.uint8)
+        ok = np.zeros(max_frames, np.int32)
+        nf = _sz(0)
+        st = self._parse_frames(buf.ctypes.data, len(data), feed, ty.ctypes.data, pl.ctypes.data, ep.ctypes.data,
+                                ci.ctypes.data, pr.ctypes.data, ok.ctypes.data, max_frames, C.byref(nf))
+        if st == ESERIAL:
+            raise ValueError("SerializationError")
+        assert st == OK, st
+        k = nf.value
+        return [{"type": int(ty[i]), "payload_len": int(pl[i]), "epoch": int(ep[i]), "chunk_index": int(ci[i]),
+                 "precision": int(pr[i]), "ok": bool(ok[i])} for i in range(k)]
 
     # -- CPU baseline harness (reference only) -----------------------------------
     def bench_outer(self, threads, slice_len, k, precision, iters, lr=0.7, mu=0.9):

@@ -10,7 +10,9 @@
 // Uses: (1) pin the C restatement (oracle/diloco_oracle.c) bit-for-bit,
 // (2) generate tests/golden fixtures, (3) the CPU baseline / `bench.py --impl
 // reference` arm (ref_bench_*), timing the reference's own functions.
+#include <algorithm>
 #include <atomic>
+#include <stdexcept>
 #include <barrier>
 #include <chrono>
 #include <cstdint>
@@ -24,6 +26,7 @@
 #include "diloco/reduce.hpp"
 #include "diloco/rng.hpp"
 #include "diloco/tensor.hpp"
+#include "diloco/wire.hpp"
 
 #define REF_API extern "C" __attribute__((visibility("default")))
 
@@ -31,7 +34,7 @@ using namespace diloco;
 
 namespace {
 
-enum { kOk = 0, kShape = 1, kConfig = 2, kNumeric = 3, kCollective = 4, kOther = 9 };
+enum { kOk = 0, kShape = 1, kConfig = 2, kNumeric = 3, kCollective = 4, kSerial = 5, kOther = 9 };
 
 ParamVector pv(const float* data, size_t n) {
   return ParamVector(Layout::single("p", n), std::vector<float>(data, data + n));
@@ -54,6 +57,8 @@ int guarded(F&& f) {
     return kNumeric;
   } catch (const CollectiveError&) {
     return kCollective;
+  } catch (const SerializationError&) {
+    return kSerial;
   } catch (const std::exception&) {
     return kOther;
   }
@@ -394,5 +399,65 @@ REF_API int ref_checkpoint_write(const char* path, size_t n, const float* tt, co
     s.scaler.scale = (float)d[6];
     ck.engines.push_back(std::move(s));
     save_checkpoint(ck, path);
+  });
+}
+
+// ---- wire codec (wire.cpp:10-104): frames and reduce payloads -------------------
+
+REF_API int ref_encode_frame(uint8_t type, const uint8_t* payload, size_t len, uint8_t* out, size_t* out_len) {
+  return guarded([&] {
+    WireMessage m;
+    m.type = static_cast<MsgType>(type);
+    m.payload.assign(payload, payload + len);
+    const std::vector<uint8_t> f = encode_frame(m);
+    std::memcpy(out, f.data(), f.size());
+    *out_len = f.size();
+  });
+}
+
+REF_API int ref_encode_reduce_payload(uint64_t epoch, uint32_t chunk_index, uint8_t precision, const uint8_t* seg,
+                                      size_t seglen, uint8_t* out, size_t* out_len) {
+  return guarded([&] {
+    ReduceChunkHeader h;
+    h.outer_epoch = epoch;
+    h.chunk_index = chunk_index;
+    h.precision = precision;
+    const std::vector<uint8_t> p = encode_reduce_payload(h, std::span<const uint8_t>(seg, seglen));
+    std::memcpy(out, p.data(), p.size());
+    *out_len = p.size();
+  });
+}
+
+// Feeds `in` to a FrameParser in pieces of `feed` bytes and pops every complete
+// frame: types[i], payload lengths, and each payload's reduce header when it
+// decodes (ok[i] = 0 when decode_reduce_payload throws).
+REF_API int ref_parse_frames(const uint8_t* in, size_t n, size_t feed, uint8_t* types, uint64_t* payload_lens,
+                             uint64_t* epochs, uint32_t* chunk_indices, uint8_t* precisions, int* ok,
+                             size_t max_frames, size_t* nframes) {
+  return guarded([&] {
+    FrameParser parser;
+    size_t count = 0;
+    for (size_t at = 0; at < n;) {
+      const size_t take = std::min(feed ? feed : n, n - at);
+      parser.feed(std::span<const uint8_t>(in + at, take));
+      at += take;
+      while (auto m = parser.next()) {
+        if (count >= max_frames) throw std::runtime_error("too many frames");
+        types[count] = static_cast<uint8_t>(m->type);
+        payload_lens[count] = m->payload.size();
+        ok[count] = 0;
+        try {
+          std::span<const uint8_t> seg;
+          const ReduceChunkHeader h = decode_reduce_payload(m->payload, seg);
+          epochs[count] = h.outer_epoch;
+          chunk_indices[count] = h.chunk_index;
+          precisions[count] = h.precision;
+          ok[count] = 1;
+        } catch (const SerializationError&) {
+        }
+        ++count;
+      }
+    }
+    *nframes = count;
   });
 }

@@ -14,12 +14,14 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libdiloco_cuda.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "diloco_cuda.h")
 
-OK, ESHAPE, ECONFIG, ENUMERIC, ECOLLECTIVE, ECUDA, ENCCL, EINVAL = range(8)
+OK, ESHAPE, ECONFIG, ENUMERIC, ECOLLECTIVE, ECUDA, ENCCL, EINVAL, ESERIAL = range(9)
 FP32, FP16 = 0, 1
 LR_NONE, LR_COSINE = 0, 1
 MODE_ORDERED, MODE_ALLREDUCE, MODE_P2P = 0, 1, 2
 INNER_PINGPONG, INNER_INPLACE = 0, 1
 THETA_T, THETA_LOCAL, ADAM_M, ADAM_V, MOMENTUM, GRAD = range(6)
+MSG_REDUCE_CHUNK, MSG_REDUCE_RESULT = 5, 6
+WIRE_DELTA, WIRE_MEAN, WIRE_ROW = range(3)
 
 
 class AdamWState(C.Structure):
@@ -44,6 +46,20 @@ class ReduceReport(C.Structure):
     _fields_ = [("outer_epoch", C.c_uint64), ("contributors", C.c_size_t), ("data_bytes_sent", C.c_uint64),
                 ("data_bytes_received", C.c_uint64), ("wire_bytes_sent", C.c_uint64),
                 ("wire_bytes_received", C.c_uint64), ("wall_ms", C.c_double), ("attempts", C.c_uint32)]
+
+
+class WireTags(C.Structure):
+    _fields_ = [("msg_type", C.c_uint8), ("precision", C.c_int), ("outer_epoch", C.c_uint64),
+                ("attempt", C.c_uint32), ("partition", C.c_uint32), ("from_hi", C.c_uint64),
+                ("from_lo", C.c_uint64), ("chunk_size_bytes", C.c_uint64)]
+
+
+class WireChunk(C.Structure):
+    _fields_ = [("msg_type", C.c_uint8), ("precision", C.c_uint8), ("accepted", C.c_int),
+                ("chunk_index", C.c_uint32), ("attempt", C.c_uint32), ("partition", C.c_uint32),
+                ("outer_epoch", C.c_uint64), ("from_hi", C.c_uint64), ("from_lo", C.c_uint64),
+                ("offset", C.c_uint64), ("length", C.c_uint64), ("frame_offset", C.c_uint64),
+                ("frame_bytes", C.c_uint64)]
 
 
 class Config(C.Structure):
@@ -141,6 +157,15 @@ _SIGS = {
     "dlc_rng_fill_device": (I, [P, I, U64, U64, F, F]),
     "dlc_rng_perturb": (I, [P, P, U64, F, F]),
     "dlc_fp16_encode_bits": (I, [C.c_uint32, SZ, P]),
+    "dlc_wire_frames_size": (I, [U64, C.POINTER(WireTags), C.POINTER(SZ), C.POINTER(C.c_uint64)]),
+    "dlc_wire_encode": (I, [P, U64, U64, C.POINTER(WireTags), P, SZ, C.POINTER(SZ), P]),
+    "dlc_wire_decode": (I, [P, SZ, I, U64, U64, P, C.POINTER(WireChunk), SZ, C.POINTER(SZ), C.POINTER(SZ), P]),
+    "dlc_engine_wire_begin": (I, [P, C.POINTER(C.c_uint64)]),
+    "dlc_engine_wire_encode": (I, [P, I, U64, U64, C.POINTER(WireTags), P, SZ, C.POINTER(SZ)]),
+    "dlc_engine_wire_decode": (I, [P, I, I, U64, U64, P, SZ, C.POINTER(WireChunk), SZ, C.POINTER(SZ),
+                                   C.POINTER(SZ)]),
+    "dlc_engine_wire_fold": (I, [P, I, I, U64, U64]),
+    "dlc_engine_wire_finish": (I, [P, C.c_uint64, C.POINTER(OuterResult)]),
 }
 
 

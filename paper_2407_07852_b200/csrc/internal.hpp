@@ -50,4 +50,11 @@ int guard(F&& f) {
   }
 }
 
+// wire.cu: the reference's reduce-chunk framing from / into device memory
+void wire_encode_impl(const void* dev, uint64_t global_offset, uint64_t elems, const dlc_wire_tags* t,
+                      uint8_t* host_out, size_t cap, size_t* used, cudaStream_t stream);
+void wire_decode_impl(const uint8_t* in, size_t bytes, int precision, uint64_t base, uint64_t capacity, void* dev_out,
+                      dlc_wire_chunk* chunks, size_t max_chunks, size_t* n_chunks, size_t* consumed,
+                      cudaStream_t stream);
+
 }  // namespace dlc

@@ -39,8 +39,12 @@ class CollectiveError(Error):
     pass
 
 
+class SerializationError(Error):
+    pass
+
+
 _EXC = {A.ESHAPE: ShapeError, A.ECONFIG: ConfigError, A.ENUMERIC: NumericError,
-        A.ECOLLECTIVE: CollectiveError, A.ENCCL: CollectiveError}
+        A.ECOLLECTIVE: CollectiveError, A.ENCCL: CollectiveError, A.ESERIAL: SerializationError}
 
 
 def _check(status: int) -> None:
@@ -416,6 +420,41 @@ class DilocoEngine:
             raise ShapeError(A.ESHAPE, "apply_outer_step: length mismatch")
         res = A.OuterResult()
         _check(lib.dlc_engine_apply_outer_step(self.handle, _ptr(m), outer_epoch, C.byref(res)))
+        return OuterStepResult(bool(res.applied), int(res.outer_epoch))
+
+    # -- wire rounds (include/diloco_cuda.h section 5; paper_2407_07852_b200/wire.py) --
+    def wire_begin(self) -> int:
+        ep = C.c_uint64(0)
+        _check(lib.dlc_engine_wire_begin(self.handle, C.byref(ep)))
+        return int(ep.value)
+
+    def wire_encode(self, which: int, offset: int, length: int, tags: A.WireTags, out=None) -> np.ndarray:
+        """Frames of DELTA / MEAN [offset, offset + length) as a uint8 array (or into `out`)."""
+        size = C.c_size_t(0)
+        _check(lib.dlc_wire_frames_size(length, C.byref(tags), C.byref(size), None))
+        if out is None:
+            out = np.empty(max(size.value, 1), np.uint8)
+        used = C.c_size_t(0)
+        _check(lib.dlc_engine_wire_encode(self.handle, which, offset, length, C.byref(tags),
+                                          C.c_void_p(out.ctypes.data), out.nbytes, C.byref(used)))
+        return out[:used.value]
+
+    def wire_decode(self, which: int, row: int, base_offset: int, capacity: int, data, max_chunks: int = 4096):
+        """Returns (list of WireChunk, bytes consumed)."""
+        buf = np.frombuffer(data, np.uint8) if not isinstance(data, np.ndarray) else data
+        chunks = (A.WireChunk * max_chunks)()
+        nc, used = C.c_size_t(0), C.c_size_t(0)
+        _check(lib.dlc_engine_wire_decode(self.handle, which, row, base_offset, capacity,
+                                          C.c_void_p(buf.ctypes.data) if buf.size else None, buf.nbytes, chunks,
+                                          max_chunks, C.byref(nc), C.byref(used)))
+        return [chunks[i] for i in range(min(nc.value, max_chunks))], int(used.value)
+
+    def wire_fold(self, rank: int, k: int, offset: int, length: int) -> None:
+        _check(lib.dlc_engine_wire_fold(self.handle, rank, k, offset, length))
+
+    def wire_finish(self, outer_epoch: int) -> OuterStepResult:
+        res = A.OuterResult()
+        _check(lib.dlc_engine_wire_finish(self.handle, outer_epoch, C.byref(res)))
         return OuterStepResult(bool(res.applied), int(res.outer_epoch))
 
     def set_timing(self, on: bool) -> None:
