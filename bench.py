@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
+    ap.add_argument("--no-wire", action="store_true")
     return ap.parse_args()
 
 
@@ -197,6 +198,54 @@ def workload_config(args, k):
             "theta_local_refresh": "follows theta_t until the next applied inner step (no store)"
             if args.inner_mode == "pingpong" else "stored by K4",
             "l2": "inputs larger than L2 (every vector >= 126 MB)" if args.params * 2 > 126e6 else "L2-resident"}
+
+
+# ---- wire codec ------------------------------------------------------
+
+def measure_wire(D, eng, n, prec, steps=3, cpu=True):
+    """Frames of the whole pseudo-gradient (the scatter side of a cross-box round)
+    produced from HBM into a pinned host buffer, and decoded back into the
+    device mean buffer: wall time through the public API, PCIe-bound.  Beside it
+    the reference's own framing of the same vector on the host cores."""
+    import torch
+
+    from paper_2407_07852_b200 import _capi as A
+    from paper_2407_07852_b200 import wire as W
+    tags = W.make_tags(A.MSG_REDUCE_CHUNK, prec, 0, 0, 1, (0x0123456789ABCDEF, 0xFEDCBA9876543210))
+    import ctypes as C
+    size = C.c_size_t(0)
+    A.lib.dlc_wire_frames_size(n, C.byref(tags), C.byref(size), None)
+    host = torch.empty(size.value, dtype=torch.uint8, pin_memory=True)
+    arr = host.numpy()
+    eng.wire_begin()
+    eng.wire_encode(A.WIRE_DELTA, 0, n, tags, out=arr)  # warm
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        eng.wire_encode(A.WIRE_DELTA, 0, n, tags, out=arr)
+    enc = (time.perf_counter() - t0) / steps
+    eng.wire_decode(A.WIRE_MEAN, 0, 0, n, arr)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        _, used = eng.wire_decode(A.WIRE_MEAN, 0, 0, n, arr)
+    dec = (time.perf_counter() - t0) / steps
+    assert used == size.value
+    out = {"frame_bytes": size.value, "chunk_size_bytes": int(tags.chunk_size_bytes),
+           "encode_ms": enc * 1e3, "encode_gbs": size.value / enc / 1e9, "encode_params_per_s": n / enc,
+           "decode_ms": dec * 1e3, "decode_gbs": size.value / dec / 1e9, "decode_params_per_s": n / dec,
+           "host_buffer": "pinned", "note": "device -> frames in host memory over PCIe (copy engine, strided)"}
+    del host, arr
+    if cpu:
+        from oracle import oracle as O
+        lib = O.reference()
+        if lib is not None:
+            threads = os.cpu_count() or 1
+            slice_len = max(1 << 16, min(1 << 24, n // threads))
+            sec, fbytes = lib.bench_wire(threads, slice_len, prec, int(tags.chunk_size_bytes), 2)
+            out["cpu_reference"] = {"params_per_s": threads * slice_len / sec, "gbs": fbytes / sec / 1e9,
+                                    "cores": threads, "kind": "reference",
+                                    "sample": f"{threads} threads x {slice_len} params: axpy + encode_fp16 + "
+                                              f"send_chunk_span framing (collective.cpp:1318-1345)"}
+    return out
 
 
 # ---- our arm -----------------------------------------------------------------------------
@@ -378,6 +427,8 @@ def run_ours(args):
         if res is not None:
             v, secs, desc = res
             line["cpu_baseline"] = dict(desc, value=v, unit="params/s")
+    if world == 1 and not args.no_wire:
+        line["wire"] = measure_wire(D, eng, n, prec, cpu=not args.no_cpu_baseline)
     if rank == 0:
         print(json.dumps(line))
     eng.close()

@@ -107,6 +107,7 @@ class _Lib:
             self._frame = fn("encode_frame", C.c_int, C.c_uint8, vp, _sz, vp, P(_sz))
             self._rpayload = fn("encode_reduce_payload", C.c_int, _u64, C.c_uint32, C.c_uint8, vp, _sz, vp, P(_sz))
             self._parse_frames = fn("parse_frames", C.c_int, vp, _sz, _sz, vp, vp, vp, vp, vp, vp, _sz, P(_sz))
+            self._bench_wire = fn("bench_wire", C.c_int, C.c_int, _sz, C.c_int, _sz, C.c_int, P(C.c_double), P(_u64))
 
     # -- checkpoints through the reference's save/load_checkpoint (reference only) --------
     _CK_U = ("step_count", "growth_interval", "consecutive_good", "inner_step", "outer_epoch", "engines")
@@ -319,6 +320,14 @@ class _Lib:
         if st:
             raise RuntimeError(f"ref_bench_outer failed with status {st}")
         return float(t.value)
+
+    def bench_wire(self, threads, slice_len, precision, chunk_bytes, iters):
+        """(seconds per iteration, frame bytes per iteration) of the reference's scatter-side framing."""
+        t, b = C.c_double(0), _u64(0)
+        st = self._bench_wire(threads, slice_len, precision, chunk_bytes, iters, C.byref(t), C.byref(b))
+        if st:
+            raise RuntimeError(f"ref_bench_wire failed with status {st}")
+        return float(t.value), int(b.value)
 
     def bench_inner(self, threads, slice_len, iters):
         t = C.c_double(0)

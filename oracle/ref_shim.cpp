@@ -461,3 +461,91 @@ REF_API int ref_parse_frames(const uint8_t* in, size_t n, size_t feed, uint8_t* 
     *nframes = count;
   });
 }
+
+// ---- CPU baseline of the wire path: the scatter side of Node::Impl::all_reduce ----
+// Per thread slice: axpy pseudo-gradient (engine.cpp:122), encode_fp16 once at the
+// source (collective.cpp:1356-1366), then send_chunk_span's framing of the slice
+// (collective.cpp:1318-1345) with the reference's encode_reduce_payload /
+// encode_frame (wire.cpp); the chunk segment header (collective.cpp:63-81, in an
+// anonymous namespace there) is rebuilt inline.  Frames go to a byte vector in
+// place of the socket.
+REF_API int ref_bench_wire(int threads, size_t slice, int precision, size_t chunk_bytes, int iters,
+                           double* sec_per_iter, uint64_t* frame_bytes) {
+  if (threads < 1 || iters < 1 || slice < 1) return kConfig;
+  std::barrier sync(threads + 1);
+  std::vector<double> t_thread(threads, 0.0);
+  std::vector<uint64_t> bytes_thread(threads, 0);
+  std::atomic<int> err{0};
+  auto work = [&](int tid) {
+    try {
+      auto layout = Layout::single("p", slice);
+      const ParamVector tt(layout, fill(4242, "theta", 0, tid * slice, slice, -0.05f, 0.05f));
+      std::vector<float> loc = tt.values().size() ? std::vector<float>(tt.values().begin(), tt.values().end())
+                                                  : std::vector<float>();
+      const std::vector<float> noise = fill(4242, "local", 0, tid * slice, slice, -1e-3f, 1e-3f);
+      for (size_t i = 0; i < slice; ++i) loc[i] -= noise[i];
+      const ParamVector tl(layout, std::move(loc));
+      const std::string name = "a0.p1.f0123456789abcdeffedcba9876543210";
+      for (int it = 0; it < iters; ++it) {
+        sync.arrive_and_wait();
+        const auto t0 = std::chrono::steady_clock::now();
+        const ParamVector delta = axpy(-1.0f, tl, tt);
+        Fp16Buffer codes;
+        const uint8_t* bytes = reinterpret_cast<const uint8_t*>(delta.values().data());
+        size_t width = 4;
+        if (precision) {
+          codes = encode_fp16(delta);
+          bytes = reinterpret_cast<const uint8_t*>(codes.bits.data());
+          width = 2;
+        }
+        const uint64_t max_elems = std::max<uint64_t>(1, chunk_bytes / width);
+        uint64_t total = 0;
+        uint32_t chunk_index = 0;
+        for (uint64_t start = 0; start < slice; start += max_elems) {
+          const uint64_t count = std::min<uint64_t>(max_elems, slice - start);
+          std::vector<uint8_t> seg;
+          seg.reserve(32 + name.size() + count * width);
+          auto put_u64 = [&seg](uint64_t v) {
+            for (int i = 0; i < 8; ++i) seg.push_back(static_cast<uint8_t>(v >> (8 * i)));
+          };
+          put_u64(1);
+          put_u64(name.size());
+          seg.insert(seg.end(), name.begin(), name.end());
+          put_u64(start);
+          put_u64(count);
+          seg.insert(seg.end(), bytes + start * width, bytes + (start + count) * width);
+          ReduceChunkHeader h;
+          h.outer_epoch = 0;
+          h.chunk_index = chunk_index++;
+          h.precision = precision ? 1 : 0;
+          WireMessage m;
+          m.type = MsgType::reduce_chunk;
+          m.payload = encode_reduce_payload(h, seg);
+          total += encode_frame(m).size();
+        }
+        t_thread[tid] += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        bytes_thread[tid] = total;
+        sync.arrive_and_wait();
+      }
+    } catch (...) {
+      err = 1;
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 0; t < threads; ++t) pool.emplace_back(work, t);
+  for (int it = 0; it < iters; ++it) {
+    sync.arrive_and_wait();
+    sync.arrive_and_wait();
+  }
+  for (auto& th : pool) th.join();
+  if (err) return kOther;
+  double worst = 0.0;
+  uint64_t total = 0;
+  for (int t = 0; t < threads; ++t) {
+    worst = t_thread[t] > worst ? t_thread[t] : worst;
+    total += bytes_thread[t];
+  }
+  *sec_per_iter = worst / iters;
+  *frame_bytes = total;
+  return kOk;
+}

@@ -1717,6 +1717,27 @@ char* wire_vector(dlc_engine* e, int which) {
   fail(DLC_EINVAL, "wire: unknown buffer " + std::to_string(which));
 }
 
+// Fold rows are stored 8 elements apart at least (16-byte aligned vectors for
+// the fold kernel, whatever the owned range's length).
+uint64_t row_stride(uint64_t capacity) { return (capacity + 7) / 8 * 8; }
+
+// Grows the row buffer to `rows` rows of the current stride, keeping its contents.
+char* wire_rows(dlc_engine* e, size_t rows) {
+  const size_t need = std::max<size_t>(rows * row_stride(e->wire_stride) * elem_width(e->prec), 256);
+  if (need > e->wire_rows_bytes) {
+    DLC_CUDA(cudaStreamSynchronize(e->stream));
+    void* fresh = nullptr;
+    DLC_CUDA(cudaMalloc(&fresh, need));
+    if (e->wire_rows) {
+      DLC_CUDA(cudaMemcpy(fresh, e->wire_rows, e->wire_rows_bytes, cudaMemcpyDeviceToDevice));
+      cudaFree(e->wire_rows);
+    }
+    e->wire_rows = fresh;
+    e->wire_rows_bytes = need;
+  }
+  return static_cast<char*>(e->wire_rows);
+}
+
 void check_range(dlc_engine* e, uint64_t offset, uint64_t length) {
   if (offset > e->n || length > e->n - offset)
     fail(DLC_ESHAPE, "wire: range [" + std::to_string(offset) + ", +" + std::to_string(length) +
@@ -1762,23 +1783,8 @@ int dlc_engine_wire_decode(dlc_engine* e, int which, int row, uint64_t base_offs
     char* dst = nullptr;
     if (which == DLC_WIRE_ROW) {  // contributor `row`'s slice of the owned range
       if (row < 0 || row >= kMaxK) fail(DLC_EINVAL, "wire decode: row out of range");
-      if (capacity != e->wire_stride) {
-        e->wire_stride = capacity;  // a new range (round / membership): earlier rows are stale
-      }
-      const size_t need = std::max<size_t>((size_t)(row + 1) * capacity * w, 256);
-      if (need > e->wire_rows_bytes) {
-        DLC_CUDA(cudaStreamSynchronize(e->stream));
-        void* fresh = nullptr;
-        const size_t bytes_new = std::max(need, (size_t)kMaxK * capacity * w / 4);
-        DLC_CUDA(cudaMalloc(&fresh, bytes_new));
-        if (e->wire_rows) {
-          DLC_CUDA(cudaMemcpy(fresh, e->wire_rows, e->wire_rows_bytes, cudaMemcpyDeviceToDevice));
-          cudaFree(e->wire_rows);
-        }
-        e->wire_rows = fresh;
-        e->wire_rows_bytes = bytes_new;
-      }
-      dst = static_cast<char*>(e->wire_rows) + (size_t)row * capacity * w;
+      e->wire_stride = capacity;  // a new range (round / membership) makes earlier rows stale
+      dst = wire_rows(e, (size_t)row + 1) + (size_t)row * row_stride(capacity) * w;
     } else if (which == DLC_WIRE_MEAN || which == DLC_WIRE_DELTA) {
       dst = wire_vector(e, which) + base_offset * w;
     } else {
@@ -1794,20 +1800,29 @@ int dlc_engine_wire_fold(dlc_engine* e, int rank, int k, uint64_t offset, uint64
     if (!e) fail(DLC_EINVAL, "dlc_engine_wire_fold: null engine");
     if (k < 1 || k > kMaxK || rank < 0 || rank >= k) fail(DLC_EINVAL, "wire fold: bad rank / contributor count");
     check_range(e, offset, length);
-    if (k > 1 && length != e->wire_stride)
+    if (k > 1 && length != e->wire_stride && e->wire_rows)
       fail(DLC_ESHAPE, "wire fold: rows were decoded for a range of " + std::to_string(e->wire_stride) +
                            " elements, fold asks for " + std::to_string(length));
     if (k > 1 && !e->wire_rows) fail(DLC_EINVAL, "wire fold: no contributions decoded");
     DeviceGuard dg(e->device);
     const size_t w = elem_width(e->prec);
+    e->wire_stride = length;
+    const size_t stride = row_stride(length) * w;
+    char* rows = wire_rows(e, (size_t)k + 1);  // k contributions + an aligned output row
+    char* own = reinterpret_cast<char*>(e->grad) + offset * w;
+    char* out = static_cast<char*>(e->send) + offset * w;
+    const bool aligned = (offset * w) % 16 == 0;  // vector loads / stores of the fold kernel
+    if (!aligned && length)  // our own slice joins the rows
+      DLC_CUDA(cudaMemcpyAsync(rows + (size_t)rank * stride, own, length * w, cudaMemcpyDeviceToDevice, e->stream));
     PtrList in{};
-    for (int j = 0; j < k; ++j)  // peer-sorted order; our own slice straight from DELTA (collective.cpp:1460-1474)
-      in.ptr[j] = j == rank ? reinterpret_cast<char*>(e->grad) + offset * w
-                            : static_cast<char*>(e->wire_rows) + (size_t)j * length * w;
+    for (int j = 0; j < k; ++j)  // peer-sorted order; our own slice from DELTA (collective.cpp:1460-1474)
+      in.ptr[j] = (j == rank && aligned) ? own : rows + (size_t)j * stride;
     DLC_CUDA(cudaMemsetAsync(e->flags, 0, sizeof(int), e->stream));
     if (length) {
-      launch_fold(in, k, e->prec, static_cast<char*>(e->send) + offset * w, e->prec, e->flags, length, e->stream);
+      char* dst = aligned ? out : rows + (size_t)k * stride;
+      launch_fold(in, k, e->prec, dst, e->prec, e->flags, length, e->stream);
       launched("fold");
+      if (!aligned) DLC_CUDA(cudaMemcpyAsync(out, dst, length * w, cudaMemcpyDeviceToDevice, e->stream));
     }
     DLC_CUDA(cudaStreamSynchronize(e->stream));
   });
