@@ -361,6 +361,21 @@ DLC_API int dlc_engine_set_timing(dlc_engine* e, int on);
 DLC_API int dlc_engine_phase_times(dlc_engine* e, double total_ms[4], uint64_t count[4]);
 
 /* =========================================================================
+ * 4. Synthetic inputs and test probes (bench / parity tests).  Counter-based
+ *    streams identical to the reference's CounterRng (rng.hpp:38-74).
+ * ========================================================================= */
+
+/* key of CounterRng(seed, purpose, index) */
+DLC_API uint64_t dlc_rng_key(uint64_t seed, const char* purpose, uint64_t index);
+/* dev[i] = draw (first + i) of the stream `key`, uniform in [lo, hi). */
+DLC_API int dlc_rng_fill_device(dlc_engine* e, int which, uint64_t key, uint64_t first, float lo, float hi);
+/* dst = theta_t - U(lo, hi) drawn from `key` (synthetic end-of-window weights);
+ * dst = NULL writes the engine's own theta_local, else a caller device buffer of n. */
+DLC_API int dlc_rng_perturb(dlc_engine* e, float* dst, uint64_t key, float lo, float hi);
+/* FP16 codes of the 2^32 FP32 bit patterns [start, start + n) (host out). */
+DLC_API int dlc_fp16_encode_bits(uint32_t start, size_t n, uint16_t* out);
+
+/* =========================================================================
  * 5. Wire codec for cross-box transports.
  *
  *    The reference's TCP collective moves pseudo-gradient slices as framed
@@ -448,21 +463,6 @@ DLC_API int dlc_engine_wire_decode(dlc_engine* e, int which, int row, uint64_t b
                                    size_t* n_chunks, size_t* consumed);
 DLC_API int dlc_engine_wire_fold(dlc_engine* e, int rank, int k, uint64_t offset, uint64_t length);
 DLC_API int dlc_engine_wire_finish(dlc_engine* e, uint64_t outer_epoch, dlc_outer_result* result);
-
-/* =========================================================================
- * 4. Synthetic inputs and test probes (bench / parity tests).  Counter-based
- *    streams identical to the reference's CounterRng (rng.hpp:38-74).
- * ========================================================================= */
-
-/* key of CounterRng(seed, purpose, index) */
-DLC_API uint64_t dlc_rng_key(uint64_t seed, const char* purpose, uint64_t index);
-/* dev[i] = draw (first + i) of the stream `key`, uniform in [lo, hi). */
-DLC_API int dlc_rng_fill_device(dlc_engine* e, int which, uint64_t key, uint64_t first, float lo, float hi);
-/* dst = theta_t - U(lo, hi) drawn from `key` (synthetic end-of-window weights);
- * dst = NULL writes the engine's own theta_local, else a caller device buffer of n. */
-DLC_API int dlc_rng_perturb(dlc_engine* e, float* dst, uint64_t key, float lo, float hi);
-/* FP16 codes of the 2^32 FP32 bit patterns [start, start + n) (host out). */
-DLC_API int dlc_fp16_encode_bits(uint32_t start, size_t n, uint16_t* out);
 
 #ifdef __cplusplus
 }

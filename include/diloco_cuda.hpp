@@ -15,6 +15,7 @@
 // classes (errors.hpp:12-51), so error behaviour is unchanged for callers.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <string>
 #include <utility>
@@ -37,6 +38,7 @@ inline void throw_status(int st) {
     case DLC_ENUMERIC: throw NumericError(msg);
     case DLC_ECOLLECTIVE:
     case DLC_ENCCL: throw CollectiveError(msg);
+    case DLC_ESERIAL: throw SerializationError(msg);
     default: throw Error(msg);
   }
 }
@@ -231,6 +233,43 @@ class DeviceEngine {
   }
 
   dlc_engine* handle() const { return e_; }
+
+  // ---- wire rounds for the reference's TCP Node (diloco_cuda.h section 5) ----
+  /// K2 into the DELTA buffer in the engine's precision; returns the outer epoch.
+  uint64_t wire_begin() {
+    uint64_t epoch = 0;
+    throw_status(dlc_engine_wire_begin(e_, &epoch));
+    return epoch;
+  }
+  /// The bytes send_chunk_span (collective.cpp:1318-1345) puts on the wire for
+  /// DELTA / MEAN [offset, offset + length).
+  std::vector<uint8_t> wire_encode(int which, uint64_t offset, uint64_t length, const dlc_wire_tags& tags) {
+    size_t bytes = 0;
+    throw_status(dlc_wire_frames_size(length, &tags, &bytes, nullptr));
+    std::vector<uint8_t> out(bytes);
+    size_t used = 0;
+    throw_status(dlc_engine_wire_encode(e_, which, offset, length, &tags, out.data(), out.size(), &used));
+    out.resize(used);
+    return out;
+  }
+  /// Decodes the complete frames of `bytes` into a fold row / MEAN; returns the bytes consumed.
+  size_t wire_decode(int which, int row, uint64_t base_offset, uint64_t capacity, const std::vector<uint8_t>& bytes,
+                     std::vector<dlc_wire_chunk>* chunks = nullptr) {
+    size_t n_chunks = 0, consumed = 0;
+    std::vector<dlc_wire_chunk> scratch(chunks ? 4096 : 0);
+    throw_status(dlc_engine_wire_decode(e_, which, row, base_offset, capacity, bytes.data(), bytes.size(),
+                                        chunks ? scratch.data() : nullptr, scratch.size(), &n_chunks, &consumed));
+    if (chunks) chunks->assign(scratch.begin(), scratch.begin() + std::min(n_chunks, scratch.size()));
+    return consumed;
+  }
+  void wire_fold(int rank, int k, uint64_t offset, uint64_t length) {
+    throw_status(dlc_engine_wire_fold(e_, rank, k, offset, length));
+  }
+  dlc_outer_result wire_finish(uint64_t epoch) {
+    dlc_outer_result r{};
+    throw_status(dlc_engine_wire_finish(e_, epoch, &r));
+    return r;
+  }
 
  private:
   LayoutPtr layout_;

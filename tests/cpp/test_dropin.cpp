@@ -7,11 +7,14 @@
 // Every check compares diloco::X (reference CPU) with diloco::cuda::X (B200)
 // using the reference's bitwise ParamVector equality (tensor.cpp:106-116).
 #include <cmath>
+#include <cstring>
+#include <span>
 #include <cstdio>
 #include <string>
 #include <vector>
 
 #include "diloco/rng.hpp"
+#include "diloco/wire.hpp"
 #include "diloco_cuda.hpp"
 
 using namespace diloco;
@@ -37,6 +40,10 @@ static bool throws(F&& f) {
     return false;
   }
   return false;
+}
+
+static void throw_status_ok(int st) {
+  if (st != DLC_OK) throw Error(dlc_last_error());
 }
 
 static ParamVector random_vec(LayoutPtr layout, uint64_t seed, const char* purpose, float lo, float hi) {
@@ -224,6 +231,76 @@ int main() {
     bad[3] = NAN;
     CHECK(dlc_engine_apply_outer_step(eng.handle(), bad.data(), eng.scalars().outer_epoch, &r) == DLC_OK);
     CHECK(r.applied == 0 && eng.download(DLC_THETA_T) == theta_t && eng.download(DLC_THETA_LOCAL) == theta_t);
+  }
+  // ---- wire codec: frames from the device engine through the reference's own
+  // FrameParser / decode_reduce_payload (wire.cpp); scalars = encode_fp16 of the
+  // reference's axpy pseudo-gradient; then a 2-worker round whose only exchange
+  // is those bytes, against reduce_average + nesterov_step.
+  {
+    const size_t n = 5003;
+    auto layout = Layout::single("p", n);
+    const ParamVector theta0 = random_vec(layout, 31, "theta", -1.0f, 1.0f);
+    dlc_config cfg{1, 2, DLC_FP16, 4};
+    dlc_hyperparams hp;
+    dlc_hyperparams_default(&hp);
+    cuda::DeviceEngine e0(cfg, hp, theta0, 0, DLC_INNER_PINGPONG), e1(cfg, hp, theta0, 0, DLC_INNER_PINGPONG);
+    std::vector<ParamVector> locals;
+    for (int j = 0; j < 2; ++j) {
+      std::vector<float> l(theta0.values().begin(), theta0.values().end());
+      const ParamVector noise = random_vec(layout, 40 + j, "local", -1e-2f, 1e-2f);
+      for (size_t i = 0; i < n; ++i) l[i] -= noise.values()[i];
+      locals.emplace_back(layout, std::move(l));
+    }
+    throw_status_ok(dlc_engine_upload(e0.handle(), DLC_THETA_LOCAL, locals[0].values().data(), n));
+    throw_status_ok(dlc_engine_upload(e1.handle(), DLC_THETA_LOCAL, locals[1].values().data(), n));
+    cuda::DeviceEngine* eng[2] = {&e0, &e1};
+    const uint64_t epoch = e0.wire_begin();
+    CHECK(e1.wire_begin() == epoch);
+    const auto ranges = partition_ranges(n, 2);
+    const dlc_wire_tags t{DLC_MSG_REDUCE_CHUNK, DLC_FP16, epoch, 0, 1, 0x11, 0x22, 4096};
+    const std::vector<uint8_t> frames = e0.wire_encode(DLC_WIRE_DELTA, ranges[1].offset, ranges[1].length, t);
+    FrameParser parser;
+    parser.feed(frames);
+    const Fp16Buffer want = encode_fp16(axpy(-1.0f, locals[0], theta0));
+    size_t elems = 0, chunks = 0;
+    while (auto m = parser.next()) {
+      std::span<const uint8_t> seg;
+      const ReduceChunkHeader h = decode_reduce_payload(m->payload, seg);
+      CHECK(m->type == MsgType::reduce_chunk && h.outer_epoch == epoch && h.chunk_index == chunks && h.precision == 1);
+      const size_t header = 32 + std::string("a0.p1.f00000000000000110000000000000022").size();
+      const size_t count = (seg.size() - header) / 2;
+      CHECK(std::memcmp(seg.data() + header, want.bits.data() + ranges[1].offset + elems, count * 2) == 0);
+      elems += count;
+      ++chunks;
+    }
+    CHECK(elems == ranges[1].length && chunks == (ranges[1].length + 2047) / 2048);
+    // the round: scatter, fold, ring all-gather, outer step
+    for (int r = 0; r < 2; ++r) {
+      const int p = 1 - r;
+      const dlc_wire_tags ts{DLC_MSG_REDUCE_CHUNK, DLC_FP16, epoch, 0, (uint32_t)p, 0x11, (uint64_t)r, 4096};
+      const auto bytes = eng[r]->wire_encode(DLC_WIRE_DELTA, ranges[p].offset, ranges[p].length, ts);
+      CHECK(eng[p]->wire_decode(DLC_WIRE_ROW, r, ranges[p].offset, ranges[p].length, bytes) == bytes.size());
+    }
+    for (int r = 0; r < 2; ++r) eng[r]->wire_fold(r, 2, ranges[r].offset, ranges[r].length);
+    for (int r = 0; r < 2; ++r) {
+      const dlc_wire_tags ts{DLC_MSG_REDUCE_RESULT, DLC_FP16, epoch, 0, (uint32_t)r, 0x11, (uint64_t)r, 4096};
+      const auto bytes = eng[r]->wire_encode(DLC_WIRE_MEAN, ranges[r].offset, ranges[r].length, ts);
+      CHECK(eng[1 - r]->wire_decode(DLC_WIRE_MEAN, 0, 0, n, bytes) == bytes.size());
+    }
+    const ParamVector d0 = axpy(-1.0f, locals[0], theta0), d1 = axpy(-1.0f, locals[1], theta0);
+    std::vector<const ParamVector*> ptrs{&d0, &d1};
+    const ParamVector dbar = reduce_average(ptrs, Precision::fp16);
+    NesterovState outer = NesterovState::init(layout, hp.outer_lr, hp.outer_momentum);
+    const ParamVector theta1 = nesterov_step(outer, theta0, dbar);
+    for (int r = 0; r < 2; ++r) {
+      const dlc_outer_result o = eng[r]->wire_finish(epoch);
+      CHECK(o.applied == 1 && o.outer_epoch == epoch + 1);
+      CHECK(eng[r]->download(DLC_THETA_T) == theta1 && eng[r]->download(DLC_THETA_LOCAL) == theta1);
+      CHECK(eng[r]->download(DLC_MOMENTUM) == outer.momentum_buf);
+    }
+    std::vector<uint8_t> bad = frames;
+    bad[0] = 'X';
+    CHECK(throws<SerializationError>([&] { e1.wire_decode(DLC_WIRE_MEAN, 0, 0, n, bad); }));
   }
   std::printf("test_dropin: %d passed, %d failed\n", g_pass, g_fail);
   return g_fail == 0 ? 0 : 1;
