@@ -194,6 +194,12 @@ bool p2p_mover_push() {
   const char* s = std::getenv("DLC_P2P_COPY");
   return s && std::string(s) == "push";
 }
+// push/push: K2 writes locally, a scatter kernel on the comm stream pushes the
+// rows to their owners, the owners fold locally and push the means
+bool p2p_mover_push2() {
+  const char* s = std::getenv("DLC_P2P_COPY");
+  return s && std::string(s) == "push2";
+}
 
 // CTAs of the persistent SM mover (0 = one CTA per window, no SM partitioning);
 // default 384 of the 1184 resident CTA slots (profiles/r1_sweep_p2p_*_barrier.log).
@@ -660,18 +666,33 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
   cudaEvent_t c0 = pooled_event(e), c1 = pooled_event(e);
   DLC_CUDA(cudaEventRecord(c0, e->cstream));
   const bool sm_mover = p2p_mover_sm();
+  const bool push2 = p2p_mover_push2();
   for (size_t p = 0; p < P && sm_mover; ++p) {
     // SM mover: a persistent fold kernel on a few CTAs pulls slot r / piece p of
     // every rank's delta and pushes the mean (and a non-finite mark) into slot r
     // of every rank's gather buffer (flags reset by each rank before its K2(0)).
     DLC_CUDA(cudaStreamWaitEvent(e->cstream, evK2[p], 0));
+    if (push2) {  // push/push: our piece of every foreign slot into its owner's recv row r
+      PtrList src{}, dst{};
+      int nrow = 0;
+      for (size_t q = 0; q < K; ++q) {
+        if ((int)q == r) continue;
+        src.ptr[nrow] = send + (q * S + po(p)) * w;
+        dst.ptr[nrow] = static_cast<char*>(e->peer_recv[q]) + (r * S + po(p)) * w;
+        ++nrow;
+      }
+      cudaEvent_t ts = trace_begin(e, e->cstream);
+      launch_scatter_push(src, dst, nrow, pl(p) * w, comm_ctas(), e->cstream);
+      trace_end(e, e->cstream, "scatter", (int)p, ts);
+    }
     cudaEvent_t ta = trace_begin(e, e->cstream);
     p2p_barrier(e, c, e->cstream);  // A_p
     trace_end(e, e->cstream, "barrierA", (int)p, ta);
     PtrList in{}, outs{}, pfl{};
     for (size_t j = 0; j < K; ++j) {
-      in.ptr[j] = push_mover ? recv + (j * S + po(p)) * w  // rows already pushed here by K2
-                             : static_cast<char*>(e->peer_send[j]) + (r * S + po(p)) * w;
+      in.ptr[j] = (int)j == r && push2 ? send + (r * S + po(p)) * w  // own row stays local
+                  : (push_mover || push2) ? recv + (j * S + po(p)) * w   // rows already pushed here
+                                          : static_cast<char*>(e->peer_send[j]) + (r * S + po(p)) * w;
       outs.ptr[j] = static_cast<char*>(e->peer_gather[j]) + (r * S + po(p)) * w;
       pfl.ptr[j] = e->peer_flags[j] + r;
     }

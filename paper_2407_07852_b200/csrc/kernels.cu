@@ -431,6 +431,24 @@ __global__ void __launch_bounds__(kThreads) fold_push_kernel(const __grid_consta
   if (threadIdx.x == 0) __threadfence_system();
 }
 
+// Scatter half of the push/push P2P mover: row q of `src` (this rank's piece of
+// owner q's slot, in local HBM) is stored into row `me` of owner q's receive
+// buffer over NVLink.  Consecutive 16-byte vectors go to different owners so
+// every link carries traffic at once.
+__global__ void __launch_bounds__(kThreads) scatter_push_kernel(const __grid_constant__ PtrList src,
+                                                                const __grid_constant__ PtrList dst, int nrow,
+                                                                size_t bytes) {
+  const size_t n16 = bytes / 16, total = n16 * (size_t)nrow;
+  for (size_t i = gtid(); i < total; i += gstride()) {
+    const int q = (int)(i % (size_t)nrow);
+    const size_t j = i / (size_t)nrow;
+    const uint4 v = ld_stream(reinterpret_cast<const uint4*>(src.ptr[q]) + j);
+    st_stream(reinterpret_cast<uint4*>(const_cast<void*>(dst.ptr[q])) + j, v);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) __threadfence_system();  // the CTA's stores land before the barrier that follows
+}
+
 // =============================================================================
 // K4: finite-gated Nesterov on theta_t + theta_local refresh (engine.cpp:136-144).
 // =============================================================================
@@ -902,6 +920,12 @@ void launch_fold_push(const PtrList& in, int k, int precision, const PtrList& ou
     fold_push_kernel<0><<<grid, kThreads, 0, s>>>(in, k, outs, nout, flags, n);
   else
     fold_push_kernel<1><<<grid, kThreads, 0, s>>>(in, k, outs, nout, flags, n);
+}
+
+void launch_scatter_push(const PtrList& src, const PtrList& dst, int nrow, size_t bytes, int ctas, cudaStream_t s) {
+  const size_t vecs = bytes / 16 * (size_t)nrow;
+  const int grid = (int)std::max<size_t>(1, std::min<size_t>(ctas > 0 ? ctas : 4 * num_sms(), (vecs + kThreads - 1) / kThreads));
+  scatter_push_kernel<<<grid, kThreads, 0, s>>>(src, dst, nrow, bytes);
 }
 
 void launch_flag_barrier(const PtrList& remote, const uint64_t* local, int k, int me, uint64_t epoch, int* err,

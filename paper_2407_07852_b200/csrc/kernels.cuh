@@ -128,6 +128,8 @@ void launch_fold_push(const PtrList& in, int k, int precision, const PtrList& ou
 // slot `me` of every peer's signal array (`remote`, after a system fence), then
 // waits until every peer's store has landed in `local`.  A peer silent for
 // ~10 s sets *err and the kernel exits instead of hanging the GPU.
+// push/push mover: rows src[q] -> dst[q] (`bytes` each, a multiple of 16), a persistent grid of `ctas`
+void launch_scatter_push(const PtrList& src, const PtrList& dst, int nrow, size_t bytes, int ctas, cudaStream_t s);
 void launch_flag_barrier(const PtrList& remote, const uint64_t* local, int k, int me, uint64_t epoch,
                          int* err, cudaStream_t s);
 void launch_pseudo_grad_piece(Pair theta_t, Pair theta_local, const DevState* st, void* send,

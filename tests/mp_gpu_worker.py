@@ -46,6 +46,7 @@ def main():
     # P2P runs once per data mover and barrier flavour (read per step from the environment)
     cases = [("ordered", D.MODE_ORDERED, {}), ("p2p", D.MODE_P2P, {"DLC_P2P_COPY": "sm"}),
              ("p2p-push", D.MODE_P2P, {"DLC_P2P_COPY": "push", "DLC_P2P_PLAN": "2,2,2,2"}),
+             ("p2p-push2", D.MODE_P2P, {"DLC_P2P_COPY": "push2", "DLC_P2P_PLAN": "1,3,4"}),
              ("p2p-ce", D.MODE_P2P, {"DLC_P2P_COPY": "ce", "DLC_P2P_BARRIER": "nccl", "DLC_P2P_PIECES": "2"}),
              ("allreduce", D.MODE_ALLREDUCE, {})]
     for mode_name, mode, env in cases:

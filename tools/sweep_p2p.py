@@ -46,7 +46,7 @@ def main():
     for barrier in barriers:
         for mover in movers:
             for pieces in (plans or pieces_l):
-                for ctas in (ctas_l if mover in ("sm", "push") else (0,)):
+                for ctas in (ctas_l if mover in ("sm", "push", "push2") else (0,)):
                     configs.append(("p2p", mover, pieces, ctas, barrier))
     results = []
     for mode, mover, pieces, ctas, barrier in configs:
