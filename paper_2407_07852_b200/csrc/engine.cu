@@ -569,21 +569,25 @@ void outer_collective(dlc_engine* e, dlc_collective* c, dlc_reduce_report* rep) 
   }
 }
 
-// DLC_MODE_P2P: the rank-ordered owner fold with the bytes moved by the DMA
-// copy engines over NVLink (pulls from CUDA-IPC peer pointers), pipelined over
-// P = p2p_pieces() pieces, piece p being a sub-range of every owner slot:
-//   main       K2(p)                                              -> evK2[p]
-//   cstream    wait evK2[p]; A_p (4-byte NCCL all-reduce)         -> evA[p]
-//   pull[j]    wait evA[p];  recv row j <- rank j's send (slot r, piece p)
-//   cstream    wait pulls;   fold(p) -> my gather slot + my flag; B_p -> evB[p]
-//   gath[q]    wait evB[p];  gather slot q <- owner q's gather slot (piece p)
-//   main       wait gathers; K4(p) speculative;  ...;  finish (all owner flags)
-// Copy engines need no SMs, so the NVLink time of piece p overlaps the HBM
-// kernels of pieces p-1 / p+1.  A_p orders every rank's K2(p) (and, for p = 0,
-// every rank's previous finish) before anyone pulls; B_p orders every fold(p)
-// before anyone gathers.  flags[r] (read remotely by every finish) is only
-// cleared after A_0.  With host buffers (`hsrc` / `hdst`) piece p is also
-// copied in before K2(p) and its new theta_t copied out after K4(p).
+// DLC_MODE_P2P: the rank-ordered owner fold fused with its own data movement
+// over NVLink peer memory (CUDA IPC), pipelined over the pieces of piece_plan()
+// (piece p = the same sub-range of every owner slot):
+//   main     K2(p) into my send buffer                                 -> evK2[p]
+//   cstream  wait evK2[p]; barrier A_p (every rank's K2(p) is done);
+//            fold_push(p): the owner pulls piece p of slot r from every rank,
+//            folds in rank order, pushes the mean + a non-finite mark into
+//            slot r of every rank's gather buffer; barrier B_p          -> evB[p]
+//   main     wait evB[p]; K4(p) speculative into the idle theta_t / momentum;
+//            ...; finish (flip ocur when every owner flag is clean)
+// The fold kernel keeps DLC_COMM_CTAS CTAs, so the NVLink time of piece p
+// overlaps the HBM-bound K2 / K4 pieces on the other SMs.  Other movers
+// (DLC_P2P_COPY): "ce" pulls / gathers with the copy engines around a local
+// fold; "push" stores K2's rows straight into the owners' receive buffers;
+// "push2" pushes them from a scatter kernel on the comm stream.  A_p orders
+// every rank's K2(p) (and, for p = 0, every rank's previous finish) before
+// anyone reads them; B_p orders every push of piece p before any K4(p).  With
+// host buffers (`hsrc` / `hdst`) piece p is also copied in before K2(p) and its
+// new theta_t copied out after K4(p).
 void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc_reduce_report* rep,
                          const float* hsrc, float* hdst, int oc_host) {
   p2p_bind(e, c);
