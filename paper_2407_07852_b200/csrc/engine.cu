@@ -207,6 +207,11 @@ int comm_ctas() {
   const char* s = std::getenv("DLC_COMM_CTAS");
   return s ? (int)std::strtol(s, nullptr, 10) : 384;
 }
+// CTAs of the K2 / K4 piece kernels running beside the fold (0: one per window)
+int piece_ctas() {
+  const char* s = std::getenv("DLC_P2P_PIECE_CTAS");
+  return s ? (int)std::strtol(s, nullptr, 10) : 0;
+}
 
 void ensure_copy_streams(dlc_engine* e) {
   if (!e->h2d) DLC_CUDA(cudaStreamCreateWithFlags(&e->h2d, cudaStreamNonBlocking));
@@ -659,7 +664,8 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
       for (size_t q = 0; q < K; ++q) rows.ptr[q] = static_cast<char*>(e->peer_recv[q]) + r * S * w;
       launch_pseudo_grad_push_piece(tt_pair(e), tl, e->st, rows, e->prec, (int)K, S, po(p), pl(p), n, e->stream);
     } else {
-      launch_pseudo_grad_piece(tt_pair(e), tl, e->st, e->send, e->prec, (int)K, S, po(p), pl(p), n, e->stream);
+      launch_pseudo_grad_piece(tt_pair(e), tl, e->st, e->send, e->prec, (int)K, S, po(p), pl(p), n, piece_ctas(),
+                               e->stream);
     }
     trace_end(e, e->stream, "K2", (int)p, t0);
     DLC_CUDA(cudaEventRecord(evK2[p], e->stream));
@@ -760,7 +766,7 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
       if ((int)q != r) DLC_CUDA(cudaStreamWaitEvent(e->stream, evGath[q * P + p], 0));
     cudaEvent_t t4 = trace_begin(e, e->stream);
     launch_nesterov_p2p_piece(tt_pair(e), buf_pair(e), local_pair(e), slots, (int)K, S, po(p), pl(p), e->prec, e->st,
-                              lr, mu, n, e->stream);
+                              lr, mu, n, piece_ctas(), e->stream);
     trace_end(e, e->stream, "K4", (int)p, t4);
     if (hdst) {
       DLC_CUDA(cudaEventRecord(evK4[p], e->stream));

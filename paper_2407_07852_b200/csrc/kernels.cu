@@ -551,15 +551,12 @@ __global__ void flag_barrier_kernel(const __grid_constant__ PtrList remote, cons
 // piece, so every piece launch spreads over all slots.
 
 template <int PREC>
-__global__ void __launch_bounds__(kThreads) pseudo_grad_piece_kernel(Pair ttp, Pair tl, const DevState* st,
-                                                                     void* send, int k, size_t S, size_t po,
-                                                                     size_t plen, size_t n) {
-  const int q = (int)(blockIdx.x % (unsigned)k);
-  const size_t j = (size_t)(blockIdx.x / (unsigned)k) * kThreads + threadIdx.x;
+__device__ __forceinline__ void pseudo_grad_piece_block(const float* T, const float* L, void* send, size_t blk, int k,
+                                                        size_t S, size_t po, size_t plen, size_t n) {
+  const int q = (int)(blk % (unsigned)k);
+  const size_t j = (blk / (unsigned)k) * kThreads + threadIdx.x;
   const size_t e0 = (size_t)q * S + po + 4 * j;
   if (4 * j >= plen || e0 >= n) return;
-  const float* T = sel(ttp, st->ocur);
-  const float* L = local_src(tl, ttp, st);
   if (e0 + 3 < n) {
     const float4 x = ld_stream(reinterpret_cast<const float4*>(T + e0));
     const float4 y = ld_stream(reinterpret_cast<const float4*>(L + e0));
@@ -580,6 +577,17 @@ __global__ void __launch_bounds__(kThreads) pseudo_grad_piece_kernel(Pair ttp, P
         static_cast<uint16_t*>(send)[e] = fp16_encode(d);
     }
   }
+}
+
+// `nblk` logical blocks (one 256-vector window of one owner slot each) over a
+// grid that may be smaller (DLC_P2P_PIECE_CTAS), leaving SMs to the fold.
+template <int PREC>
+__global__ void __launch_bounds__(kThreads) pseudo_grad_piece_kernel(Pair ttp, Pair tl, const DevState* st,
+                                                                     void* send, int k, size_t S, size_t po,
+                                                                     size_t plen, size_t n, size_t nblk) {
+  const float* T = sel(ttp, st->ocur);
+  const float* L = local_src(tl, ttp, st);
+  for (size_t b = blockIdx.x; b < nblk; b += gridDim.x) pseudo_grad_piece_block<PREC>(T, L, send, b, k, S, po, plen, n);
 }
 
 template <int PREC>
@@ -621,20 +629,13 @@ __global__ void __launch_bounds__(kThreads) pseudo_grad_push_piece_kernel(Pair t
 }
 
 template <int PREC>
-__global__ void __launch_bounds__(kThreads) nesterov_p2p_piece_kernel(Pair ttp, Pair bufp, Pair tl,
-                                                                      const __grid_constant__ PtrList slots, int k,
-                                                                      size_t S, size_t po, size_t plen,
-                                                                      DevState* st, float lr, float mu, size_t n) {
-  const int q = (int)(blockIdx.x % (unsigned)k);
-  const size_t j = (size_t)(blockIdx.x / (unsigned)k) * kThreads + threadIdx.x;
+__device__ __forceinline__ void nesterov_p2p_piece_block(const float* T, const float* B, float* To, float* Bo, float* L,
+                                                         const PtrList& slots, size_t blk, int k, size_t S, size_t po,
+                                                         size_t plen, float lr, float mu, size_t n) {
+  const int q = (int)(blk % (unsigned)k);
+  const size_t j = (blk / (unsigned)k) * kThreads + threadIdx.x;
   const size_t e0 = (size_t)q * S + po + 4 * j;
   if (4 * j >= plen || e0 >= n) return;
-  const int oc = st->ocur;
-  const float* T = sel(ttp, oc);
-  const float* B = sel(bufp, oc);
-  float* To = sel(ttp, oc ^ 1);
-  float* Bo = sel(bufp, oc ^ 1);
-  float* L = tl.follow ? nullptr : sel(tl, st->cur);
   const void* dbar = slots.ptr[q];
   const size_t o0 = po + 4 * j;  // offset inside owner q's mean slot
   if (e0 + 3 < n) {
@@ -662,6 +663,22 @@ __global__ void __launch_bounds__(kThreads) nesterov_p2p_piece_kernel(Pair ttp, 
       if (L) L[e] = v;
     }
   }
+}
+
+template <int PREC>
+__global__ void __launch_bounds__(kThreads) nesterov_p2p_piece_kernel(Pair ttp, Pair bufp, Pair tl,
+                                                                      const __grid_constant__ PtrList slots, int k,
+                                                                      size_t S, size_t po, size_t plen,
+                                                                      DevState* st, float lr, float mu, size_t n,
+                                                                      size_t nblk) {
+  const int oc = st->ocur;
+  const float* T = sel(ttp, oc);
+  const float* B = sel(bufp, oc);
+  float* To = sel(ttp, oc ^ 1);
+  float* Bo = sel(bufp, oc ^ 1);
+  float* L = tl.follow ? nullptr : sel(tl, st->cur);
+  for (size_t b = blockIdx.x; b < nblk; b += gridDim.x)
+    nesterov_p2p_piece_block<PREC>(T, B, To, Bo, L, slots, b, k, S, po, plen, lr, mu, n);
 }
 
 // Gate of the pipelined P2P step: flip `ocur` when all K owner flags are clean
@@ -934,12 +951,13 @@ void launch_flag_barrier(const PtrList& remote, const uint64_t* local, int k, in
 }
 
 void launch_pseudo_grad_piece(Pair tt, Pair tl, const DevState* st, void* send, int precision, int k, size_t S,
-                              size_t po, size_t plen, size_t n, cudaStream_t s) {
-  const int grid = (int)(std::max<size_t>(1, (plen / 4 + kThreads - 1) / kThreads) * (size_t)k);
+                              size_t po, size_t plen, size_t n, int ctas, cudaStream_t s) {
+  const size_t nblk = std::max<size_t>(1, (plen / 4 + kThreads - 1) / kThreads) * (size_t)k;
+  const int grid = (int)(ctas > 0 ? std::min<size_t>(nblk, (size_t)ctas) : nblk);
   if (precision == 0)
-    pseudo_grad_piece_kernel<0><<<grid, kThreads, 0, s>>>(tt, tl, st, send, k, S, po, plen, n);
+    pseudo_grad_piece_kernel<0><<<grid, kThreads, 0, s>>>(tt, tl, st, send, k, S, po, plen, n, nblk);
   else
-    pseudo_grad_piece_kernel<1><<<grid, kThreads, 0, s>>>(tt, tl, st, send, k, S, po, plen, n);
+    pseudo_grad_piece_kernel<1><<<grid, kThreads, 0, s>>>(tt, tl, st, send, k, S, po, plen, n, nblk);
 }
 
 void launch_pseudo_grad_push_piece(Pair tt, Pair tl, const DevState* st, const PtrList& rows, int precision, int k,
@@ -952,13 +970,14 @@ void launch_pseudo_grad_push_piece(Pair tt, Pair tl, const DevState* st, const P
 }
 
 void launch_nesterov_p2p_piece(Pair tt, Pair buf, Pair tl, const PtrList& slots, int k, size_t S, size_t po,
-                               size_t plen, int precision, DevState* st, float lr, float mu, size_t n,
+                               size_t plen, int precision, DevState* st, float lr, float mu, size_t n, int ctas,
                                cudaStream_t s) {
-  const int grid = (int)(std::max<size_t>(1, (plen / 4 + kThreads - 1) / kThreads) * (size_t)k);
+  const size_t nblk = std::max<size_t>(1, (plen / 4 + kThreads - 1) / kThreads) * (size_t)k;
+  const int grid = (int)(ctas > 0 ? std::min<size_t>(nblk, (size_t)ctas) : nblk);
   if (precision == 0)
-    nesterov_p2p_piece_kernel<0><<<grid, kThreads, 0, s>>>(tt, buf, tl, slots, k, S, po, plen, st, lr, mu, n);
+    nesterov_p2p_piece_kernel<0><<<grid, kThreads, 0, s>>>(tt, buf, tl, slots, k, S, po, plen, st, lr, mu, n, nblk);
   else
-    nesterov_p2p_piece_kernel<1><<<grid, kThreads, 0, s>>>(tt, buf, tl, slots, k, S, po, plen, st, lr, mu, n);
+    nesterov_p2p_piece_kernel<1><<<grid, kThreads, 0, s>>>(tt, buf, tl, slots, k, S, po, plen, st, lr, mu, n, nblk);
 }
 
 void launch_p2p_finish(Pair tt, Pair tl, const PtrList& flags, int k, DevState* st, size_t n, cudaStream_t s) {

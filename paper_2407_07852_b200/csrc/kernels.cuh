@@ -134,7 +134,7 @@ void launch_flag_barrier(const PtrList& remote, const uint64_t* local, int k, in
                          int* err, cudaStream_t s);
 void launch_pseudo_grad_piece(Pair theta_t, Pair theta_local, const DevState* st, void* send,
                               int precision, int k, size_t S, size_t po, size_t plen, size_t n,
-                              cudaStream_t s);
+                              int ctas, cudaStream_t s);
 // K2 piece with the scatter fused in: the delta of owner q's slot is stored
 // straight into `rows.ptr[q]` (this rank's row of owner q's recv buffer, a
 // peer pointer for q != me), ending with a system fence per CTA.
@@ -143,7 +143,7 @@ void launch_pseudo_grad_push_piece(Pair theta_t, Pair theta_local, const DevStat
                                    size_t plen, size_t n, cudaStream_t s);
 void launch_nesterov_p2p_piece(Pair theta_t, Pair buf, Pair theta_local, const PtrList& slots,
                                int k, size_t S, size_t po, size_t plen, int precision,
-                               DevState* st, float lr, float mu, size_t n, cudaStream_t s);
+                               DevState* st, float lr, float mu, size_t n, int ctas, cudaStream_t s);
 void launch_p2p_finish(Pair theta_t, Pair theta_local, const PtrList& flags, int k, DevState* st,
                        size_t n, cudaStream_t s);
 // K2+K4 fused for a single worker (SoloCollective, reduce.cpp:113-126): one

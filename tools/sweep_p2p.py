@@ -37,19 +37,22 @@ def main():
     for i, x in enumerate(xs):
         eng.rng_perturb(4242, "local", r.rank * 16 + i, -1e-3, 1e-3, dst_dev_ptr=x.data_ptr())
     stream = torch.cuda.ExternalStream(eng.stream, device=f"cuda:{r.local}")
-    configs = [("ordered", None, None, None, None)]
+    configs = [("ordered", None, None, None, None, 0)]
     movers = os.environ.get("SWEEP_MOVERS", "sm,ce").split(",")
     pieces_l = [int(x) for x in os.environ.get("SWEEP_PIECES", "1,2,4,8").split(",")]
     ctas_l = [int(x) for x in os.environ.get("SWEEP_CTAS", "0,32,64,128,256").split(",")]
     barriers = os.environ.get("SWEEP_BARRIERS", "flag").split(",")
+    piece_ctas_l = [int(x) for x in os.environ.get("SWEEP_PIECE_CTAS", "0").split(",")]
     plans = os.environ.get("SWEEP_PLANS", "").split(";") if os.environ.get("SWEEP_PLANS") else None
     for barrier in barriers:
         for mover in movers:
             for pieces in (plans or pieces_l):
                 for ctas in (ctas_l if mover in ("sm", "push", "push2") else (0,)):
-                    configs.append(("p2p", mover, pieces, ctas, barrier))
+                    for pc in piece_ctas_l:
+                        configs.append(("p2p", mover, pieces, ctas, barrier, pc))
     results = []
-    for mode, mover, pieces, ctas, barrier in configs:
+    for mode, mover, pieces, ctas, barrier, pc in configs:
+        os.environ["DLC_P2P_PIECE_CTAS"] = str(pc)
         if mover:
             os.environ["DLC_P2P_COPY"] = mover
             if isinstance(pieces, str):
@@ -71,7 +74,8 @@ def main():
         e1.record(stream)
         e1.synchronize()
         ms = PD.max_over_ranks(e0.elapsed_time(e1) / a.steps, r.world)
-        results.append({"mode": mode, "mover": mover, "pieces": pieces, "ctas": ctas, "barrier": barrier, "ms": ms})
+        results.append({"mode": mode, "mover": mover, "pieces": pieces, "ctas": ctas, "barrier": barrier,
+                        "piece_ctas": pc, "ms": ms})
         if r.rank == 0:
             print(json.dumps(results[-1]), flush=True)
     eng.close()
