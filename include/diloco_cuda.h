@@ -257,6 +257,9 @@ DLC_API int dlc_engine_stream(dlc_engine* e, void** stream);
 /* Host <-> device copies of one buffer (synchronous). */
 DLC_API int dlc_engine_upload(dlc_engine* e, int which, const float* host, size_t n);
 DLC_API int dlc_engine_download(dlc_engine* e, int which, float* host, size_t n);
+/* Elements [offset, offset + count) of one buffer (synchronous). */
+DLC_API int dlc_engine_download_range(dlc_engine* e, int which, size_t offset, float* host, size_t count);
+DLC_API int dlc_engine_upload_range(dlc_engine* e, int which, size_t offset, const float* host, size_t count);
 /* Current device address of a buffer (synchronises: the live p/m/v buffer is
  * chosen on the device in PINGPONG mode). */
 DLC_API int dlc_engine_device_ptr(dlc_engine* e, int which, float** dev);

@@ -135,6 +135,8 @@ _SIGS = {
     "dlc_engine_stream": (I, [P, C.POINTER(P)]),
     "dlc_engine_upload": (I, [P, I, P, SZ]),
     "dlc_engine_download": (I, [P, I, P, SZ]),
+    "dlc_engine_download_range": (I, [P, I, SZ, P, SZ]),
+    "dlc_engine_upload_range": (I, [P, I, SZ, P, SZ]),
     "dlc_engine_device_ptr": (I, [P, I, C.POINTER(P)]),
     "dlc_engine_get_scalars": (I, [P, C.POINTER(EngineScalars)]),
     "dlc_engine_set_scalars": (I, [P, C.POINTER(EngineScalars)]),

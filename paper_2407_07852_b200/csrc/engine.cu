@@ -1023,6 +1023,32 @@ int dlc_engine_download(dlc_engine* e, int which, float* host, size_t n) {
   });
 }
 
+int dlc_engine_download_range(dlc_engine* e, int which, size_t offset, float* host, size_t count) {
+  return guard([&] {
+    if (!e || (count && !host)) fail(DLC_EINVAL, "dlc_engine_download_range: null argument");
+    if (offset > e->n || count > e->n - offset)
+      fail(DLC_ESHAPE, "download range [" + std::to_string(offset) + ", +" + std::to_string(count) + ") outside " +
+                           std::to_string(e->n) + " elements");
+    DeviceGuard dg(e->device);
+    const float* d = live(e, which);
+    DLC_CUDA(cudaMemcpyAsync(host, d + offset, count * sizeof(float), cudaMemcpyDeviceToHost, e->stream));
+    DLC_CUDA(cudaStreamSynchronize(e->stream));
+  });
+}
+
+int dlc_engine_upload_range(dlc_engine* e, int which, size_t offset, const float* host, size_t count) {
+  return guard([&] {
+    if (!e || (count && !host)) fail(DLC_EINVAL, "dlc_engine_upload_range: null argument");
+    if (offset > e->n || count > e->n - offset)
+      fail(DLC_ESHAPE, "upload range [" + std::to_string(offset) + ", +" + std::to_string(count) + ") outside " +
+                           std::to_string(e->n) + " elements");
+    DeviceGuard dg(e->device);
+    float* d = writable(e, which);
+    DLC_CUDA(cudaMemcpyAsync(d + offset, host, count * sizeof(float), cudaMemcpyHostToDevice, e->stream));
+    DLC_CUDA(cudaStreamSynchronize(e->stream));
+  });
+}
+
 int dlc_engine_device_ptr(dlc_engine* e, int which, float** dev) {
   return guard([&] {
     if (!e || !dev) fail(DLC_EINVAL, "dlc_engine_device_ptr: null argument");

@@ -345,6 +345,15 @@ class DilocoEngine:
         _check(lib.dlc_engine_download(self.handle, which, _ptr(out), self.n))
         return out
 
+    def download_range(self, which: int, offset: int, count: int) -> np.ndarray:
+        out = np.empty(count, np.float32)
+        _check(lib.dlc_engine_download_range(self.handle, which, offset, _ptr(out), count))
+        return out
+
+    def upload_range(self, which: int, offset: int, host) -> None:
+        a = _f32(host)
+        _check(lib.dlc_engine_upload_range(self.handle, which, offset, _ptr(a), a.size))
+
     def device_ptr(self, which: int) -> int:
         p = C.c_void_p()
         _check(lib.dlc_engine_device_ptr(self.handle, which, C.byref(p)))

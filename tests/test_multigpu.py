@@ -32,3 +32,15 @@ def test_multigpu_parity(nproc):
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
     # ranks share stdout, so their result lines may interleave: count markers
     assert p.returncode == 0 and p.stdout.count("MPRESULT") == nproc, p.stdout[-3000:] + p.stderr[-3000:]
+
+
+@pytest.mark.parametrize("nproc", [2, 4])
+def test_multigpu_full_size(nproc):
+    """Config 4 at its full size (1.1B parameters per worker), slices checked bitwise."""
+    if gpus() < nproc:
+        pytest.skip(f"needs {nproc} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29620 + nproc),
+           os.path.join(ROOT, "tests", "mp_full_worker.py")]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert p.returncode == 0 and p.stdout.count("MPRESULT") == nproc, p.stdout[-3000:] + p.stderr[-3000:]
