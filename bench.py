@@ -402,6 +402,9 @@ def run_ours(args):
         per_outer = 3 * pieces + 1 + (2 * pieces if flag else 0)  # K2, fold_push, K4 pieces, finish, barriers
         if os.environ.get("DLC_P2P_COPY") == "push2":
             per_outer += pieces  # scatter kernels
+    elif mode == D.MODE_ALLREDUCE and os.environ.get("DLC_AR_SERIAL") != "1":
+        pieces = len(os.environ.get("DLC_P2P_PLAN", "1,1,2,2,1,1").split(","))
+        per_outer = 3 * pieces + 1  # K2, non-finite check, K4 pieces, finish (NCCL's own kernels not counted)
     else:
         per_outer = 3  # K2, fold / non-finite check, K4
     per_inner = 2 if args.inner_mode == "pingpong" else 3  # (pre-pass,) AdamW, finalize

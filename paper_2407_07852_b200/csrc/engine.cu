@@ -783,9 +783,96 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
   trace_dump(e, origin);
 }
 
+// DLC_MODE_ALLREDUCE, pipelined: ncclAllReduce(ncclAvg) of contiguous pieces of
+// the flat pseudo-gradient on the high-priority comm stream, overlapped with
+// K2 of the next piece and the speculative K4 of the previous one:
+//   main     K2(p) -> evK2[p]
+//   cstream  wait evK2[p]; ncclAllReduce(piece p, in place); non-finite(p) -> evB[p]
+//   main     wait evB[p]; K4(p) into the idle theta_t / momentum; ...; finish
+// (DLC_AR_SERIAL=1: the unpipelined K2 -> all-reduce -> K4 of outer_collective.)
+bool allreduce_pipelined() {
+  const char* s = std::getenv("DLC_AR_SERIAL");
+  return !(s && std::string(s) == "1");
+}
+
+void outer_allreduce_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc_reduce_report* rep) {
+  const size_t n = e->n, w = elem_width(e->prec);
+  if (!e->cstream) {
+    int lo = 0, hi = 0;
+    DLC_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    DLC_CUDA(cudaStreamCreateWithPriority(&e->cstream, cudaStreamNonBlocking, hi));
+  }
+  std::vector<size_t> pb = piece_plan((n + 511) / 512 * 512);  // contiguous pieces of [0, n)
+  for (size_t& b : pb) b = std::min(b, n);
+  const size_t P = pb.size() - 1;
+  while (e->piece_ev.size() < 2 * P + 1) {
+    cudaEvent_t ev;
+    DLC_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    e->piece_ev.push_back(ev);
+  }
+  cudaEvent_t* evK2 = e->piece_ev.data();
+  cudaEvent_t* evB = evK2 + P;
+  cudaEvent_t evStart = evB[P];
+  float* s = const_cast<float*>(src);
+  const Pair tl = s ? Pair{{s, s}} : local_pair(e);
+  char* send = static_cast<char*>(e->send);
+  if (rep) DLC_CUDA(cudaEventRecord(e->ev0, e->stream));
+  DLC_CUDA(cudaMemsetAsync(e->flags, 0, sizeof(int), e->stream));
+  DLC_CUDA(cudaEventRecord(evStart, e->stream));
+  phase_begin(e);
+  for (size_t p = 0; p < P; ++p) {  // k = 1: piece p is the contiguous range [pb[p], pb[p+1])
+    launch_pseudo_grad_piece(tt_pair(e), tl, e->st, e->send, e->prec, 1, 0, pb[p], pb[p + 1] - pb[p], n, 0,
+                             e->stream);
+    DLC_CUDA(cudaEventRecord(evK2[p], e->stream));
+  }
+  launched("pseudo_grad_piece");
+  phase_end(e, DLC_PHASE_PSEUDO);
+  DLC_CUDA(cudaStreamWaitEvent(e->cstream, evStart, 0));
+  cudaEvent_t c0 = pooled_event(e), c1 = pooled_event(e);
+  DLC_CUDA(cudaEventRecord(c0, e->cstream));
+  for (size_t p = 0; p < P; ++p) {
+    const size_t len = pb[p + 1] - pb[p];
+    DLC_CUDA(cudaStreamWaitEvent(e->cstream, evK2[p], 0));
+    if (len) {
+      char* x = send + pb[p] * w;
+      DLC_NCCL(ncclAllReduce(x, x, len, nccl_type(e->prec), ncclAvg, c->comm, e->cstream));
+      if (e->prec == DLC_FP16)  // engine.cpp:136 on the piece
+        launch_nonfinite_codes(reinterpret_cast<const uint16_t*>(x), e->flags, len, e->cstream);
+      else
+        launch_nonfinite(reinterpret_cast<const float*>(x), e->flags, len, e->cstream);
+    }
+    DLC_CUDA(cudaEventRecord(evB[p], e->cstream));
+  }
+  launched("nonfinite");
+  DLC_CUDA(cudaEventRecord(c1, e->cstream));
+  if (e->timing) {
+    e->pending.push_back({DLC_PHASE_COLLECTIVE, c0, c1});
+  } else {
+    e->pool.push_back(c0);
+    e->pool.push_back(c1);
+  }
+  if (rep) DLC_CUDA(cudaEventRecord(e->ev1, e->cstream));
+  PtrList slots{}, fl{};
+  slots.ptr[0] = send;
+  fl.ptr[0] = e->flags;
+  phase_begin(e);
+  for (size_t p = 0; p < P; ++p) {
+    DLC_CUDA(cudaStreamWaitEvent(e->stream, evB[p], 0));
+    launch_nesterov_p2p_piece(tt_pair(e), buf_pair(e), local_pair(e), slots, 1, 0, pb[p], pb[p + 1] - pb[p],
+                              e->prec, e->st, e->hyper.outer_lr, e->hyper.outer_momentum, n, 0, e->stream);
+  }
+  launch_p2p_finish(tt_pair(e), local_pair(e), fl, 1, e->st, n, e->stream);
+  phase_end(e, DLC_PHASE_OUTER);
+  launched("nesterov_p2p_piece");
+}
+
 void outer_round(dlc_engine* e, dlc_collective* c, const float* src, dlc_reduce_report* rep) {
   if (e->k > 1 && c->mode == DLC_MODE_P2P) {  // manages its own flag (read remotely by peers)
     outer_p2p_pipelined(e, c, src, rep, nullptr, nullptr, 0);
+    return;
+  }
+  if (e->k > 1 && c->mode == DLC_MODE_ALLREDUCE && allreduce_pipelined()) {
+    outer_allreduce_pipelined(e, c, src, rep);
     return;
   }
   reset_flags(e);
