@@ -96,6 +96,7 @@ struct dlc_engine {
   std::vector<cudaEvent_t> chunk_ev;
   // pipelined P2P: high-priority stream for barriers + owner folds, per-piece events
   cudaStream_t cstream = nullptr;
+  cudaStream_t sstream = nullptr;  // "push2" mover: scatter kernels, concurrent with the folds
   struct TraceMark {
     const char* label;
     int piece;
@@ -602,6 +603,7 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
     int lo = 0, hi = 0;
     DLC_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     DLC_CUDA(cudaStreamCreateWithPriority(&e->cstream, cudaStreamNonBlocking, hi));
+    DLC_CUDA(cudaStreamCreateWithPriority(&e->sstream, cudaStreamNonBlocking, hi));
     for (size_t j = 0; j < K; ++j) {
       DLC_CUDA(cudaStreamCreateWithFlags(&e->pull[j], cudaStreamNonBlocking));
       DLC_CUDA(cudaStreamCreateWithFlags(&e->gath[j], cudaStreamNonBlocking));
@@ -677,24 +679,30 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
   DLC_CUDA(cudaEventRecord(c0, e->cstream));
   const bool sm_mover = p2p_mover_sm();
   const bool push2 = p2p_mover_push2();
+  cudaEvent_t* evS = evA;  // (evA is only used by the copy-engine mover)
+  for (size_t p = 0; p < P && push2; ++p) {
+    // push/push: our piece of every foreign slot into its owner's recv row r, on
+    // its own stream so that scatter(p + 1) overlaps fold(p): every NVLink byte
+    // is a remote store and both link directions stay busy
+    DLC_CUDA(cudaStreamWaitEvent(e->sstream, evK2[p], 0));
+    PtrList src{}, dst{};
+    int nrow = 0;
+    for (size_t q = 0; q < K; ++q) {
+      if ((int)q == r) continue;
+      src.ptr[nrow] = send + (q * S + po(p)) * w;
+      dst.ptr[nrow] = static_cast<char*>(e->peer_recv[q]) + (r * S + po(p)) * w;
+      ++nrow;
+    }
+    cudaEvent_t ts = trace_begin(e, e->sstream);
+    launch_scatter_push(src, dst, nrow, pl(p) * w, comm_ctas(), e->sstream);
+    trace_end(e, e->sstream, "scatter", (int)p, ts);
+    DLC_CUDA(cudaEventRecord(evS[p], e->sstream));
+  }
   for (size_t p = 0; p < P && sm_mover; ++p) {
     // SM mover: a persistent fold kernel on a few CTAs pulls slot r / piece p of
     // every rank's delta and pushes the mean (and a non-finite mark) into slot r
     // of every rank's gather buffer (flags reset by each rank before its K2(0)).
-    DLC_CUDA(cudaStreamWaitEvent(e->cstream, evK2[p], 0));
-    if (push2) {  // push/push: our piece of every foreign slot into its owner's recv row r
-      PtrList src{}, dst{};
-      int nrow = 0;
-      for (size_t q = 0; q < K; ++q) {
-        if ((int)q == r) continue;
-        src.ptr[nrow] = send + (q * S + po(p)) * w;
-        dst.ptr[nrow] = static_cast<char*>(e->peer_recv[q]) + (r * S + po(p)) * w;
-        ++nrow;
-      }
-      cudaEvent_t ts = trace_begin(e, e->cstream);
-      launch_scatter_push(src, dst, nrow, pl(p) * w, comm_ctas(), e->cstream);
-      trace_end(e, e->cstream, "scatter", (int)p, ts);
-    }
+    DLC_CUDA(cudaStreamWaitEvent(e->cstream, push2 ? evS[p] : evK2[p], 0));
     cudaEvent_t ta = trace_begin(e, e->cstream);
     p2p_barrier(e, c, e->cstream);  // A_p
     trace_end(e, e->cstream, "barrierA", (int)p, ta);
@@ -1072,6 +1080,7 @@ int dlc_engine_destroy(dlc_engine* e) {
       if (e->gath[j]) cudaStreamDestroy(e->gath[j]);
     }
     if (e->cstream) cudaStreamDestroy(e->cstream);
+    if (e->sstream) cudaStreamDestroy(e->sstream);
     if (e->h2d) cudaStreamDestroy(e->h2d);
     if (e->d2h) cudaStreamDestroy(e->d2h);
     if (e->stream) cudaStreamDestroy(e->stream);
