@@ -1632,7 +1632,7 @@ struct File {
     if (b && std::fwrite(d, 1, b, f) != b) fail(DLC_EINVAL, "checkpoint write failed: " + path);
   }
   void read(void* d, size_t b) {
-    if (b && std::fread(d, 1, b, f) != b) fail(DLC_ESHAPE, "checkpoint truncated: " + path);  // SerializationError
+    if (b && std::fread(d, 1, b, f) != b) fail(DLC_ESERIAL, "checkpoint truncated: " + path);  // checkpoint.cpp:45,60
   }
   void u64(uint64_t v) {
     uint8_t b[8];
@@ -1706,7 +1706,7 @@ void ckpt_read_vector(File& f, float* dev, size_t n, float* stage, cudaStream_t 
   uint64_t used = 8, total = 0, expect = 0;
   for (uint64_t i = 0; i < nseg; ++i) {
     const uint64_t len = f.u64();
-    if (len > (1u << 20)) fail(DLC_ESHAPE, "checkpoint: implausible segment name");
+    if (len > (1u << 20)) fail(DLC_ESERIAL, "checkpoint: implausible segment name");  // tensor.cpp:169-176
     std::string name(len, '\0');
     f.read(name.data(), len);
     const uint64_t off = f.u64(), length = f.u64();
@@ -1784,7 +1784,7 @@ int dlc_checkpoint_load(dlc_engine* const* engines, size_t count, const char* pa
     File f(path, "rb");
     char magic[8];
     f.read(magic, 8);
-    if (std::memcmp(magic, kCkptMagic, 8) != 0) fail(DLC_ESHAPE, "not a checkpoint file: bad magic");
+    if (std::memcmp(magic, kCkptMagic, 8) != 0) fail(DLC_ESERIAL, "not a checkpoint file: bad magic");  // checkpoint.cpp:170
     dlc_checkpoint_meta m{};
     m.config_hash = f.u64();
     m.completed_rounds = f.u64();
@@ -1801,7 +1801,7 @@ int dlc_checkpoint_load(dlc_engine* const* engines, size_t count, const char* pa
       if (!e) fail(DLC_EINVAL, "dlc_checkpoint_load: null engine");
       DeviceGuard dg(e->device);
       const uint64_t hl = f.u64();
-      if (hl > 4096) fail(DLC_ESHAPE, "checkpoint: implausible scalar header");
+      if (hl > 4096) fail(DLC_ESERIAL, "checkpoint: implausible scalar header");
       std::string text(hl, '\0');
       f.read(text.data(), hl);
       std::map<std::string, std::string> kv;  // parse_scalar_header, checkpoint.cpp:93-129
@@ -1815,7 +1815,7 @@ int dlc_checkpoint_load(dlc_engine* const* engines, size_t count, const char* pa
       }
       auto need = [&](const char* key) {
         const auto it = kv.find(key);
-        if (it == kv.end()) fail(DLC_ESHAPE, std::string("checkpoint header missing '") + key + "'");
+        if (it == kv.end()) fail(DLC_ESERIAL, std::string("checkpoint header missing '") + key + "'");  // checkpoint.cpp:109
         return it->second;
       };
       unalias(e);

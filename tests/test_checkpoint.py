@@ -100,5 +100,13 @@ def test_resume_is_bitwise(gpu, tmp_path, segments):
         assert got["step_count"] == 6 and got["outer_epoch"] == 3 and got["inner_step"] == 6
     with pytest.raises(D.ShapeError):
         D.checkpoint_load([D.DilocoEngine(cfg, hyper, n + 1)], path)
+    # SerializationError like checkpoint.cpp:45,60,170: truncated file, bad magic
+    raw = open(path, "rb").read()
+    bad = path + ".bad"
+    for blob in (raw[: len(raw) // 2], b"XXXXXXXX" + raw[8:]):
+        with open(bad, "wb") as f:
+            f.write(blob)
+        with pytest.raises(D.SerializationError):
+            D.checkpoint_load([D.DilocoEngine(cfg, hyper, n)], bad)
     a.close()
     b.close()
