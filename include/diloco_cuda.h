@@ -324,6 +324,22 @@ DLC_API int dlc_engine_apply_outer_step(dlc_engine* e, const float* host_mean, u
  * one fold in index order, K outer steps. */
 DLC_API int dlc_engines_outer_step_local(dlc_engine* const* engines, size_t k, dlc_outer_result* result);
 
+/* Single-process multi-GPU world: K engines, engine r on devices[r], driven by
+ * ONE host thread (the device analogue of run_simulated's K workers,
+ * netsim.cpp:325-357, and of SURVEY.md §8b's dlc_world_create).  DLC_MODE_P2P
+ * joins the engines by direct NVLink peer access (no IPC); ORDERED / ALLREDUCE
+ * use communicators from ncclCommInitAll with the per-rank calls grouped.
+ * The engines belong to the world (use dlc_world_engine for inner steps,
+ * uploads and downloads; do not destroy them).  dlc_world_outer_step runs
+ * every rank's outer step; `result` (may be NULL: asynchronous) is rank 0's,
+ * checked equal on every rank. */
+typedef struct dlc_world dlc_world;
+DLC_API int dlc_world_create(const dlc_config* cfg, const dlc_hyperparams* hyper, size_t n_params, const int* devices,
+                             int inner_mode, int mode, dlc_world** out);
+DLC_API int dlc_world_destroy(dlc_world* w);
+DLC_API int dlc_world_engine(dlc_world* w, int rank, dlc_engine** e);
+DLC_API int dlc_world_outer_step(dlc_world* w, dlc_outer_result* result);
+
 /* DilocoOptimizer::step (engine.cpp:162-174): one inner step, then the outer
  * step when the window boundary is reached.  `round_completed` may be NULL. */
 DLC_API int dlc_optimizer_step(dlc_engine* e, dlc_collective* c, const float* grad, int grad_is_scaled,

@@ -159,6 +159,10 @@ _SIGS = {
     "dlc_rng_fill_device": (I, [P, I, U64, U64, F, F]),
     "dlc_rng_perturb": (I, [P, P, U64, F, F]),
     "dlc_fp16_encode_bits": (I, [C.c_uint32, SZ, P]),
+    "dlc_world_create": (I, [C.POINTER(Config), C.POINTER(Hyperparams), SZ, P, I, I, C.POINTER(P)]),
+    "dlc_world_destroy": (I, [P]),
+    "dlc_world_engine": (I, [P, I, C.POINTER(P)]),
+    "dlc_world_outer_step": (I, [P, C.POINTER(OuterResult)]),
     "dlc_wire_frames_size": (I, [U64, C.POINTER(WireTags), C.POINTER(SZ), C.POINTER(C.c_uint64)]),
     "dlc_wire_encode": (I, [P, U64, U64, C.POINTER(WireTags), P, SZ, C.POINTER(SZ), P]),
     "dlc_wire_decode": (I, [P, SZ, I, U64, U64, P, C.POINTER(WireChunk), SZ, C.POINTER(SZ), C.POINTER(SZ), P]),

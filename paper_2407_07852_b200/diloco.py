@@ -486,7 +486,54 @@ class DilocoEngine:
 
     def close(self):
         if getattr(self, "handle", None):
-            _check(lib.dlc_engine_destroy(self.handle))
+            if getattr(self, "_owned", True):
+                _check(lib.dlc_engine_destroy(self.handle))
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class World:
+    """Single-process multi-GPU world (include/diloco_cuda.h): K engines on K
+    devices driven by one host thread, the device analogue of run_simulated's
+    K workers (netsim.cpp:325-357)."""
+
+    def __init__(self, config: DilocoConfig, hyper: OptimHyperparams, n_params: int, devices,
+                 inner_mode: int = A.INNER_PINGPONG, mode: int = A.MODE_P2P):
+        cfg = A.Config(config.local_steps_h, config.num_workers_k, config.reduce_precision,
+                       config.total_inner_steps)
+        hp = A.Hyperparams(hyper.inner_lr, hyper.warmup_steps, hyper.lr_decay, hyper.weight_decay, hyper.beta1,
+                           hyper.beta2, hyper.adam_eps, hyper.outer_lr, hyper.outer_momentum,
+                           hyper.scaler_init_scale, hyper.scaler_growth_interval)
+        devs = (C.c_int * len(devices))(*devices)
+        h = C.c_void_p()
+        _check(lib.dlc_world_create(C.byref(cfg), C.byref(hp), n_params, devs, inner_mode, mode, C.byref(h)))
+        self.handle = h
+        self.engines = []
+        for r, d in enumerate(devices):
+            eh = C.c_void_p()
+            _check(lib.dlc_world_engine(h, r, C.byref(eh)))
+            e = DilocoEngine.__new__(DilocoEngine)
+            e.handle, e.n, e.device, e.config, e.hyper, e._owned = eh, n_params, d, config, hyper, False
+            self.engines.append(e)
+
+    def outer_step(self, wait: bool = True):
+        if not wait:
+            _check(lib.dlc_world_outer_step(self.handle, None))
+            return None
+        res = A.OuterResult()
+        _check(lib.dlc_world_outer_step(self.handle, C.byref(res)))
+        return OuterStepResult(bool(res.applied), int(res.outer_epoch))
+
+    def close(self):
+        if getattr(self, "handle", None):
+            for e in self.engines:
+                e.handle = None
+            _check(lib.dlc_world_destroy(self.handle))
             self.handle = None
 
     def __del__(self):
