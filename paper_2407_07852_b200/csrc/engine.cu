@@ -207,7 +207,19 @@ bool p2p_mover_push2() {
 // default 384 of the 1184 resident CTA slots (profiles/r1_sweep_p2p_*_barrier.log).
 int comm_ctas() {
   const char* s = std::getenv("DLC_COMM_CTAS");
-  return s ? (int)std::strtol(s, nullptr, 10) : 384;
+  return s ? (int)std::strtol(s, nullptr, 10) : 256;  // profiles/r1_sweep_p2p_4gpu_kk.log
+}
+// SM mover fold on the bulk-copy engine (fold_push_tma_kernel), and its CTAs
+bool fold_tma() {
+  const char* s = std::getenv("DLC_FOLD_TMA");
+  return !(s && std::string(s) == "0");
+}
+// Each TMA fold CTA keeps 3 stages x K inputs x 8 KB of reads in flight; about
+// 7.5 MB in flight per GPU saturates the links, hence ~320 / K CTAs
+// (profiles/r1_sweep_p2p_*_tma.log).
+int tma_ctas(size_t k) {
+  const char* s = std::getenv("DLC_TMA_CTAS");
+  return s ? (int)std::strtol(s, nullptr, 10) : (int)std::max<size_t>(16, 320 / std::max<size_t>(k, 1));
 }
 // CTAs of the K2 / K4 piece kernels running beside the fold (0: one per window)
 int piece_ctas() {
@@ -716,7 +728,8 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
       pfl.ptr[j] = e->peer_flags[j] + r;
     }
     cudaEvent_t tf = trace_begin(e, e->cstream);
-    launch_fold_push(in, (int)K, e->prec, outs, (int)K, pfl, pl(p), comm_ctas(), e->cstream);
+    if (!(fold_tma() && launch_fold_push_tma(in, (int)K, e->prec, outs, (int)K, pfl, pl(p), tma_ctas(K), e->cstream)))
+      launch_fold_push(in, (int)K, e->prec, outs, (int)K, pfl, pl(p), comm_ctas(), e->cstream);
     trace_end(e, e->cstream, "fold_push", (int)p, tf);
     cudaEvent_t tb = trace_begin(e, e->cstream);
     p2p_barrier(e, c, e->cstream);  // B_p

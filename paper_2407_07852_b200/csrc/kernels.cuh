@@ -128,6 +128,10 @@ void launch_fold_push(const PtrList& in, int k, int precision, const PtrList& ou
 // slot `me` of every peer's signal array (`remote`, after a system fence), then
 // waits until every peer's store has landed in `local`.  A peer silent for
 // ~10 s sets *err and the kernel exits instead of hanging the GPU.
+// fold_push with the bulk-copy engine (TMA) moving the tiles; false when k is outside 2..8
+// (the caller then uses launch_fold_push)
+bool launch_fold_push_tma(const PtrList& in, int k, int precision, const PtrList& outs, int nout,
+                          const PtrList& flags, size_t n, int ctas, cudaStream_t s);
 // push/push mover: rows src[q] -> dst[q] (`bytes` each, a multiple of 16), a persistent grid of `ctas`
 void launch_scatter_push(const PtrList& src, const PtrList& dst, int nrow, size_t bytes, int ctas, cudaStream_t s);
 void launch_flag_barrier(const PtrList& remote, const uint64_t* local, int k, int me, uint64_t epoch,
