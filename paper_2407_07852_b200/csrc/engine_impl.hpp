@@ -1,0 +1,176 @@
+// engine_impl.hpp — the engine and collective state shared by the engine's
+// translation units (engine.cu: the C ABI of the device engine; engine_util.cu:
+// buffers, tables, timing, inner step; p2p.cu: the outer step's collectives;
+// collective.cu, checkpoint.cu, wire_engine.cu, world.cu).  Internal: nothing
+// here is exported from libdiloco_cuda.so.
+#pragma once
+
+#include <algorithm>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "internal.hpp"
+#include "kernels.cuh"
+
+struct dlc_collective {
+  int kind = 0;  // 0 solo, 1 nccl
+  int rank = 0;
+  int world = 1;
+  int device = 0;
+  int mode = DLC_MODE_ORDERED;
+  ncclComm_t comm = nullptr;
+  cudaStream_t stream = nullptr;  // used only by the host-buffer plugin call
+  bool in_world = false;          // one of the K collectives of a dlc_world (one host thread)
+};
+
+struct dlc_engine {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  dlc_config cfg{};
+  dlc_hyperparams hyper{};
+  int inner_mode = DLC_INNER_PINGPONG;
+  size_t n = 0, k = 1, S = 0;
+  int prec = DLC_FP32;
+  // theta_t / momentum: a ping-pong pair for a single worker (fused solo outer
+  // step, DevState::ocur selects the live one); both entries alias for K > 1.
+  float* theta_t[2] = {nullptr, nullptr};
+  float* p[2] = {nullptr, nullptr};
+  float* m[2] = {nullptr, nullptr};
+  float* v[2] = {nullptr, nullptr};
+  float* buf[2] = {nullptr, nullptr};
+  float* grad = nullptr;
+  void* send = nullptr;
+  void* recv = nullptr;
+  void* gather = nullptr;
+  int* flags = nullptr;
+  dlc::DevState* st = nullptr;
+  float* tab = nullptr;  // corr1 | corr2 | lr, tab_cap entries each
+  size_t tab_cap = 0;
+  uint64_t issued_inner = 0;  // host mirror of the data cursor (always advances)
+  std::vector<void*> allocs;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // per-phase event timing (dlc_engine_set_timing)
+  struct Mark {
+    int phase;
+    cudaEvent_t a, b;
+  };
+  bool timing = false;
+  std::vector<Mark> pending;
+  std::vector<cudaEvent_t> pool;
+  double phase_ms[4] = {0, 0, 0, 0};
+  uint64_t phase_n[4] = {0, 0, 0, 0};
+  cudaEvent_t open_ev = nullptr;
+  // DLC_MODE_P2P: every rank's send buffer, gather buffer and flag array mapped
+  // into this process through CUDA IPC (own entries are local).
+  int* barrier_buf = nullptr;
+  const dlc_collective* p2p_bound = nullptr;
+  void* peer_send[dlc::kMaxK] = {};
+  void* peer_gather[dlc::kMaxK] = {};
+  int* peer_flags[dlc::kMaxK] = {};
+  void* peer_recv[dlc::kMaxK] = {};  // "push" mover: owners' recv buffers
+  uint64_t* sig = nullptr;  // flag-barrier signal slots, one per rank
+  uint64_t* peer_sig[dlc::kMaxK] = {};
+  uint64_t sig_epoch = 0;
+  int* sig_err = nullptr;
+  std::vector<void*> ipc_opened;
+  // host-buffer path: copy streams and per-chunk events
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  std::vector<cudaEvent_t> chunk_ev;
+  // pipelined P2P: high-priority stream for barriers + owner folds, per-piece events
+  cudaStream_t cstream = nullptr;
+  cudaStream_t sstream = nullptr;  // "push2" mover: scatter kernels, concurrent with the folds
+  struct TraceMark {
+    const char* label;
+    int piece;
+    cudaEvent_t a, b;
+  };
+  std::vector<TraceMark> trace;  // DLC_TRACE=1: per-op timeline of the P2P step
+  cudaStream_t pull[dlc::kMaxK] = {};  // copy-engine pulls of peers' delta slices
+  cudaStream_t gath[dlc::kMaxK] = {};  // copy-engine pulls of owners' mean slices
+  std::vector<cudaEvent_t> piece_ev;
+  // wire rounds (dlc_engine_wire_*): fold rows of the owned range, `wire_stride` elements each
+  void* wire_rows = nullptr;
+  size_t wire_rows_bytes = 0;
+  uint64_t wire_stride = 0;
+};
+
+
+namespace dlc {
+
+inline size_t elem_width(int prec) { return prec == DLC_FP16 ? 2 : 4; }
+
+struct DeviceGuard {
+  int prev = 0;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) DLC_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+inline void launched(const char* what) { DLC_LAUNCHED(what); }
+
+inline ncclDataType_t nccl_type(int prec) { return prec == DLC_FP16 ? ncclFloat16 : ncclFloat32; }
+
+// Host <-> device chunk of the host-buffer outer step (64 MB of FP32).
+constexpr size_t kHostChunk = size_t(16) << 20;
+// Pieces of the pipelined P2P outer step (DLC_MODE_P2P).
+// Owner slots are a multiple of 64 * kMaxPieces elements; the split actually
+// used comes from DLC_P2P_PLAN / DLC_P2P_PIECES (profiles/r1_sweep_p2p_*.log).
+constexpr size_t kMaxPieces = 8;
+
+// ---- engine_util.cu ----
+void* dalloc(dlc_engine* e, size_t bytes);
+size_t p2p_pieces();
+std::vector<size_t> piece_plan(size_t S);
+bool p2p_mover_sm();
+bool p2p_mover_push();
+bool p2p_mover_push2();
+int comm_ctas();
+bool fold_tma();
+int tma_ctas(size_t k);
+int piece_ctas();
+void ensure_copy_streams(dlc_engine* e);
+void ensure_chunk_events(dlc_engine* e, size_t count);
+void harvest(dlc_engine* e);
+cudaEvent_t pooled_event(dlc_engine* e);
+void phase_begin(dlc_engine* e);
+void phase_end(dlc_engine* e, int phase);
+bool tracing();
+cudaEvent_t trace_begin(dlc_engine* e, cudaStream_t s);
+void trace_end(dlc_engine* e, cudaStream_t s, const char* label, int piece, cudaEvent_t a);
+void trace_dump(dlc_engine* e, cudaEvent_t origin);
+void ensure_tables(dlc_engine* e, uint64_t t_max);
+DevState read_state(dlc_engine* e);
+float* live(dlc_engine* e, int which);
+void unalias(dlc_engine* e);
+float* writable(dlc_engine* e, int which);
+void engine_inner(dlc_engine* e, const float* grad, int grad_is_scaled);
+// PINGPONG: theta_local follows theta_t after every outer step (Pair::follow).
+inline Pair local_pair(dlc_engine* e) { return Pair{{e->p[0], e->p[1]}, e->inner_mode == DLC_INNER_PINGPONG}; }
+inline Pair tt_pair(dlc_engine* e) { return Pair{{e->theta_t[0], e->theta_t[1]}}; }
+inline Pair buf_pair(dlc_engine* e) { return Pair{{e->buf[0], e->buf[1]}}; }
+void reset_flags(dlc_engine* e);
+void pseudo_grad(dlc_engine* e, Pair tl);
+void nesterov(dlc_engine* e, const void* dbar, const int* flags, int nflags);
+
+// ---- p2p.cu ----
+void p2p_unbind(dlc_engine* e);
+void p2p_bind(dlc_engine* e, dlc_collective* c);
+void fleet_barrier(dlc_engine* e, dlc_collective* c);
+void p2p_barrier(dlc_engine* e, dlc_collective* c, cudaStream_t s);
+void outer_collective(dlc_engine* e, dlc_collective* c, dlc_reduce_report* rep);
+void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc_reduce_report* rep,
+                         const float* hsrc, float* hdst, int oc_host);
+bool allreduce_pipelined();
+void outer_allreduce_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc_reduce_report* rep);
+void outer_round(dlc_engine* e, dlc_collective* c, const float* src, dlc_reduce_report* rep);
+
+// ---- engine_util.cu (results) ----
+void fill_report(dlc_engine* e, dlc_collective* c, dlc_reduce_report* rep, uint64_t epoch);
+void check_collective(dlc_engine* e, dlc_collective* c);
+void check_barrier(dlc_engine* e);
+void outer_result(dlc_engine* e, dlc_outer_result* res);
+
+}  // namespace dlc

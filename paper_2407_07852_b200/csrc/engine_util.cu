@@ -1,0 +1,371 @@
+// engine_util.cu — engine internals shared by the engine translation units:
+// allocation, runtime knobs, per-phase timing and tracing, the per-step lr /
+// bias-correction tables, the live-buffer view of the ping-pong pairs, the
+// inner step (K1) and the pieces of the outer step used by every mode.
+#include <chrono>
+#include <cinttypes>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "engine_impl.hpp"
+
+namespace dlc {
+
+void* dalloc(dlc_engine* e, size_t bytes) {
+  void* p = nullptr;
+  DLC_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 256)));
+  e->allocs.push_back(p);
+  return p;
+}
+
+
+
+
+// (read on every step so a tuning sweep can change them in-process)
+size_t p2p_pieces() {
+  const char* s = std::getenv("DLC_P2P_PIECES");
+  const long v = s ? std::strtol(s, nullptr, 10) : 4;
+  size_t p = 1;  // a power of two <= kMaxPieces, so every piece is a whole number of 64-element vectors
+  while (p * 2 <= (size_t)std::min<long>(std::max<long>(v, 1), (long)kMaxPieces)) p *= 2;
+  return p;
+}
+
+// Piece boundaries inside an owner slot of S elements (S a multiple of
+// 64 * kMaxPieces): DLC_P2P_PLAN lists piece weights in eighths of a slot
+// (default "1,1,2,2,1,1": short first and last pieces shrink the pipeline's
+// fill (K2 of piece 0) and drain (K4 of the last piece)); DLC_P2P_PIECES asks
+// for equal pieces instead.
+std::vector<size_t> piece_plan(size_t S) {
+  std::vector<size_t> w;
+  const char* plan = std::getenv("DLC_P2P_PLAN");
+  if (plan || !std::getenv("DLC_P2P_PIECES")) {
+    std::string str = plan ? plan : "1,1,2,2,1,1";
+    size_t pos = 0, sum = 0;
+    while (pos <= str.size()) {
+      const size_t comma = str.find(',', pos);
+      const std::string tok = str.substr(pos, comma == std::string::npos ? std::string::npos : comma - pos);
+      const long v = std::strtol(tok.c_str(), nullptr, 10);
+      if (v <= 0) {
+        w.clear();
+        break;
+      }
+      w.push_back((size_t)v);
+      sum += (size_t)v;
+      if (comma == std::string::npos) break;
+      pos = comma + 1;
+    }
+    if (sum != kMaxPieces) w.clear();
+  }
+  if (w.empty()) w.assign(p2p_pieces(), kMaxPieces / p2p_pieces());
+  std::vector<size_t> b{0};
+  for (size_t x : w) b.push_back(b.back() + x * (S / kMaxPieces));
+  return b;
+}
+
+// Who moves the bytes in DLC_MODE_P2P: "sm" (default) = a persistent fold
+// kernel pulling deltas and pushing means over NVLink; "ce" = DMA copy engines.
+bool p2p_mover_sm() {
+  const char* s = std::getenv("DLC_P2P_COPY");
+  return !(s && std::string(s) == "ce");
+}
+
+// "push": the scatter is fused into K2 (deltas stored straight into the
+// owners' recv rows over NVLink), so every NVLink byte is a posted store.
+bool p2p_mover_push() {
+  const char* s = std::getenv("DLC_P2P_COPY");
+  return s && std::string(s) == "push";
+}
+// push/push: K2 writes locally, a scatter kernel on the comm stream pushes the
+// rows to their owners, the owners fold locally and push the means
+bool p2p_mover_push2() {
+  const char* s = std::getenv("DLC_P2P_COPY");
+  return s && std::string(s) == "push2";
+}
+
+// CTAs of the persistent SM mover (0 = one CTA per window, no SM partitioning);
+// default 384 of the 1184 resident CTA slots (profiles/r1_sweep_p2p_*_barrier.log).
+int comm_ctas() {
+  const char* s = std::getenv("DLC_COMM_CTAS");
+  return s ? (int)std::strtol(s, nullptr, 10) : 256;  // profiles/r1_sweep_p2p_4gpu_kk.log
+}
+// SM mover fold on the bulk-copy engine (fold_push_tma_kernel), and its CTAs
+bool fold_tma() {
+  const char* s = std::getenv("DLC_FOLD_TMA");
+  return !(s && std::string(s) == "0");
+}
+// Each TMA fold CTA keeps 3 stages x K inputs x 8 KB of reads in flight; about
+// 7.5 MB in flight per GPU saturates the links, hence ~320 / K CTAs
+// (profiles/r1_sweep_p2p_*_tma.log).
+int tma_ctas(size_t k) {
+  const char* s = std::getenv("DLC_TMA_CTAS");
+  return s ? (int)std::strtol(s, nullptr, 10) : (int)std::max<size_t>(16, 320 / std::max<size_t>(k, 1));
+}
+// CTAs of the K2 / K4 piece kernels running beside the fold (0: one per window)
+int piece_ctas() {
+  const char* s = std::getenv("DLC_P2P_PIECE_CTAS");
+  return s ? (int)std::strtol(s, nullptr, 10) : 0;
+}
+
+void ensure_copy_streams(dlc_engine* e) {
+  if (!e->h2d) DLC_CUDA(cudaStreamCreateWithFlags(&e->h2d, cudaStreamNonBlocking));
+  if (!e->d2h) DLC_CUDA(cudaStreamCreateWithFlags(&e->d2h, cudaStreamNonBlocking));
+}
+
+void ensure_chunk_events(dlc_engine* e, size_t count) {
+  while (e->chunk_ev.size() < count) {
+    cudaEvent_t ev;
+    DLC_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    e->chunk_ev.push_back(ev);
+  }
+}
+
+void harvest(dlc_engine* e) {
+  if (e->pending.empty()) return;
+  DLC_CUDA(cudaStreamSynchronize(e->stream));
+  for (const auto& mk : e->pending) {
+    float ms = 0.0f;
+    DLC_CUDA(cudaEventElapsedTime(&ms, mk.a, mk.b));
+    e->phase_ms[mk.phase] += ms;
+    e->phase_n[mk.phase] += 1;
+    e->pool.push_back(mk.a);
+    e->pool.push_back(mk.b);
+  }
+  e->pending.clear();
+}
+
+cudaEvent_t pooled_event(dlc_engine* e) {
+  if (e->pool.empty()) {
+    cudaEvent_t ev;
+    DLC_CUDA(cudaEventCreate(&ev));
+    return ev;
+  }
+  cudaEvent_t ev = e->pool.back();
+  e->pool.pop_back();
+  return ev;
+}
+
+// Brackets one phase on the engine stream when timing is on.
+void phase_begin(dlc_engine* e) {
+  if (!e->timing) return;
+  if (e->pending.size() > 8192) harvest(e);
+  e->open_ev = pooled_event(e);
+  DLC_CUDA(cudaEventRecord(e->open_ev, e->stream));
+}
+
+void phase_end(dlc_engine* e, int phase) {
+  if (!e->timing) return;
+  cudaEvent_t b = pooled_event(e);
+  DLC_CUDA(cudaEventRecord(b, e->stream));
+  e->pending.push_back({phase, e->open_ev, b});
+}
+
+// DLC_TRACE=1: events around every op of the pipelined P2P step, printed to
+// stderr as a timeline (ms from the step start) once the step completes.
+bool tracing() {
+  const char* s = std::getenv("DLC_TRACE");
+  return s && s[0] == '1';
+}
+
+cudaEvent_t trace_begin(dlc_engine* e, cudaStream_t s) {
+  if (!tracing()) return nullptr;
+  cudaEvent_t a = pooled_event(e);
+  DLC_CUDA(cudaEventRecord(a, s));
+  return a;
+}
+
+void trace_end(dlc_engine* e, cudaStream_t s, const char* label, int piece, cudaEvent_t a) {
+  if (!a) return;
+  cudaEvent_t b = pooled_event(e);
+  DLC_CUDA(cudaEventRecord(b, s));
+  e->trace.push_back({label, piece, a, b});
+}
+
+void trace_dump(dlc_engine* e, cudaEvent_t origin) {
+  if (!origin) return;
+  DLC_CUDA(cudaDeviceSynchronize());
+  for (const auto& m : e->trace) {
+    float t0 = 0, t1 = 0;
+    DLC_CUDA(cudaEventElapsedTime(&t0, origin, m.a));
+    DLC_CUDA(cudaEventElapsedTime(&t1, origin, m.b));
+    std::fprintf(stderr, "[dlc trace dev%d] %-10s p%-2d %8.3f -> %8.3f ms (%.3f)\n", e->device, m.label, m.piece, t0,
+                 t1, t1 - t0);
+    e->pool.push_back(m.a);
+    e->pool.push_back(m.b);
+  }
+  e->trace.clear();
+  e->pool.push_back(origin);
+}
+
+// Host tables of the per-step scalars the reference computes on the host:
+// corr1/corr2 from std::pow(float, float) (optim.cpp:73-76) and lr_at
+// (optim.cpp:37-56, indexed as engine.cpp:64).  Index = the 1-based step t.
+void ensure_tables(dlc_engine* e, uint64_t t_max) {
+  if (t_max < e->tab_cap) return;
+  size_t cap = std::max<size_t>(e->tab_cap * 2, 4096);
+  while (cap <= t_max) cap *= 2;
+  std::vector<float> h(3 * cap);
+  const float b1 = e->hyper.beta1, b2 = e->hyper.beta2;
+  dlc_lr_schedule sch{e->hyper.warmup_steps, e->cfg.total_inner_steps, e->hyper.inner_lr, e->hyper.lr_decay};
+  for (size_t t = 0; t < cap; ++t) {
+    h[t] = 1.0f - std::pow(b1, static_cast<float>(t));
+    h[cap + t] = 1.0f - std::pow(b2, static_cast<float>(t));
+    h[2 * cap + t] = dlc_lr_at(&sch, t);
+  }
+  float* fresh = nullptr;
+  DLC_CUDA(cudaMalloc(&fresh, 3 * cap * sizeof(float)));
+  DLC_CUDA(cudaMemcpyAsync(fresh, h.data(), 3 * cap * sizeof(float), cudaMemcpyHostToDevice, e->stream));
+  DLC_CUDA(cudaStreamSynchronize(e->stream));  // in-flight K1 launches still read the old table
+  if (e->tab) cudaFree(e->tab);
+  e->tab = fresh;
+  e->tab_cap = cap;
+}
+
+DevState read_state(dlc_engine* e) {
+  DevState s;
+  DLC_CUDA(cudaStreamSynchronize(e->stream));
+  DLC_CUDA(cudaMemcpy(&s, e->st, sizeof(DevState), cudaMemcpyDeviceToHost));
+  return s;
+}
+
+float* live(dlc_engine* e, int which) {
+  const DevState s = read_state(e);
+  const int cur = s.cur, oc = s.ocur;
+  switch (which) {
+    case DLC_THETA_T: return e->theta_t[oc];
+    case DLC_THETA_LOCAL: return s.lalias ? e->theta_t[oc] : e->p[cur];
+    case DLC_ADAM_M: return e->m[cur];
+    case DLC_ADAM_V: return e->v[cur];
+    case DLC_MOMENTUM: return e->buf[oc];
+    case DLC_GRAD: return e->grad;
+  }
+  fail(DLC_EINVAL, "unknown engine buffer " + std::to_string(which));
+}
+
+// Before a caller writes theta_t or theta_local: give theta_local its own copy
+// again (one D2D copy; every kernel path keeps the follow state consistent).
+void unalias(dlc_engine* e) {
+  DevState s = read_state(e);
+  if (!s.lalias) return;
+  DLC_CUDA(cudaMemcpyAsync(e->p[s.cur], e->theta_t[s.ocur], e->n * sizeof(float), cudaMemcpyDeviceToDevice,
+                           e->stream));
+  const int zero = 0;
+  DLC_CUDA(cudaMemcpyAsync(&e->st->lalias, &zero, sizeof(int), cudaMemcpyHostToDevice, e->stream));
+  DLC_CUDA(cudaStreamSynchronize(e->stream));
+}
+
+// live() for a caller that writes through the pointer
+float* writable(dlc_engine* e, int which) {
+  if (which == DLC_THETA_T || which == DLC_THETA_LOCAL) unalias(e);
+  return live(e, which);
+}
+
+void engine_inner(dlc_engine* e, const float* grad, int grad_is_scaled) {
+  if (e->issued_inner >= e->cfg.total_inner_steps) fail(DLC_EINVAL, "inner_step called after total_inner_steps");
+  ensure_tables(e, e->issued_inner + 2);
+  const float* g = grad;
+  if (!grad_is_scaled) {  // engine.cpp:56: closed-form backward of the scaled loss
+    launch_scale_gradient(grad, e->st, e->grad, e->n, e->stream);
+    g = e->grad;
+  }
+  AdamWArgs a{};
+  for (int i = 0; i < 2; ++i) {
+    a.p[i] = e->p[i];
+    a.m[i] = e->m[i];
+    a.v[i] = e->v[i];
+    a.tt[i] = e->theta_t[i];
+  }
+  a.g = g;
+  a.corr1 = e->tab;
+  a.corr2 = e->tab + e->tab_cap;
+  a.lr = e->tab + 2 * e->tab_cap;
+  a.st = e->st;
+  a.n = e->n;
+  a.b1 = e->hyper.beta1;
+  a.b2 = e->hyper.beta2;
+  a.eps = e->hyper.adam_eps;
+  a.wd = e->hyper.weight_decay;
+  a.omb1 = 1.0f - e->hyper.beta1;
+  a.omb2 = 1.0f - e->hyper.beta2;
+  a.pingpong = e->inner_mode == DLC_INNER_PINGPONG;
+  phase_begin(e);
+  launch_adamw(a, e->stream);
+  phase_end(e, DLC_PHASE_INNER);
+  launched("adamw");
+  e->issued_inner += 1;
+}
+
+
+void reset_flags(dlc_engine* e) {
+  DLC_CUDA(cudaMemsetAsync(e->flags, 0, kMaxK * sizeof(int), e->stream));
+  DLC_CUDA(cudaMemsetAsync(&e->st->delta_nonfinite, 0, sizeof(int), e->stream));
+}
+
+// K2 from an explicit theta_local pair (the engine's own, or a staging buffer).
+void pseudo_grad(dlc_engine* e, Pair tl) {
+  phase_begin(e);
+  launch_pseudo_grad(tt_pair(e), tl, e->st, e->send, e->prec, &e->st->delta_nonfinite, 0, e->n, e->stream);
+  phase_end(e, DLC_PHASE_PSEUDO);
+  launched("pseudo_grad");
+}
+
+void nesterov(dlc_engine* e, const void* dbar, const int* flags, int nflags) {
+  phase_begin(e);
+  launch_nesterov_outer(tt_pair(e), buf_pair(e), local_pair(e), dbar, e->prec, flags, nflags, e->st,
+                        e->hyper.outer_lr, e->hyper.outer_momentum, e->n, e->stream);
+  phase_end(e, DLC_PHASE_OUTER);
+  launched("nesterov_outer");
+}
+
+void fill_report(dlc_engine* e, dlc_collective* c, dlc_reduce_report* rep, uint64_t epoch) {
+  if (!rep) return;
+  *rep = dlc_reduce_report{};
+  rep->outer_epoch = epoch;
+  rep->contributors = e->k;
+  rep->attempts = 1;
+  if (e->k > 1) {
+    const uint64_t bytes = 2ull * (e->k - 1) * e->S * elem_width(e->prec);
+    rep->data_bytes_sent = rep->data_bytes_received = bytes;
+    rep->wire_bytes_sent = rep->wire_bytes_received = bytes;
+    DLC_CUDA(cudaEventSynchronize(e->ev1));
+    float ms = 0;
+    DLC_CUDA(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
+    rep->wall_ms = ms;
+  }
+  (void)c;
+}
+
+void check_collective(dlc_engine* e, dlc_collective* c) {
+  const size_t world = c ? (size_t)c->world : 1;
+  if (world != e->k)
+    fail(DLC_ECOLLECTIVE, "collective world size " + std::to_string(world) + " != num_workers_k " +
+                              std::to_string(e->k));
+  if (c && c->kind == 1 && c->device != e->device) fail(DLC_ECOLLECTIVE, "collective and engine devices differ");
+  if (e->issued_inner % e->cfg.local_steps_h != 0)  // engine.cpp:116-120
+    fail(DLC_EINVAL, "pseudo-gradient requested mid-window (inner_step " + std::to_string(e->issued_inner) +
+                         ", H " + std::to_string(e->cfg.local_steps_h) + ")");
+}
+
+// A flag barrier that timed out (a peer never arrived) surfaces as CollectiveError.
+void check_barrier(dlc_engine* e) {
+  if (!e->sig_err) return;
+  int err = 0;
+  DLC_CUDA(cudaStreamSynchronize(e->stream));
+  if (e->cstream) DLC_CUDA(cudaStreamSynchronize(e->cstream));
+  DLC_CUDA(cudaMemcpy(&err, e->sig_err, sizeof(int), cudaMemcpyDeviceToHost));
+  if (err) fail(DLC_ECOLLECTIVE, "P2P barrier timed out: a peer rank stopped participating");
+}
+
+void outer_result(dlc_engine* e, dlc_outer_result* res) {
+  if (!res) return;  // asynchronous call: nothing is synchronised here
+  check_barrier(e);
+  const DevState s = read_state(e);
+  res->applied = s.last_applied;
+  res->outer_epoch = s.outer_epoch;
+}
+
+}  // namespace dlc

@@ -1,0 +1,231 @@
+// world.cu — the single-process multi-GPU world (dlc_world_*): K engines on
+// K GPUs driven by one host thread.
+#include <chrono>
+#include <cinttypes>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "engine_impl.hpp"
+
+using namespace dlc;
+
+// ---- single-process multi-GPU world (include/diloco_cuda.h section 3) ----------
+
+struct dlc_world {
+  int k = 0;
+  int mode = DLC_MODE_P2P;
+  std::vector<int> devices;
+  std::vector<dlc_engine*> engines;
+  std::vector<dlc_collective*> colls;
+};
+
+namespace {
+
+// Every engine's peer tables point straight at the other engines' buffers
+// (one address space, peer access enabled): no IPC, no handle exchange.
+void world_bind_p2p(dlc_world* w) {
+  for (int a = 0; a < w->k; ++a) {
+    DeviceGuard dg(w->devices[a]);
+    for (int b = 0; b < w->k; ++b) {
+      if (a == b || w->devices[a] == w->devices[b]) continue;
+      const cudaError_t st = cudaDeviceEnablePeerAccess(w->devices[b], 0);
+      if (st == cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+      } else if (st != cudaSuccess) {
+        fail(DLC_ECUDA, std::string("cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(st));
+      }
+    }
+  }
+  for (int r = 0; r < w->k; ++r) {
+    dlc_engine* e = w->engines[r];
+    for (int j = 0; j < w->k; ++j) {
+      dlc_engine* q = w->engines[j];
+      e->peer_send[j] = q->send;
+      e->peer_gather[j] = q->gather;
+      e->peer_flags[j] = q->flags;
+      e->peer_sig[j] = q->sig;
+      e->peer_recv[j] = q->recv;
+    }
+    e->p2p_bound = w->colls[r];
+  }
+}
+
+// DLC_MODE_ORDERED from one thread: the per-rank NCCL calls of
+// outer_collective, grouped across the K communicators.
+void world_outer_nccl(dlc_world* w) {
+  const int K = w->k;
+  dlc_engine* e0 = w->engines[0];
+  const size_t S = e0->S, wd = elem_width(e0->prec);
+  const ncclDataType_t type = nccl_type(e0->prec);
+  for (int r = 0; r < K; ++r) {
+    DeviceGuard dg(w->devices[r]);
+    dlc_engine* e = w->engines[r];
+    reset_flags(e);
+    pseudo_grad(e, local_pair(e));
+  }
+  if (w->mode == DLC_MODE_ORDERED) {
+    DLC_NCCL(ncclGroupStart());
+    for (int r = 0; r < K; ++r) {
+      dlc_engine* e = w->engines[r];
+      char* send = static_cast<char*>(e->send);
+      char* recv = static_cast<char*>(e->recv);
+      for (int j = 0; j < K; ++j) {
+        if (j == r) continue;
+        DLC_NCCL(ncclSend(send + j * S * wd, S, type, j, w->colls[r]->comm, e->stream));
+        DLC_NCCL(ncclRecv(recv + j * S * wd, S, type, j, w->colls[r]->comm, e->stream));
+      }
+    }
+    DLC_NCCL(ncclGroupEnd());
+    for (int r = 0; r < K; ++r) {  // owner fold in rank order (collective.cpp:1444-1489)
+      DeviceGuard dg(w->devices[r]);
+      dlc_engine* e = w->engines[r];
+      char* send = static_cast<char*>(e->send);
+      char* recv = static_cast<char*>(e->recv);
+      PtrList in{};
+      for (int j = 0; j < K; ++j) in.ptr[j] = j == r ? send + r * S * wd : recv + j * S * wd;
+      launch_fold(in, K, e->prec, static_cast<char*>(e->gather) + r * S * wd, e->prec, e->flags + r, S, e->stream);
+      launched("fold");
+    }
+    DLC_NCCL(ncclGroupStart());
+    for (int r = 0; r < K; ++r) {
+      dlc_engine* e = w->engines[r];
+      char* gather = static_cast<char*>(e->gather);
+      DLC_NCCL(ncclAllGather(gather + r * S * wd, gather, S, type, w->colls[r]->comm, e->stream));
+      DLC_NCCL(ncclAllGather(e->flags + r, e->flags, 1, ncclInt32, w->colls[r]->comm, e->stream));
+    }
+    DLC_NCCL(ncclGroupEnd());
+    for (int r = 0; r < K; ++r) {
+      DeviceGuard dg(w->devices[r]);
+      nesterov(w->engines[r], w->engines[r]->gather, w->engines[r]->flags, K);
+    }
+  } else {  // DLC_MODE_ALLREDUCE
+    DLC_NCCL(ncclGroupStart());
+    for (int r = 0; r < K; ++r) {
+      dlc_engine* e = w->engines[r];
+      DLC_NCCL(ncclAllReduce(e->send, e->send, K * S, type, ncclAvg, w->colls[r]->comm, e->stream));
+    }
+    DLC_NCCL(ncclGroupEnd());
+    for (int r = 0; r < K; ++r) {
+      DeviceGuard dg(w->devices[r]);
+      dlc_engine* e = w->engines[r];
+      if (e->prec == DLC_FP16)
+        launch_nonfinite_codes(static_cast<const uint16_t*>(e->send), e->flags, e->n, e->stream);
+      else
+        launch_nonfinite(static_cast<const float*>(e->send), e->flags, e->n, e->stream);
+      launched("nonfinite");
+      nesterov(e, e->send, e->flags, 1);
+    }
+  }
+}
+
+}  // namespace
+
+int dlc_world_create(const dlc_config* cfg, const dlc_hyperparams* hyper, size_t n_params, const int* devices,
+                     int inner_mode, int mode, dlc_world** out) {
+  dlc_world* w = nullptr;
+  const int st = guard([&] {
+    if (!cfg || !hyper || !devices || !out) fail(DLC_EINVAL, "dlc_world_create: null argument");
+    *out = nullptr;
+    if (mode != DLC_MODE_ORDERED && mode != DLC_MODE_ALLREDUCE && mode != DLC_MODE_P2P)
+      fail(DLC_ECONFIG, "unknown reduce mode");
+    const int k = (int)cfg->num_workers_k;
+    if (k < 1 || k > kMaxK) fail(DLC_ECONFIG, "world size must be 1..32");
+    w = new dlc_world();
+    w->k = k;
+    w->mode = mode;
+    w->devices.assign(devices, devices + k);
+    for (int r = 0; r < k; ++r) {
+      dlc_engine* e = nullptr;
+      const int s2 = dlc_engine_create(cfg, hyper, n_params, devices[r], inner_mode, &e);
+      if (s2 != DLC_OK) fail(s2, std::string("world engine ") + std::to_string(r) + ": " + dlc_last_error());
+      w->engines.push_back(e);
+    }
+    std::vector<ncclComm_t> comms(k, nullptr);
+    if (k > 1) {
+      for (int r = 1; r < k; ++r)
+        for (int q = 0; q < r; ++q)
+          if (devices[q] == devices[r]) fail(DLC_ECONFIG, "world ranks need distinct devices");
+      DLC_NCCL(ncclCommInitAll(comms.data(), k, devices));
+    }
+    for (int r = 0; r < k; ++r) {
+      auto* c = new dlc_collective();
+      c->kind = k > 1 ? 1 : 0;
+      c->rank = r;
+      c->world = k;
+      c->device = devices[r];
+      c->mode = mode;
+      c->comm = comms[r];
+      c->in_world = true;
+      w->colls.push_back(c);
+    }
+    if (k > 1 && mode == DLC_MODE_P2P) world_bind_p2p(w);
+    *out = w;
+  });
+  if (st != DLC_OK && w) dlc_world_destroy(w);
+  return st;
+}
+
+int dlc_world_destroy(dlc_world* w) {
+  if (!w) return DLC_OK;
+  return guard([&] {
+    for (size_t r = 0; r < w->engines.size(); ++r) {  // everything in flight on every GPU first
+      DeviceGuard dg(w->devices[r]);
+      cudaDeviceSynchronize();
+    }
+    for (dlc_engine* e : w->engines) {
+      e->p2p_bound = nullptr;  // direct pointers: nothing to unmap, no fleet barrier
+      dlc_engine_destroy(e);
+    }
+    for (size_t r = 0; r < w->colls.size(); ++r) {
+      DeviceGuard dg(w->devices[r]);
+      if (w->colls[r]->comm) ncclCommDestroy(w->colls[r]->comm);
+      delete w->colls[r];
+    }
+    delete w;
+  });
+}
+
+int dlc_world_engine(dlc_world* w, int rank, dlc_engine** e) {
+  return guard([&] {
+    if (!w || !e) fail(DLC_EINVAL, "dlc_world_engine: null argument");
+    if (rank < 0 || rank >= w->k) fail(DLC_EINVAL, "dlc_world_engine: rank out of range");
+    *e = w->engines[rank];
+  });
+}
+
+int dlc_world_outer_step(dlc_world* w, dlc_outer_result* result) {
+  return guard([&] {
+    if (!w) fail(DLC_EINVAL, "dlc_world_outer_step: null world");
+    for (int r = 0; r < w->k; ++r) check_collective(w->engines[r], w->k > 1 ? w->colls[r] : nullptr);
+    if (w->k == 1) {
+      DeviceGuard dg(w->devices[0]);
+      outer_round(w->engines[0], nullptr, nullptr, nullptr);
+    } else if (w->mode == DLC_MODE_P2P) {
+      // every rank's pipelined step is enqueued without a host wait; the
+      // flag barriers inside synchronise the GPUs with each other
+      for (int r = 0; r < w->k; ++r) {
+        DeviceGuard dg(w->devices[r]);
+        outer_p2p_pipelined(w->engines[r], w->colls[r], nullptr, nullptr, nullptr, nullptr, 0);
+      }
+    } else {
+      world_outer_nccl(w);
+    }
+    if (result) {
+      dlc_outer_result r0{};
+      for (int r = 0; r < w->k; ++r) {
+        DeviceGuard dg(w->devices[r]);
+        dlc_outer_result rr{};
+        outer_result(w->engines[r], &rr);
+        if (r == 0) r0 = rr;
+        if (rr.applied != r0.applied || rr.outer_epoch != r0.outer_epoch)
+          fail(DLC_ECOLLECTIVE, "world ranks disagree on the outer step");
+      }
+      *result = r0;
+    }
+  });
+}
