@@ -591,3 +591,23 @@ def test_reruns_are_bitwise_deterministic():
     a, b = run(), run()
     for x, y in zip(a, b):
         assert np.array_equal(bits(x), bits(y))
+
+
+@pytest.mark.parametrize("n", [0, 1, 3, 7, 513])
+@pytest.mark.parametrize("prec", [0, 1])
+def test_tiny_and_empty_vectors(port, n, prec):
+    """Degenerate sizes through every engine path: solo (fused K2+K4) and an
+    in-process fleet of 3 (K2 -> fold -> K4), against the oracle."""
+    hyper = DR.Hyper(inner_lr=1e-3, warmup_steps=1)
+    theta0 = O.rng_fill(31, "theta", 0, n, -1, 1)
+    grad_fn = lambda w, t: O.rng_fill(31, "grad", w * 10 + t, n, -1e-2, 1e-2)  # noqa: E731
+    for k in (1, 3):
+        workers, _ = DR.simulate(port, theta0, grad_fn, k, 2, 2, prec, hyper)
+        engines = run_engines(k, 2, 2, prec, n, hyper, grad_fn, theta0)
+        for wi, e in enumerate(engines):
+            for which, want in ((A.THETA_T, workers[wi].theta_t), (A.THETA_LOCAL, workers[wi].theta_local),
+                                (A.MOMENTUM, workers[wi].buf), (A.ADAM_M, workers[wi].m)):
+                got = e.download(which)
+                assert got.size == n and np.array_equal(bits(got), bits(want)), (k, wi, which)
+            assert e.scalars().outer_epoch == 2
+            e.close()
