@@ -393,9 +393,7 @@ def run_ours(args):
         per_outer = 2  # outer_solo + finish
     elif mode == D.MODE_P2P:
         if "DLC_P2P_PIECES" in os.environ and "DLC_P2P_PLAN" not in os.environ:
-            pieces = 1
-            while pieces * 2 <= min(max(int(os.environ["DLC_P2P_PIECES"]), 1), 8):
-                pieces *= 2
+            pieces = min(max(int(os.environ["DLC_P2P_PIECES"]), 1), 32)
         else:
             pieces = len(os.environ.get("DLC_P2P_PLAN", "1,1,2,2,1,1").split(","))
         flag = os.environ.get("DLC_P2P_BARRIER", "flag") != "nccl"

@@ -30,40 +30,43 @@ void* dalloc(dlc_engine* e, size_t bytes) {
 size_t p2p_pieces() {
   const char* s = std::getenv("DLC_P2P_PIECES");
   const long v = s ? std::strtol(s, nullptr, 10) : 4;
-  size_t p = 1;  // a power of two <= kMaxPieces, so every piece is a whole number of 64-element vectors
-  while (p * 2 <= (size_t)std::min<long>(std::max<long>(v, 1), (long)kMaxPieces)) p *= 2;
-  return p;
+  return (size_t)std::min<long>(std::max<long>(v, 1), 32);
 }
 
-// Piece boundaries inside an owner slot of S elements (S a multiple of
-// 64 * kMaxPieces): DLC_P2P_PLAN lists piece weights in eighths of a slot
-// (default "1,1,2,2,1,1": short first and last pieces shrink the pipeline's
-// fill (K2 of piece 0) and drain (K4 of the last piece)); DLC_P2P_PIECES asks
-// for equal pieces instead.
+// Piece boundaries inside an owner slot of S elements (S a multiple of 64):
+// DLC_P2P_PLAN lists relative piece weights (default "1,1,2,2,1,1": short first
+// and last pieces shrink the pipeline's fill (K2 of piece 0) and drain (K4 of
+// the last piece)); boundaries are rounded down to whole 64-element vectors.
+// DLC_P2P_PIECES asks for that many equal pieces instead.
 std::vector<size_t> piece_plan(size_t S) {
   std::vector<size_t> w;
+  size_t sum = 0;
   const char* plan = std::getenv("DLC_P2P_PLAN");
   if (plan || !std::getenv("DLC_P2P_PIECES")) {
     std::string str = plan ? plan : "1,1,2,2,1,1";
-    size_t pos = 0, sum = 0;
+    size_t pos = 0;
     while (pos <= str.size()) {
       const size_t comma = str.find(',', pos);
       const std::string tok = str.substr(pos, comma == std::string::npos ? std::string::npos : comma - pos);
       const long v = std::strtol(tok.c_str(), nullptr, 10);
-      if (v <= 0) {
+      if (v <= 0 || v > 1024 || w.size() >= 32) {
         w.clear();
         break;
       }
       w.push_back((size_t)v);
-      sum += (size_t)v;
       if (comma == std::string::npos) break;
       pos = comma + 1;
     }
-    if (sum != kMaxPieces) w.clear();
   }
-  if (w.empty()) w.assign(p2p_pieces(), kMaxPieces / p2p_pieces());
+  if (w.empty()) w.assign(p2p_pieces(), 1);
+  sum = 0;
+  for (size_t x : w) sum += x;
   std::vector<size_t> b{0};
-  for (size_t x : w) b.push_back(b.back() + x * (S / kMaxPieces));
+  size_t cum = 0;
+  for (size_t x : w) {
+    cum += x;
+    b.push_back(cum == sum ? S : (S / 64) * cum / sum * 64);
+  }
   return b;
 }
 
