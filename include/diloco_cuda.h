@@ -327,8 +327,9 @@ DLC_API int dlc_engines_outer_step_local(dlc_engine* const* engines, size_t k, d
 /* Single-process multi-GPU world: K engines, engine r on devices[r], driven by
  * ONE host thread (the device analogue of run_simulated's K workers,
  * netsim.cpp:325-357, and of SURVEY.md §8b's dlc_world_create).  DLC_MODE_P2P
- * joins the engines by direct NVLink peer access (no IPC); ORDERED / ALLREDUCE
- * use communicators from ncclCommInitAll with the per-rank calls grouped.
+ * joins the engines by direct NVLink peer access (no IPC, no communicator);
+ * ORDERED / ALLREDUCE use communicators from ncclCommInitAll with the
+ * per-rank calls grouped.  Every rank needs its own device.
  * The engines belong to the world (use dlc_world_engine for inner steps,
  * uploads and downloads; do not destroy them).  dlc_world_outer_step runs
  * every rank's outer step; `result` (may be NULL: asynchronous) is rank 0's,
@@ -393,6 +394,13 @@ DLC_API int dlc_rng_fill_device(dlc_engine* e, int which, uint64_t key, uint64_t
 DLC_API int dlc_rng_perturb(dlc_engine* e, float* dst, uint64_t key, float lo, float hi);
 /* FP16 codes of the 2^32 FP32 bit patterns [start, start + n) (host out). */
 DLC_API int dlc_fp16_encode_bits(uint32_t start, size_t n, uint16_t* out);
+/* The P2P owner fold (K3 + push) on HOST buffers staged through the current
+ * device: k contributions of n elements (FP32 values or FP16 codes per
+ * `precision`, n a multiple of 64) folded in order into `out`, with the TMA
+ * kernel (tma = 1, k in 2..8) or the per-thread one; *nonfinite = the mark the
+ * owner pushes.  Probe for the kernels every world size uses. */
+DLC_API int dlc_fold_push_probe(const void* const* contribs, int k, size_t n, int precision, int tma, void* out,
+                                int* nonfinite);
 
 /* =========================================================================
  * 5. Wire codec for cross-box transports.

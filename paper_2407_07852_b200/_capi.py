@@ -159,6 +159,7 @@ _SIGS = {
     "dlc_rng_fill_device": (I, [P, I, U64, U64, F, F]),
     "dlc_rng_perturb": (I, [P, P, U64, F, F]),
     "dlc_fp16_encode_bits": (I, [C.c_uint32, SZ, P]),
+    "dlc_fold_push_probe": (I, [PP, I, SZ, I, I, P, C.POINTER(I)]),
     "dlc_world_create": (I, [C.POINTER(Config), C.POINTER(Hyperparams), SZ, P, I, I, C.POINTER(P)]),
     "dlc_world_destroy": (I, [P]),
     "dlc_world_engine": (I, [P, I, C.POINTER(P)]),

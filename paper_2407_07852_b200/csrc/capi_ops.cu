@@ -399,4 +399,35 @@ int dlc_fp16_encode_bits(uint32_t start, size_t n, uint16_t* out) {
   });
 }
 
+int dlc_fold_push_probe(const void* const* contribs, int k, size_t n, int precision, int tma, void* out,
+                        int* nonfinite) {
+  return guard([&] {
+    if (k < 1 || k > kMaxK) fail(DLC_EINVAL, "fold_push_probe: k must be 1..32");
+    if (precision != DLC_FP32 && precision != DLC_FP16) fail(DLC_ECONFIG, "unknown precision");
+    if (n % 64) fail(DLC_ESHAPE, "fold_push_probe: n must be a multiple of 64");
+    if (!contribs || !nonfinite) fail(DLC_EINVAL, "fold_push_probe: null argument");
+    need(out, n, "fold_push_probe out");
+    const size_t w = precision == DLC_FP16 ? 2 : 4, b = al(n * w);
+    ThreadCtx& c = ctx();
+    Arena ar(c, b * (k + 1) + 256);
+    PtrList in{}, outs{}, flags{};
+    for (int j = 0; j < k; ++j) {
+      need(contribs[j], n, "fold_push_probe contribution");
+      void* d = ar.take<uint8_t>(b);
+      h2d(d, contribs[j], n * w, c.stream);
+      in.ptr[j] = d;
+    }
+    void* d_out = ar.take<uint8_t>(b);
+    int* d_flag = ar.take<int>(64);
+    DLC_CUDA(cudaMemsetAsync(d_flag, 0, sizeof(int), c.stream));
+    outs.ptr[0] = d_out;
+    flags.ptr[0] = d_flag;
+    if (!(tma && launch_fold_push_tma(in, k, precision, outs, 1, flags, n, 0, c.stream)))
+      launch_fold_push(in, k, precision, outs, 1, flags, n, 0, c.stream);
+    d2h(out, d_out, n * w, c.stream);
+    d2h(nonfinite, d_flag, sizeof(int), c.stream);
+    finish(c);
+  });
+}
+
 }  // extern "C"

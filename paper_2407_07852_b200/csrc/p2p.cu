@@ -186,6 +186,8 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
     DLC_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     DLC_CUDA(cudaStreamCreateWithPriority(&e->cstream, cudaStreamNonBlocking, hi));
     DLC_CUDA(cudaStreamCreateWithPriority(&e->sstream, cudaStreamNonBlocking, hi));
+  }
+  if (!p2p_mover_sm() && !e->pull[0]) {  // copy-engine mover: one pull and one gather stream per peer
     for (size_t j = 0; j < K; ++j) {
       DLC_CUDA(cudaStreamCreateWithFlags(&e->pull[j], cudaStreamNonBlocking));
       DLC_CUDA(cudaStreamCreateWithFlags(&e->gath[j], cudaStreamNonBlocking));

@@ -145,13 +145,13 @@ int dlc_world_create(const dlc_config* cfg, const dlc_hyperparams* hyper, size_t
       if (s2 != DLC_OK) fail(s2, std::string("world engine ") + std::to_string(r) + ": " + dlc_last_error());
       w->engines.push_back(e);
     }
+    // one rank per device: two ranks' spinning flag barriers on one device could
+    // share a hardware queue with the work they wait for
+    for (int r = 1; r < k; ++r)
+      for (int q = 0; q < r; ++q)
+        if (devices[q] == devices[r]) fail(DLC_ECONFIG, "world ranks need distinct devices");
     std::vector<ncclComm_t> comms(k, nullptr);
-    if (k > 1) {
-      for (int r = 1; r < k; ++r)
-        for (int q = 0; q < r; ++q)
-          if (devices[q] == devices[r]) fail(DLC_ECONFIG, "world ranks need distinct devices");
-      DLC_NCCL(ncclCommInitAll(comms.data(), k, devices));
-    }
+    if (k > 1 && mode != DLC_MODE_P2P) DLC_NCCL(ncclCommInitAll(comms.data(), k, devices));  // P2P needs none
     for (int r = 0; r < k; ++r) {
       auto* c = new dlc_collective();
       c->kind = k > 1 ? 1 : 0;

@@ -6,6 +6,7 @@ oracle is the C restatement (pinned to the reference build by
 tests/test_oracle.py) and the committed golden fixtures produced by the
 reference itself.
 """
+import ctypes as C
 import numpy as np
 import pytest
 
@@ -611,3 +612,31 @@ def test_tiny_and_empty_vectors(port, n, prec):
                 assert got.size == n and np.array_equal(bits(got), bits(want)), (k, wi, which)
             assert e.scalars().outer_epoch == 2
             e.close()
+
+
+@pytest.mark.parametrize("tma", [1, 0])
+@pytest.mark.parametrize("prec", [0, 1])
+def test_fold_push_kernels_every_world_size(port, prec, tma):
+    """The P2P owner fold for K = 1..9 and 16 (the compile-time-K TMA and
+    per-thread kernels and the generic one), bit for bit against
+    reduce_average in rank order, with the non-finite mark."""
+    n = 64 * 301
+    rng = np.random.default_rng(prec * 10 + tma)
+    for k in list(range(1, 10)) + [16]:
+        xs = [(rng.uniform(-1, 1, n) * 2.0 ** rng.integers(-12, 12, n)).astype(np.float32) for _ in range(k)]
+        if k == 5:
+            xs[3][77] = np.inf
+        if prec:
+            codes = [port.encode_fp16(x)[0] for x in xs]
+            ins = [port.decode_fp16(c) for c in codes]
+            raw = codes
+        else:
+            ins = raw = xs
+        arr = (C.c_void_p * k)(*[c.ctypes.data for c in raw])
+        out = np.empty(n, np.uint16 if prec else np.float32)
+        bad = C.c_int(0)
+        assert A.lib.dlc_fold_push_probe(arr, k, n, prec, tma, out.ctypes.data, C.byref(bad)) == 0
+        _, want = port.reduce_average(ins, prec)
+        got = port.decode_fp16(out) if prec else out
+        assert same(got, want), (k, prec, tma)
+        assert bool(bad.value) == (not np.all(np.isfinite(want))), k

@@ -63,3 +63,4 @@ def test_world_matches_oracle(port, mode, k, prec):
             assert np.array_equal(bits(got_t), bits(world.engines[0].download(A.THETA_T)))
             assert np.max(np.abs(got_t - w.theta_t)) <= 1e-3
     world.close()
+
