@@ -1,0 +1,103 @@
+// device.cuh — device helpers shared by the kernel translation units: grid
+// shapes (streaming window, persistent), thread indexing, the counter RNG and
+// the per-element arithmetic of SURVEY.md Appendix A (FP32 evaluation order of
+// the reference, explicit round-to-nearest ops).
+#pragma once
+
+#include <algorithm>
+#include <mutex>
+#include <unordered_map>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace dlc {
+
+namespace {
+
+// Persistent grid for the setup / host-staged helpers (not on the hot path).
+template <typename Kern>
+int grid_persist(Kern kernel, size_t work) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, int> per_sm;
+  int bps;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = per_sm.find((const void*)kernel);
+    if (it == per_sm.end()) {
+      int b = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, kThreads, 0);
+      it = per_sm.emplace((const void*)kernel, std::max(b, 1)).first;
+    }
+    bps = it->second;
+  }
+  const size_t cap = (size_t)num_sms() * (size_t)bps;
+  const size_t need = (work + kThreads - 1) / kThreads;
+  return (int)std::max<size_t>(1, std::min(cap, need));
+}
+
+// Streaming-window grid: one CTA per kThreads*U work items.
+template <int U>
+int grid_window(size_t items) {
+  return (int)std::max<size_t>(1, (items + (size_t)kThreads * U - 1) / ((size_t)kThreads * U));
+}
+
+__device__ __forceinline__ size_t gtid() { return (size_t)blockIdx.x * blockDim.x + threadIdx.x; }
+__device__ __forceinline__ size_t gstride() { return (size_t)gridDim.x * blockDim.x; }
+// first work item of this thread in the streaming window (items u*kThreads apart)
+template <int U>
+__device__ __forceinline__ size_t wbase() {
+  return (size_t)blockIdx.x * kThreads * U + threadIdx.x;
+}
+
+// ---- counter RNG, rng.hpp:17-56 ---------------------------------------------
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+__device__ __forceinline__ float rng_uniform_at(uint64_t key, uint64_t i, float lo, float hi) {
+  const float u = __fmul_rn((float)(splitmix64(key + (i + 1) * 0x9E3779B97F4A7C15ull) >> 40), 0x1p-24f);
+  return __fadd_rn(lo, __fmul_rn(__fsub_rn(hi, lo), u));
+}
+
+// ---- per-element arithmetic, Appendix A of SURVEY.md ------------------------
+struct AdamScalars {
+  float b1, b2, eps, wd, omb1, omb2, c1, c2, lr;
+};
+
+// optim.cpp:84-90 for one element; p is the OLD parameter.
+__device__ __forceinline__ float adamw_elem(float p, float g, float& m, float& v, const AdamScalars& s) {
+  m = __fadd_rn(__fmul_rn(s.b1, m), __fmul_rn(s.omb1, g));
+  v = __fadd_rn(__fmul_rn(s.b2, v), __fmul_rn(__fmul_rn(s.omb2, g), g));
+  const float mh = __fdiv_rn(m, s.c1);
+  const float vh = __fdiv_rn(v, s.c2);
+  const float upd = __fadd_rn(__fdiv_rn(mh, __fadd_rn(__fsqrt_rn(vh), s.eps)), __fmul_rn(s.wd, p));
+  return __fsub_rn(p, __fmul_rn(s.lr, upd));
+}
+
+// optim.cpp:111-112 for one element.
+__device__ __forceinline__ float nesterov_elem(float p, float g, float& buf, float lr, float mu) {
+  buf = __fadd_rn(__fmul_rn(mu, buf), g);
+  return __fsub_rn(p, __fmul_rn(lr, __fadd_rn(g, __fmul_rn(mu, buf))));
+}
+
+// tensor.cpp:126 with alpha = -1: theta_t + (-1 * theta_local).
+__device__ __forceinline__ float delta_elem(float tt, float tl) { return __fadd_rn(tt, __fmul_rn(-1.0f, tl)); }
+
+__device__ __forceinline__ float4 decode4(uint2 w) {
+  return make_float4(fp16_decode(lo16(w.x)), fp16_decode(hi16(w.x)), fp16_decode(lo16(w.y)), fp16_decode(hi16(w.y)));
+}
+
+__device__ __forceinline__ float* sel(const Pair& p, int i) { return i ? p.ptr[1] : p.ptr[0]; }
+
+// theta_local as held right now: theta_t[ocur] while the two are equal by
+// construction (Pair::follow + DevState::lalias), else the live p buffer.
+__device__ __forceinline__ const float* local_src(const Pair& tl, const Pair& tt, const DevState* st) {
+  return (tl.follow && st->lalias) ? sel(tt, st->ocur) : sel(tl, st->cur);
+}
+
+}  // namespace
+
+}  // namespace dlc

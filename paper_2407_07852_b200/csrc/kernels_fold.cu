@@ -1,0 +1,526 @@
+// kernels_fold.cu — K3: the rank-ordered fold of the cross-worker average
+// (reduce.cpp:33-89, collective.cpp:1444-1489) on local rows, fused with the
+// push of the mean to every rank (per-thread and TMA bulk-copy versions), the
+// push/push scatter, and the NVLink flag barrier of the P2P step.
+#include <algorithm>
+#include <mutex>
+#include <unordered_map>
+
+#include "common.cuh"
+#include "device.cuh"
+#include "kernels.cuh"
+
+namespace dlc {
+
+namespace {
+
+// =============================================================================
+// K3: ordered fold of K contributions (reduce.cpp:33-44 / 70-88).
+// Each thread owns 8 consecutive elements; contributions are visited in rank
+// order 0..K-1 so the FP32 sum is bit-identical to fold_mean.  Contributions
+// may live in peer GPUs' memory (DLC_MODE_P2P): the loads then travel NVLink.
+// =============================================================================
+
+template <int IN>
+__device__ __forceinline__ void load8(const void* base, size_t e8, float (&x)[8]) {
+  if (IN == 1) {
+    const uint4 w = ld_stream(reinterpret_cast<const uint4*>(base) + e8);
+    x[0] = fp16_decode(lo16(w.x)); x[1] = fp16_decode(hi16(w.x));
+    x[2] = fp16_decode(lo16(w.y)); x[3] = fp16_decode(hi16(w.y));
+    x[4] = fp16_decode(lo16(w.z)); x[5] = fp16_decode(hi16(w.z));
+    x[6] = fp16_decode(lo16(w.w)); x[7] = fp16_decode(hi16(w.w));
+  } else {
+    const float4 a = ld_stream(reinterpret_cast<const float4*>(base) + 2 * e8);
+    const float4 b = ld_stream(reinterpret_cast<const float4*>(base) + 2 * e8 + 1);
+    x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
+    x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+    if (IN == 2) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) x[q] = fp16_decode(fp16_encode(x[q]));
+    }
+  }
+}
+
+// Raw 8-element group of one contribution (16 B of FP16 codes, 32 B of FP32),
+// loaded first and decoded later, so the K loads of a group are all in flight
+// together (for peer memory they are NVLink round trips).
+template <int IN>
+struct Raw8 {
+  float4 a, b;
+};
+template <>
+struct Raw8<1> {
+  uint4 w;
+};
+
+// volatile: the K loads of a group stay adjacent (the scheduler would
+// otherwise interleave the decode of load j with the issue of load j + 1)
+__device__ __forceinline__ uint4 ld_cs_v4(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.cs.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+template <int IN>
+__device__ __forceinline__ void ld_raw(const void* base, size_t e8, Raw8<IN>& r) {
+  if constexpr (IN == 1) {
+    r.w = ld_cs_v4(reinterpret_cast<const uint4*>(base) + e8);
+  } else {
+    const uint4 a = ld_cs_v4(reinterpret_cast<const float4*>(base) + 2 * e8);
+    const uint4 b = ld_cs_v4(reinterpret_cast<const float4*>(base) + 2 * e8 + 1);
+    r.a = make_float4(__uint_as_float(a.x), __uint_as_float(a.y), __uint_as_float(a.z), __uint_as_float(a.w));
+    r.b = make_float4(__uint_as_float(b.x), __uint_as_float(b.y), __uint_as_float(b.z), __uint_as_float(b.w));
+  }
+}
+
+template <int IN>
+__device__ __forceinline__ void unpack(const Raw8<IN>& r, float (&x)[8]) {
+  if constexpr (IN == 1) {
+    x[0] = fp16_decode(lo16(r.w.x)); x[1] = fp16_decode(hi16(r.w.x));
+    x[2] = fp16_decode(lo16(r.w.y)); x[3] = fp16_decode(hi16(r.w.y));
+    x[4] = fp16_decode(lo16(r.w.z)); x[5] = fp16_decode(hi16(r.w.z));
+    x[6] = fp16_decode(lo16(r.w.w)); x[7] = fp16_decode(hi16(r.w.w));
+  } else {
+    x[0] = r.a.x; x[1] = r.a.y; x[2] = r.a.z; x[3] = r.a.w;
+    x[4] = r.b.x; x[5] = r.b.y; x[6] = r.b.z; x[7] = r.b.w;
+    if (IN == 2) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) x[q] = fp16_decode(fp16_encode(x[q]));
+    }
+  }
+}
+
+template <int IN>
+__device__ __forceinline__ float load1(const void* base, size_t e) {
+  if (IN == 1) return fp16_decode(reinterpret_cast<const uint16_t*>(base)[e]);
+  const float x = reinterpret_cast<const float*>(base)[e];
+  return IN == 2 ? fp16_decode(fp16_encode(x)) : x;
+}
+
+template <int OUT>
+__device__ __forceinline__ bool store1(void* out, size_t e, float mean) {
+  if (OUT == 1) {
+    const uint16_t h = fp16_encode(mean);
+    reinterpret_cast<uint16_t*>(out)[e] = h;
+    return fp16_nonfinite(h);
+  }
+  const float y = OUT == 2 ? fp16_decode(fp16_encode(mean)) : mean;
+  reinterpret_cast<float*>(out)[e] = y;
+  return !finite_f(y);
+}
+
+template <int IN, int OUT>
+__global__ void __launch_bounds__(kThreads) fold_kernel(const __grid_constant__ PtrList in, int k, void* out,
+                                                        int* flag, size_t n) {
+  const float divisor = (float)k;  // reduce.cpp:36
+  bool bad = false;
+  const size_t n8 = n / 8, i = gtid();
+  if (i < n8) {
+    float acc[8], x[8];
+    load8<IN>(in.ptr[0], i, acc);
+    for (int j = 1; j < k; ++j) {
+      load8<IN>(in.ptr[j], i, x);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[q] = __fadd_rn(acc[q], x[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = __fdiv_rn(acc[q], divisor);
+    if (OUT == 1) {
+      uint16_t h[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        h[q] = fp16_encode(acc[q]);
+        bad |= fp16_nonfinite(h[q]);
+      }
+      st_stream(reinterpret_cast<uint4*>(out) + i,
+                make_uint4(pack2(h[0], h[1]), pack2(h[2], h[3]), pack2(h[4], h[5]), pack2(h[6], h[7])));
+    } else {
+      if (OUT == 2) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] = fp16_decode(fp16_encode(acc[q]));
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) bad |= !finite_f(acc[q]);
+      float4* o = reinterpret_cast<float4*>(out) + 2 * i;
+      st_stream(o, make_float4(acc[0], acc[1], acc[2], acc[3]));
+      st_stream(o + 1, make_float4(acc[4], acc[5], acc[6], acc[7]));
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x < n - n8 * 8) {
+    const size_t e = n8 * 8 + threadIdx.x;
+    float acc = load1<IN>(in.ptr[0], e);
+    for (int j = 1; j < k; ++j) acc = __fadd_rn(acc, load1<IN>(in.ptr[j], e));
+    bad |= store1<OUT>(out, e, __fdiv_rn(acc, divisor));
+  }
+  if (flag) block_or_flag(bad, flag);
+}
+
+// K3 fused with the all-gather: the owner pushes its mean to every rank.
+// KK > 0: the contributor count at compile time, so the KK loads of a group
+// are issued back to back (KK NVLink round trips in flight per thread instead
+// of one); KK == 0: any k, one load at a time.
+template <int PREC, int KK>
+__global__ void __launch_bounds__(kThreads) fold_push_kernel(const __grid_constant__ PtrList in, int k,
+                                                             const __grid_constant__ PtrList outs, int nout,
+                                                             const __grid_constant__ PtrList flags, size_t n) {
+  const float divisor = (float)k;  // reduce.cpp:36
+  bool bad = false;
+  const size_t n8 = n / 8;
+  // grid-stride: a persistent grid of a few CTAs leaves the other SMs to the
+  // HBM-bound K2 / K4 pieces running concurrently on the main stream
+  for (size_t i = gtid(); i < n8; i += gstride()) {
+    float acc[8], x[8];
+    if constexpr (KK > 0) {
+      Raw8<PREC> raw[KK];
+#pragma unroll
+      for (int j = 0; j < KK; ++j) ld_raw<PREC>(in.ptr[j], i, raw[j]);
+      unpack<PREC>(raw[0], acc);
+#pragma unroll
+      for (int j = 1; j < KK; ++j) {  // rank order (reduce.cpp:37-43)
+        unpack<PREC>(raw[j], x);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] = __fadd_rn(acc[q], x[q]);
+      }
+    } else {
+      load8<PREC>(in.ptr[0], i, acc);
+      for (int j = 1; j < k; ++j) {
+        load8<PREC>(in.ptr[j], i, x);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] = __fadd_rn(acc[q], x[q]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = __fdiv_rn(acc[q], divisor);
+    if (PREC == 1) {
+      uint16_t h[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        h[q] = fp16_encode(acc[q]);
+        bad |= fp16_nonfinite(h[q]);
+      }
+      const uint4 w = make_uint4(pack2(h[0], h[1]), pack2(h[2], h[3]), pack2(h[4], h[5]), pack2(h[6], h[7]));
+      for (int o = 0; o < nout; ++o) st_stream(reinterpret_cast<uint4*>(const_cast<void*>(outs.ptr[o])) + i, w);
+    } else {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) bad |= !finite_f(acc[q]);
+      const float4 a = make_float4(acc[0], acc[1], acc[2], acc[3]), b = make_float4(acc[4], acc[5], acc[6], acc[7]);
+      for (int o = 0; o < nout; ++o) {
+        float4* d = reinterpret_cast<float4*>(const_cast<void*>(outs.ptr[o])) + 2 * i;
+        st_stream(d, a);
+        st_stream(d + 1, b);
+      }
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x < n - n8 * 8) {
+    const size_t e = n8 * 8 + threadIdx.x;
+    float acc = load1<PREC>(in.ptr[0], e);
+    for (int j = 1; j < k; ++j) acc = __fadd_rn(acc, load1<PREC>(in.ptr[j], e));
+    const float mean = __fdiv_rn(acc, divisor);
+    for (int o = 0; o < nout; ++o) bad |= store1<PREC>(const_cast<void*>(outs.ptr[o]), e, mean);
+  }
+  if (__syncthreads_or(bad ? 1 : 0) && threadIdx.x == 0) {
+    for (int o = 0; o < nout; ++o) *reinterpret_cast<volatile int*>(const_cast<void*>(flags.ptr[o])) = 1;
+  }
+  // The CTA's pushed slots are visible system-wide before the barrier that
+  // follows: the __syncthreads_or above orders every thread's stores before
+  // this (cumulative) system-scope fence of one thread.
+  if (threadIdx.x == 0) __threadfence_system();
+}
+
+// ---- K3 fused with the all-gather, TMA version -------------------------------
+// The same rank-ordered fold as fold_push_kernel, with the data moved by the
+// bulk-copy engine (cp.async.bulk) instead of per-thread loads and stores:
+// one elected thread streams 8 KB tiles of the KK inputs (peer memory over
+// NVLink, or local HBM) into a STAGES-deep shared-memory ring, arming an
+// mbarrier with the expected bytes; 128 threads fold the tile in rank order
+// into an output tile, which the elected thread bulk-stores into every
+// destination (the owners' mean slots in every rank's gather buffer).  Each CTA
+// keeps STAGES * KK * 8 KB of NVLink reads in flight with a handful of
+// instructions, so a few dozen CTAs saturate the links and leave the SMs to the
+// HBM-bound K2 / K4 pieces.
+constexpr int kTmaThreads = 128;
+constexpr int kTmaTileBytes = 8192;
+constexpr int kTmaStages = 3;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_load(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst_smem)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void bulk_store(void* dst, const void* src_smem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src_smem)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+template <int PREC, int KK>
+__global__ void __launch_bounds__(kTmaThreads) fold_push_tma_kernel(const __grid_constant__ PtrList in,
+                                                                    const __grid_constant__ PtrList outs, int nout,
+                                                                    const __grid_constant__ PtrList flags,
+                                                                    size_t n) {
+  constexpr int W = PREC == 1 ? 2 : 4;
+  constexpr int TILE = kTmaTileBytes / W;  // elements per tile
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* in_buf = smem;                                          // [STAGES][KK][8 KB]
+  uint8_t* out_buf = smem + kTmaStages * KK * kTmaTileBytes;       // [STAGES][8 KB]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(out_buf + kTmaStages * kTmaTileBytes);  // [STAGES]
+  const float divisor = (float)KK;  // reduce.cpp:36
+  const size_t ntiles = (n + TILE - 1) / TILE;
+  const size_t mine = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const bool leader = threadIdx.x == 0;
+  auto tile_of = [&](size_t i) { return blockIdx.x + i * gridDim.x; };
+  auto tile_bytes = [&](size_t t) {
+    const size_t e = t * (size_t)TILE;
+    return (uint32_t)((n - e < (size_t)TILE ? n - e : (size_t)TILE) * W);
+  };
+  auto issue = [&](size_t i) {  // tile i of this CTA into stage i % STAGES
+    const int st = (int)(i % kTmaStages);
+    const size_t t = tile_of(i);
+    const uint32_t bytes = tile_bytes(t);
+    mbar_expect_tx(&bar[st], bytes * KK);
+#pragma unroll
+    for (int j = 0; j < KK; ++j)
+      bulk_load(in_buf + ((size_t)st * KK + j) * kTmaTileBytes,
+                static_cast<const uint8_t*>(in.ptr[j]) + t * (size_t)kTmaTileBytes, bytes, &bar[st]);
+  };
+  if (leader) {
+    for (int st = 0; st < kTmaStages; ++st) mbar_init(&bar[st], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (leader)
+    for (size_t i = 0; i < mine && i < (size_t)kTmaStages; ++i) issue(i);
+  bool bad = false;
+  for (size_t i = 0; i < mine; ++i) {
+    const int st = (int)(i % kTmaStages);
+    const size_t t = tile_of(i);
+    const uint32_t bytes = tile_bytes(t);
+    if (leader && i >= (size_t)kTmaStages) bulk_wait_read<kTmaStages - 1>();  // out_buf[st] read by its store
+    __syncthreads();
+    mbar_wait(&bar[st], (uint32_t)((i / kTmaStages) & 1));
+    const uint8_t* src = in_buf + (size_t)st * KK * kTmaTileBytes;
+    uint8_t* dst = out_buf + (size_t)st * kTmaTileBytes;
+    for (uint32_t off = threadIdx.x * 16; off < bytes; off += kTmaThreads * 16) {  // 16 B per thread and step
+      constexpr int E = 16 / W;  // 8 FP16 or 4 FP32 elements
+      float acc[E], x[E];
+#pragma unroll
+      for (int j = 0; j < KK; ++j) {  // rank order (reduce.cpp:37-43)
+        const uint4 v = *reinterpret_cast<const uint4*>(src + (size_t)j * kTmaTileBytes + off);
+        if constexpr (PREC == 1) {
+          x[0] = fp16_decode(lo16(v.x)); x[1] = fp16_decode(hi16(v.x));
+          x[2] = fp16_decode(lo16(v.y)); x[3] = fp16_decode(hi16(v.y));
+          x[4] = fp16_decode(lo16(v.z)); x[5] = fp16_decode(hi16(v.z));
+          x[6] = fp16_decode(lo16(v.w)); x[7] = fp16_decode(hi16(v.w));
+        } else {
+          x[0] = __uint_as_float(v.x); x[1] = __uint_as_float(v.y);
+          x[2] = __uint_as_float(v.z); x[3] = __uint_as_float(v.w);
+        }
+#pragma unroll
+        for (int q = 0; q < E; ++q) acc[q] = j == 0 ? x[q] : __fadd_rn(acc[q], x[q]);
+      }
+      uint4 o;
+      if constexpr (PREC == 1) {
+        uint16_t h[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          h[q] = fp16_encode(__fdiv_rn(acc[q], divisor));
+          bad |= fp16_nonfinite(h[q]);
+        }
+        o = make_uint4(pack2(h[0], h[1]), pack2(h[2], h[3]), pack2(h[4], h[5]), pack2(h[6], h[7]));
+      } else {
+        float m[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          m[q] = __fdiv_rn(acc[q], divisor);
+          bad |= !finite_f(m[q]);
+        }
+        o = make_uint4(__float_as_uint(m[0]), __float_as_uint(m[1]), __float_as_uint(m[2]), __float_as_uint(m[3]));
+      }
+      *reinterpret_cast<uint4*>(dst + off) = o;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // our smem writes -> the bulk store's reads
+    __syncthreads();  // every thread is done with in_buf[st] and out_buf[st]
+    if (leader) {
+      for (int o = 0; o < nout; ++o)
+        bulk_store(static_cast<uint8_t*>(const_cast<void*>(outs.ptr[o])) + t * (size_t)kTmaTileBytes, dst, bytes);
+      bulk_commit();
+      if (i + kTmaStages < mine) issue(i + kTmaStages);  // in_buf[st] is free again
+    }
+  }
+  if (__syncthreads_or(bad ? 1 : 0) && threadIdx.x == 0) {
+    for (int o = 0; o < nout; ++o) *reinterpret_cast<volatile int*>(const_cast<void*>(flags.ptr[o])) = 1;
+  }
+  if (leader) {
+    bulk_wait_all();  // every bulk store of this CTA has landed
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    __threadfence_system();  // ... and is visible system-wide before the barrier that follows
+  }
+}
+
+size_t fold_push_tma_smem(int k) { return (size_t)kTmaStages * (k + 1) * kTmaTileBytes + kTmaStages * 8; }
+
+// Scatter half of the push/push P2P mover: row q of `src` (this rank's piece of
+// owner q's slot, in local HBM) is stored into row `me` of owner q's receive
+// buffer over NVLink.  Consecutive 16-byte vectors go to different owners so
+// every link carries traffic at once.
+__global__ void __launch_bounds__(kThreads) scatter_push_kernel(const __grid_constant__ PtrList src,
+                                                                const __grid_constant__ PtrList dst, int nrow,
+                                                                size_t bytes) {
+  const size_t n16 = bytes / 16, total = n16 * (size_t)nrow;
+  for (size_t i = gtid(); i < total; i += gstride()) {
+    const int q = (int)(i % (size_t)nrow);
+    const size_t j = i / (size_t)nrow;
+    const uint4 v = ld_stream(reinterpret_cast<const uint4*>(src.ptr[q]) + j);
+    st_stream(reinterpret_cast<uint4*>(const_cast<void*>(dst.ptr[q])) + j, v);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) __threadfence_system();  // the CTA's stores land before the barrier that follows
+}
+
+// ---- NVLink flag barrier ----------------------------------------------------
+__global__ void flag_barrier_kernel(const __grid_constant__ PtrList remote, const uint64_t* local, int k, int me,
+                                    uint64_t epoch, int* err) {
+  const int j = threadIdx.x;
+  if (j < k && j != me) {
+    __threadfence_system();  // everything this GPU wrote before the barrier is visible first
+    *reinterpret_cast<volatile unsigned long long*>(const_cast<void*>(remote.ptr[j])) = epoch;
+    const long long start = clock64();
+    const volatile unsigned long long* mine = reinterpret_cast<const volatile unsigned long long*>(local + j);
+    while (*mine < epoch) {
+      if (clock64() - start > (1ll << 35)) {  // ~17 s at 2 GHz: a peer is gone
+        atomicExch(err, 1);
+        break;
+      }
+    }
+    __threadfence_system();
+  }
+  __syncthreads();
+}
+
+}  // namespace
+
+void launch_fold(const PtrList& in, int k, int in_kind, void* out, int out_kind, int* flag, size_t n,
+                 cudaStream_t s) {
+  const int grid = grid_window<1>(n / 8);
+#define DLC_FOLD(I, O)                                                      \
+  if (in_kind == I && out_kind == O) {                                      \
+    fold_kernel<I, O><<<grid, kThreads, 0, s>>>(in, k, out, flag, n);       \
+    return;                                                                 \
+  }
+  DLC_FOLD(0, 0) DLC_FOLD(0, 1) DLC_FOLD(0, 2) DLC_FOLD(1, 0) DLC_FOLD(1, 1) DLC_FOLD(1, 2)
+  DLC_FOLD(2, 0) DLC_FOLD(2, 1) DLC_FOLD(2, 2)
+#undef DLC_FOLD
+}
+
+void launch_fold_push(const PtrList& in, int k, int precision, const PtrList& outs, int nout, const PtrList& flags,
+                      size_t n, int ctas, cudaStream_t s) {
+  const int grid = ctas > 0 ? std::min(ctas, grid_window<1>(n / 8)) : grid_window<1>(n / 8);
+#define DLC_FOLD_PUSH(P, KK) fold_push_kernel<P, KK><<<grid, kThreads, 0, s>>>(in, k, outs, nout, flags, n)
+#define DLC_FOLD_PUSH_K(P)      \
+  switch (k) {                  \
+    case 2: DLC_FOLD_PUSH(P, 2); break; \
+    case 3: DLC_FOLD_PUSH(P, 3); break; \
+    case 4: DLC_FOLD_PUSH(P, 4); break; \
+    case 5: DLC_FOLD_PUSH(P, 5); break; \
+    case 6: DLC_FOLD_PUSH(P, 6); break; \
+    case 7: DLC_FOLD_PUSH(P, 7); break; \
+    case 8: DLC_FOLD_PUSH(P, 8); break; \
+    default: DLC_FOLD_PUSH(P, 0); break; \
+  }
+  if (precision == 0) {
+    DLC_FOLD_PUSH_K(0)
+  } else {
+    DLC_FOLD_PUSH_K(1)
+  }
+#undef DLC_FOLD_PUSH_K
+#undef DLC_FOLD_PUSH
+}
+
+bool launch_fold_push_tma(const PtrList& in, int k, int precision, const PtrList& outs, int nout,
+                          const PtrList& flags, size_t n, int ctas, cudaStream_t s) {
+  const size_t smem = fold_push_tma_smem(k);
+  const int W = precision == 1 ? 2 : 4;
+  const size_t ntiles = (n + kTmaTileBytes / W - 1) / (kTmaTileBytes / W);
+  const int grid = (int)std::max<size_t>(1, std::min<size_t>(ctas > 0 ? ctas : num_sms(), ntiles));
+#define DLC_TMA(P, KK)                                                                                   \
+  {                                                                                                      \
+    static unsigned attr_devices = 0; /* per-device function attribute, set once */                      \
+    int dev = 0;                                                                                         \
+    cudaGetDevice(&dev);                                                                                 \
+    if (!(attr_devices & (1u << (dev & 31)))) {                                                          \
+      cudaFuncSetAttribute(fold_push_tma_kernel<P, KK>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+                           (int)fold_push_tma_smem(KK));                                                 \
+      attr_devices |= 1u << (dev & 31);                                                                  \
+    }                                                                                                    \
+    fold_push_tma_kernel<P, KK><<<grid, kTmaThreads, smem, s>>>(in, outs, nout, flags, n);               \
+    return true;                                                                                         \
+  }
+#define DLC_TMA_K(P)             \
+  switch (k) {                   \
+    case 2: DLC_TMA(P, 2)        \
+    case 3: DLC_TMA(P, 3)        \
+    case 4: DLC_TMA(P, 4)        \
+    case 5: DLC_TMA(P, 5)        \
+    case 6: DLC_TMA(P, 6)        \
+    case 7: DLC_TMA(P, 7)        \
+    case 8: DLC_TMA(P, 8)        \
+    default: return false;       \
+  }
+  if (precision == 0) {
+    DLC_TMA_K(0)
+  } else {
+    DLC_TMA_K(1)
+  }
+#undef DLC_TMA_K
+#undef DLC_TMA
+}
+
+void launch_scatter_push(const PtrList& src, const PtrList& dst, int nrow, size_t bytes, int ctas, cudaStream_t s) {
+  const size_t vecs = bytes / 16 * (size_t)nrow;
+  const int grid = (int)std::max<size_t>(1, std::min<size_t>(ctas > 0 ? ctas : 4 * num_sms(), (vecs + kThreads - 1) / kThreads));
+  scatter_push_kernel<<<grid, kThreads, 0, s>>>(src, dst, nrow, bytes);
+}
+
+void launch_flag_barrier(const PtrList& remote, const uint64_t* local, int k, int me, uint64_t epoch, int* err,
+                         cudaStream_t s) {
+  flag_barrier_kernel<<<1, 32, 0, s>>>(remote, local, k, me, epoch, err);
+}
+
+}  // namespace dlc
