@@ -375,11 +375,16 @@ def run_ours(args):
     wire_bytes = 2 * (k - 1) * (-(-n // k)) * wire if k > 1 else 0
     hbm_ms = hbm_bpp * n / (peak * 1e9) * 1e3
     nvl_ms = wire_bytes / (nvlink_peak * 1e9) * 1e3
+    # the exchange itself also streams through HBM: every delta is read once
+    # (by its owner, locally or over NVLink) and every mean written once
+    hbm_coll = 2 * wire * n if k > 1 else 0
+    hbm_all_ms = (hbm_bpp * n + hbm_coll) / (peak * 1e9) * 1e3
     line["step_roofline"] = {"hbm_bytes": hbm_bpp * n, "nvlink_bytes_per_direction": wire_bytes,
                              "hbm_ms": hbm_ms, "nvlink_ms": nvl_ms, "serial_ms": hbm_ms + nvl_ms,
                              "bound_ms": max(hbm_ms, nvl_ms), "frac_of_serial": (hbm_ms + nvl_ms) / ms_step,
                              "frac_of_bound": max(hbm_ms, nvl_ms) / ms_step, "nvlink_peak_gbs": nvlink_peak,
-                             "hbm_peak_gbs": peak}
+                             "hbm_peak_gbs": peak, "hbm_bytes_incl_exchange": hbm_bpp * n + hbm_coll,
+                             "frac_of_bound_incl_exchange": max(hbm_all_ms, nvl_ms) / ms_step}
     if k > 1:
         line["nvlink_gbs_over_step"] = wire_bytes / (ms_step * 1e-3) / 1e9
         line["nccl_bus_gbs"] = wire_bytes / (coll_ms * 1e-3) / 1e9 if coll_ms else None
