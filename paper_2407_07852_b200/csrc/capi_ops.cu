@@ -422,8 +422,8 @@ int dlc_fold_push_probe(const void* const* contribs, int k, size_t n, int precis
     DLC_CUDA(cudaMemsetAsync(d_flag, 0, sizeof(int), c.stream));
     outs.ptr[0] = d_out;
     flags.ptr[0] = d_flag;
-    if (!(tma && launch_fold_push_tma(in, k, precision, outs, 1, flags, n, 0, c.stream)))
-      launch_fold_push(in, k, precision, outs, 1, flags, n, 0, c.stream);
+    if (!(tma && launch_fold_push_tma(in, k, precision, outs, 1, flags, 1, n, 0, c.stream)))
+      launch_fold_push(in, k, precision, outs, 1, flags, 1, n, 0, c.stream);
     d2h(out, d_out, n * w, c.stream);
     d2h(nonfinite, d_flag, sizeof(int), c.stream);
     finish(c);

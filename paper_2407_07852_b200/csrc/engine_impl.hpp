@@ -130,6 +130,7 @@ bool p2p_mover_push2();
 int comm_ctas();
 bool fold_tma();
 int tma_ctas(size_t k);
+bool p2p_k4_pull();
 int piece_ctas();
 void ensure_copy_streams(dlc_engine* e);
 void ensure_chunk_events(dlc_engine* e, size_t count);

@@ -108,6 +108,12 @@ int tma_ctas(size_t k) {
   const char* s = std::getenv("DLC_TMA_CTAS");
   return s ? (int)std::strtol(s, nullptr, 10) : (int)std::max<size_t>(16, 320 / std::max<size_t>(k, 1));
 }
+// SM mover: K4 reads each owner's mean from the owner's gather slot over
+// NVLink instead of the owner pushing it to every rank (DLC_P2P_K4_PULL=1)
+bool p2p_k4_pull() {
+  const char* s = std::getenv("DLC_P2P_K4_PULL");
+  return s && std::string(s) == "1";
+}
 // CTAs of the K2 / K4 piece kernels running beside the fold (0: one per window)
 int piece_ctas() {
   const char* s = std::getenv("DLC_P2P_PIECE_CTAS");

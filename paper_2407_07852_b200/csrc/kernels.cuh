@@ -123,7 +123,7 @@ void launch_nesterov_outer(Pair theta_t, Pair buf, Pair theta_local,
 // mean marked by storing 1 to every `flags` entry; ends with a system fence.
 // `ctas` > 0 runs a persistent grid of that many CTAs (0: one CTA per window).
 void launch_fold_push(const PtrList& in, int k, int precision, const PtrList& outs, int nout,
-                      const PtrList& flags, size_t n, int ctas, cudaStream_t s);
+                      const PtrList& flags, int nflags, size_t n, int ctas, cudaStream_t s);
 // Fleet barrier over NVLink flags (DLC_MODE_P2P): one CTA stores `epoch` into
 // slot `me` of every peer's signal array (`remote`, after a system fence), then
 // waits until every peer's store has landed in `local`.  A peer silent for
@@ -131,7 +131,7 @@ void launch_fold_push(const PtrList& in, int k, int precision, const PtrList& ou
 // fold_push with the bulk-copy engine (TMA) moving the tiles; false when k is outside 2..8
 // (the caller then uses launch_fold_push)
 bool launch_fold_push_tma(const PtrList& in, int k, int precision, const PtrList& outs, int nout,
-                          const PtrList& flags, size_t n, int ctas, cudaStream_t s);
+                          const PtrList& flags, int nflags, size_t n, int ctas, cudaStream_t s);
 // push/push mover: rows src[q] -> dst[q] (`bytes` each, a multiple of 16), a persistent grid of `ctas`
 void launch_scatter_push(const PtrList& src, const PtrList& dst, int nrow, size_t bytes, int ctas, cudaStream_t s);
 void launch_flag_barrier(const PtrList& remote, const uint64_t* local, int k, int me, uint64_t epoch,

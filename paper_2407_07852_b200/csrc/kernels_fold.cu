@@ -164,7 +164,8 @@ __global__ void __launch_bounds__(kThreads) fold_kernel(const __grid_constant__ 
 template <int PREC, int KK>
 __global__ void __launch_bounds__(kThreads) fold_push_kernel(const __grid_constant__ PtrList in, int k,
                                                              const __grid_constant__ PtrList outs, int nout,
-                                                             const __grid_constant__ PtrList flags, size_t n) {
+                                                             const __grid_constant__ PtrList flags, int nflags,
+                                                             size_t n) {
   const float divisor = (float)k;  // reduce.cpp:36
   bool bad = false;
   const size_t n8 = n / 8;
@@ -221,7 +222,7 @@ __global__ void __launch_bounds__(kThreads) fold_push_kernel(const __grid_consta
     for (int o = 0; o < nout; ++o) bad |= store1<PREC>(const_cast<void*>(outs.ptr[o]), e, mean);
   }
   if (__syncthreads_or(bad ? 1 : 0) && threadIdx.x == 0) {
-    for (int o = 0; o < nout; ++o) *reinterpret_cast<volatile int*>(const_cast<void*>(flags.ptr[o])) = 1;
+    for (int o = 0; o < nflags; ++o) *reinterpret_cast<volatile int*>(const_cast<void*>(flags.ptr[o])) = 1;
   }
   // The CTA's pushed slots are visible system-wide before the barrier that
   // follows: the __syncthreads_or above orders every thread's stores before
@@ -294,7 +295,7 @@ template <int PREC, int KK>
 __global__ void __launch_bounds__(kTmaThreads) fold_push_tma_kernel(const __grid_constant__ PtrList in,
                                                                     const __grid_constant__ PtrList outs, int nout,
                                                                     const __grid_constant__ PtrList flags,
-                                                                    size_t n) {
+                                                                    int nflags, size_t n) {
   constexpr int W = PREC == 1 ? 2 : 4;
   constexpr int TILE = kTmaTileBytes / W;  // elements per tile
   extern __shared__ __align__(128) uint8_t smem[];
@@ -385,7 +386,7 @@ __global__ void __launch_bounds__(kTmaThreads) fold_push_tma_kernel(const __grid
     }
   }
   if (__syncthreads_or(bad ? 1 : 0) && threadIdx.x == 0) {
-    for (int o = 0; o < nout; ++o) *reinterpret_cast<volatile int*>(const_cast<void*>(flags.ptr[o])) = 1;
+    for (int o = 0; o < nflags; ++o) *reinterpret_cast<volatile int*>(const_cast<void*>(flags.ptr[o])) = 1;
   }
   if (leader) {
     bulk_wait_all();  // every bulk store of this CTA has landed
@@ -450,9 +451,10 @@ void launch_fold(const PtrList& in, int k, int in_kind, void* out, int out_kind,
 }
 
 void launch_fold_push(const PtrList& in, int k, int precision, const PtrList& outs, int nout, const PtrList& flags,
+                      int nflags,
                       size_t n, int ctas, cudaStream_t s) {
   const int grid = ctas > 0 ? std::min(ctas, grid_window<1>(n / 8)) : grid_window<1>(n / 8);
-#define DLC_FOLD_PUSH(P, KK) fold_push_kernel<P, KK><<<grid, kThreads, 0, s>>>(in, k, outs, nout, flags, n)
+#define DLC_FOLD_PUSH(P, KK) fold_push_kernel<P, KK><<<grid, kThreads, 0, s>>>(in, k, outs, nout, flags, nflags, n)
 #define DLC_FOLD_PUSH_K(P)      \
   switch (k) {                  \
     case 2: DLC_FOLD_PUSH(P, 2); break; \
@@ -474,7 +476,7 @@ void launch_fold_push(const PtrList& in, int k, int precision, const PtrList& ou
 }
 
 bool launch_fold_push_tma(const PtrList& in, int k, int precision, const PtrList& outs, int nout,
-                          const PtrList& flags, size_t n, int ctas, cudaStream_t s) {
+                          const PtrList& flags, int nflags, size_t n, int ctas, cudaStream_t s) {
   const size_t smem = fold_push_tma_smem(k);
   const int W = precision == 1 ? 2 : 4;
   const size_t ntiles = (n + kTmaTileBytes / W - 1) / (kTmaTileBytes / W);
@@ -489,7 +491,7 @@ bool launch_fold_push_tma(const PtrList& in, int k, int precision, const PtrList
                            (int)fold_push_tma_smem(KK));                                                 \
       attr_devices |= 1u << (dev & 31);                                                                  \
     }                                                                                                    \
-    fold_push_tma_kernel<P, KK><<<grid, kTmaThreads, smem, s>>>(in, outs, nout, flags, n);               \
+    fold_push_tma_kernel<P, KK><<<grid, kTmaThreads, smem, s>>>(in, outs, nout, flags, nflags, n);               \
     return true;                                                                                         \
   }
 #define DLC_TMA_K(P)             \

@@ -263,6 +263,7 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
   DLC_CUDA(cudaEventRecord(c0, e->cstream));
   const bool sm_mover = p2p_mover_sm();
   const bool push2 = p2p_mover_push2();
+  const bool k4_pull = sm_mover && p2p_k4_pull();
   cudaEvent_t* evS = evA;  // (evA is only used by the copy-engine mover)
   for (size_t p = 0; p < P && push2; ++p) {
     // push/push: our piece of every foreign slot into its owner's recv row r, on
@@ -299,8 +300,13 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
       pfl.ptr[j] = e->peer_flags[j] + r;
     }
     cudaEvent_t tf = trace_begin(e, e->cstream);
-    if (!(fold_tma() && launch_fold_push_tma(in, (int)K, e->prec, outs, (int)K, pfl, pl(p), tma_ctas(K), e->cstream)))
-      launch_fold_push(in, (int)K, e->prec, outs, (int)K, pfl, pl(p), comm_ctas(), e->cstream);
+    // K4 pull: the mean stays in the owner's own gather slot; every rank's K4
+    // reads it from there over NVLink (no remote stores of means)
+    const int nout = k4_pull ? 1 : (int)K;
+    if (k4_pull) outs.ptr[0] = gather + (r * S + po(p)) * w;
+    if (!(fold_tma() && launch_fold_push_tma(in, (int)K, e->prec, outs, nout, pfl, (int)K, pl(p), tma_ctas(K),
+                                             e->cstream)))
+      launch_fold_push(in, (int)K, e->prec, outs, nout, pfl, (int)K, pl(p), comm_ctas(), e->cstream);
     trace_end(e, e->cstream, "fold_push", (int)p, tf);
     cudaEvent_t tb = trace_begin(e, e->cstream);
     p2p_barrier(e, c, e->cstream);  // B_p
@@ -347,7 +353,7 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
   // K4 pieces on the local gather buffer, speculative into the idle theta_t / momentum
   PtrList slots{}, fl{};
   for (size_t q = 0; q < K; ++q) {
-    slots.ptr[q] = gather + q * S * w;
+    slots.ptr[q] = k4_pull ? static_cast<char*>(e->peer_gather[q]) + q * S * w : gather + q * S * w;
     // SM mover: owners pushed their marks into my flag array; CE mover: owner
     // q's flag lives in owner q's memory
     fl.ptr[q] = sm_mover ? e->flags + q : e->peer_flags[q] + q;
