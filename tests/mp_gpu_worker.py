@@ -132,6 +132,15 @@ def main():
                 assert np.max(np.abs(got - want)) <= (2.0 ** -10 if prec else k * 2.0 ** -23)
             assert rep.contributors == k and rep.outer_epoch == 3
             assert rep.data_bytes_sent == D.per_peer_reduce_bytes(10_007, k, r.rank, prec)
+        # linearity (test_collective.cpp:398-419) and the byte law: FP16 halves the bytes (:421-458)
+        x = O.rng_fill(10, "x", r.rank, 4099, -1, 1)
+        y = O.rng_fill(10, "y", r.rank, 4099, -1, 1)
+        ax, rx = coll.all_reduce_avg(x, D.FP32)
+        ay, _ = coll.all_reduce_avg(y, D.FP32)
+        axy, _ = coll.all_reduce_avg((x + y).astype(np.float32), D.FP32)
+        assert np.max(np.abs((ax + ay) - axy)) <= 1e-6 * max(1.0, float(np.max(np.abs(axy))))
+        _, r16 = coll.all_reduce_avg(x, D.FP16)
+        assert 2 * r16.data_bytes_sent == rx.data_bytes_sent
         coll.close()
     PD.barrier(r.world)
     print("MPRESULT " + json.dumps(out), flush=True)

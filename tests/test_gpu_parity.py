@@ -640,3 +640,21 @@ def test_fold_push_kernels_every_world_size(port, prec, tma):
         got = port.decode_fp16(out) if prec else out
         assert same(got, want), (k, prec, tma)
         assert bool(bad.value) == (not np.all(np.isfinite(want))), k
+
+
+def test_fp16_reduction_bounds(port):
+    """test_engine.cpp:296-324 on the device: the FP16 average stays within
+    2^-10 of the FP32 one, relative to the result for same-sign contributions
+    and to the largest contribution for mixed signs."""
+    rng = np.random.default_rng(21)
+    n = 50_000
+    for k in (2, 3, 8):
+        same_sign = [rng.uniform(0.5, 2.0, n).astype(np.float32) * np.float32(2.0 ** -j) for j in range(k)]
+        f32 = D.reduce_average(same_sign, A.FP32)
+        f16 = D.reduce_average(same_sign, A.FP16)
+        assert np.all(np.abs(f16 - f32) / np.abs(f32) <= 2.0 ** -10)
+        mixed = [rng.uniform(-1, 1, n).astype(np.float32) for _ in range(k)]
+        m32 = D.reduce_average(mixed, A.FP32)
+        m16 = D.reduce_average(mixed, A.FP16)
+        scale = np.max(np.abs(np.stack(mixed)), axis=0)
+        assert np.all(np.abs(m16 - m32) / scale <= 2.0 ** -10)
