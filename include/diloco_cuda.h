@@ -346,6 +346,39 @@ DLC_API int dlc_world_outer_step(dlc_world* w, dlc_outer_result* result);
 DLC_API int dlc_optimizer_step(dlc_engine* e, dlc_collective* c, const float* grad, int grad_is_scaled,
                        int* round_completed);
 
+/* run_training (engine.cpp:176-240): total_inner_steps inner steps with an
+ * outer round every H, one record per step and per round (and per skip
+ * event) through `sink` with the fields of MetricsRecord (metrics.hpp:19-34),
+ * `on_round` after every completed round (the checkpoint hook).  The gradient
+ * producer (task.cpp, out of scope here) is the caller's `producer`: given the
+ * inner step, it returns a DEVICE gradient on the engine's device (loss-scaled
+ * when *grad_is_scaled), the step's loss, and 0 (non-zero aborts with
+ * DLC_EINVAL).  `sink` / `on_round` may be NULL.  Result: RunResult
+ * (engine.hpp:142-150). */
+enum dlc_record_kind { DLC_RECORD_STEP = 0, DLC_RECORD_ROUND = 1, DLC_RECORD_EVENT = 2 };
+typedef struct {
+  int kind;
+  int worker;
+  uint64_t inner_step, outer_epoch;
+  float loss, perplexity, lr;
+  double compute_ms, comm_ms;
+  uint64_t bytes_sent;
+  size_t contributors;
+  const char* event; /* kind == DLC_RECORD_EVENT: "inner_overflow_skip" | "outer_skip_nonfinite" */
+} dlc_metrics_record;
+typedef struct {
+  uint64_t steps_done, rounds_done;
+  float final_train_loss;
+  uint64_t reduce_data_bytes, reduce_wire_bytes;
+  double comm_ms, compute_ms;
+} dlc_run_result;
+typedef int (*dlc_grad_producer)(void* user, uint64_t inner_step, const float** grad, int* grad_is_scaled,
+                                 float* loss);
+typedef void (*dlc_metrics_sink)(void* user, const dlc_metrics_record* record);
+typedef void (*dlc_round_hook)(void* user, uint64_t rounds_done);
+DLC_API int dlc_run_training(dlc_engine* e, dlc_collective* c, dlc_grad_producer producer, dlc_metrics_sink sink,
+                             dlc_round_hook on_round, void* user, int worker_index, dlc_run_result* out);
+
 /* Checkpoint / resume of device-resident engines in the reference's ODLCKPT1
  * format (save_checkpoint / load_checkpoint, checkpoint.cpp:17,74-198):
  * magic, config hash, completed rounds, clock, reduce bytes, utilization

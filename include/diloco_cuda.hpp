@@ -17,11 +17,14 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <exception>
+#include <functional>
 #include <string>
 #include <utility>
 #include <vector>
 
 #include "diloco/errors.hpp"
+#include "diloco/metrics.hpp"
 #include "diloco/optim.hpp"
 #include "diloco/reduce.hpp"
 #include "diloco/tensor.hpp"
@@ -275,5 +278,70 @@ class DeviceEngine {
   LayoutPtr layout_;
   dlc_engine* e_ = nullptr;
 };
+
+/// One sample of the gradient producer (task.cpp's loss_and_grad, out of
+/// scope here): a DEVICE gradient on the engine's device and its loss.
+struct GradSample {
+  const float* grad = nullptr;
+  bool scaled = false;  // already multiplied by the current loss scale
+  float loss = 0.0f;
+};
+
+/// run_training (engine.cpp:176-240) on a DeviceEngine: the same loop, the
+/// same MetricsRecord stream into the reference's MetricsSink, the same
+/// on_round hook; returns the RunResult fields (engine.hpp:142-150).
+inline dlc_run_result run_training(DeviceEngine& engine, NcclCollective* collective,
+                                   const std::function<GradSample(uint64_t)>& producer, const MetricsSink& sink,
+                                   int worker_index = 0, const std::function<void(uint64_t)>& on_round = {}) {
+  struct Ctx {
+    const std::function<GradSample(uint64_t)>* producer;
+    const MetricsSink* sink;
+    const std::function<void(uint64_t)>* on_round;
+    std::exception_ptr error;
+  } ctx{&producer, &sink, &on_round, nullptr};
+  auto produce = [](void* u, uint64_t step, const float** grad, int* scaled, float* loss) -> int {
+    auto* c = static_cast<Ctx*>(u);
+    try {
+      const GradSample g = (*c->producer)(step);
+      *grad = g.grad;
+      *scaled = g.scaled ? 1 : 0;
+      *loss = g.loss;
+      return 0;
+    } catch (...) {
+      c->error = std::current_exception();
+      return 1;
+    }
+  };
+  auto emit = [](void* u, const dlc_metrics_record* r) {
+    auto* c = static_cast<Ctx*>(u);
+    if (!*c->sink) return;
+    MetricsRecord m;
+    m.kind = r->kind == DLC_RECORD_STEP ? RecordKind::step
+             : r->kind == DLC_RECORD_ROUND ? RecordKind::round
+                                           : RecordKind::event;
+    m.worker = r->worker;
+    m.inner_step = r->inner_step;
+    m.outer_epoch = r->outer_epoch;
+    m.loss = r->loss;
+    m.perplexity = r->perplexity;
+    m.lr = r->lr;
+    m.compute_ms = r->compute_ms;
+    m.comm_ms = r->comm_ms;
+    m.bytes_sent = r->bytes_sent;
+    m.contributors = r->contributors;
+    if (r->event) m.event = r->event;
+    (*c->sink)(m);
+  };
+  auto round = [](void* u, uint64_t n) {
+    auto* c = static_cast<Ctx*>(u);
+    if (*c->on_round) (*c->on_round)(n);
+  };
+  dlc_run_result res{};
+  const int st = dlc_run_training(engine.handle(), collective ? collective->handle() : nullptr, produce, emit, round,
+                                  &ctx, worker_index, &res);
+  if (ctx.error) std::rethrow_exception(ctx.error);
+  throw_status(st);
+  return res;
+}
 
 }  // namespace diloco::cuda

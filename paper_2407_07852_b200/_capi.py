@@ -62,6 +62,26 @@ class WireChunk(C.Structure):
                 ("frame_bytes", C.c_uint64)]
 
 
+class MetricsRecord(C.Structure):
+    _fields_ = [("kind", C.c_int), ("worker", C.c_int), ("inner_step", C.c_uint64), ("outer_epoch", C.c_uint64),
+                ("loss", C.c_float), ("perplexity", C.c_float), ("lr", C.c_float), ("compute_ms", C.c_double),
+                ("comm_ms", C.c_double), ("bytes_sent", C.c_uint64), ("contributors", C.c_size_t),
+                ("event", C.c_char_p)]
+
+
+class RunResult(C.Structure):
+    _fields_ = [("steps_done", C.c_uint64), ("rounds_done", C.c_uint64), ("final_train_loss", C.c_float),
+                ("reduce_data_bytes", C.c_uint64), ("reduce_wire_bytes", C.c_uint64), ("comm_ms", C.c_double),
+                ("compute_ms", C.c_double)]
+
+
+GRAD_PRODUCER = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint64, C.POINTER(C.c_void_p), C.POINTER(C.c_int),
+                            C.POINTER(C.c_float))
+METRICS_SINK = C.CFUNCTYPE(None, C.c_void_p, C.POINTER(MetricsRecord))
+ROUND_HOOK = C.CFUNCTYPE(None, C.c_void_p, C.c_uint64)
+RECORD_STEP, RECORD_ROUND, RECORD_EVENT = 0, 1, 2
+
+
 class Config(C.Structure):
     _fields_ = [("local_steps_h", C.c_uint64), ("num_workers_k", C.c_size_t), ("reduce_precision", C.c_int),
                 ("total_inner_steps", C.c_uint64)]
@@ -160,6 +180,7 @@ _SIGS = {
     "dlc_rng_perturb": (I, [P, P, U64, F, F]),
     "dlc_fp16_encode_bits": (I, [C.c_uint32, SZ, P]),
     "dlc_fold_push_probe": (I, [PP, I, SZ, I, I, P, C.POINTER(I)]),
+    "dlc_run_training": (I, [P, P, GRAD_PRODUCER, METRICS_SINK, ROUND_HOOK, P, I, C.POINTER(RunResult)]),
     "dlc_world_create": (I, [C.POINTER(Config), C.POINTER(Hyperparams), SZ, P, I, I, C.POINTER(P)]),
     "dlc_world_destroy": (I, [P]),
     "dlc_world_engine": (I, [P, I, C.POINTER(P)]),

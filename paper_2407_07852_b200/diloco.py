@@ -580,6 +580,49 @@ def checkpoint_load(engines, path: str) -> dict:
             "ledger_workers": int(meta.ledger_workers)}
 
 
+def run_training(engine: "DilocoEngine", collective=None, producer=None, sink=None, on_round=None,
+                 worker_index: int = 0) -> dict:
+    """run_training (engine.cpp:176-240) on a device engine.
+
+    producer(inner_step) -> (grad_device_ptr, grad_is_scaled, loss): the
+    gradient producer (task.cpp, out of scope).  sink(record: dict) receives the
+    MetricsRecord stream; on_round(rounds_done) fires after every outer round.
+    Returns the RunResult fields as a dict."""
+    errors = []
+
+    def _producer(_user, step, grad_out, scaled_out, loss_out):
+        try:
+            g, scaled, loss = producer(int(step))
+            grad_out[0] = C.c_void_p(int(g))
+            scaled_out[0] = int(bool(scaled))
+            loss_out[0] = float(loss)
+            return 0
+        except Exception as e:  # reported after the call
+            errors.append(e)
+            return 1
+
+    def _sink(_user, rec):
+        r = rec.contents
+        sink({"kind": ("step", "round", "event")[r.kind], "worker": r.worker, "inner_step": r.inner_step,
+              "outer_epoch": r.outer_epoch, "loss": r.loss, "perplexity": r.perplexity, "lr": r.lr,
+              "compute_ms": r.compute_ms, "comm_ms": r.comm_ms, "bytes_sent": r.bytes_sent,
+              "contributors": r.contributors, "event": r.event.decode() if r.event else ""})
+
+    def _round(_user, n):
+        on_round(int(n))
+
+    cb_p = A.GRAD_PRODUCER(_producer)
+    cb_s = A.METRICS_SINK(_sink) if sink else A.METRICS_SINK()
+    cb_r = A.ROUND_HOOK(_round) if on_round else A.ROUND_HOOK()
+    res = A.RunResult()
+    st = lib.dlc_run_training(engine.handle, collective.handle if collective is not None else None, cb_p, cb_s, cb_r,
+                              None, worker_index, C.byref(res))
+    if errors:
+        raise errors[0]
+    _check(st)
+    return {f: getattr(res, f) for f, _ in A.RunResult._fields_}
+
+
 class DilocoOptimizer:
     """Single-optimizer facade (engine.hpp:122-140; paper Fig. 2)."""
 

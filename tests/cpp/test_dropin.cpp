@@ -302,6 +302,45 @@ int main() {
     bad[0] = 'X';
     CHECK(throws<SerializationError>([&] { e1.wire_decode(DLC_WIRE_MEAN, 0, 0, n, bad); }));
   }
+  // ---- run_training (engine.cpp:176-240) on a DeviceEngine: the record stream
+  // and the final state of the same window sequence driven step by step
+  {
+    const size_t n = 3001;
+    auto layout = Layout::single("p", n);
+    const ParamVector theta0 = random_vec(layout, 51, "theta", -1.0f, 1.0f);
+    dlc_config cfg{3, 1, DLC_FP16, 9};
+    dlc_hyperparams hp;
+    dlc_hyperparams_default(&hp);
+    hp.warmup_steps = 2;
+    cuda::DeviceEngine a(cfg, hp, theta0, 0, DLC_INNER_PINGPONG), b(cfg, hp, theta0, 0, DLC_INNER_PINGPONG);
+    std::vector<ParamVector> grads;
+    for (int t = 0; t < 9; ++t) grads.push_back(random_vec(layout, 60 + t, "grad", -1e-2f, 1e-2f));
+    for (int t = 0; t < 9; ++t) {  // step by step
+      a.inner_step(grads[t]);
+      if ((t + 1) % 3 == 0) a.outer_step(nullptr);
+    }
+    float* gdev = nullptr;
+    throw_status_ok(dlc_engine_device_ptr(b.handle(), DLC_GRAD, &gdev));
+    std::vector<MetricsRecord> records;
+    std::vector<uint64_t> rounds;
+    const dlc_run_result res = cuda::run_training(
+        b, nullptr,
+        [&](uint64_t step) {
+          throw_status_ok(dlc_engine_upload(b.handle(), DLC_GRAD, grads[step].values().data(), n));
+          return cuda::GradSample{gdev, false, 0.5f * (float)step};
+        },
+        [&](const MetricsRecord& r) { records.push_back(r); }, 0, [&](uint64_t k) { rounds.push_back(k); });
+    CHECK(res.steps_done == 9 && res.rounds_done == 3 && res.final_train_loss == 4.0f);
+    size_t steps = 0, round_records = 0;
+    for (const MetricsRecord& r : records) {
+      steps += r.kind == RecordKind::step;
+      round_records += r.kind == RecordKind::round;
+    }
+    CHECK(steps == 9 && round_records == 3 && rounds == std::vector<uint64_t>({1, 2, 3}));
+    CHECK(a.download(DLC_THETA_T) == b.download(DLC_THETA_T));
+    CHECK(a.download(DLC_THETA_LOCAL) == b.download(DLC_THETA_LOCAL));
+    CHECK(a.download(DLC_MOMENTUM) == b.download(DLC_MOMENTUM) && a.download(DLC_ADAM_V) == b.download(DLC_ADAM_V));
+  }
   std::printf("test_dropin: %d passed, %d failed\n", g_pass, g_fail);
   return g_fail == 0 ? 0 : 1;
 }

@@ -103,6 +103,27 @@ def main():
                                      f"{float(np.max(err / tol)):.3f}")
                 e1.close()
             e.close()
+        if mode_name == "p2p":  # run_training (engine.cpp:176-240) over this collective
+            workers, _ = DR.simulate(port, theta0, grad_fn, k, h, rounds, D.FP16, hyper)
+            e = D.DilocoEngine(D.DilocoConfig(h, k, D.FP16, h * rounds),
+                               D.OptimHyperparams(inner_lr=1e-3, warmup_steps=2), n, r.local)
+            e.upload(D.THETA_T, theta0)
+            e.upload(D.THETA_LOCAL, theta0)
+            gptr = e.device_ptr(D.GRAD)
+
+            def producer(step, e=e, gptr=gptr):
+                e.upload(D.GRAD, grad_fn(r.rank, step))
+                return gptr, False, 1.0
+
+            recs = []
+            res = D.run_training(e, coll, producer, sink=recs.append, worker_index=r.rank)
+            assert res["rounds_done"] == rounds and res["reduce_data_bytes"] == rounds * 2 * (k - 1) * \
+                PD.slot_elems(n, k) * 2
+            assert sum(1 for x in recs if x["kind"] == "round" and x["contributors"] == k) == rounds
+            for w, want in ((D.THETA_T, workers[r.rank].theta_t), (D.MOMENTUM, workers[r.rank].buf)):
+                assert np.array_equal(bits(e.download(w)), bits(want)), ("run_training", w)
+            e.close()
+            out["checks"].append("run_training over p2p: bitwise")
         # e2e host-buffer outer step (dlc_engine_outer_step_host) vs the oracle's outer round
         for prec, n2 in ((D.FP32, 20_011), (D.FP16, 20_011), (D.FP16, 5), (D.FP32, 1)):  # tiny: N < K slots
             th = O.rng_fill(5, "theta", 0, n2, -1, 1)

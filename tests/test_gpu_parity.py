@@ -658,3 +658,49 @@ def test_fp16_reduction_bounds(port):
         m16 = D.reduce_average(mixed, A.FP16)
         scale = np.max(np.abs(np.stack(mixed)), axis=0)
         assert np.all(np.abs(m16 - m32) / scale <= 2.0 ** -10)
+
+
+def test_run_training_records_and_state(port):
+    """run_training (engine.cpp:176-240): the record stream (step / round /
+    event kinds, skip events), the round hook, RunResult, and the final state
+    bitwise against the oracle's K=1 run with the same gradients."""
+    n, h, total = 5003, 3, 9
+    hyper = DR.Hyper(inner_lr=1e-3, warmup_steps=2)
+    hp = D.OptimHyperparams(inner_lr=1e-3, warmup_steps=2)
+    theta0 = O.rng_fill(41, "theta", 0, n, -0.5, 0.5)
+
+    def grad_np(t):
+        g = O.rng_fill(41, "grad", t, n, -1e-2, 1e-2)
+        if t == 4:
+            g[n - 1] = np.inf
+        return g
+
+    e = D.DilocoEngine(D.DilocoConfig(h, 1, A.FP16, total), hp, n)
+    e.upload(A.THETA_T, theta0)
+    e.upload(A.THETA_LOCAL, theta0)
+    gptr = e.device_ptr(A.GRAD)
+
+    def producer(step):
+        e.upload(A.GRAD, grad_np(step))
+        return gptr, False, 0.25 * step
+
+    records, rounds = [], []
+    res = D.run_training(e, None, producer, sink=records.append, on_round=rounds.append)
+    assert res["steps_done"] == total and res["rounds_done"] == total // h
+    assert res["final_train_loss"] == np.float32(0.25 * (total - 1)) and res["reduce_data_bytes"] == 0
+    kinds = [r["kind"] for r in records]
+    assert kinds.count("step") == total and kinds.count("round") == total // h
+    assert [r["event"] for r in records if r["kind"] == "event"] == ["inner_overflow_skip"]
+    assert rounds == [1, 2, 3]
+    steps = [r for r in records if r["kind"] == "step"]
+    assert [r["inner_step"] for r in steps] == list(range(1, total + 1))
+    assert [r["outer_epoch"] for r in steps] == [0, 0, 1, 1, 1, 2, 2, 2, 3]
+    assert steps[4]["lr"] == 0.0 and abs(steps[1]["perplexity"] - np.exp(0.25)) < 1e-6
+    workers, _ = DR.simulate(port, theta0, lambda w, t: grad_np(t), 1, h, total // h, A.FP16, hyper)
+    for which, want in ((A.THETA_T, workers[0].theta_t), (A.THETA_LOCAL, workers[0].theta_local),
+                        (A.ADAM_M, workers[0].m), (A.MOMENTUM, workers[0].buf)):
+        assert np.array_equal(bits(e.download(which)), bits(want)), which
+    with pytest.raises(ZeroDivisionError):  # a failing producer aborts the loop with its own error
+        e2 = D.DilocoEngine(D.DilocoConfig(h, 1, A.FP16, total), hp, n)
+        D.run_training(e2, None, lambda step: 1 / 0)
+    e.close()
