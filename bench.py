@@ -402,7 +402,9 @@ def run_ours(args):
         else:
             pieces = len(os.environ.get("DLC_P2P_PLAN", "1,1,2,2,1,1").split(","))
         flag = os.environ.get("DLC_P2P_BARRIER", "flag") != "nccl"
-        per_outer = 3 * pieces + 1 + (2 * pieces if flag else 0)  # K2, fold_push, K4 pieces, finish, barriers
+        merged = os.environ.get("DLC_P2P_MERGE", "1") != "0"
+        barriers = (pieces + 1 if merged else 2 * pieces) if flag else 0
+        per_outer = 3 * pieces + 1 + barriers  # K2, fold_push, K4 pieces, finish, barriers
         if os.environ.get("DLC_P2P_COPY") == "push2":
             per_outer += pieces  # scatter kernels
     elif mode == D.MODE_ALLREDUCE and os.environ.get("DLC_AR_SERIAL") != "1":

@@ -131,6 +131,7 @@ int comm_ctas();
 bool fold_tma();
 int tma_ctas(size_t k);
 bool p2p_k4_pull();
+bool p2p_merge_barriers();
 int piece_ctas();
 void ensure_copy_streams(dlc_engine* e);
 void ensure_chunk_events(dlc_engine* e, size_t count);

@@ -23,9 +23,6 @@ void* dalloc(dlc_engine* e, size_t bytes) {
   return p;
 }
 
-
-
-
 // (read on every step so a tuning sweep can change them in-process)
 size_t p2p_pieces() {
   const char* s = std::getenv("DLC_P2P_PIECES");
@@ -90,11 +87,11 @@ bool p2p_mover_push2() {
   return s && std::string(s) == "push2";
 }
 
-// CTAs of the persistent SM mover (0 = one CTA per window, no SM partitioning);
-// default 384 of the 1184 resident CTA slots (profiles/r1_sweep_p2p_*_barrier.log).
+// CTAs of the per-thread SM-mover fold and of the push2 scatter (0 = one CTA
+// per window, no SM partitioning); 256 from profiles/r1_sweep_p2p_{2,4}gpu_kk.log.
 int comm_ctas() {
   const char* s = std::getenv("DLC_COMM_CTAS");
-  return s ? (int)std::strtol(s, nullptr, 10) : 256;  // profiles/r1_sweep_p2p_4gpu_kk.log
+  return s ? (int)std::strtol(s, nullptr, 10) : 256;
 }
 // SM mover fold on the bulk-copy engine (fold_push_tma_kernel), and its CTAs
 bool fold_tma() {
@@ -108,6 +105,13 @@ int tma_ctas(size_t k) {
   const char* s = std::getenv("DLC_TMA_CTAS");
   return s ? (int)std::strtol(s, nullptr, 10) : (int)std::max<size_t>(16, 320 / std::max<size_t>(k, 1));
 }
+// SM mover: one flag barrier between the fold of piece p and the fold of piece
+// p + 1 instead of two (DLC_P2P_MERGE=0: separate barriers A and B)
+bool p2p_merge_barriers() {
+  const char* s = std::getenv("DLC_P2P_MERGE");
+  return !(s && std::string(s) == "0");
+}
+
 // SM mover: K4 reads each owner's mean from the owner's gather slot over
 // NVLink instead of the owner pushing it to every rank (DLC_P2P_K4_PULL=1)
 bool p2p_k4_pull() {

@@ -264,6 +264,7 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
   const bool sm_mover = p2p_mover_sm();
   const bool push2 = p2p_mover_push2();
   const bool k4_pull = sm_mover && p2p_k4_pull();
+  const bool merge = p2p_merge_barriers();
   cudaEvent_t* evS = evA;  // (evA is only used by the copy-engine mover)
   for (size_t p = 0; p < P && push2; ++p) {
     // push/push: our piece of every foreign slot into its owner's recv row r, on
@@ -288,9 +289,11 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
     // every rank's delta and pushes the mean (and a non-finite mark) into slot r
     // of every rank's gather buffer (flags reset by each rank before its K2(0)).
     DLC_CUDA(cudaStreamWaitEvent(e->cstream, push2 ? evS[p] : evK2[p], 0));
-    cudaEvent_t ta = trace_begin(e, e->cstream);
-    p2p_barrier(e, c, e->cstream);  // A_p
-    trace_end(e, e->cstream, "barrierA", (int)p, ta);
+    if (!merge || p == 0) {
+      cudaEvent_t ta = trace_begin(e, e->cstream);
+      p2p_barrier(e, c, e->cstream);  // A_p
+      trace_end(e, e->cstream, "barrierA", (int)p, ta);
+    }
     PtrList in{}, outs{}, pfl{};
     for (size_t j = 0; j < K; ++j) {
       in.ptr[j] = (int)j == r && push2 ? send + (r * S + po(p)) * w  // own row stays local
@@ -308,6 +311,9 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
                                              e->cstream)))
       launch_fold_push(in, (int)K, e->prec, outs, nout, pfl, (int)K, pl(p), comm_ctas(), e->cstream);
     trace_end(e, e->cstream, "fold_push", (int)p, tf);
+    // merged barriers: B_p also serves as A_{p+1} once our K2(p+1) is done
+    // (it precedes K4(p) on the main stream anyway, so K4(p) waits no longer)
+    if (merge && p + 1 < P) DLC_CUDA(cudaStreamWaitEvent(e->cstream, push2 ? evS[p + 1] : evK2[p + 1], 0));
     cudaEvent_t tb = trace_begin(e, e->cstream);
     p2p_barrier(e, c, e->cstream);  // B_p
     trace_end(e, e->cstream, "barrierB", (int)p, tb);

@@ -50,11 +50,12 @@ def main():
              ("p2p-tma3", D.MODE_P2P, {"DLC_TMA_CTAS": "3"}),
              ("p2p-ldst", D.MODE_P2P, {"DLC_FOLD_TMA": "0"}),
              ("p2p-k4pull", D.MODE_P2P, {"DLC_P2P_K4_PULL": "1"}),
+             ("p2p-nomerge", D.MODE_P2P, {"DLC_P2P_MERGE": "0"}),
              ("p2p-ce", D.MODE_P2P, {"DLC_P2P_COPY": "ce", "DLC_P2P_BARRIER": "nccl", "DLC_P2P_PIECES": "2"}),
              ("allreduce", D.MODE_ALLREDUCE, {})]
     for mode_name, mode, env in cases:
         for key in ("DLC_P2P_COPY", "DLC_P2P_PLAN", "DLC_P2P_BARRIER", "DLC_P2P_PIECES", "DLC_FOLD_TMA", "DLC_TMA_CTAS",
-                    "DLC_P2P_K4_PULL"):
+                    "DLC_P2P_K4_PULL", "DLC_P2P_MERGE"):
             os.environ.pop(key, None)
         os.environ.update(env)
         coll = PD.make_nccl_collective(r, mode)
