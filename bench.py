@@ -449,8 +449,27 @@ def run_ours(args):
     return 0
 
 
+def _json_stdout():
+    """Keep stdout for the one JSON line: native libraries (NCCL's version banner
+    under NCCL_DEBUG, CUDA) write to fd 1 directly, so fd 1 becomes stderr and the
+    result line goes to the saved stdout."""
+    global print
+    sys.stdout.flush()
+    saved = os.dup(1)
+    os.dup2(2, 1)
+    out = os.fdopen(saved, "w", buffering=1)
+    import builtins
+
+    def print(*a, **kw):  # noqa: A001
+        kw.setdefault("file", out)
+        kw.setdefault("flush", True)
+        builtins.print(*a, **kw)
+
+
 def main():
     args = parse()
+    if "WORLD_SIZE" in os.environ or args.gpus <= 1:
+        _json_stdout()
     rank, world, _ = dist_env()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # not launched by torchrun: relaunch one process per GPU

@@ -15,6 +15,7 @@
  *   DLC_ENUMERIC    NumericError     non-finite input where finite math is required
  *   DLC_ECOLLECTIVE CollectiveError  epoch mismatch, no contributions
  *   DLC_ENCCL       CollectiveError  NCCL failure
+ *   DLC_EQUORUM     QuorumError      membership below quorum_min (errors.hpp:42)
  *   DLC_ECUDA       Error            CUDA failure / no device
  *   DLC_EINVAL      Error            null pointer or out-of-range argument
  * Overflow is a signal, not an error (UnscaleResult.overflow,
@@ -52,7 +53,8 @@ enum dlc_status {
   DLC_ECUDA = 5,
   DLC_ENCCL = 6,
   DLC_EINVAL = 7,
-  DLC_ESERIAL = 8 /* SerializationError, errors.hpp:48 (wire frames) */
+  DLC_ESERIAL = 8, /* SerializationError, errors.hpp:48 (wire frames) */
+  DLC_EQUORUM = 9  /* QuorumError, errors.hpp:42 (membership change below quorum) */
 };
 
 /* Precision, reduce.hpp:22 */
@@ -166,7 +168,9 @@ enum dlc_reduce_mode { DLC_MODE_ORDERED = 0, DLC_MODE_ALLREDUCE = 1, DLC_MODE_P2
  *   movement over NVLink peer memory (CUDA IPC): each owner folds its slot
  *   straight out of the peers' send buffers, and the outer Nesterov kernel
  *   reads every owner's mean slot in place, so there are no recv / gather
- *   copies in HBM.  Two 4-byte NCCL all-reduces order the phases.  Bitwise
+ *   copies in HBM.  Flag barriers over NVLink order the phases; they are also
+ *   the failure detector (a peer silent for reduce_timeout_ms fails the round
+ *   with DLC_ECOLLECTIVE and leaves the engine's state unchanged).  Bitwise
  *   equal to ORDERED.  Engine path only; the host-buffer plugin call uses
  *   ORDERED semantics. */
 
@@ -184,6 +188,42 @@ DLC_API int dlc_collective_rank(const dlc_collective* c);
 DLC_API int dlc_collective_all_reduce_avg(dlc_collective* c, const float* local_delta, size_t n,
                                   int precision, uint64_t outer_epoch, float* out,
                                   dlc_reduce_report* report);
+
+/* Membership.  The reference's Node restarts a failed
+ * round over the live members minus the suspects: contributors sorted, quorum
+ * checked, rank = position, divisor = contributor count
+ * (collective.cpp:1369-1395; test_collective.cpp:460-531).  On one NVLink box:
+ *
+ *   dlc_collective_shrink   called by the SURVIVORS only (ncclCommShrink):
+ *                           a new collective over the world minus
+ *                           `exclude_ranks` (ranks of `c`), survivors keeping
+ *                           their relative order.  DLC_ECOLLECTIVE "excluded
+ *                           from round" when the caller is in the list,
+ *                           DLC_EQUORUM when fewer than max(quorum_min, 1)
+ *                           ranks remain.  DLC_SHRINK_ABORT first aborts
+ *                           operations still pending on `c`.  An engine made
+ *                           for num_workers_k >= the new world re-lays its
+ *                           owner slots at its next outer step on the new
+ *                           collective (ReduceReport::contributors = survivors,
+ *                           attempts = failed tries at this epoch + 1).
+ *                           `c` stays valid (destroy aborts its communicator).
+ *   dlc_collective_members  original ranks of the current members, sorted;
+ *                           returns the member count.
+ *   dlc_collective_set_reduce_timeout_ms
+ *                           NodeOptions::reduce_timeout_ms: how long a DLC_MODE_P2P
+ *                           barrier waits for a peer (default 20000).
+ *   dlc_collective_inject_stall
+ *                           fault injection (SocketCollective::set_stage_hook,
+ *                           test_collective.cpp:485-492): this rank stops
+ *                           arriving from its `barrier_index`-th P2P barrier
+ *                           on (counted from now; < 0 disables), so its round
+ *                           and its peers' rounds fail with DLC_ECOLLECTIVE. */
+enum dlc_shrink_flags { DLC_SHRINK_DEFAULT = 0, DLC_SHRINK_ABORT = 1 };
+DLC_API int dlc_collective_shrink(dlc_collective* c, const int* exclude_ranks, size_t n_exclude, size_t quorum_min,
+                                  int flags, dlc_collective** out);
+DLC_API size_t dlc_collective_members(const dlc_collective* c, int* ranks, size_t cap);
+DLC_API int dlc_collective_set_reduce_timeout_ms(dlc_collective* c, uint64_t ms);
+DLC_API int dlc_collective_inject_stall(dlc_collective* c, int64_t barrier_index);
 
 /* =========================================================================
  * 3. Device-resident engine: DilocoEngine (engine.hpp:76-116) with theta_t,

@@ -19,6 +19,7 @@
 #include <cstdint>
 #include <exception>
 #include <functional>
+#include <memory>
 #include <string>
 #include <utility>
 #include <vector>
@@ -42,6 +43,7 @@ inline void throw_status(int st) {
     case DLC_ECOLLECTIVE:
     case DLC_ENCCL: throw CollectiveError(msg);
     case DLC_ESERIAL: throw SerializationError(msg);
+    case DLC_EQUORUM: throw QuorumError(msg);
     default: throw Error(msg);
   }
 }
@@ -168,7 +170,28 @@ class NcclCollective final : public Collective {
 
   dlc_collective* handle() const { return c_; }
 
+  /// Survivors-only membership change (collective.cpp:1369-1395): this world
+  /// minus `exclude`, survivors in order; QuorumError below `quorum_min`,
+  /// CollectiveError("excluded from round") for an excluded caller.
+  std::unique_ptr<NcclCollective> shrink(const std::vector<int>& exclude, size_t quorum_min = 1,
+                                         bool abort_pending = false) {
+    dlc_collective* n = nullptr;
+    throw_status(dlc_collective_shrink(c_, exclude.data(), exclude.size(), quorum_min,
+                                       abort_pending ? DLC_SHRINK_ABORT : DLC_SHRINK_DEFAULT, &n));
+    return std::unique_ptr<NcclCollective>(new NcclCollective(n));
+  }
+
+  /// Original ranks of the current members (the round's sorted contributors).
+  std::vector<int> members() const {
+    std::vector<int> r(32);
+    r.resize(std::min<size_t>(dlc_collective_members(c_, r.data(), r.size()), r.size()));
+    return r;
+  }
+
+  void set_reduce_timeout_ms(uint64_t ms) { throw_status(dlc_collective_set_reduce_timeout_ms(c_, ms)); }
+
  private:
+  explicit NcclCollective(dlc_collective* c) : c_(c) {}
   dlc_collective* c_ = nullptr;
 };
 

@@ -14,7 +14,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libdiloco_cuda.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "diloco_cuda.h")
 
-OK, ESHAPE, ECONFIG, ENUMERIC, ECOLLECTIVE, ECUDA, ENCCL, EINVAL, ESERIAL = range(9)
+OK, ESHAPE, ECONFIG, ENUMERIC, ECOLLECTIVE, ECUDA, ENCCL, EINVAL, ESERIAL, EQUORUM = range(10)
+SHRINK_DEFAULT, SHRINK_ABORT = 0, 1
 FP32, FP16 = 0, 1
 LR_NONE, LR_COSINE = 0, 1
 MODE_ORDERED, MODE_ALLREDUCE, MODE_P2P = 0, 1, 2
@@ -148,6 +149,10 @@ _SIGS = {
     "dlc_collective_world_size": (SZ, [P]),
     "dlc_collective_rank": (I, [P]),
     "dlc_collective_all_reduce_avg": (I, [P, P, SZ, I, U64, P, C.POINTER(ReduceReport)]),
+    "dlc_collective_shrink": (I, [P, C.POINTER(I), SZ, SZ, I, C.POINTER(P)]),
+    "dlc_collective_members": (SZ, [P, C.POINTER(I), SZ]),
+    "dlc_collective_set_reduce_timeout_ms": (I, [P, U64]),
+    "dlc_collective_inject_stall": (I, [P, C.c_int64]),
     "dlc_hyperparams_default": (None, [C.POINTER(Hyperparams)]),
     "dlc_engine_create": (I, [C.POINTER(Config), C.POINTER(Hyperparams), SZ, I, I, C.POINTER(P)]),
     "dlc_engine_destroy": (I, [P]),

@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <map>
 #include <string>
 #include <vector>
@@ -50,7 +51,90 @@ int dlc_collective_create_nccl(int rank, int world, const uint8_t id[128], int d
       fail(DLC_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
     }
     cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    for (int i = 0; i < world && i < kMaxK; ++i) c->members[i] = i;
     *out = c;
+  });
+}
+
+// Membership change.  The reference's barrier picks the
+// round's contributors from the live members minus the suspects, checks the
+// quorum, renumbers them in sorted order and divides by their count
+// (collective.cpp:1369-1395).  On one NVLink box the same step is an
+// ncclCommShrink of the communicator: the survivors call it, the excluded
+// ranks do not, NCCL keeps the survivors' relative order, and the engines
+// re-lay their owner slots for the new fleet at their next outer step.
+int dlc_collective_shrink(dlc_collective* c, const int* exclude_ranks, size_t n_exclude, size_t quorum_min,
+                          int flags, dlc_collective** out) {
+  return guard([&] {
+    if (!c || !out || (n_exclude && !exclude_ranks)) fail(DLC_EINVAL, "dlc_collective_shrink: null argument");
+    *out = nullptr;
+    if (c->kind != 1) fail(DLC_ECONFIG, "dlc_collective_shrink: only an NCCL collective has a membership");
+    if (c->in_world) fail(DLC_ECONFIG, "dlc_collective_shrink: a dlc_world's collectives are fixed");
+    if (flags != DLC_SHRINK_DEFAULT && flags != DLC_SHRINK_ABORT) fail(DLC_ECONFIG, "unknown shrink flags");
+    std::vector<int> ex(exclude_ranks, exclude_ranks + n_exclude);
+    std::sort(ex.begin(), ex.end());
+    ex.erase(std::unique(ex.begin(), ex.end()), ex.end());
+    for (int r : ex)
+      if (r < 0 || r >= c->world) fail(DLC_ECONFIG, "dlc_collective_shrink: rank " + std::to_string(r) + " not in the world");
+    if (std::binary_search(ex.begin(), ex.end(), c->rank)) {  // collective.cpp:1382-1386
+      c->broken = true;
+      fail(DLC_ECOLLECTIVE, "excluded from round");
+    }
+    const int survivors = c->world - (int)ex.size();
+    if ((size_t)survivors < std::max<size_t>(quorum_min, 1))  // collective.cpp:1376-1378
+      fail(DLC_EQUORUM, "contributor set below quorum");
+    DeviceGuard dg(c->device);
+    auto* n = new dlc_collective();
+    n->kind = 1;
+    n->device = c->device;
+    n->mode = c->mode;
+    n->timeout_ms = c->timeout_ms;
+    n->shrunk = true;
+    const ncclResult_t r = ncclCommShrink(c->comm, ex.data(), (int)ex.size(), &n->comm, nullptr,
+                                          flags == DLC_SHRINK_ABORT ? NCCL_SHRINK_ABORT : NCCL_SHRINK_DEFAULT);
+    if (r != ncclSuccess) {
+      delete n;
+      fail(DLC_ENCCL, std::string("ncclCommShrink: ") + ncclGetErrorString(r));
+    }
+    int nr = -1, nw = 0;
+    ncclCommUserRank(n->comm, &nr);
+    ncclCommCount(n->comm, &nw);
+    int j = 0;
+    for (int i = 0; i < c->world; ++i)
+      if (!std::binary_search(ex.begin(), ex.end(), i)) n->members[j++] = c->members[i];
+    const int want = c->rank - (int)(std::lower_bound(ex.begin(), ex.end(), c->rank) - ex.begin());
+    if (nw != survivors || nr != want) {
+      ncclCommAbort(n->comm);
+      delete n;
+      fail(DLC_ENCCL, "ncclCommShrink: unexpected rank " + std::to_string(nr) + " of " + std::to_string(nw));
+    }
+    n->rank = nr;
+    n->world = nw;
+    c->broken = true;  // its peers are gone: destroying it must not wait for them
+    cudaStreamCreateWithFlags(&n->stream, cudaStreamNonBlocking);
+    *out = n;
+  });
+}
+
+size_t dlc_collective_members(const dlc_collective* c, int* ranks, size_t cap) {
+  if (!c) return 0;
+  const size_t w = c->kind == 1 ? (size_t)c->world : 1;
+  for (size_t i = 0; i < w && i < cap && ranks; ++i) ranks[i] = c->kind == 1 ? c->members[i] : 0;
+  return w;
+}
+
+int dlc_collective_set_reduce_timeout_ms(dlc_collective* c, uint64_t ms) {
+  return guard([&] {
+    if (!c) fail(DLC_EINVAL, "dlc_collective_set_reduce_timeout_ms: null collective");
+    if (ms == 0) fail(DLC_ECONFIG, "reduce_timeout_ms must be > 0");
+    c->timeout_ms = ms;
+  });
+}
+
+int dlc_collective_inject_stall(dlc_collective* c, int64_t barrier_index) {
+  return guard([&] {
+    if (!c) fail(DLC_EINVAL, "dlc_collective_inject_stall: null collective");
+    c->stall_at = barrier_index < 0 ? -1 : c->barriers + barrier_index;
   });
 }
 
@@ -69,7 +153,10 @@ int dlc_collective_destroy(dlc_collective* c) {
     if (c->kind == 1) {
       DeviceGuard dg(c->device);
       if (c->stream) cudaStreamDestroy(c->stream);
-      ncclCommDestroy(c->comm);
+      if (c->broken)
+        ncclCommAbort(c->comm);  // some peers are gone: do not wait for them
+      else
+        ncclCommDestroy(c->comm);
     }
     delete c;
   });

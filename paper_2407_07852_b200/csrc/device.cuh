@@ -15,6 +15,13 @@ namespace dlc {
 
 namespace {
 
+// Wall-clock nanoseconds (%globaltimer), independent of the SM clock.
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 // Persistent grid for the setup / host-staged helpers (not on the hot path).
 template <typename Kern>
 int grid_persist(Kern kernel, size_t work) {

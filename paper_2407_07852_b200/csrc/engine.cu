@@ -73,9 +73,11 @@ int dlc_engine_create(const dlc_config* cfg, const dlc_hyperparams* hyper, size_
     e->n = n;
     e->k = cfg->num_workers_k;
     e->prec = cfg->reduce_precision;
-    // owner slot: a multiple of 64 elements per P2P piece
-    const size_t quantum = 64 * kMaxPieces;
-    e->S = (((n + e->k - 1) / e->k) + quantum - 1) / quantum * quantum;
+    e->S = slot_elems(n, e->k);
+    // the collective buffers also fit every smaller fleet a membership change
+    // (dlc_collective_shrink) can leave behind
+    e->k_cap = e->k;
+    for (size_t kk = 1; kk <= e->k; ++kk) e->slot_cap = std::max(e->slot_cap, kk * slot_elems(n, kk));
     DLC_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
     DLC_CUDA(cudaEventCreate(&e->ev0));
     DLC_CUDA(cudaEventCreate(&e->ev1));
@@ -98,7 +100,7 @@ int dlc_engine_create(const dlc_config* cfg, const dlc_hyperparams* hyper, size_
       e->v[1] = e->v[0];
     }
     e->grad = (float*)dalloc(e, vb);
-    const size_t pb = e->k * e->S * elem_width(e->prec);
+    const size_t pb = e->slot_cap * elem_width(e->prec);
     e->send = dalloc(e, pb);
     DLC_CUDA(cudaMemsetAsync(e->send, 0, pb, e->stream));  // padding stays zero
     if (e->k > 1) {

@@ -22,6 +22,14 @@ struct dlc_collective {
   ncclComm_t comm = nullptr;
   cudaStream_t stream = nullptr;  // used only by the host-buffer plugin call
   bool in_world = false;          // one of the K collectives of a dlc_world (one host thread)
+  // membership: members[i] = rank in the ORIGINAL world of
+  // this communicator's rank i (the reference's sorted contributor list)
+  int members[dlc::kMaxK] = {};
+  bool shrunk = false;                 // made by dlc_collective_shrink (engines re-layout for it)
+  bool broken = false;                 // a round failed on it, or ranks were excluded from it: abort on destroy
+  uint64_t timeout_ms = 20000;         // NodeOptions::reduce_timeout_ms: P2P barrier failure detector
+  int64_t stall_at = -1;               // fault injection: stop arriving from this barrier on (-1 off)
+  int64_t barriers = 0;                // P2P barriers issued on this collective
 };
 
 struct dlc_engine {
@@ -73,6 +81,9 @@ struct dlc_engine {
   uint64_t* peer_sig[dlc::kMaxK] = {};
   uint64_t sig_epoch = 0;
   int* sig_err = nullptr;
+  size_t k_cap = 1;      // collective buffers hold any layout k' <= k_cap (membership changes)
+  size_t slot_cap = 0;   // elements per collective buffer: max over k' <= k_cap of k' * S(k')
+  uint64_t failed_tries = 0;  // consecutive failed rounds at the current epoch (ReduceReport::attempts - 1)
   std::vector<void*> ipc_opened;
   // host-buffer path: copy streams and per-chunk events
   cudaStream_t h2d = nullptr, d2h = nullptr;
@@ -162,6 +173,7 @@ void p2p_unbind(dlc_engine* e);
 void p2p_bind(dlc_engine* e, dlc_collective* c);
 void fleet_barrier(dlc_engine* e, dlc_collective* c);
 void p2p_barrier(dlc_engine* e, dlc_collective* c, cudaStream_t s);
+bool flag_barriers(const dlc_collective* c);
 void outer_collective(dlc_engine* e, dlc_collective* c, dlc_reduce_report* rep);
 void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc_reduce_report* rep,
                          const float* hsrc, float* hdst, int oc_host);
@@ -173,6 +185,8 @@ void outer_round(dlc_engine* e, dlc_collective* c, const float* src, dlc_reduce_
 void fill_report(dlc_engine* e, dlc_collective* c, dlc_reduce_report* rep, uint64_t epoch);
 void check_collective(dlc_engine* e, dlc_collective* c);
 void check_barrier(dlc_engine* e);
+size_t slot_elems(size_t n, size_t k);
+void relayout(dlc_engine* e, size_t k);
 void outer_result(dlc_engine* e, dlc_outer_result* res);
 
 }  // namespace dlc

@@ -338,8 +338,8 @@ void fill_report(dlc_engine* e, dlc_collective* c, dlc_reduce_report* rep, uint6
   if (!rep) return;
   *rep = dlc_reduce_report{};
   rep->outer_epoch = epoch;
-  rep->contributors = e->k;
-  rep->attempts = 1;
+  rep->contributors = e->k;  // the survivor count after a membership change (collective.cpp:1378-1389)
+  rep->attempts = 1 + e->failed_tries;
   if (e->k > 1) {
     const uint64_t bytes = 2ull * (e->k - 1) * e->S * elem_width(e->prec);
     rep->data_bytes_sent = rep->data_bytes_received = bytes;
@@ -352,8 +352,38 @@ void fill_report(dlc_engine* e, dlc_collective* c, dlc_reduce_report* rep, uint6
   (void)c;
 }
 
+// Owner slot S for k workers: ceil(n / k) rounded up to 64 elements per P2P piece.
+size_t slot_elems(size_t n, size_t k) {
+  const size_t quantum = 64 * kMaxPieces;
+  return ((n + k - 1) / k + quantum - 1) / quantum * quantum;
+}
+
+// Membership change: lay the collective buffers out for a
+// fleet of k workers (k <= k_cap, so the buffers made at creation suffice).
+// Padding must read as zero again and the P2P peer mappings are rebuilt by
+// the next bind over the new communicator.
+void relayout(dlc_engine* e, size_t k) {
+  if (k == e->k) return;
+  if (k < 1 || k > e->k_cap) fail(DLC_ECOLLECTIVE, "membership of " + std::to_string(k) + " workers exceeds the " +
+                                                       std::to_string(e->k_cap) + " this engine was made for");
+  DLC_CUDA(cudaStreamSynchronize(e->stream));
+  if (e->cstream) DLC_CUDA(cudaStreamSynchronize(e->cstream));
+  p2p_unbind(e);
+  const size_t pb = e->slot_cap * elem_width(e->prec);
+  DLC_CUDA(cudaMemsetAsync(e->send, 0, pb, e->stream));
+  if (e->gather) DLC_CUDA(cudaMemsetAsync(e->gather, 0, pb, e->stream));
+  if (e->recv) DLC_CUDA(cudaMemsetAsync(e->recv, 0, pb, e->stream));
+  DLC_CUDA(cudaMemsetAsync(e->flags, 0, kMaxK * sizeof(int), e->stream));
+  DLC_CUDA(cudaStreamSynchronize(e->stream));
+  e->k = k;
+  e->S = slot_elems(e->n, k);
+}
+
 void check_collective(dlc_engine* e, dlc_collective* c) {
   const size_t world = c ? (size_t)c->world : 1;
+  if (world != e->k && c && c->shrunk && c->kind == 1 && world <= e->k_cap &&
+      e->issued_inner % e->cfg.local_steps_h == 0)
+    relayout(e, world);  // the fleet lost members: survivor slots and divisor
   if (world != e->k)
     fail(DLC_ECOLLECTIVE, "collective world size " + std::to_string(world) + " != num_workers_k " +
                               std::to_string(e->k));
@@ -364,18 +394,33 @@ void check_collective(dlc_engine* e, dlc_collective* c) {
 }
 
 // A flag barrier that timed out (a peer never arrived) surfaces as CollectiveError.
+// The round then changed nothing (p2p_finish_kernel's abort gate): the caller
+// shrinks the collective around the silent peer and retries the same epoch,
+// as Node::Impl::all_reduce restarts with the suspect excluded
+// (collective.cpp:1369-1440).  The barrier epochs of the failed round are
+// abandoned: the next bind (over the new communicator) agrees on fresh ones.
 void check_barrier(dlc_engine* e) {
   if (!e->sig_err) return;
   int err = 0;
   DLC_CUDA(cudaStreamSynchronize(e->stream));
   if (e->cstream) DLC_CUDA(cudaStreamSynchronize(e->cstream));
   DLC_CUDA(cudaMemcpy(&err, e->sig_err, sizeof(int), cudaMemcpyDeviceToHost));
-  if (err) fail(DLC_ECOLLECTIVE, "P2P barrier timed out: a peer rank stopped participating");
+  if (!err) return;
+  DLC_CUDA(cudaMemset(e->sig_err, 0, sizeof(int)));
+  if (e->p2p_bound) const_cast<dlc_collective*>(e->p2p_bound)->broken = true;
+  p2p_unbind(e);
+  e->failed_tries += 1;
+  if (e->inner_mode != DLC_INNER_PINGPONG)
+    fail(DLC_ECOLLECTIVE, "P2P barrier timed out: a peer rank stopped participating (DLC_INNER_INPLACE: theta_local "
+                          "was overwritten, restore it before retrying)");
+  fail(DLC_ECOLLECTIVE, "P2P barrier timed out: a peer rank stopped participating; state unchanged, shrink the "
+                        "collective and retry");
 }
 
 void outer_result(dlc_engine* e, dlc_outer_result* res) {
   if (!res) return;  // asynchronous call: nothing is synchronised here
   check_barrier(e);
+  e->failed_tries = 0;
   const DevState s = read_state(e);
   res->applied = s.last_applied;
   res->outer_epoch = s.outer_epoch;

@@ -127,7 +127,11 @@ void launch_fold_push(const PtrList& in, int k, int precision, const PtrList& ou
 // Fleet barrier over NVLink flags (DLC_MODE_P2P): one CTA stores `epoch` into
 // slot `me` of every peer's signal array (`remote`, after a system fence), then
 // waits until every peer's store has landed in `local`.  A peer silent for
-// ~10 s sets *err and the kernel exits instead of hanging the GPU.
+// `timeout_ns` (globaltimer; NodeOptions::reduce_timeout_ms, collective.hpp)
+// sets *err and the kernel exits instead of hanging the GPU; once *err is set
+// (this round already failed) later barriers neither signal nor wait.
+// `stall` (fault injection, the reference's set_stage_hook) makes this rank
+// stop arriving: it sets *err without signalling its peers.
 // fold_push with the bulk-copy engine (TMA) moving the tiles; false when k is outside 2..8
 // (the caller then uses launch_fold_push)
 bool launch_fold_push_tma(const PtrList& in, int k, int precision, const PtrList& outs, int nout,
@@ -135,7 +139,7 @@ bool launch_fold_push_tma(const PtrList& in, int k, int precision, const PtrList
 // push/push mover: rows src[q] -> dst[q] (`bytes` each, a multiple of 16), a persistent grid of `ctas`
 void launch_scatter_push(const PtrList& src, const PtrList& dst, int nrow, size_t bytes, int ctas, cudaStream_t s);
 void launch_flag_barrier(const PtrList& remote, const uint64_t* local, int k, int me, uint64_t epoch,
-                         int* err, cudaStream_t s);
+                         int* err, uint64_t timeout_ns, bool stall, cudaStream_t s);
 void launch_pseudo_grad_piece(Pair theta_t, Pair theta_local, const DevState* st, void* send,
                               int precision, int k, size_t S, size_t po, size_t plen, size_t n,
                               int ctas, cudaStream_t s);
@@ -148,8 +152,10 @@ void launch_pseudo_grad_push_piece(Pair theta_t, Pair theta_local, const DevStat
 void launch_nesterov_p2p_piece(Pair theta_t, Pair buf, Pair theta_local, const PtrList& slots,
                                int k, size_t S, size_t po, size_t plen, int precision,
                                DevState* st, float lr, float mu, size_t n, int ctas, cudaStream_t s);
+// `abort` (nullable): a failed round (a barrier timed out) leaves every state
+// buffer and counter as it was, so the round can be retried on a shrunk world.
 void launch_p2p_finish(Pair theta_t, Pair theta_local, const PtrList& flags, int k, DevState* st,
-                       size_t n, cudaStream_t s);
+                       size_t n, const int* abort, cudaStream_t s);
 // K2+K4 fused for a single worker (SoloCollective, reduce.cpp:113-126): one
 // HBM pass reading theta_t[ocur], buf[ocur], theta_local and writing
 // theta_t[ocur^1], buf[ocur^1], theta_local (24 B/param), then a finish kernel

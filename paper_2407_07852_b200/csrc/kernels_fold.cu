@@ -417,15 +417,25 @@ __global__ void __launch_bounds__(kThreads) scatter_push_kernel(const __grid_con
 
 // ---- NVLink flag barrier ----------------------------------------------------
 __global__ void flag_barrier_kernel(const __grid_constant__ PtrList remote, const uint64_t* local, int k, int me,
-                                    uint64_t epoch, int* err) {
+                                    uint64_t epoch, int* err, uint64_t timeout_ns, int stall) {
   const int j = threadIdx.x;
+  __shared__ int s_failed;
+  if (j == 0) {
+    s_failed = *reinterpret_cast<volatile int*>(err);
+    if (stall && !s_failed) {  // fault injection: stop arriving, fail this rank's round
+      atomicExch(err, 1);
+      s_failed = 1;
+    }
+  }
+  __syncthreads();
+  if (s_failed) return;  // the round already failed: no signal, no wait
   if (j < k && j != me) {
     __threadfence_system();  // everything this GPU wrote before the barrier is visible first
     *reinterpret_cast<volatile unsigned long long*>(const_cast<void*>(remote.ptr[j])) = epoch;
-    const long long start = clock64();
+    const uint64_t start = globaltimer_ns();
     const volatile unsigned long long* mine = reinterpret_cast<const volatile unsigned long long*>(local + j);
     while (*mine < epoch) {
-      if (clock64() - start > (1ll << 35)) {  // ~17 s at 2 GHz: a peer is gone
+      if (globaltimer_ns() - start > timeout_ns) {  // a peer stopped participating
         atomicExch(err, 1);
         break;
       }
@@ -521,8 +531,9 @@ void launch_scatter_push(const PtrList& src, const PtrList& dst, int nrow, size_
 }
 
 void launch_flag_barrier(const PtrList& remote, const uint64_t* local, int k, int me, uint64_t epoch, int* err,
+                         uint64_t timeout_ns, bool stall,
                          cudaStream_t s) {
-  flag_barrier_kernel<<<1, 32, 0, s>>>(remote, local, k, me, epoch, err);
+  flag_barrier_kernel<<<1, 32, 0, s>>>(remote, local, k, me, epoch, err, timeout_ns, stall ? 1 : 0);
 }
 
 }  // namespace dlc

@@ -283,7 +283,9 @@ __global__ void __launch_bounds__(kThreads) nesterov_p2p_piece_kernel(Pair ttp, 
 // Gate of the pipelined P2P step: flip `ocur` when all K owner flags are clean
 // (engine.cpp:136-139), else theta_local := theta_t (engine.cpp:143).
 __global__ void __launch_bounds__(kThreads) p2p_finish_kernel(Pair ttp, Pair tl, const __grid_constant__ PtrList flags,
-                                                              int k, DevState* st, size_t n) {
+                                                              int k, DevState* st, size_t n, const int* abort) {
+  // a failed round (abort) changes nothing: no flip, no epoch, no theta_local
+  if (abort && *reinterpret_cast<const volatile int*>(abort)) return;
   __shared__ int s_skip;
   if (threadIdx.x == 0) {
     int nf = 0;
@@ -427,8 +429,9 @@ void launch_nesterov_p2p_piece(Pair tt, Pair buf, Pair tl, const PtrList& slots,
     nesterov_p2p_piece_kernel<1><<<grid, kThreads, 0, s>>>(tt, buf, tl, slots, k, S, po, plen, st, lr, mu, n, nblk);
 }
 
-void launch_p2p_finish(Pair tt, Pair tl, const PtrList& flags, int k, DevState* st, size_t n, cudaStream_t s) {
-  p2p_finish_kernel<<<num_sms() * 4, kThreads, 0, s>>>(tt, tl, flags, k, st, n);
+void launch_p2p_finish(Pair tt, Pair tl, const PtrList& flags, int k, DevState* st, size_t n, const int* abort,
+                       cudaStream_t s) {
+  p2p_finish_kernel<<<num_sms() * 4, kThreads, 0, s>>>(tt, tl, flags, k, st, n, abort);
 }
 
 void launch_outer_solo_chunk(Pair tt, Pair buf, Pair tl, const float* src, int precision, DevState* st, float lr,

@@ -31,8 +31,10 @@ void p2p_bind(dlc_engine* e, dlc_collective* c) {
   const int K = (int)e->k, r = c->rank;
   struct Handles {
     cudaIpcMemHandle_t send, gather, flags, sig, recv;
+    uint64_t sig_epoch;
   };
   Handles mine;
+  mine.sig_epoch = e->sig_epoch;
   DLC_CUDA(cudaIpcGetMemHandle(&mine.recv, e->recv));
   DLC_CUDA(cudaIpcGetMemHandle(&mine.send, e->send));
   DLC_CUDA(cudaIpcGetMemHandle(&mine.gather, e->gather));
@@ -52,6 +54,10 @@ void p2p_bind(dlc_engine* e, dlc_collective* c) {
     throw;
   }
   cudaFree(dbuf);
+  // Barrier epochs continue above every epoch any rank has used, so a signal
+  // left over from an abandoned round (or an earlier membership) never
+  // satisfies a barrier of this one.
+  for (int j = 0; j < K; ++j) e->sig_epoch = std::max(e->sig_epoch, all[j].sig_epoch);
   for (int j = 0; j < K; ++j) {
     if (j == r) {
       e->peer_send[j] = e->send;
@@ -95,16 +101,23 @@ void fleet_barrier(dlc_engine* e, dlc_collective* c) {
 
 // Phase barrier of the P2P step on stream `s`: NVLink flags by default
 // (one CTA, a few microseconds), DLC_P2P_BARRIER=nccl for the NCCL all-reduce.
-void p2p_barrier(dlc_engine* e, dlc_collective* c, cudaStream_t s) {
+bool flag_barriers(const dlc_collective* c) {
   const char* b = std::getenv("DLC_P2P_BARRIER");
-  if (b && std::string(b) == "nccl" && !c->in_world) {  // (one thread drives a world: flags only)
+  return !(b && std::string(b) == "nccl" && !c->in_world);  // (one thread drives a world: flags only)
+}
+
+void p2p_barrier(dlc_engine* e, dlc_collective* c, cudaStream_t s) {
+  if (!flag_barriers(c)) {
     DLC_NCCL(ncclAllReduce(e->barrier_buf, e->barrier_buf, 1, ncclInt32, ncclSum, c->comm, s));
     return;
   }
   PtrList remote{};
   for (size_t j = 0; j < e->k; ++j) remote.ptr[j] = e->peer_sig[j] + c->rank;
   e->sig_epoch += 1;
-  launch_flag_barrier(remote, e->sig, (int)e->k, c->rank, e->sig_epoch, e->sig_err, s);
+  const bool stall = c->stall_at >= 0 && c->barriers >= c->stall_at;
+  c->barriers += 1;
+  launch_flag_barrier(remote, e->sig, (int)e->k, c->rank, e->sig_epoch, e->sig_err, c->timeout_ms * 1000000ull, stall,
+                      s);
   launched("flag_barrier");
 }
 
@@ -382,7 +395,8 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
       });
     }
   }
-  launch_p2p_finish(tt_pair(e), local_pair(e), fl, (int)K, e->st, n, e->stream);
+  launch_p2p_finish(tt_pair(e), local_pair(e), fl, (int)K, e->st, n, flag_barriers(c) ? e->sig_err : nullptr,
+                    e->stream);
   phase_end(e, DLC_PHASE_OUTER);
   launched("nesterov_p2p_piece");
   trace_dump(e, origin);
@@ -466,7 +480,7 @@ void outer_allreduce_pipelined(dlc_engine* e, dlc_collective* c, const float* sr
     launch_nesterov_p2p_piece(tt_pair(e), buf_pair(e), local_pair(e), slots, 1, 0, pb[p], pb[p + 1] - pb[p],
                               e->prec, e->st, e->hyper.outer_lr, e->hyper.outer_momentum, n, 0, e->stream);
   }
-  launch_p2p_finish(tt_pair(e), local_pair(e), fl, 1, e->st, n, e->stream);
+  launch_p2p_finish(tt_pair(e), local_pair(e), fl, 1, e->st, n, nullptr, e->stream);
   phase_end(e, DLC_PHASE_OUTER);
   launched("nesterov_p2p_piece");
 }

@@ -43,8 +43,13 @@ class SerializationError(Error):
     pass
 
 
+class QuorumError(Error):
+    """errors.hpp:42: a membership change left fewer than quorum_min workers."""
+
+
 _EXC = {A.ESHAPE: ShapeError, A.ECONFIG: ConfigError, A.ENUMERIC: NumericError,
-        A.ECOLLECTIVE: CollectiveError, A.ENCCL: CollectiveError, A.ESERIAL: SerializationError}
+        A.ECOLLECTIVE: CollectiveError, A.ENCCL: CollectiveError, A.ESERIAL: SerializationError,
+        A.EQUORUM: QuorumError}
 
 
 def _check(status: int) -> None:
@@ -275,6 +280,34 @@ class NcclCollective(Collective):
         _check(lib.dlc_collective_create_nccl(rank, world, unique_id, device, mode, C.byref(h)))
         self.handle = h
         self.mode = mode
+
+    def shrink(self, exclude, quorum_min: int = 1, abort: bool = False) -> "NcclCollective":
+        """Survivors-only membership change (collective.cpp:1369-1395): a new collective
+        over this world minus `exclude` (ranks of this collective).  Raises
+        CollectiveError("excluded from round") on an excluded caller and QuorumError
+        below quorum_min."""
+        ex = (C.c_int * max(len(exclude), 1))(*exclude)
+        h = C.c_void_p()
+        _check(lib.dlc_collective_shrink(self.handle, ex, len(exclude), quorum_min,
+                                         A.SHRINK_ABORT if abort else A.SHRINK_DEFAULT, C.byref(h)))
+        n = NcclCollective.__new__(NcclCollective)
+        n.handle = h
+        n.mode = self.mode
+        return n
+
+    def members(self):
+        """Original ranks of the current members, sorted (the round's contributors)."""
+        buf = (C.c_int * 32)()
+        k = int(lib.dlc_collective_members(self.handle, buf, 32))
+        return [int(buf[i]) for i in range(k)]
+
+    def set_reduce_timeout_ms(self, ms: int) -> None:
+        """NodeOptions::reduce_timeout_ms: the P2P barriers' failure detector."""
+        _check(lib.dlc_collective_set_reduce_timeout_ms(self.handle, ms))
+
+    def inject_stall(self, barrier_index: int) -> None:
+        """Fault injection (set_stage_hook): stop arriving from the n-th P2P barrier on."""
+        _check(lib.dlc_collective_inject_stall(self.handle, barrier_index))
 
 
 # ---- device-resident engine, engine.hpp:76-157 ------------------------------------------

@@ -44,3 +44,16 @@ def test_multigpu_full_size(nproc):
            os.path.join(ROOT, "tests", "mp_full_worker.py")]
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert p.returncode == 0 and p.stdout.count("MPRESULT") == nproc, p.stdout[-3000:] + p.stderr[-3000:]
+
+
+@pytest.mark.parametrize("nproc", [2, 3, 4])
+def test_multigpu_membership_change(nproc):
+    """A peer stalls mid-reduce (P2P) or leaves (ordered / allreduce): survivors shrink
+    the collective and finish the round with the survivor mean (test_collective.cpp:460-531)."""
+    if gpus() < nproc:
+        pytest.skip(f"needs {nproc} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29640 + nproc),
+           os.path.join(ROOT, "tests", "mp_fault_worker.py")]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert p.returncode == 0 and p.stdout.count("MPRESULT") == nproc, p.stdout[-3000:] + p.stderr[-3000:]
