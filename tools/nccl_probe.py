@@ -18,7 +18,8 @@ def main():
     r, k = dist.get_rank(), dist.get_world_size()
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
     n = int(os.environ.get("PROBE_N", 1_100_000_000))
-    for dtype in (torch.float16, torch.float32):
+    dtypes = [getattr(torch, d) for d in os.environ.get("PROBE_DTYPES", "float16,float32").split(",")]
+    for dtype in dtypes:
         x = torch.randn(n, dtype=dtype, device="cuda") * 1e-3
         for op_name, op in (("sum", dist.ReduceOp.SUM), ("avg", dist.ReduceOp.AVG)):
             for _ in range(2):
@@ -31,9 +32,9 @@ def main():
                 dist.all_reduce(x, op=op)
             b.record()
             b.synchronize()
-            ms = torch.tensor([a.elapsed_time(b) / steps], device="cuda")
-            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-            ms = float(ms.item())
+            got = [None] * k  # (object gather: NCCL_ALGO=NVLS has no FP32 all-reduce)
+            dist.all_gather_object(got, a.elapsed_time(b) / steps)
+            ms = max(got)
             bus = x.numel() * x.element_size() * 2 * (k - 1) / k / (ms * 1e-3) / 1e9
             if r == 0:
                 print(json.dumps({"dtype": str(dtype), "op": op_name, "algo": os.environ.get("NCCL_ALGO", "default"),
