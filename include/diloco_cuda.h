@@ -475,6 +475,16 @@ DLC_API int dlc_fp16_encode_bits(uint32_t start, size_t n, uint16_t* out);
 DLC_API int dlc_fold_push_probe(const void* const* contribs, int k, size_t n, int precision, int tma, void* out,
                                 int* nonfinite);
 
+/* Kernel probe for the K > 1 outer step on ONE device (development / ncu tool,
+ * no reference counterpart): allocates full-size synthetic buffers for n
+ * parameters and k owner slots and times, each averaged over `reps` launches,
+ * ms3[0] = K2 pseudo_grad_piece over a whole slot range (10 / 12 B/param FP16 /
+ * FP32), ms3[1] = the owner fold + mean push over k local rows (the DRAM bytes
+ * one GPU serves and receives in the exchange: 2w B/param), ms3[2] = K4
+ * nesterov_p2p_piece (16 + w B/param).  Lets ncu capture the multi-GPU kernels
+ * in a single process. */
+DLC_API int dlc_p2p_kernels_probe(int k, size_t n, int precision, int reps, float* ms3);
+
 /* =========================================================================
  * 5. Wire codec for cross-box transports.
  *

@@ -430,4 +430,81 @@ int dlc_fold_push_probe(const void* const* contribs, int k, size_t n, int precis
   });
 }
 
+int dlc_p2p_kernels_probe(int k, size_t n, int precision, int reps, float* ms3) {
+  return guard([&] {
+    if (k < 2 || k > kMaxK) fail(DLC_EINVAL, "p2p_kernels_probe: k must be 2..32");
+    if (precision != DLC_FP32 && precision != DLC_FP16) fail(DLC_ECONFIG, "unknown precision");
+    if (n == 0 || reps < 1 || !ms3) fail(DLC_EINVAL, "p2p_kernels_probe: bad argument");
+    const size_t w = precision == DLC_FP16 ? 2 : 4;
+    const size_t quantum = 64 * 8;  // the engine's owner-slot quantum (engine_impl.hpp kMaxPieces)
+    const size_t S = ((n + k - 1) / k + quantum - 1) / quantum * quantum;
+    ThreadCtx& c = ctx();
+    // dedicated allocations (full-size vectors do not belong in the staging arena)
+    std::vector<void*> owned;
+    auto dmalloc = [&](size_t bytes) {
+      void* p = nullptr;
+      DLC_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 256)));
+      owned.push_back(p);
+      return p;
+    };
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    try {
+      float* tt[2] = {(float*)dmalloc(n * 4), (float*)dmalloc(n * 4)};
+      float* bf[2] = {(float*)dmalloc(n * 4), (float*)dmalloc(n * 4)};
+      float* x = (float*)dmalloc(n * 4);
+      char* send = (char*)dmalloc((size_t)k * S * w);
+      char* gather = (char*)dmalloc((size_t)k * S * w);
+      int* flags = (int*)dmalloc(kMaxK * sizeof(int));
+      DevState* st = (DevState*)dmalloc(sizeof(DevState));
+      DLC_CUDA(cudaMemsetAsync(st, 0, sizeof(DevState), c.stream));
+      DLC_CUDA(cudaMemsetAsync(flags, 0, kMaxK * sizeof(int), c.stream));
+      DLC_CUDA(cudaMemsetAsync(bf[0], 0, n * 4, c.stream));
+      launch_rng_fill(1, 0, -0.05f, 0.05f, tt[0], n, c.stream);
+      launch_rng_fill(2, 0, -0.05f, 0.05f, x, n, c.stream);
+      const Pair ttp{{tt[0], tt[1]}, 0}, bufp{{bf[0], bf[1]}, 0};
+      const Pair src{{x, x}, 0}, follow{{x, x}, 1};
+      // owner r's view, emulated on one device: the K contributions to a slot are
+      // the K rows of the send buffer, the mean goes to K gather rows -- the same
+      // DRAM bytes one GPU serves and receives in the real exchange
+      PtrList in{}, outs{}, fl{}, slots{};
+      for (int j = 0; j < k; ++j) {
+        in.ptr[j] = send + (size_t)j * S * w;
+        outs.ptr[j] = gather + (size_t)j * S * w;
+        fl.ptr[j] = flags + j;
+        slots.ptr[j] = gather + (size_t)j * S * w;
+      }
+      DLC_CUDA(cudaEventCreate(&ev[0]));
+      DLC_CUDA(cudaEventCreate(&ev[1]));
+      auto timed = [&](auto&& launch) {
+        launch();  // warm
+        DLC_CUDA(cudaEventRecord(ev[0], c.stream));
+        for (int i = 0; i < reps; ++i) launch();
+        DLC_CUDA(cudaEventRecord(ev[1], c.stream));
+        DLC_CUDA(cudaEventSynchronize(ev[1]));
+        float ms = 0.f;
+        DLC_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+        DLC_CUDA(cudaGetLastError());
+        return ms / (float)reps;
+      };
+      ms3[0] = timed([&] {
+        launch_pseudo_grad_piece(ttp, src, st, send, precision, k, S, 0, S, n, 0, c.stream);
+      });
+      ms3[1] = timed([&] {
+        if (!launch_fold_push_tma(in, k, precision, outs, k, fl, k, S, 0, c.stream))
+          launch_fold_push(in, k, precision, outs, k, fl, k, S, 0, c.stream);
+      });
+      ms3[2] = timed([&] {
+        launch_nesterov_p2p_piece(ttp, bufp, follow, slots, k, S, 0, S, precision, st, 0.7f, 0.9f, n, 0, c.stream);
+      });
+    } catch (...) {
+      for (cudaEvent_t e : ev)
+        if (e) cudaEventDestroy(e);
+      for (void* p : owned) cudaFree(p);
+      throw;
+    }
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
+    for (void* p : owned) DLC_CUDA(cudaFree(p));
+  });
+}
+
 }  // extern "C"
