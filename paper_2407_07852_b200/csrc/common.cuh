@@ -60,6 +60,21 @@ __device__ __forceinline__ uint32_t pack2(uint16_t a, uint16_t b) { return (uint
 __device__ __forceinline__ uint16_t lo16(uint32_t w) { return (uint16_t)(w & 0xFFFFu); }
 __device__ __forceinline__ uint16_t hi16(uint32_t w) { return (uint16_t)(w >> 16); }
 
+// ---- the mean's division, reduce.cpp:43 (acc / (float)K) --------------------
+// For K a power of two, 1/K is exact, and RN(acc * 2^-m) is the same real value
+// as RN(acc / 2^m) rounded once: bit-identical for every finite, infinite and
+// subnormal result (NaNs stay NaNs; payloads compare by class), at
+// one FMUL instead of the IEEE division sequence.  Other K divide.
+struct MeanDiv {
+  float divisor, inv;  // inv = 1/K for power-of-two K, else 0
+};
+__host__ __device__ inline MeanDiv mean_div(int k) {
+  return MeanDiv{(float)k, (k > 0 && (k & (k - 1)) == 0) ? 1.0f / (float)k : 0.0f};
+}
+__device__ __forceinline__ float div_mean(float acc, const MeanDiv& d) {
+  return d.inv != 0.0f ? __fmul_rn(acc, d.inv) : __fdiv_rn(acc, d.divisor);
+}
+
 // Block-wide OR of a predicate, then one atomicOr per CTA into *flag.
 __device__ __forceinline__ void block_or_flag(bool pred, int* flag) {
   const int any = __syncthreads_or(pred ? 1 : 0);

@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(kThreads) nonfinite_codes_kernel(const uint16_
 // reduce.cpp:46-89 for any k: contributions visited in index order.
 __global__ void __launch_bounds__(kThreads) fold_many_kernel(const float* const* ptrs, size_t k, int fp16,
                                                              float* out, size_t n) {
-  const float divisor = (float)k;
+  const MeanDiv divisor = mean_div(k);
   for (size_t e = gtid(); e < n; e += gstride()) {
     float acc = ptrs[0][e];
     if (fp16) acc = fp16_decode(fp16_encode(acc));
@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(kThreads) fold_many_kernel(const float* const*
       const float x = ptrs[j][e];
       acc = __fadd_rn(acc, fp16 ? fp16_decode(fp16_encode(x)) : x);
     }
-    const float mean = __fdiv_rn(acc, divisor);
+    const float mean = div_mean(acc, divisor);
     out[e] = fp16 ? fp16_decode(fp16_encode(mean)) : mean;
   }
 }

@@ -6,6 +6,8 @@
 #include <mutex>
 #include <unordered_map>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "device.cuh"
 #include "kernels.cuh"
@@ -114,7 +116,7 @@ __device__ __forceinline__ bool store1(void* out, size_t e, float mean) {
 template <int IN, int OUT>
 __global__ void __launch_bounds__(kThreads) fold_kernel(const __grid_constant__ PtrList in, int k, void* out,
                                                         int* flag, size_t n) {
-  const float divisor = (float)k;  // reduce.cpp:36
+  const MeanDiv divisor = mean_div(k);  // reduce.cpp:36, 43
   bool bad = false;
   const size_t n8 = n / 8, i = gtid();
   if (i < n8) {
@@ -126,7 +128,7 @@ __global__ void __launch_bounds__(kThreads) fold_kernel(const __grid_constant__ 
       for (int q = 0; q < 8; ++q) acc[q] = __fadd_rn(acc[q], x[q]);
     }
 #pragma unroll
-    for (int q = 0; q < 8; ++q) acc[q] = __fdiv_rn(acc[q], divisor);
+    for (int q = 0; q < 8; ++q) acc[q] = div_mean(acc[q], divisor);
     if (OUT == 1) {
       uint16_t h[8];
 #pragma unroll
@@ -152,7 +154,7 @@ __global__ void __launch_bounds__(kThreads) fold_kernel(const __grid_constant__ 
     const size_t e = n8 * 8 + threadIdx.x;
     float acc = load1<IN>(in.ptr[0], e);
     for (int j = 1; j < k; ++j) acc = __fadd_rn(acc, load1<IN>(in.ptr[j], e));
-    bad |= store1<OUT>(out, e, __fdiv_rn(acc, divisor));
+    bad |= store1<OUT>(out, e, div_mean(acc, divisor));
   }
   if (flag) block_or_flag(bad, flag);
 }
@@ -166,7 +168,7 @@ __global__ void __launch_bounds__(kThreads) fold_push_kernel(const __grid_consta
                                                              const __grid_constant__ PtrList outs, int nout,
                                                              const __grid_constant__ PtrList flags, int nflags,
                                                              size_t n) {
-  const float divisor = (float)k;  // reduce.cpp:36
+  const MeanDiv divisor = mean_div(k);  // reduce.cpp:36, 43
   bool bad = false;
   const size_t n8 = n / 8;
   // grid-stride: a persistent grid of a few CTAs leaves the other SMs to the
@@ -193,7 +195,7 @@ __global__ void __launch_bounds__(kThreads) fold_push_kernel(const __grid_consta
       }
     }
 #pragma unroll
-    for (int q = 0; q < 8; ++q) acc[q] = __fdiv_rn(acc[q], divisor);
+    for (int q = 0; q < 8; ++q) acc[q] = div_mean(acc[q], divisor);
     if (PREC == 1) {
       uint16_t h[8];
 #pragma unroll
@@ -218,7 +220,7 @@ __global__ void __launch_bounds__(kThreads) fold_push_kernel(const __grid_consta
     const size_t e = n8 * 8 + threadIdx.x;
     float acc = load1<PREC>(in.ptr[0], e);
     for (int j = 1; j < k; ++j) acc = __fadd_rn(acc, load1<PREC>(in.ptr[j], e));
-    const float mean = __fdiv_rn(acc, divisor);
+    const float mean = div_mean(acc, divisor);
     for (int o = 0; o < nout; ++o) bad |= store1<PREC>(const_cast<void*>(outs.ptr[o]), e, mean);
   }
   if (__syncthreads_or(bad ? 1 : 0) && threadIdx.x == 0) {
@@ -235,12 +237,15 @@ __global__ void __launch_bounds__(kThreads) fold_push_kernel(const __grid_consta
 // bulk-copy engine (cp.async.bulk) instead of per-thread loads and stores:
 // one elected thread streams 8 KB tiles of the KK inputs (peer memory over
 // NVLink, or local HBM) into a STAGES-deep shared-memory ring, arming an
-// mbarrier with the expected bytes; 128 threads fold the tile in rank order
+// mbarrier with the expected bytes; NT threads fold the tile in rank order
 // into an output tile, which the elected thread bulk-stores into every
 // destination (the owners' mean slots in every rank's gather buffer).  Each CTA
 // keeps STAGES * KK * 8 KB of NVLink reads in flight with a handful of
 // instructions, so a few dozen CTAs saturate the links and leave the SMs to the
 // HBM-bound K2 / K4 pieces.
+// NT (DLC_TMA_THREADS, default kTmaThreads): the fold's decode / add / encode
+// work is latency-bound with one warp per scheduler (ncu: 1.15 IPC per SM at
+// 128 threads), so more warps per CTA shorten the time a stage is held.
 constexpr int kTmaThreads = 128;
 constexpr int kTmaTileBytes = 8192;
 constexpr int kTmaStages = 3;
@@ -291,8 +296,8 @@ __device__ __forceinline__ void bulk_wait_read() {
 
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
-template <int PREC, int KK>
-__global__ void __launch_bounds__(kTmaThreads) fold_push_tma_kernel(const __grid_constant__ PtrList in,
+template <int PREC, int KK, int NT>
+__global__ void __launch_bounds__(NT) fold_push_tma_kernel(const __grid_constant__ PtrList in,
                                                                     const __grid_constant__ PtrList outs, int nout,
                                                                     const __grid_constant__ PtrList flags,
                                                                     int nflags, size_t n) {
@@ -302,7 +307,7 @@ __global__ void __launch_bounds__(kTmaThreads) fold_push_tma_kernel(const __grid
   uint8_t* in_buf = smem;                                          // [STAGES][KK][8 KB]
   uint8_t* out_buf = smem + kTmaStages * KK * kTmaTileBytes;       // [STAGES][8 KB]
   uint64_t* bar = reinterpret_cast<uint64_t*>(out_buf + kTmaStages * kTmaTileBytes);  // [STAGES]
-  const float divisor = (float)KK;  // reduce.cpp:36
+  constexpr MeanDiv divisor = {(float)KK, (KK & (KK - 1)) == 0 ? 1.0f / KK : 0.0f};  // reduce.cpp:36, 43
   const size_t ntiles = (n + TILE - 1) / TILE;
   const size_t mine = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const bool leader = threadIdx.x == 0;
@@ -338,7 +343,7 @@ __global__ void __launch_bounds__(kTmaThreads) fold_push_tma_kernel(const __grid
     mbar_wait(&bar[st], (uint32_t)((i / kTmaStages) & 1));
     const uint8_t* src = in_buf + (size_t)st * KK * kTmaTileBytes;
     uint8_t* dst = out_buf + (size_t)st * kTmaTileBytes;
-    for (uint32_t off = threadIdx.x * 16; off < bytes; off += kTmaThreads * 16) {  // 16 B per thread and step
+    for (uint32_t off = threadIdx.x * 16; off < bytes; off += NT * 16) {  // 16 B per thread and step
       constexpr int E = 16 / W;  // 8 FP16 or 4 FP32 elements
       float acc[E], x[E];
 #pragma unroll
@@ -361,7 +366,7 @@ __global__ void __launch_bounds__(kTmaThreads) fold_push_tma_kernel(const __grid
         uint16_t h[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          h[q] = fp16_encode(__fdiv_rn(acc[q], divisor));
+          h[q] = fp16_encode(div_mean(acc[q], divisor));
           bad |= fp16_nonfinite(h[q]);
         }
         o = make_uint4(pack2(h[0], h[1]), pack2(h[2], h[3]), pack2(h[4], h[5]), pack2(h[6], h[7]));
@@ -369,7 +374,7 @@ __global__ void __launch_bounds__(kTmaThreads) fold_push_tma_kernel(const __grid
         float m[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          m[q] = __fdiv_rn(acc[q], divisor);
+          m[q] = div_mean(acc[q], divisor);
           bad |= !finite_f(m[q]);
         }
         o = make_uint4(__float_as_uint(m[0]), __float_as_uint(m[1]), __float_as_uint(m[2]), __float_as_uint(m[3]));
@@ -485,24 +490,37 @@ void launch_fold_push(const PtrList& in, int k, int precision, const PtrList& ou
 #undef DLC_FOLD_PUSH
 }
 
+// DLC_TMA_THREADS: 128, 256 or 512 threads per TMA fold CTA.
+static int tma_threads() {
+  const char* v = std::getenv("DLC_TMA_THREADS");
+  return v ? (int)std::strtol(v, nullptr, 10) : kTmaThreads;
+}
+
 bool launch_fold_push_tma(const PtrList& in, int k, int precision, const PtrList& outs, int nout,
                           const PtrList& flags, int nflags, size_t n, int ctas, cudaStream_t s) {
   const size_t smem = fold_push_tma_smem(k);
+  const int nt = tma_threads();
   const int W = precision == 1 ? 2 : 4;
   const size_t ntiles = (n + kTmaTileBytes / W - 1) / (kTmaTileBytes / W);
   const int grid = (int)std::max<size_t>(1, std::min<size_t>(ctas > 0 ? ctas : num_sms(), ntiles));
-#define DLC_TMA(P, KK)                                                                                   \
+#define DLC_TMA_NT(P, KK, NT)                                                                            \
   {                                                                                                      \
     static unsigned attr_devices = 0; /* per-device function attribute, set once */                      \
     int dev = 0;                                                                                         \
     cudaGetDevice(&dev);                                                                                 \
     if (!(attr_devices & (1u << (dev & 31)))) {                                                          \
-      cudaFuncSetAttribute(fold_push_tma_kernel<P, KK>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+      cudaFuncSetAttribute(fold_push_tma_kernel<P, KK, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                            (int)fold_push_tma_smem(KK));                                                 \
       attr_devices |= 1u << (dev & 31);                                                                  \
     }                                                                                                    \
-    fold_push_tma_kernel<P, KK><<<grid, kTmaThreads, smem, s>>>(in, outs, nout, flags, nflags, n);               \
+    fold_push_tma_kernel<P, KK, NT><<<grid, NT, smem, s>>>(in, outs, nout, flags, nflags, n);            \
     return true;                                                                                         \
+  }
+#define DLC_TMA(P, KK)                          \
+  {                                             \
+    if (nt >= 512) DLC_TMA_NT(P, KK, 512)       \
+    if (nt >= 256) DLC_TMA_NT(P, KK, 256)       \
+    DLC_TMA_NT(P, KK, 128)                      \
   }
 #define DLC_TMA_K(P)             \
   switch (k) {                   \
@@ -522,6 +540,7 @@ bool launch_fold_push_tma(const PtrList& in, int k, int precision, const PtrList
   }
 #undef DLC_TMA_K
 #undef DLC_TMA
+#undef DLC_TMA_NT
 }
 
 void launch_scatter_push(const PtrList& src, const PtrList& dst, int nrow, size_t bytes, int ctas, cudaStream_t s) {

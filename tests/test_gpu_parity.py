@@ -642,6 +642,17 @@ def test_fold_push_kernels_every_world_size(port, prec, tma):
         assert bool(bad.value) == (not np.all(np.isfinite(want))), k
 
 
+@pytest.mark.parametrize("k", [2, 8, 9])
+def test_p2p_kernels_probe_runs(k):
+    """The single-device probe of the K > 1 kernels (tools/p2p_kernels_probe.py)
+    launches K2, the owner fold (TMA for k <= 8, per-thread above) and K4 on a
+    ragged size and reports a positive time for each."""
+    ms = (C.c_float * 3)()
+    assert A.lib.dlc_p2p_kernels_probe(k, 1_000_003, 1, 2, ms) == 0, A.lib.dlc_last_error()
+    assert all(t > 0 for t in ms)
+    assert A.lib.dlc_p2p_kernels_probe(1, 1024, 1, 1, ms) == A.EINVAL
+
+
 def test_fp16_reduction_bounds(port):
     """test_engine.cpp:296-324 on the device: the FP16 average stays within
     2^-10 of the FP32 one, relative to the result for same-sign contributions

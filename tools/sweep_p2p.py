@@ -37,13 +37,14 @@ def main():
     for i, x in enumerate(xs):
         eng.rng_perturb(4242, "local", r.rank * 16 + i, -1e-3, 1e-3, dst_dev_ptr=x.data_ptr())
     stream = torch.cuda.ExternalStream(eng.stream, device=f"cuda:{r.local}")
-    configs = [("ordered", None, None, None, None, 0, 0)]
+    configs = [("ordered", None, None, None, None, 0, 0, 128)]
     movers = os.environ.get("SWEEP_MOVERS", "sm,ce").split(",")
     pieces_l = [int(x) for x in os.environ.get("SWEEP_PIECES", "1,2,4,8").split(",")]
     ctas_l = [int(x) for x in os.environ.get("SWEEP_CTAS", "0,32,64,128,256").split(",")]
     barriers = os.environ.get("SWEEP_BARRIERS", "flag").split(",")
     piece_ctas_l = [int(x) for x in os.environ.get("SWEEP_PIECE_CTAS", "0").split(",")]
     tma_l = [int(x) for x in os.environ.get("SWEEP_TMA_CTAS", "0").split(",")]  # 0: per-thread fold
+    tthr_l = [int(x) for x in os.environ.get("SWEEP_TMA_THREADS", "128").split(",")]
     plans = os.environ.get("SWEEP_PLANS", "").split(";") if os.environ.get("SWEEP_PLANS") else None
     for barrier in barriers:
         for mover in movers:
@@ -51,12 +52,17 @@ def main():
                 for ctas in (ctas_l if mover in ("sm", "push", "push2") else (0,)):
                     for pc in piece_ctas_l:
                         for tc in tma_l:
-                            configs.append(("p2p", mover, pieces, ctas, barrier, pc, tc))
+                            for tt in tthr_l:
+                                configs.append(("p2p", mover, pieces, ctas, barrier, pc, tc, tt))
     results = []
-    for mode, mover, pieces, ctas, barrier, pc, tc in configs:
+    for mode, mover, pieces, ctas, barrier, pc, tc, tt in configs:
+        os.environ["DLC_TMA_THREADS"] = str(tt)
         os.environ["DLC_P2P_PIECE_CTAS"] = str(pc)
-        os.environ["DLC_FOLD_TMA"] = "1" if tc else "0"
-        os.environ["DLC_TMA_CTAS"] = str(tc)
+        os.environ["DLC_FOLD_TMA"] = "1" if tc else "0"  # tc < 0: TMA fold, default CTA count
+        if tc > 0:
+            os.environ["DLC_TMA_CTAS"] = str(tc)
+        else:
+            os.environ.pop("DLC_TMA_CTAS", None)
         if mover:
             os.environ["DLC_P2P_COPY"] = mover
             if isinstance(pieces, str):
@@ -79,7 +85,7 @@ def main():
         e1.synchronize()
         ms = PD.max_over_ranks(e0.elapsed_time(e1) / a.steps, r.world)
         results.append({"mode": mode, "mover": mover, "pieces": pieces, "ctas": ctas, "barrier": barrier,
-                        "piece_ctas": pc, "tma_ctas": tc, "ms": ms})
+                        "piece_ctas": pc, "tma_ctas": tc, "tma_threads": tt, "ms": ms})
         if r.rank == 0:
             print(json.dumps(results[-1]), flush=True)
     eng.close()
