@@ -360,13 +360,29 @@ def run_ours(args):
         line["phase_roofline"] = {"outer_solo_K2K4": rl["frac"]}
     else:
         rl = roof(b_k4, k4_ms)
-        rl["kernel"] = "nesterov_outer%s_kernel (K4)" % ("_p2p" if mode == D.MODE_P2P else "")
+        rl["kernel"] = ("nesterov_p2p_piece_kernel (K4)" if mode == D.MODE_P2P else "nesterov_outer_kernel (K4)")
         line["phases_ms"] = {"pseudo_grad_K2": k2_ms, "collective_C1_K3": coll_ms, "nesterov_K4": k4_ms}
         line["phase_roofline"] = {"pseudo_grad_K2": roof(b_k2, k2_ms)["frac"], "nesterov_K4": rl["frac"]}
-    rl["traffic"] = ncu_traffic("outer_solo_kernel" if k == 1 else "nesterov_", n)
-    if k > 1 and rl["traffic"] is not None:
-        rl["traffic"] = None  # the committed capture is single-GPU; multi-rank ncu is not run
+    if k == 1:
+        rl["traffic"] = ncu_traffic("outer_solo_kernel", n)
+    elif mode == D.MODE_P2P:
+        # multi-rank runs cannot be profiled: the capture is the same kernel over all N
+        # params on one GPU (tools/p2p_kernels_probe.py), i.e. one step's pieces
+        rl["traffic"] = ncu_traffic("nesterov_p2p_piece_kernel<%d>" % (1 if prec == D.FP16 else 0), n)
+        rl["traffic_source"] = "ncu of the kernel alone on one GPU (tools/p2p_kernels_probe.py)"
+    else:
+        rl["traffic"] = None
     line["roofline"] = rl
+    if k > 1 and mode == D.MODE_P2P and rank == 0:
+        # the same kernels alone on this GPU (no exchange traffic sharing HBM): each
+        # kernel's own ceiling, against which the in-step phase_roofline is read
+        import ctypes
+        ms3 = (ctypes.c_float * 3)()
+        if D.lib.dlc_p2p_kernels_probe(k, n, prec, 3, ms3) == 0:
+            line["kernels_alone"] = {
+                name: {"ms": t, "bytes_per_param": bpp, "frac": roof(bpp, t)["frac"]}
+                for name, bpp, t in (("pseudo_grad_K2", b_k2, ms3[0]), ("fold_push", 2 * wire, ms3[1]),
+                                     ("nesterov_K4", 16 + wire, ms3[2]))}
     # whole-step roofline: HBM bytes at the measured copy peak and
     # NVLink bytes per direction at the pool's measured 770 GB/s peer copy
     # (B200_PROFILING.md); serial = sum, bound = max (perfect overlap).

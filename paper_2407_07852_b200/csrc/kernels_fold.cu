@@ -3,6 +3,7 @@
 // push of the mean to every rank (per-thread and TMA bulk-copy versions), the
 // push/push scatter, and the NVLink flag barrier of the P2P step.
 #include <algorithm>
+#include <atomic>
 #include <mutex>
 #include <unordered_map>
 
@@ -505,13 +506,14 @@ bool launch_fold_push_tma(const PtrList& in, int k, int precision, const PtrList
   const int grid = (int)std::max<size_t>(1, std::min<size_t>(ctas > 0 ? ctas : num_sms(), ntiles));
 #define DLC_TMA_NT(P, KK, NT)                                                                            \
   {                                                                                                      \
-    static unsigned attr_devices = 0; /* per-device function attribute, set once */                      \
+    /* per-device function attribute, set once (rank threads may launch concurrently) */                \
+    static std::atomic<unsigned> attr_devices{0};                                                        \
     int dev = 0;                                                                                         \
     cudaGetDevice(&dev);                                                                                 \
-    if (!(attr_devices & (1u << (dev & 31)))) {                                                          \
+    if (!(attr_devices.load() & (1u << (dev & 31)))) {                                                   \
       cudaFuncSetAttribute(fold_push_tma_kernel<P, KK, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                           (int)fold_push_tma_smem(KK));                                                 \
-      attr_devices |= 1u << (dev & 31);                                                                  \
+                           (int)fold_push_tma_smem(KK)); /* a failure surfaces as the launch error */    \
+      attr_devices.fetch_or(1u << (dev & 31));                                                           \
     }                                                                                                    \
     fold_push_tma_kernel<P, KK, NT><<<grid, NT, smem, s>>>(in, outs, nout, flags, nflags, n);            \
     return true;                                                                                         \
