@@ -301,14 +301,13 @@ template <int PREC, int KK, int NT>
 __global__ void __launch_bounds__(NT) fold_push_tma_kernel(const __grid_constant__ PtrList in,
                                                                     const __grid_constant__ PtrList outs, int nout,
                                                                     const __grid_constant__ PtrList flags,
-                                                                    int nflags, size_t n) {
+                                                                    int nflags, size_t n, MeanDiv divisor) {
   constexpr int W = PREC == 1 ? 2 : 4;
   constexpr int TILE = kTmaTileBytes / W;  // elements per tile
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* in_buf = smem;                                          // [STAGES][KK][8 KB]
   uint8_t* out_buf = smem + kTmaStages * KK * kTmaTileBytes;       // [STAGES][8 KB]
   uint64_t* bar = reinterpret_cast<uint64_t*>(out_buf + kTmaStages * kTmaTileBytes);  // [STAGES]
-  constexpr MeanDiv divisor = {(float)KK, (KK & (KK - 1)) == 0 ? 1.0f / KK : 0.0f};  // reduce.cpp:36, 43
   const size_t ntiles = (n + TILE - 1) / TILE;
   const size_t mine = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const bool leader = threadIdx.x == 0;
@@ -501,6 +500,9 @@ bool launch_fold_push_tma(const PtrList& in, int k, int precision, const PtrList
                           const PtrList& flags, int nflags, size_t n, int ctas, cudaStream_t s) {
   const size_t smem = fold_push_tma_smem(k);
   const int nt = tma_threads();
+  // reduce.cpp:36, 43; DLC_FOLD_DIV=1 keeps the IEEE division for power-of-two K too (A/B knob)
+  MeanDiv md = mean_div(k);
+  if (const char* v = std::getenv("DLC_FOLD_DIV"); v && v[0] == '1') md.inv = 0.0f;
   const int W = precision == 1 ? 2 : 4;
   const size_t ntiles = (n + kTmaTileBytes / W - 1) / (kTmaTileBytes / W);
   const int grid = (int)std::max<size_t>(1, std::min<size_t>(ctas > 0 ? ctas : num_sms(), ntiles));
@@ -515,7 +517,7 @@ bool launch_fold_push_tma(const PtrList& in, int k, int precision, const PtrList
                            (int)fold_push_tma_smem(KK)); /* a failure surfaces as the launch error */    \
       attr_devices.fetch_or(1u << (dev & 31));                                                           \
     }                                                                                                    \
-    fold_push_tma_kernel<P, KK, NT><<<grid, NT, smem, s>>>(in, outs, nout, flags, nflags, n);            \
+    fold_push_tma_kernel<P, KK, NT><<<grid, NT, smem, s>>>(in, outs, nout, flags, nflags, n, md);        \
     return true;                                                                                         \
   }
 #define DLC_TMA(P, KK)                          \

@@ -37,7 +37,7 @@ def main():
     for i, x in enumerate(xs):
         eng.rng_perturb(4242, "local", r.rank * 16 + i, -1e-3, 1e-3, dst_dev_ptr=x.data_ptr())
     stream = torch.cuda.ExternalStream(eng.stream, device=f"cuda:{r.local}")
-    configs = [("ordered", None, None, None, None, 0, 0, 128)]
+    configs = [("ordered", None, None, None, None, 0, 0, 128, "")]
     movers = os.environ.get("SWEEP_MOVERS", "sm,ce").split(",")
     pieces_l = [int(x) for x in os.environ.get("SWEEP_PIECES", "1,2,4,8").split(",")]
     ctas_l = [int(x) for x in os.environ.get("SWEEP_CTAS", "0,32,64,128,256").split(",")]
@@ -45,6 +45,8 @@ def main():
     piece_ctas_l = [int(x) for x in os.environ.get("SWEEP_PIECE_CTAS", "0").split(",")]
     tma_l = [int(x) for x in os.environ.get("SWEEP_TMA_CTAS", "0").split(",")]  # 0: per-thread fold
     tthr_l = [int(x) for x in os.environ.get("SWEEP_TMA_THREADS", "128").split(",")]
+    # SWEEP_ENV="A=1,B=2;A=0": extra environment per config; SWEEP_REPEAT: interleaved repeats (A/B)
+    env_l = os.environ.get("SWEEP_ENV", "").split(";")
     plans = os.environ.get("SWEEP_PLANS", "").split(";") if os.environ.get("SWEEP_PLANS") else None
     for barrier in barriers:
         for mover in movers:
@@ -53,9 +55,14 @@ def main():
                     for pc in piece_ctas_l:
                         for tc in tma_l:
                             for tt in tthr_l:
-                                configs.append(("p2p", mover, pieces, ctas, barrier, pc, tc, tt))
+                                for ev in env_l:
+                                    configs.append(("p2p", mover, pieces, ctas, barrier, pc, tc, tt, ev))
+    configs = configs * int(os.environ.get("SWEEP_REPEAT", "1"))
     results = []
-    for mode, mover, pieces, ctas, barrier, pc, tc, tt in configs:
+    for mode, mover, pieces, ctas, barrier, pc, tc, tt, ev in configs:
+        for kv in filter(None, ev.split(",")):
+            key, val = kv.split("=", 1)
+            os.environ[key] = val
         os.environ["DLC_TMA_THREADS"] = str(tt)
         os.environ["DLC_P2P_PIECE_CTAS"] = str(pc)
         os.environ["DLC_FOLD_TMA"] = "1" if tc else "0"  # tc < 0: TMA fold, default CTA count
@@ -85,7 +92,7 @@ def main():
         e1.synchronize()
         ms = PD.max_over_ranks(e0.elapsed_time(e1) / a.steps, r.world)
         results.append({"mode": mode, "mover": mover, "pieces": pieces, "ctas": ctas, "barrier": barrier,
-                        "piece_ctas": pc, "tma_ctas": tc, "tma_threads": tt, "ms": ms})
+                        "piece_ctas": pc, "tma_ctas": tc, "tma_threads": tt, "env": ev, "ms": ms})
         if r.rank == 0:
             print(json.dumps(results[-1]), flush=True)
     eng.close()
