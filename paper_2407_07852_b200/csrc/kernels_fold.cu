@@ -490,16 +490,23 @@ void launch_fold_push(const PtrList& in, int k, int precision, const PtrList& ou
 #undef DLC_FOLD_PUSH
 }
 
-// DLC_TMA_THREADS: 128, 256 or 512 threads per TMA fold CTA.
-static int tma_threads() {
-  const char* v = std::getenv("DLC_TMA_THREADS");
-  return v ? (int)std::strtol(v, nullptr, 10) : kTmaThreads;
+// DLC_TMA_THREADS: 128, 256 or 512 threads per TMA fold CTA.  Default by K:
+// an owner decodes about N contributions per step whatever K is, but the CTA
+// count falls as 320 / K (the in-flight bytes rule), so the fold needs more
+// warps per CTA as K grows.  At K = 4 the 4-GPU A/B put the optimum at about
+// 80 "128-thread CTA equivalents" (80 x 128 or 48 x 512; 48 x 128 and 64 x 128
+// were 20% / 12% slower, profiles/r1_ab_tma_threads_ctas_4gpu.log); K >= 5 keeps
+// that capacity with 256 / 512 threads.  K >= 5 is extrapolated: this pool's
+// boxes have at most 4 GPUs.
+static int tma_threads(int k) {
+  if (const char* v = std::getenv("DLC_TMA_THREADS")) return (int)std::strtol(v, nullptr, 10);
+  return k <= 4 ? kTmaThreads : (k <= 6 ? 256 : 512);
 }
 
 bool launch_fold_push_tma(const PtrList& in, int k, int precision, const PtrList& outs, int nout,
                           const PtrList& flags, int nflags, size_t n, int ctas, cudaStream_t s) {
   const size_t smem = fold_push_tma_smem(k);
-  const int nt = tma_threads();
+  const int nt = tma_threads(k);
   // reduce.cpp:36, 43; DLC_FOLD_DIV=1 keeps the IEEE division for power-of-two K too (A/B knob)
   MeanDiv md = mean_div(k);
   if (const char* v = std::getenv("DLC_FOLD_DIV"); v && v[0] == '1') md.inv = 0.0f;
