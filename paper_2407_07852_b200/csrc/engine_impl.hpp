@@ -134,7 +134,10 @@ constexpr size_t kMaxPieces = 8;
 // ---- engine_util.cu ----
 void* dalloc(dlc_engine* e, size_t bytes);
 size_t p2p_pieces();
-std::vector<size_t> piece_plan(size_t S);
+// host_path: the e2e call with host buffers, where the step is PCIe-bound and
+// the pipeline fill / drain is one piece of H2D / D2H: 16 equal pieces unless
+// DLC_P2P_PLAN / DLC_P2P_PIECES say otherwise.
+std::vector<size_t> piece_plan(size_t S, bool host_path = false);
 bool p2p_mover_sm();
 bool p2p_mover_push();
 bool p2p_mover_push2();

@@ -206,7 +206,7 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
       DLC_CUDA(cudaStreamCreateWithFlags(&e->gath[j], cudaStreamNonBlocking));
     }
   }
-  const std::vector<size_t> pb = piece_plan(S);  // piece boundaries inside a slot
+  const std::vector<size_t> pb = piece_plan(S, hsrc != nullptr);  // piece boundaries inside a slot
   const size_t P = pb.size() - 1;
   auto po = [&](size_t p) { return pb[p]; };
   auto pl = [&](size_t p) { return pb[p + 1] - pb[p]; };
@@ -248,8 +248,12 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
     ensure_copy_streams(e);
     DLC_CUDA(cudaStreamWaitEvent(e->h2d, evStart, 0));  // staging buffer free
   }
-  phase_begin(e);
-  for (size_t p = 0; p < P; ++p) {
+  const bool sm_mover = p2p_mover_sm();
+  const bool push2 = p2p_mover_push2();
+  const bool k4_pull = sm_mover && p2p_k4_pull();
+  const bool merge = p2p_merge_barriers();
+  cudaEvent_t* evS = evA;  // (evA is only used by the copy-engine mover)
+  auto k2_piece = [&](size_t p) {
     if (hsrc) {
       rows(p, [&](size_t lo, size_t len) {
         DLC_CUDA(cudaMemcpyAsync(s + lo, hsrc + lo, len * sizeof(float), cudaMemcpyHostToDevice, e->h2d));
@@ -268,18 +272,8 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
     }
     trace_end(e, e->stream, "K2", (int)p, t0);
     DLC_CUDA(cudaEventRecord(evK2[p], e->stream));
-  }
-  launched("pseudo_grad_piece");
-  phase_end(e, DLC_PHASE_PSEUDO);
-  DLC_CUDA(cudaStreamWaitEvent(e->cstream, evStart, 0));
-  cudaEvent_t c0 = pooled_event(e), c1 = pooled_event(e);
-  DLC_CUDA(cudaEventRecord(c0, e->cstream));
-  const bool sm_mover = p2p_mover_sm();
-  const bool push2 = p2p_mover_push2();
-  const bool k4_pull = sm_mover && p2p_k4_pull();
-  const bool merge = p2p_merge_barriers();
-  cudaEvent_t* evS = evA;  // (evA is only used by the copy-engine mover)
-  for (size_t p = 0; p < P && push2; ++p) {
+  };
+  auto scatter_piece = [&](size_t p) {
     // push/push: our piece of every foreign slot into its owner's recv row r, on
     // its own stream so that scatter(p + 1) overlaps fold(p): every NVLink byte
     // is a remote store and both link directions stay busy
@@ -296,43 +290,44 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
     launch_scatter_push(src, dst, nrow, pl(p) * w, comm_ctas(), e->sstream);
     trace_end(e, e->sstream, "scatter", (int)p, ts);
     DLC_CUDA(cudaEventRecord(evS[p], e->sstream));
-  }
-  for (size_t p = 0; p < P && sm_mover; ++p) {
-    // SM mover: a persistent fold kernel on a few CTAs pulls slot r / piece p of
-    // every rank's delta and pushes the mean (and a non-finite mark) into slot r
-    // of every rank's gather buffer (flags reset by each rank before its K2(0)).
-    DLC_CUDA(cudaStreamWaitEvent(e->cstream, push2 ? evS[p] : evK2[p], 0));
-    if (!merge || p == 0) {
-      cudaEvent_t ta = trace_begin(e, e->cstream);
-      p2p_barrier(e, c, e->cstream);  // A_p
-      trace_end(e, e->cstream, "barrierA", (int)p, ta);
+  };
+  auto fold_piece = [&](size_t p) {
+    if (sm_mover) {
+      // SM mover: a persistent fold kernel on a few CTAs pulls slot r / piece p of
+      // every rank's delta and pushes the mean (and a non-finite mark) into slot r
+      // of every rank's gather buffer (flags reset by each rank before its K2(0)).
+      DLC_CUDA(cudaStreamWaitEvent(e->cstream, push2 ? evS[p] : evK2[p], 0));
+      if (!merge || p == 0) {
+        cudaEvent_t ta = trace_begin(e, e->cstream);
+        p2p_barrier(e, c, e->cstream);  // A_p
+        trace_end(e, e->cstream, "barrierA", (int)p, ta);
+      }
+      PtrList in{}, outs{}, pfl{};
+      for (size_t j = 0; j < K; ++j) {
+        in.ptr[j] = (int)j == r && push2 ? send + (r * S + po(p)) * w  // own row stays local
+                    : (push_mover || push2) ? recv + (j * S + po(p)) * w   // rows already pushed here
+                                            : static_cast<char*>(e->peer_send[j]) + (r * S + po(p)) * w;
+        outs.ptr[j] = static_cast<char*>(e->peer_gather[j]) + (r * S + po(p)) * w;
+        pfl.ptr[j] = e->peer_flags[j] + r;
+      }
+      cudaEvent_t tf = trace_begin(e, e->cstream);
+      // K4 pull: the mean stays in the owner's own gather slot; every rank's K4
+      // reads it from there over NVLink (no remote stores of means)
+      const int nout = k4_pull ? 1 : (int)K;
+      if (k4_pull) outs.ptr[0] = gather + (r * S + po(p)) * w;
+      if (!(fold_tma() && launch_fold_push_tma(in, (int)K, e->prec, outs, nout, pfl, (int)K, pl(p), tma_ctas(K),
+                                               e->cstream)))
+        launch_fold_push(in, (int)K, e->prec, outs, nout, pfl, (int)K, pl(p), comm_ctas(), e->cstream);
+      trace_end(e, e->cstream, "fold_push", (int)p, tf);
+      // merged barriers: B_p also serves as A_{p+1} once our K2(p+1) is done
+      // (it precedes K4(p) on the main stream anyway, so K4(p) waits no longer)
+      if (merge && p + 1 < P) DLC_CUDA(cudaStreamWaitEvent(e->cstream, push2 ? evS[p + 1] : evK2[p + 1], 0));
+      cudaEvent_t tb = trace_begin(e, e->cstream);
+      p2p_barrier(e, c, e->cstream);  // B_p
+      trace_end(e, e->cstream, "barrierB", (int)p, tb);
+      DLC_CUDA(cudaEventRecord(evB[p], e->cstream));
+      return;
     }
-    PtrList in{}, outs{}, pfl{};
-    for (size_t j = 0; j < K; ++j) {
-      in.ptr[j] = (int)j == r && push2 ? send + (r * S + po(p)) * w  // own row stays local
-                  : (push_mover || push2) ? recv + (j * S + po(p)) * w   // rows already pushed here
-                                          : static_cast<char*>(e->peer_send[j]) + (r * S + po(p)) * w;
-      outs.ptr[j] = static_cast<char*>(e->peer_gather[j]) + (r * S + po(p)) * w;
-      pfl.ptr[j] = e->peer_flags[j] + r;
-    }
-    cudaEvent_t tf = trace_begin(e, e->cstream);
-    // K4 pull: the mean stays in the owner's own gather slot; every rank's K4
-    // reads it from there over NVLink (no remote stores of means)
-    const int nout = k4_pull ? 1 : (int)K;
-    if (k4_pull) outs.ptr[0] = gather + (r * S + po(p)) * w;
-    if (!(fold_tma() && launch_fold_push_tma(in, (int)K, e->prec, outs, nout, pfl, (int)K, pl(p), tma_ctas(K),
-                                             e->cstream)))
-      launch_fold_push(in, (int)K, e->prec, outs, nout, pfl, (int)K, pl(p), comm_ctas(), e->cstream);
-    trace_end(e, e->cstream, "fold_push", (int)p, tf);
-    // merged barriers: B_p also serves as A_{p+1} once our K2(p+1) is done
-    // (it precedes K4(p) on the main stream anyway, so K4(p) waits no longer)
-    if (merge && p + 1 < P) DLC_CUDA(cudaStreamWaitEvent(e->cstream, push2 ? evS[p + 1] : evK2[p + 1], 0));
-    cudaEvent_t tb = trace_begin(e, e->cstream);
-    p2p_barrier(e, c, e->cstream);  // B_p
-    trace_end(e, e->cstream, "barrierB", (int)p, tb);
-    DLC_CUDA(cudaEventRecord(evB[p], e->cstream));
-  }
-  for (size_t p = 0; p < P && !sm_mover; ++p) {
     DLC_CUDA(cudaStreamWaitEvent(e->cstream, evK2[p], 0));
     p2p_barrier(e, c, e->cstream);  // A_p
     if (p == 0) DLC_CUDA(cudaMemsetAsync(e->flags + r, 0, sizeof(int), e->cstream));
@@ -359,16 +354,7 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
                                cudaMemcpyDefault, e->gath[q]));
       DLC_CUDA(cudaEventRecord(evGath[q * P + p], e->gath[q]));
     }
-  }
-  launched("fold_p2p");
-  DLC_CUDA(cudaEventRecord(c1, e->cstream));
-  if (e->timing) {
-    e->pending.push_back({DLC_PHASE_COLLECTIVE, c0, c1});
-  } else {
-    e->pool.push_back(c0);
-    e->pool.push_back(c1);
-  }
-  if (rep) DLC_CUDA(cudaEventRecord(e->ev1, e->cstream));
+  };
   // K4 pieces on the local gather buffer, speculative into the idle theta_t / momentum
   PtrList slots{}, fl{};
   for (size_t q = 0; q < K; ++q) {
@@ -377,8 +363,7 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
     // q's flag lives in owner q's memory
     fl.ptr[q] = sm_mover ? e->flags + q : e->peer_flags[q] + q;
   }
-  phase_begin(e);
-  for (size_t p = 0; p < P; ++p) {
+  auto k4_piece = [&](size_t p) {
     DLC_CUDA(cudaStreamWaitEvent(e->stream, evB[p], 0));
     for (size_t q = 0; q < K && !sm_mover; ++q)
       if ((int)q != r) DLC_CUDA(cudaStreamWaitEvent(e->stream, evGath[q * P + p], 0));
@@ -394,6 +379,56 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
                                  cudaMemcpyDeviceToHost, e->d2h));
       });
     }
+  };
+  cudaEvent_t c0 = pooled_event(e), c1 = pooled_event(e);
+  auto fold_begin = [&] {
+    DLC_CUDA(cudaStreamWaitEvent(e->cstream, evStart, 0));
+    DLC_CUDA(cudaEventRecord(c0, e->cstream));
+  };
+  auto fold_end = [&] {
+    launched("fold_p2p");
+    DLC_CUDA(cudaEventRecord(c1, e->cstream));
+    if (e->timing) {
+      e->pending.push_back({DLC_PHASE_COLLECTIVE, c0, c1});
+    } else {
+      e->pool.push_back(c0);
+      e->pool.push_back(c1);
+    }
+    if (rep) DLC_CUDA(cudaEventRecord(e->ev1, e->cstream));
+  };
+  if (!hsrc) {
+    // device buffers: every K2 piece first (the folds of the early pieces run
+    // beside the later K2 pieces), then the K4 pieces as their means land
+    phase_begin(e);
+    for (size_t p = 0; p < P; ++p) k2_piece(p);
+    launched("pseudo_grad_piece");
+    phase_end(e, DLC_PHASE_PSEUDO);
+    fold_begin();
+    for (size_t p = 0; p < P && push2; ++p) scatter_piece(p);
+    for (size_t p = 0; p < P; ++p) fold_piece(p);
+    fold_end();
+    phase_begin(e);
+    for (size_t p = 0; p < P; ++p) k4_piece(p);
+  } else {
+    // host buffers: K2(p+1) then K4(p) on the engine stream, so the D2H of
+    // piece p's new theta_t starts while later pieces are still arriving (H2D
+    // and D2H overlap on the two copy streams instead of running back to back).
+    // Issue order keeps every event recorded before a stream waits on it: the
+    // merged barrier after fold(p) waits on K2(p + 1), K4(p) on fold(p).
+    phase_begin(e);
+    k2_piece(0);
+    if (push2) scatter_piece(0);
+    fold_begin();
+    for (size_t p = 0; p < P; ++p) {
+      if (p + 1 < P) {
+        k2_piece(p + 1);
+        if (push2) scatter_piece(p + 1);
+      }
+      fold_piece(p);
+      k4_piece(p);
+    }
+    launched("pseudo_grad_piece");
+    fold_end();
   }
   launch_p2p_finish(tt_pair(e), local_pair(e), fl, (int)K, e->st, n, flag_barriers(c) ? e->sig_err : nullptr,
                     e->stream);

@@ -143,6 +143,20 @@ def main():
             else:
                 assert np.max(np.abs(out_t - ws[r.rank].theta_t)) <= 1e-3
             e2.close()
+        # e2e host path with a non-finite delta on the last rank: the step is skipped
+        # everywhere and the returned theta_t is the unchanged one (engine.cpp:136-144)
+        n2 = 30_001
+        th = O.rng_fill(6, "theta", 0, n2, -1, 1)
+        loc = (th - O.rng_fill(6, "local", r.rank, n2, -1e-3, 1e-3)).astype(np.float32)
+        if r.rank == k - 1:
+            loc[n2 // 2] = np.inf
+        e2 = D.DilocoEngine(D.DilocoConfig(1, k, D.FP16, 1), D.OptimHyperparams(), n2, r.local)
+        e2.upload(D.THETA_T, th)
+        out_t = np.full(n2, np.nan, np.float32)
+        res = e2.outer_step_host(coll, loc, out_t)
+        assert not res.applied and res.outer_epoch == 1, (mode_name, res)
+        assert np.array_equal(bits(out_t), bits(th)), mode_name
+        e2.close()
         # host-buffer plugin call (Collective::all_reduce_avg) vs reduce_average in rank order
         for prec in (D.FP32, D.FP16):
             deltas = [O.rng_fill(9, "delta", j, 10_007, -1, 1) for j in range(k)]
