@@ -396,7 +396,8 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
     }
     if (rep) DLC_CUDA(cudaEventRecord(e->ev1, e->cstream));
   };
-  if (!hsrc) {
+  const char* il = std::getenv("DLC_P2P_INTERLEAVE");  // device buffers: A/B knob (default 0)
+  if (!hsrc && !(il && il[0] == '1')) {
     // device buffers: every K2 piece first (the folds of the early pieces run
     // beside the later K2 pieces), then the K4 pieces as their means land
     phase_begin(e);
