@@ -89,3 +89,20 @@ def test_gloo_world(world):
     for p in procs:
         p.join(timeout=60)
     assert all(v == "ok" for v in results.values()), results
+
+
+def test_gpu_local_memory_is_a_noop_without_nvml_or_when_disabled(monkeypatch):
+    """dist.gpu_local_memory: with DLC_NUMA_BIND=0, or where NVML cannot answer (this
+    container has no driver), the body runs with the caller's affinity untouched."""
+    from paper_2407_07852_b200 import dist as PD
+    before = os.sched_getaffinity(0)
+    monkeypatch.setenv("DLC_NUMA_BIND", "0")
+    with PD.gpu_local_memory(0) as cpus:
+        assert cpus is None and os.sched_getaffinity(0) == before
+    monkeypatch.delenv("DLC_NUMA_BIND")
+    with PD.gpu_local_memory(0) as cpus:
+        if cpus is None:
+            assert os.sched_getaffinity(0) == before
+        else:  # a GPU host: pinned to the GPU-local CPUs inside, restored after
+            assert os.sched_getaffinity(0) == set(cpus)
+    assert os.sched_getaffinity(0) == before
