@@ -337,7 +337,9 @@ def run_ours(args):
     follow = args.inner_mode == "pingpong"
     b_solo = 20 if follow else 24
     b_k1, b_k2, b_k4 = 28, 8 + wire, (16 if follow else 20) + wire
-    k4_ms = max_over_ranks(ph_ms[3] / max(ph_n[3], 1))
+    # per step: the summed intervals (K > 1 P2P times every K4 piece launch and the
+    # finish gate on their own, so this is K4's busy time, not its waits for means)
+    k4_ms = max_over_ranks(ph_ms[3] / args.steps)
     k2_ms = max_over_ranks(ph_ms[1] / max(ph_n[1], 1))
     coll_ms = max_over_ranks(ph_ms[2] / max(ph_n[2], 1)) if ph_n[2] else 0.0
     k1_ms = max_over_ranks(ph2_ms[0] / max(ph2_n[0], 1))

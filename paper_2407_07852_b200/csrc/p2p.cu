@@ -368,8 +368,13 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
     for (size_t q = 0; q < K && !sm_mover; ++q)
       if ((int)q != r) DLC_CUDA(cudaStreamWaitEvent(e->stream, evGath[q * P + p], 0));
     cudaEvent_t t4 = trace_begin(e, e->stream);
+    // device buffers: time each piece's launch on its own (after its wait), so
+    // the OUTER phase sums K4's busy time, not the waits for the means
+    const bool piece_timing = e->timing && !hsrc;
+    if (piece_timing) phase_begin(e);
     launch_nesterov_p2p_piece(tt_pair(e), buf_pair(e), local_pair(e), slots, (int)K, S, po(p), pl(p), e->prec, e->st,
                               lr, mu, n, piece_ctas(), e->stream);
+    if (piece_timing) phase_end(e, DLC_PHASE_OUTER);
     trace_end(e, e->stream, "K4", (int)p, t4);
     if (hdst) {
       DLC_CUDA(cudaEventRecord(evK4[p], e->stream));
@@ -408,8 +413,8 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
     for (size_t p = 0; p < P && push2; ++p) scatter_piece(p);
     for (size_t p = 0; p < P; ++p) fold_piece(p);
     fold_end();
-    phase_begin(e);
     for (size_t p = 0; p < P; ++p) k4_piece(p);
+    phase_begin(e);  // the finish gate below is one more OUTER interval
   } else {
     // host buffers: K2(p+1) then K4(p) on the engine stream, so the D2H of
     // piece p's new theta_t starts while later pieces are still arriving (H2D
