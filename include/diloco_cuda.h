@@ -484,6 +484,11 @@ DLC_API int dlc_fold_push_probe(const void* const* contribs, int k, size_t n, in
  * nesterov_p2p_piece (16 + w B/param).  Lets ncu capture the multi-GPU kernels
  * in a single process. */
 DLC_API int dlc_p2p_kernels_probe(int k, size_t n, int precision, int reps, float* ms3);
+/* The same, plus overlap_ms[0] = K4 per launch while the fold (fold_ctas CTAs,
+ * 0 = one per SM) runs back to back on a second stream, overlap_ms[1] = the
+ * fold per launch meanwhile: on-chip interference without NVLink. */
+DLC_API int dlc_p2p_overlap_probe(int k, size_t n, int precision, int reps, int fold_ctas, float* ms3,
+                                  float* overlap_ms);
 
 /* =========================================================================
  * 5. Wire codec for cross-box transports.

@@ -186,6 +186,7 @@ _SIGS = {
     "dlc_fp16_encode_bits": (I, [C.c_uint32, SZ, P]),
     "dlc_fold_push_probe": (I, [PP, I, SZ, I, I, P, C.POINTER(I)]),
     "dlc_p2p_kernels_probe": (I, [I, SZ, I, I, C.POINTER(C.c_float)]),
+    "dlc_p2p_overlap_probe": (I, [I, SZ, I, I, I, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
     "dlc_run_training": (I, [P, P, GRAD_PRODUCER, METRICS_SINK, ROUND_HOOK, P, I, C.POINTER(RunResult)]),
     "dlc_world_create": (I, [C.POINTER(Config), C.POINTER(Hyperparams), SZ, P, I, I, C.POINTER(P)]),
     "dlc_world_destroy": (I, [P]),

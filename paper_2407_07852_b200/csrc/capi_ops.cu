@@ -431,6 +431,10 @@ int dlc_fold_push_probe(const void* const* contribs, int k, size_t n, int precis
 }
 
 int dlc_p2p_kernels_probe(int k, size_t n, int precision, int reps, float* ms3) {
+  return dlc_p2p_overlap_probe(k, n, precision, reps, 0, ms3, nullptr);
+}
+
+int dlc_p2p_overlap_probe(int k, size_t n, int precision, int reps, int fold_ctas, float* ms3, float* overlap_ms) {
   return guard([&] {
     if (k < 2 || k > kMaxK) fail(DLC_EINVAL, "p2p_kernels_probe: k must be 2..32");
     if (precision != DLC_FP32 && precision != DLC_FP16) fail(DLC_ECONFIG, "unknown precision");
@@ -496,6 +500,37 @@ int dlc_p2p_kernels_probe(int k, size_t n, int precision, int reps, float* ms3) 
       ms3[2] = timed([&] {
         launch_nesterov_p2p_piece(ttp, bufp, follow, slots, k, S, 0, S, precision, st, 0.7f, 0.9f, n, 0, c.stream);
       });
+      if (overlap_ms) {
+        // K4 on the staging stream while the fold (fold_ctas CTAs) runs back to
+        // back on a second stream for at least as long: on-chip interference
+        // between the two, without NVLink in the picture
+        cudaStream_t s2 = nullptr;
+        DLC_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+        cudaEvent_t f0 = nullptr, f1 = nullptr;
+        DLC_CUDA(cudaEventCreate(&f0));
+        DLC_CUDA(cudaEventCreate(&f1));
+        const int freps = std::max(1, (int)std::ceil(3.0 * reps * ms3[2] / std::max(ms3[1], 1e-3f)));
+        DLC_CUDA(cudaStreamSynchronize(c.stream));
+        DLC_CUDA(cudaEventRecord(f0, s2));
+        for (int i = 0; i < freps; ++i)
+          if (!launch_fold_push_tma(in, k, precision, outs, k, fl, k, S, fold_ctas, s2))
+            launch_fold_push(in, k, precision, outs, k, fl, k, S, fold_ctas, s2);
+        DLC_CUDA(cudaEventRecord(f1, s2));
+        DLC_CUDA(cudaEventRecord(ev[0], c.stream));
+        for (int i = 0; i < reps; ++i)
+          launch_nesterov_p2p_piece(ttp, bufp, follow, slots, k, S, 0, S, precision, st, 0.7f, 0.9f, n, 0, c.stream);
+        DLC_CUDA(cudaEventRecord(ev[1], c.stream));
+        DLC_CUDA(cudaEventSynchronize(ev[1]));
+        DLC_CUDA(cudaEventSynchronize(f1));
+        float a = 0.f, b = 0.f;
+        DLC_CUDA(cudaEventElapsedTime(&a, ev[0], ev[1]));
+        DLC_CUDA(cudaEventElapsedTime(&b, f0, f1));
+        overlap_ms[0] = a / (float)reps;   // K4 per launch while the fold runs
+        overlap_ms[1] = b / (float)freps;  // fold per launch (partly alone at the end)
+        cudaEventDestroy(f0);
+        cudaEventDestroy(f1);
+        cudaStreamDestroy(s2);
+      }
     } catch (...) {
       for (cudaEvent_t e : ev)
         if (e) cudaEventDestroy(e);

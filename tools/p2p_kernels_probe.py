@@ -29,6 +29,8 @@ def main():
     ap.add_argument("--k", type=int, nargs="+", default=[2, 4, 8])
     ap.add_argument("--precision", choices=["fp16", "fp32"], default="fp16")
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--overlap", action="store_true",
+                    help="also time K4 while the fold (320/k CTAs, as in the step) runs on a second stream")
     a = ap.parse_args()
     D.lib.dlc_set_device(0)
     prec = D.FP16 if a.precision == "fp16" else D.FP32
@@ -36,13 +38,17 @@ def main():
     n = a.params
     for k in a.k:
         ms = (C.c_float * 3)()
-        st = D.lib.dlc_p2p_kernels_probe(k, n, prec, a.reps, ms)
+        ov = (C.c_float * 2)()
+        st = D.lib.dlc_p2p_overlap_probe(k, n, prec, a.reps, max(16, 320 // k), ms, ov if a.overlap else None)
         if st != 0:
             raise RuntimeError(D.lib.dlc_last_error().decode())
         out = {"k": k, "params": n, "precision": a.precision}
         for name, bpp, t in (("K2_pseudo_grad_piece", 8 + w, ms[0]), ("fold_push", 2 * w, ms[1]),
                              ("K4_nesterov_p2p_piece", 16 + w, ms[2])):
             out[name] = {"ms": round(t, 4), "bytes_per_param": bpp, "gbs": round(bpp * n / (t * 1e-3) / 1e9, 1)}
+        if a.overlap:
+            out["K4_while_fold_runs"] = {"ms": round(ov[0], 4), "gbs": round((16 + w) * n / (ov[0] * 1e-3) / 1e9, 1),
+                                         "fold_ms": round(ov[1], 4), "fold_ctas": max(16, 320 // k)}
         print(json.dumps(out), flush=True)
 
 
