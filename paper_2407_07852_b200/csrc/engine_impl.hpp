@@ -134,10 +134,15 @@ constexpr size_t kMaxPieces = 8;
 // ---- engine_util.cu ----
 void* dalloc(dlc_engine* e, size_t bytes);
 size_t p2p_pieces();
+// Piece boundaries inside an owner slot of S elements, for a vector of n
+// elements per worker.  Default plan (no DLC_P2P_PLAN / DLC_P2P_PIECES):
+// 1,1,2,2,1,1 eighths, or 1,3,3,1 below 400M elements per worker, where the
+// step is ~1 ms and per-piece costs outweigh a shorter fill / drain (150M:
+// 1.00 vs 1.07 ms at 4 GPUs, 0.89 vs 0.95 ms at 2, profiles/r1_sweep_150m_*).
 // host_path: the e2e call with host buffers, where the step is PCIe-bound and
-// the pipeline fill / drain is one piece of H2D / D2H: 16 equal pieces unless
-// DLC_P2P_PLAN / DLC_P2P_PIECES say otherwise.
-std::vector<size_t> piece_plan(size_t S, bool host_path = false);
+// the pipeline fill / drain is one piece of H2D / D2H: 16 equal pieces.
+constexpr size_t kSmallStepElems = 400000000;
+std::vector<size_t> piece_plan(size_t S, size_t n, bool host_path = false);
 bool p2p_mover_sm();
 bool p2p_mover_push();
 bool p2p_mover_push2();

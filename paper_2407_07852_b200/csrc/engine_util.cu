@@ -35,13 +35,13 @@ size_t p2p_pieces() {
 // and last pieces shrink the pipeline's fill (K2 of piece 0) and drain (K4 of
 // the last piece)); boundaries are rounded down to whole 64-element vectors.
 // DLC_P2P_PIECES asks for that many equal pieces instead.
-std::vector<size_t> piece_plan(size_t S, bool host_path) {
+std::vector<size_t> piece_plan(size_t S, size_t n, bool host_path) {
   std::vector<size_t> w;
   size_t sum = 0;
   const char* plan = std::getenv("DLC_P2P_PLAN");
   if (host_path && !plan && !std::getenv("DLC_P2P_PIECES")) w.assign(16, 1);
   if (w.empty() && (plan || !std::getenv("DLC_P2P_PIECES"))) {
-    std::string str = plan ? plan : "1,1,2,2,1,1";
+    std::string str = plan ? plan : (n < kSmallStepElems ? "1,3,3,1" : "1,1,2,2,1,1");
     size_t pos = 0;
     while (pos <= str.size()) {
       const size_t comma = str.find(',', pos);

@@ -206,7 +206,7 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
       DLC_CUDA(cudaStreamCreateWithFlags(&e->gath[j], cudaStreamNonBlocking));
     }
   }
-  const std::vector<size_t> pb = piece_plan(S, hsrc != nullptr);  // piece boundaries inside a slot
+  const std::vector<size_t> pb = piece_plan(S, n, hsrc != nullptr);  // piece boundaries inside a slot
   const size_t P = pb.size() - 1;
   auto po = [&](size_t p) { return pb[p]; };
   auto pl = [&](size_t p) { return pb[p + 1] - pb[p]; };
@@ -462,7 +462,7 @@ void outer_allreduce_pipelined(dlc_engine* e, dlc_collective* c, const float* sr
     DLC_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     DLC_CUDA(cudaStreamCreateWithPriority(&e->cstream, cudaStreamNonBlocking, hi));
   }
-  std::vector<size_t> pb = piece_plan((n + 511) / 512 * 512);  // contiguous pieces of [0, n)
+  std::vector<size_t> pb = piece_plan((n + 511) / 512 * 512, n);  // contiguous pieces of [0, n)
   for (size_t& b : pb) b = std::min(b, n);
   const size_t P = pb.size() - 1;
   while (e->piece_ev.size() < 2 * P + 1) {
