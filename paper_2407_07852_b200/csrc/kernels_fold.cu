@@ -4,10 +4,9 @@
 // push/push scatter, and the NVLink flag barrier of the P2P step.
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <mutex>
 #include <unordered_map>
-
-#include <cstdlib>
 
 #include "common.cuh"
 #include "device.cuh"
@@ -244,9 +243,9 @@ __global__ void __launch_bounds__(kThreads) fold_push_kernel(const __grid_consta
 // keeps STAGES * KK * 8 KB of NVLink reads in flight with a handful of
 // instructions, so a few dozen CTAs saturate the links and leave the SMs to the
 // HBM-bound K2 / K4 pieces.
-// NT (DLC_TMA_THREADS, default kTmaThreads): the fold's decode / add / encode
-// work is latency-bound with one warp per scheduler (ncu: 1.15 IPC per SM at
-// 128 threads), so more warps per CTA shorten the time a stage is held.
+// NT threads per CTA (tma_threads(): 128 for K <= 4, more as the CTA count
+// falls with K): the fold's decode / add / encode work is latency-bound with one
+// warp per scheduler (ncu: 1.15 IPC per SM at 128 threads).
 constexpr int kTmaThreads = 128;
 constexpr int kTmaTileBytes = 8192;
 constexpr int kTmaStages = 3;
