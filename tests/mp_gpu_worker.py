@@ -149,7 +149,10 @@ def main():
         th = O.rng_fill(6, "theta", 0, n2, -1, 1)
         loc = (th - O.rng_fill(6, "local", r.rank, n2, -1e-3, 1e-3)).astype(np.float32)
         if r.rank == k - 1:
-            loc[n2 // 2] = np.inf
+            loc[n2 // 2] = np.inf  # in another owner's slot
+            own = (k - 1) * PD.slot_elems(n2, k) + 7  # in this rank's own slot (folded locally)
+            if own < n2:
+                loc[own] = -np.inf
         e2 = D.DilocoEngine(D.DilocoConfig(1, k, D.FP16, 1), D.OptimHyperparams(), n2, r.local)
         e2.upload(D.THETA_T, th)
         out_t = np.full(n2, np.nan, np.float32)
