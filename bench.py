@@ -360,20 +360,18 @@ def run_ours(args):
         rl["kernel"] = "outer_solo_kernel (K2+K4 fused)"
         line["phases_ms"] = {"outer_solo_K2K4": k4_ms}
         line["phase_roofline"] = {"outer_solo_K2K4": rl["frac"]}
+        rl["traffic"] = ncu_traffic("outer_solo_kernel", n)
     else:
         rl = roof(b_k4, k4_ms)
         rl["kernel"] = ("nesterov_p2p_piece_kernel (K4)" if mode == D.MODE_P2P else "nesterov_outer_kernel (K4)")
         line["phases_ms"] = {"pseudo_grad_K2": k2_ms, "collective_C1_K3": coll_ms, "nesterov_K4": k4_ms}
         line["phase_roofline"] = {"pseudo_grad_K2": roof(b_k2, k2_ms)["frac"], "nesterov_K4": rl["frac"]}
-    if k == 1:
-        rl["traffic"] = ncu_traffic("outer_solo_kernel", n)
-    elif mode == D.MODE_P2P:
-        # multi-rank runs cannot be profiled: the capture is the same kernel over all N
-        # params on one GPU (tools/p2p_kernels_probe.py), i.e. one step's pieces
-        rl["traffic"] = ncu_traffic("nesterov_p2p_piece_kernel<%d>" % (1 if prec == D.FP16 else 0), n)
-        rl["traffic_source"] = "ncu of the kernel alone on one GPU (tools/p2p_kernels_probe.py)"
-    else:
         rl["traffic"] = None
+        if mode == D.MODE_P2P:
+            # multi-rank runs cannot be profiled: the capture is the same kernel over all N
+            # params on one GPU (tools/p2p_kernels_probe.py), i.e. one step's pieces
+            rl["traffic"] = ncu_traffic("nesterov_p2p_piece_kernel<%d>" % (1 if prec == D.FP16 else 0), n)
+            rl["traffic_source"] = "ncu of the kernel alone on one GPU (tools/p2p_kernels_probe.py)"
     line["roofline"] = rl
     if k > 1 and mode == D.MODE_P2P and rank == 0:
         # the same kernels alone on this GPU (no exchange traffic sharing HBM): each
