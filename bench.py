@@ -52,7 +52,17 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--no-wire", action="store_true")
+    ap.add_argument("--plan", default=None, help="P2P piece plan override, e.g. 1,1,2,2,1,1 (dlc_p2p_set_tuning)")
+    ap.add_argument("--fold-ctas", type=int, default=0)
+    ap.add_argument("--fold-threads", type=int, default=0)
     return ap.parse_args()
+
+
+def plan_of(args, n):
+    """The piece plan of the P2P / pipelined all-reduce step (engine_util.cu piece_plan)."""
+    if args.plan:
+        return [int(x) for x in args.plan.split(",")]
+    return [1, 3, 3, 1] if n < 400_000_000 else [1, 1, 2, 2, 1, 1]
 
 
 def dist_env():
@@ -261,6 +271,9 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("gloo")
     D.lib.dlc_set_device(local)
+    if args.plan or args.fold_ctas or args.fold_threads:
+        D.set_p2p_tuning(plan=plan_of(args, args.params) if args.plan else None, fold_ctas=args.fold_ctas,
+                         fold_threads=args.fold_threads)
     k = world
     n = args.params
     prec = D.FP16 if args.precision == "fp16" else D.FP32
@@ -413,18 +426,11 @@ def run_ours(args):
     if k == 1:
         per_outer = 2  # outer_solo + finish
     elif mode == D.MODE_P2P:
-        if "DLC_P2P_PIECES" in os.environ and "DLC_P2P_PLAN" not in os.environ:
-            pieces = min(max(int(os.environ["DLC_P2P_PIECES"]), 1), 32)
-        else:
-            pieces = len(os.environ.get("DLC_P2P_PLAN", "1,1,2,2,1,1").split(","))
-        flag = os.environ.get("DLC_P2P_BARRIER", "flag") != "nccl"
-        merged = os.environ.get("DLC_P2P_MERGE", "1") != "0"
-        barriers = (pieces + 1 if merged else 2 * pieces) if flag else 0
-        per_outer = 3 * pieces + 1 + barriers  # K2, fold_push, K4 pieces, finish, barriers
-        if os.environ.get("DLC_P2P_COPY") == "push2":
-            per_outer += pieces  # scatter kernels
-    elif mode == D.MODE_ALLREDUCE and os.environ.get("DLC_AR_SERIAL") != "1":
-        pieces = len(os.environ.get("DLC_P2P_PLAN", "1,1,2,2,1,1").split(","))
+        pieces = len(plan_of(args, n))
+        # K2, fold_push, K4 per piece, the finish gate; flag barriers A_0, B_p, commit
+        per_outer = 3 * pieces + 1 + (pieces + 2)
+    elif mode == D.MODE_ALLREDUCE:
+        pieces = len(plan_of(args, n))
         per_outer = 3 * pieces + 1  # K2, non-finite check, K4 pieces, finish (NCCL's own kernels not counted)
     else:
         per_outer = 3  # K2, fold / non-finite check, K4

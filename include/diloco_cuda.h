@@ -225,6 +225,22 @@ DLC_API size_t dlc_collective_members(const dlc_collective* c, int* ranks, size_
 DLC_API int dlc_collective_set_reduce_timeout_ms(dlc_collective* c, uint64_t ms);
 DLC_API int dlc_collective_inject_stall(dlc_collective* c, int64_t barrier_index);
 
+/* DLC_MODE_P2P tuning (development sweeps; no reference counterpart).  All
+ * fields zero = the measured defaults: piece plan 1,1,2,2,1,1
+ * (1,3,3,1 below 400M params per worker, 16 equal pieces on the host-buffer
+ * path), max(16, 320 / K) fold CTAs, 128 / 256 / 512 fold threads for
+ * K <= 4 / <= 6 / <= 8, one piece-kernel CTA per 256-vector window.
+ * Process-wide; applies from the next outer step.  NULL restores the defaults. */
+typedef struct {
+  uint32_t plan[32]; /* relative piece weights inside an owner slot (1..1024 each) */
+  uint32_t plan_len; /* 0 = default plan */
+  int32_t fold_ctas;    /* TMA fold CTAs, 0 = default */
+  int32_t fold_threads; /* 128, 256 or 512; 0 = default by K */
+  int32_t piece_ctas;   /* K2 / K4 piece kernels' grid, 0 = one CTA per window */
+} dlc_p2p_tuning;
+DLC_API int dlc_p2p_set_tuning(const dlc_p2p_tuning* t);
+DLC_API int dlc_p2p_get_tuning(dlc_p2p_tuning* t);
+
 /* =========================================================================
  * 3. Device-resident engine: DilocoEngine (engine.hpp:76-116) with theta_t,
  *    theta_local, AdamW m/v, Nesterov buffer, loss scaler and counters all in

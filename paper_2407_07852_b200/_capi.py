@@ -49,6 +49,11 @@ class ReduceReport(C.Structure):
                 ("wire_bytes_received", C.c_uint64), ("wall_ms", C.c_double), ("attempts", C.c_uint32)]
 
 
+class P2PTuning(C.Structure):
+    _fields_ = [("plan", C.c_uint32 * 32), ("plan_len", C.c_uint32), ("fold_ctas", C.c_int32),
+                ("fold_threads", C.c_int32), ("piece_ctas", C.c_int32)]
+
+
 class WireTags(C.Structure):
     _fields_ = [("msg_type", C.c_uint8), ("precision", C.c_int), ("outer_epoch", C.c_uint64),
                 ("attempt", C.c_uint32), ("partition", C.c_uint32), ("from_hi", C.c_uint64),
@@ -188,6 +193,8 @@ _SIGS = {
     "dlc_p2p_kernels_probe": (I, [I, SZ, I, I, C.POINTER(C.c_float)]),
     "dlc_p2p_overlap_probe": (I, [I, SZ, I, I, I, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
     "dlc_run_training": (I, [P, P, GRAD_PRODUCER, METRICS_SINK, ROUND_HOOK, P, I, C.POINTER(RunResult)]),
+    "dlc_p2p_set_tuning": (I, [C.POINTER(P2PTuning)]),
+    "dlc_p2p_get_tuning": (I, [C.POINTER(P2PTuning)]),
     "dlc_world_create": (I, [C.POINTER(Config), C.POINTER(Hyperparams), SZ, P, I, I, C.POINTER(P)]),
     "dlc_world_destroy": (I, [P]),
     "dlc_world_engine": (I, [P, I, C.POINTER(P)]),

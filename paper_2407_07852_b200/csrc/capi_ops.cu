@@ -10,8 +10,7 @@
 #include <string>
 #include <vector>
 
-#include "internal.hpp"
-#include "kernels.cuh"
+#include "engine_impl.hpp"
 
 namespace dlc {
 
@@ -422,7 +421,7 @@ int dlc_fold_push_probe(const void* const* contribs, int k, size_t n, int precis
     DLC_CUDA(cudaMemsetAsync(d_flag, 0, sizeof(int), c.stream));
     outs.ptr[0] = d_out;
     flags.ptr[0] = d_flag;
-    if (!(tma && launch_fold_push_tma(in, k, precision, outs, 1, flags, 1, n, 0, c.stream)))
+    if (!(tma && launch_fold_push_tma(in, k, precision, outs, 1, flags, 1, n, tma_ctas(k), tma_threads(k), c.stream)))
       launch_fold_push(in, k, precision, outs, 1, flags, 1, n, 0, c.stream);
     d2h(out, d_out, n * w, c.stream);
     d2h(nonfinite, d_flag, sizeof(int), c.stream);
@@ -494,8 +493,8 @@ int dlc_p2p_overlap_probe(int k, size_t n, int precision, int reps, int fold_cta
         launch_pseudo_grad_piece(ttp, src, st, send, precision, k, S, 0, S, n, 0, c.stream);
       });
       ms3[1] = timed([&] {
-        if (!launch_fold_push_tma(in, k, precision, outs, k, fl, k, S, 0, c.stream))
-          launch_fold_push(in, k, precision, outs, k, fl, k, S, 0, c.stream);
+        if (!launch_fold_push_tma(in, k, precision, outs, k, fl, k, S, tma_ctas(k), tma_threads(k), c.stream))
+          launch_fold_push(in, k, precision, outs, k, fl, k, S, kFoldCtas, c.stream);
       });
       ms3[2] = timed([&] {
         launch_nesterov_p2p_piece(ttp, bufp, follow, slots, k, S, 0, S, precision, st, 0.7f, 0.9f, n, 0, c.stream);
@@ -513,8 +512,9 @@ int dlc_p2p_overlap_probe(int k, size_t n, int precision, int reps, int fold_cta
         DLC_CUDA(cudaStreamSynchronize(c.stream));
         DLC_CUDA(cudaEventRecord(f0, s2));
         for (int i = 0; i < freps; ++i)
-          if (!launch_fold_push_tma(in, k, precision, outs, k, fl, k, S, fold_ctas, s2))
-            launch_fold_push(in, k, precision, outs, k, fl, k, S, fold_ctas, s2);
+          if (!launch_fold_push_tma(in, k, precision, outs, k, fl, k, S, fold_ctas > 0 ? fold_ctas : tma_ctas(k),
+                                    tma_threads(k), s2))
+            launch_fold_push(in, k, precision, outs, k, fl, k, S, fold_ctas > 0 ? fold_ctas : kFoldCtas, s2);
         DLC_CUDA(cudaEventRecord(f1, s2));
         DLC_CUDA(cudaEventRecord(ev[0], c.stream));
         for (int i = 0; i < reps; ++i)

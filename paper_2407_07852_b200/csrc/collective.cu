@@ -150,6 +150,15 @@ int dlc_collective_create_solo(int device, dlc_collective** out) {
 int dlc_collective_destroy(dlc_collective* c) {
   if (!c) return DLC_OK;
   return guard([&] {
+    // engines still bound to it lose their peer mappings (no fleet barrier:
+    // the communicator is going away; their next P2P step binds again)
+    while (!c->bound.empty()) {
+      dlc_engine* e = c->bound.back();
+      DeviceGuard dg(e->device);
+      cudaStreamSynchronize(e->stream);
+      if (e->cstream) cudaStreamSynchronize(e->cstream);
+      p2p_unbind(e);  // removes e from c->bound
+    }
     if (c->kind == 1) {
       DeviceGuard dg(c->device);
       if (c->stream) cudaStreamDestroy(c->stream);
@@ -235,9 +244,13 @@ int dlc_collective_all_reduce_avg(dlc_collective* c, const float* local, size_t 
       report->outer_epoch = outer_epoch;
       report->contributors = (size_t)c->world;
       report->attempts = 1;
-      const uint64_t b = c->world > 1 ? dlc_per_peer_reduce_bytes(n, c->world, c->rank, precision) : 0;
-      report->data_bytes_sent = report->data_bytes_received = b;
-      report->wire_bytes_sent = report->wire_bytes_received = b;
+      if (c->world > 1) {
+        report->data_bytes_sent = dlc_per_peer_reduce_bytes(n, c->world, c->rank, precision);
+        report->data_bytes_received = per_peer_reduce_bytes_received(n, c->world, c->rank, precision);
+        const uint64_t S = (((n + c->world - 1) / c->world) + 63) / 64 * 64;
+        report->wire_bytes_sent = report->wire_bytes_received =
+            2ull * (c->world - 1) * S * (precision == DLC_FP16 ? 2 : 4);
+      }
       report->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     }
   });

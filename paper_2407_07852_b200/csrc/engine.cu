@@ -142,9 +142,11 @@ int dlc_engine_destroy(dlc_engine* e) {
   return guard([&] {
     DeviceGuard dg(e->device);
     if (e->stream) cudaStreamSynchronize(e->stream);
-    if (e->p2p_bound) {
+    if (e->cstream) cudaStreamSynchronize(e->cstream);
+    if (e->p2p_bound && e->p2p_bound->comm && !e->p2p_bound->broken) {
       // peers may still be reading this engine's slot / send buffer: wait for
-      // the whole fleet (engines are destroyed collectively, before their collective)
+      // the whole fleet (engines are destroyed collectively; a collective
+      // destroyed first unbinds its engines, which then skip this barrier)
       fleet_barrier(e, const_cast<dlc_collective*>(e->p2p_bound));
       cudaStreamSynchronize(e->stream);
     }
@@ -161,12 +163,7 @@ int dlc_engine_destroy(dlc_engine* e) {
     if (e->ev1) cudaEventDestroy(e->ev1);
     for (cudaEvent_t ev : e->chunk_ev) cudaEventDestroy(ev);
     for (cudaEvent_t ev : e->piece_ev) cudaEventDestroy(ev);
-    for (size_t j = 0; j < (size_t)kMaxK; ++j) {
-      if (e->pull[j]) cudaStreamDestroy(e->pull[j]);
-      if (e->gath[j]) cudaStreamDestroy(e->gath[j]);
-    }
     if (e->cstream) cudaStreamDestroy(e->cstream);
-    if (e->sstream) cudaStreamDestroy(e->sstream);
     if (e->h2d) cudaStreamDestroy(e->h2d);
     if (e->d2h) cudaStreamDestroy(e->d2h);
     if (e->stream) cudaStreamDestroy(e->stream);

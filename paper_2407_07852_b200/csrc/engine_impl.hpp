@@ -13,6 +13,8 @@
 #include "internal.hpp"
 #include "kernels.cuh"
 
+struct dlc_engine;
+
 struct dlc_collective {
   int kind = 0;  // 0 solo, 1 nccl
   int rank = 0;
@@ -30,6 +32,7 @@ struct dlc_collective {
   uint64_t timeout_ms = 20000;         // NodeOptions::reduce_timeout_ms: P2P barrier failure detector
   int64_t stall_at = -1;               // fault injection: stop arriving from this barrier on (-1 off)
   int64_t barriers = 0;                // P2P barriers issued on this collective
+  std::vector<dlc_engine*> bound;      // engines whose peer tables map this collective's members
 };
 
 struct dlc_engine {
@@ -70,13 +73,13 @@ struct dlc_engine {
   uint64_t phase_n[4] = {0, 0, 0, 0};
   cudaEvent_t open_ev = nullptr;
   // DLC_MODE_P2P: every rank's send buffer, gather buffer and flag array mapped
-  // into this process through CUDA IPC (own entries are local).
+  // into this process through CUDA IPC (own entries are local; a dlc_world
+  // points them straight at the other engines' buffers).
   int* barrier_buf = nullptr;
   const dlc_collective* p2p_bound = nullptr;
   void* peer_send[dlc::kMaxK] = {};
   void* peer_gather[dlc::kMaxK] = {};
   int* peer_flags[dlc::kMaxK] = {};
-  void* peer_recv[dlc::kMaxK] = {};  // "push" mover: owners' recv buffers
   uint64_t* sig = nullptr;  // flag-barrier signal slots, one per rank
   uint64_t* peer_sig[dlc::kMaxK] = {};
   uint64_t sig_epoch = 0;
@@ -90,15 +93,12 @@ struct dlc_engine {
   std::vector<cudaEvent_t> chunk_ev;
   // pipelined P2P: high-priority stream for barriers + owner folds, per-piece events
   cudaStream_t cstream = nullptr;
-  cudaStream_t sstream = nullptr;  // "push2" mover: scatter kernels, concurrent with the folds
   struct TraceMark {
     const char* label;
     int piece;
     cudaEvent_t a, b;
   };
   std::vector<TraceMark> trace;  // DLC_TRACE=1: per-op timeline of the P2P step
-  cudaStream_t pull[dlc::kMaxK] = {};  // copy-engine pulls of peers' delta slices
-  cudaStream_t gath[dlc::kMaxK] = {};  // copy-engine pulls of owners' mean slices
   std::vector<cudaEvent_t> piece_ev;
   // wire rounds (dlc_engine_wire_*): fold rows of the owned range, `wire_stride` elements each
   void* wire_rows = nullptr;
@@ -127,15 +127,16 @@ inline ncclDataType_t nccl_type(int prec) { return prec == DLC_FP16 ? ncclFloat1
 // Host <-> device chunk of the host-buffer outer step (64 MB of FP32).
 constexpr size_t kHostChunk = size_t(16) << 20;
 // Pieces of the pipelined P2P outer step (DLC_MODE_P2P).
-// Owner slots are a multiple of 64 * kMaxPieces elements; the split actually
-// used comes from DLC_P2P_PLAN / DLC_P2P_PIECES (profiles/r1_sweep_p2p_*.log).
+// Owner slots are a multiple of 64 * kMaxPieces elements.
 constexpr size_t kMaxPieces = 8;
+// CTAs of the per-thread fold (K > 8, where the TMA fold has no instance);
+// 256 from profiles/r1_sweep_p2p_{2,4}gpu_kk.log
+constexpr int kFoldCtas = 256;
 
 // ---- engine_util.cu ----
 void* dalloc(dlc_engine* e, size_t bytes);
-size_t p2p_pieces();
 // Piece boundaries inside an owner slot of S elements, for a vector of n
-// elements per worker.  Default plan (no DLC_P2P_PLAN / DLC_P2P_PIECES):
+// elements per worker.  Measured defaults (dlc_p2p_set_tuning overrides):
 // 1,1,2,2,1,1 eighths, or 1,3,3,1 below 400M elements per worker, where the
 // step is ~1 ms and per-piece costs outweigh a shorter fill / drain (150M:
 // 1.00 vs 1.07 ms at 4 GPUs, 0.89 vs 0.95 ms at 2, profiles/r1_sweep_150m_*).
@@ -143,18 +144,13 @@ size_t p2p_pieces();
 // the pipeline fill / drain is one piece of H2D / D2H: 16 equal pieces.
 constexpr size_t kSmallStepElems = 400000000;
 std::vector<size_t> piece_plan(size_t S, size_t n, bool host_path = false);
-bool p2p_mover_sm();
-bool p2p_mover_push();
-bool p2p_mover_push2();
-int comm_ctas();
-bool fold_tma();
 int tma_ctas(size_t k);
-bool p2p_k4_pull();
-bool p2p_merge_barriers();
+int tma_threads(size_t k);
 int piece_ctas();
 void ensure_copy_streams(dlc_engine* e);
 void ensure_chunk_events(dlc_engine* e, size_t count);
 void harvest(dlc_engine* e);
+void harvest_if_full(dlc_engine* e);
 cudaEvent_t pooled_event(dlc_engine* e);
 void phase_begin(dlc_engine* e);
 void phase_end(dlc_engine* e, int phase);
@@ -180,17 +176,40 @@ void nesterov(dlc_engine* e, const void* dbar, const int* flags, int nflags);
 void p2p_unbind(dlc_engine* e);
 void p2p_bind(dlc_engine* e, dlc_collective* c);
 void fleet_barrier(dlc_engine* e, dlc_collective* c);
-void p2p_barrier(dlc_engine* e, dlc_collective* c, cudaStream_t s);
-bool flag_barriers(const dlc_collective* c);
+void p2p_barrier(dlc_engine* e, dlc_collective* c, cudaStream_t s, bool commit);
 void outer_collective(dlc_engine* e, dlc_collective* c, dlc_reduce_report* rep);
+// One pipelined DLC_MODE_P2P outer step of one engine, in stages.  Ranks
+// synchronise between the stages: flag barriers (outer_p2p_pipelined) or
+// event dependencies (world.cu).
+struct P2PStep {
+  dlc_engine* e = nullptr;
+  int rank = 0;
+  size_t K = 0, S = 0, w = 0, n = 0, P = 0;
+  std::vector<size_t> pb;  // piece boundaries inside an owner slot
+  Pair tl{};               // theta_local source (the engine's, or a staging buffer)
+  const float* hsrc = nullptr;
+  float* hdst = nullptr;
+  int oc_host = 0;
+  bool rep = false;
+  cudaEvent_t *evK2 = nullptr, *evB = nullptr, *evH = nullptr, *evK4 = nullptr;
+  cudaEvent_t evStart = nullptr, evCommit = nullptr, c0 = nullptr, c1 = nullptr, origin = nullptr;
+  PtrList slots{}, fl{};
+};
+P2PStep p2p_begin(dlc_engine* e, int rank, const float* src, bool rep, const float* hsrc, float* hdst, int oc_host);
+void p2p_k2(P2PStep& s, size_t p);
+void p2p_fold_begin(P2PStep& s);
+void p2p_fold(P2PStep& s, size_t p);
+void p2p_fold_end(P2PStep& s);
+void p2p_k4(P2PStep& s, size_t p);
+void p2p_finish(P2PStep& s, const int* abort);
 void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc_reduce_report* rep,
                          const float* hsrc, float* hdst, int oc_host);
-bool allreduce_pipelined();
 void outer_allreduce_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc_reduce_report* rep);
 void outer_round(dlc_engine* e, dlc_collective* c, const float* src, dlc_reduce_report* rep);
 
 // ---- engine_util.cu (results) ----
 void fill_report(dlc_engine* e, dlc_collective* c, dlc_reduce_report* rep, uint64_t epoch);
+uint64_t per_peer_reduce_bytes_received(size_t n, size_t k, size_t rank, int precision);
 void check_collective(dlc_engine* e, dlc_collective* c);
 void check_barrier(dlc_engine* e);
 size_t slot_elems(size_t n, size_t k);

@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -23,41 +24,31 @@ void* dalloc(dlc_engine* e, size_t bytes) {
   return p;
 }
 
-// (read on every step so a tuning sweep can change them in-process)
-size_t p2p_pieces() {
-  const char* s = std::getenv("DLC_P2P_PIECES");
-  const long v = s ? std::strtol(s, nullptr, 10) : 4;
-  return (size_t)std::min<long>(std::max<long>(v, 1), 32);
+// ---- P2P tuning: measured defaults, overridable for sweeps (dlc_p2p_set_tuning) ----
+namespace {
+std::mutex g_tuning_mu;
+dlc_p2p_tuning g_tuning{};  // all zero: the measured defaults
+dlc_p2p_tuning tuning() {
+  std::lock_guard<std::mutex> lock(g_tuning_mu);
+  return g_tuning;
 }
+}  // namespace
 
 // Piece boundaries inside an owner slot of S elements (S a multiple of 64):
-// DLC_P2P_PLAN lists relative piece weights (default "1,1,2,2,1,1": short first
-// and last pieces shrink the pipeline's fill (K2 of piece 0) and drain (K4 of
-// the last piece)); boundaries are rounded down to whole 64-element vectors.
-// DLC_P2P_PIECES asks for that many equal pieces instead.
+// relative piece weights, boundaries rounded down to whole 64-element vectors.
 std::vector<size_t> piece_plan(size_t S, size_t n, bool host_path) {
+  const dlc_p2p_tuning t = tuning();
   std::vector<size_t> w;
-  size_t sum = 0;
-  const char* plan = std::getenv("DLC_P2P_PLAN");
-  if (host_path && !plan && !std::getenv("DLC_P2P_PIECES")) w.assign(16, 1);
-  if (w.empty() && (plan || !std::getenv("DLC_P2P_PIECES"))) {
-    std::string str = plan ? plan : (n < kSmallStepElems ? "1,3,3,1" : "1,1,2,2,1,1");
-    size_t pos = 0;
-    while (pos <= str.size()) {
-      const size_t comma = str.find(',', pos);
-      const std::string tok = str.substr(pos, comma == std::string::npos ? std::string::npos : comma - pos);
-      const long v = std::strtol(tok.c_str(), nullptr, 10);
-      if (v <= 0 || v > 1024 || w.size() >= 32) {
-        w.clear();
-        break;
-      }
-      w.push_back((size_t)v);
-      if (comma == std::string::npos) break;
-      pos = comma + 1;
-    }
+  if (t.plan_len > 0) {
+    w.assign(t.plan, t.plan + std::min<uint32_t>(t.plan_len, 32));
+  } else if (host_path) {
+    w.assign(16, 1);
+  } else if (n < kSmallStepElems) {
+    w = {1, 3, 3, 1};
+  } else {
+    w = {1, 1, 2, 2, 1, 1};  // short first and last pieces shrink the pipeline's fill and drain
   }
-  if (w.empty()) w.assign(p2p_pieces(), 1);
-  sum = 0;
+  size_t sum = 0;
   for (size_t x : w) sum += x;
   std::vector<size_t> b{0};
   size_t cum = 0;
@@ -68,62 +59,28 @@ std::vector<size_t> piece_plan(size_t S, size_t n, bool host_path) {
   return b;
 }
 
-// Who moves the bytes in DLC_MODE_P2P: "sm" (default) = a persistent fold
-// kernel pulling deltas and pushing means over NVLink; "ce" = DMA copy engines.
-bool p2p_mover_sm() {
-  const char* s = std::getenv("DLC_P2P_COPY");
-  return !(s && std::string(s) == "ce");
-}
-
-// "push": the scatter is fused into K2 (deltas stored straight into the
-// owners' recv rows over NVLink), so every NVLink byte is a posted store.
-bool p2p_mover_push() {
-  const char* s = std::getenv("DLC_P2P_COPY");
-  return s && std::string(s) == "push";
-}
-// push/push: K2 writes locally, a scatter kernel on the comm stream pushes the
-// rows to their owners, the owners fold locally and push the means
-bool p2p_mover_push2() {
-  const char* s = std::getenv("DLC_P2P_COPY");
-  return s && std::string(s) == "push2";
-}
-
-// CTAs of the per-thread SM-mover fold and of the push2 scatter (0 = one CTA
-// per window, no SM partitioning); 256 from profiles/r1_sweep_p2p_{2,4}gpu_kk.log.
-int comm_ctas() {
-  const char* s = std::getenv("DLC_COMM_CTAS");
-  return s ? (int)std::strtol(s, nullptr, 10) : 256;
-}
-// SM mover fold on the bulk-copy engine (fold_push_tma_kernel), and its CTAs
-bool fold_tma() {
-  const char* s = std::getenv("DLC_FOLD_TMA");
-  return !(s && std::string(s) == "0");
-}
 // Each TMA fold CTA keeps 3 stages x K inputs x 8 KB of reads in flight; about
 // 7.5 MB in flight per GPU saturates the links, hence ~320 / K CTAs
 // (profiles/r1_sweep_p2p_*_tma.log).
 int tma_ctas(size_t k) {
-  const char* s = std::getenv("DLC_TMA_CTAS");
-  return s ? (int)std::strtol(s, nullptr, 10) : (int)std::max<size_t>(16, 320 / std::max<size_t>(k, 1));
-}
-// SM mover: one flag barrier between the fold of piece p and the fold of piece
-// p + 1 instead of two (DLC_P2P_MERGE=0: separate barriers A and B)
-bool p2p_merge_barriers() {
-  const char* s = std::getenv("DLC_P2P_MERGE");
-  return !(s && std::string(s) == "0");
+  const dlc_p2p_tuning t = tuning();
+  return t.fold_ctas > 0 ? t.fold_ctas : (int)std::max<size_t>(16, 320 / std::max<size_t>(k, 1));
 }
 
-// SM mover: K4 reads each owner's mean from the owner's gather slot over
-// NVLink instead of the owner pushing it to every rank (DLC_P2P_K4_PULL=1)
-bool p2p_k4_pull() {
-  const char* s = std::getenv("DLC_P2P_K4_PULL");
-  return s && std::string(s) == "1";
+// Threads per TMA fold CTA.  An owner decodes about N contributions per step
+// whatever K is, but the CTA count falls as 320 / K, so the fold needs more
+// warps per CTA as K grows.  At K = 4 the 4-GPU A/B put the optimum at about
+// 80 "128-thread CTA equivalents" (80 x 128 or 48 x 512; 48 x 128 and 64 x 128
+// were 20% / 12% slower, profiles/r1_ab_tma_threads_ctas_4gpu.log); K >= 5 keeps
+// that capacity with 256 / 512 threads.
+int tma_threads(size_t k) {
+  const dlc_p2p_tuning t = tuning();
+  if (t.fold_threads > 0) return t.fold_threads;
+  return k <= 4 ? 128 : (k <= 6 ? 256 : 512);
 }
+
 // CTAs of the K2 / K4 piece kernels running beside the fold (0: one per window)
-int piece_ctas() {
-  const char* s = std::getenv("DLC_P2P_PIECE_CTAS");
-  return s ? (int)std::strtol(s, nullptr, 10) : 0;
-}
+int piece_ctas() { return tuning().piece_ctas; }
 
 void ensure_copy_streams(dlc_engine* e) {
   if (!e->h2d) DLC_CUDA(cudaStreamCreateWithFlags(&e->h2d, cudaStreamNonBlocking));
@@ -163,10 +120,16 @@ cudaEvent_t pooled_event(dlc_engine* e) {
   return ev;
 }
 
+// Bounds the pending timing events.  Called at the entry of a step, never
+// between its launches: a host wait inside a P2P step could block on a peer's
+// barrier that is not enqueued yet.
+void harvest_if_full(dlc_engine* e) {
+  if (e->pending.size() > 8192) harvest(e);
+}
+
 // Brackets one phase on the engine stream when timing is on.
 void phase_begin(dlc_engine* e) {
   if (!e->timing) return;
-  if (e->pending.size() > 8192) harvest(e);
   e->open_ev = pooled_event(e);
   DLC_CUDA(cudaEventRecord(e->open_ev, e->stream));
 }
@@ -181,8 +144,11 @@ void phase_end(dlc_engine* e, int phase) {
 // DLC_TRACE=1: events around every op of the pipelined P2P step, printed to
 // stderr as a timeline (ms from the step start) once the step completes.
 bool tracing() {
-  const char* s = std::getenv("DLC_TRACE");
-  return s && s[0] == '1';
+  static const bool on = [] {
+    const char* s = std::getenv("DLC_TRACE");
+    return s && s[0] == '1';
+  }();
+  return on;
 }
 
 cudaEvent_t trace_begin(dlc_engine* e, cudaStream_t s) {
@@ -279,6 +245,7 @@ float* writable(dlc_engine* e, int which) {
 }
 
 void engine_inner(dlc_engine* e, const float* grad, int grad_is_scaled) {
+  harvest_if_full(e);
   if (e->issued_inner >= e->cfg.total_inner_steps) fail(DLC_EINVAL, "inner_step called after total_inner_steps");
   ensure_tables(e, e->issued_inner + 2);
   const float* g = grad;
@@ -342,15 +309,28 @@ void fill_report(dlc_engine* e, dlc_collective* c, dlc_reduce_report* rep, uint6
   rep->contributors = e->k;  // the survivor count after a membership change (collective.cpp:1378-1389)
   rep->attempts = 1 + e->failed_tries;
   if (e->k > 1) {
-    const uint64_t bytes = 2ull * (e->k - 1) * e->S * elem_width(e->prec);
-    rep->data_bytes_sent = rep->data_bytes_received = bytes;
-    rep->wire_bytes_sent = rep->wire_bytes_received = bytes;
+    // data bytes: the reference's exact per-peer accounting over
+    // partition_ranges (reduce.cpp:91-104); wire bytes: what this transport
+    // moved, the owner slots padded to 512 elements (2(K-1) S w each way)
+    const int rank = c ? c->rank : 0;
+    rep->data_bytes_sent = dlc_per_peer_reduce_bytes(e->n, e->k, (size_t)rank, e->prec);
+    rep->data_bytes_received = per_peer_reduce_bytes_received(e->n, e->k, (size_t)rank, e->prec);
+    rep->wire_bytes_sent = rep->wire_bytes_received = 2ull * (e->k - 1) * e->S * elem_width(e->prec);
     DLC_CUDA(cudaEventSynchronize(e->ev1));
     float ms = 0;
     DLC_CUDA(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
     rep->wall_ms = ms;
   }
-  (void)c;
+}
+
+// What one peer receives in the reference's round: its own range from each of
+// the K - 1 others (scatter), then every other range once (ring all-gather);
+// summed over the fleet it equals the bytes sent, 2(K-1) * payload
+// (fleet_reduce_bytes, reduce.cpp:106-111).
+uint64_t per_peer_reduce_bytes_received(size_t n, size_t k, size_t rank, int precision) {
+  if (k <= 1) return 0;
+  const uint64_t len = n / k + (rank < n % k ? 1 : 0);  // partition_ranges, reduce.cpp:20-31
+  return ((k - 1) * len + (n - len)) * elem_width(precision);
 }
 
 // Owner slot S for k workers: ceil(n / k) rounded up to 64 elements per P2P piece.
@@ -428,3 +408,33 @@ void outer_result(dlc_engine* e, dlc_outer_result* res) {
 }
 
 }  // namespace dlc
+
+using namespace dlc;
+
+extern "C" {
+
+int dlc_p2p_set_tuning(const dlc_p2p_tuning* t) {
+  return guard([&] {
+    dlc_p2p_tuning v{};
+    if (t) {
+      v = *t;
+      if (v.plan_len > 32) fail(DLC_ECONFIG, "p2p tuning: at most 32 pieces");
+      for (uint32_t i = 0; i < v.plan_len; ++i)
+        if (v.plan[i] == 0 || v.plan[i] > 1024) fail(DLC_ECONFIG, "p2p tuning: piece weights must be 1..1024");
+      if (v.fold_threads != 0 && v.fold_threads != 128 && v.fold_threads != 256 && v.fold_threads != 512)
+        fail(DLC_ECONFIG, "p2p tuning: fold_threads must be 128, 256 or 512");
+      if (v.fold_ctas < 0 || v.piece_ctas < 0) fail(DLC_ECONFIG, "p2p tuning: negative CTA count");
+    }
+    std::lock_guard<std::mutex> lock(g_tuning_mu);
+    g_tuning = v;
+  });
+}
+
+int dlc_p2p_get_tuning(dlc_p2p_tuning* t) {
+  return guard([&] {
+    if (!t) fail(DLC_EINVAL, "dlc_p2p_get_tuning: null argument");
+    *t = tuning();
+  });
+}
+
+}  // extern "C"

@@ -124,31 +124,27 @@ void launch_nesterov_outer(Pair theta_t, Pair buf, Pair theta_local,
 // `ctas` > 0 runs a persistent grid of that many CTAs (0: one CTA per window).
 void launch_fold_push(const PtrList& in, int k, int precision, const PtrList& outs, int nout,
                       const PtrList& flags, int nflags, size_t n, int ctas, cudaStream_t s);
-// Fleet barrier over NVLink flags (DLC_MODE_P2P): one CTA stores `epoch` into
-// slot `me` of every peer's signal array (`remote`, after a system fence), then
-// waits until every peer's store has landed in `local`.  A peer silent for
-// `timeout_ns` (globaltimer; NodeOptions::reduce_timeout_ms, collective.hpp)
-// sets *err and the kernel exits instead of hanging the GPU; once *err is set
-// (this round already failed) later barriers neither signal nor wait.
-// `stall` (fault injection, the reference's set_stage_hook) makes this rank
-// stop arriving: it sets *err without signalling its peers.
-// fold_push with the bulk-copy engine (TMA) moving the tiles; false when k is outside 2..8
-// (the caller then uses launch_fold_push)
+// fold_push with the bulk-copy engine (TMA) moving the tiles, `threads` per CTA
+// (128 / 256 / 512); false when k is outside 2..8 (the caller then uses
+// launch_fold_push)
 bool launch_fold_push_tma(const PtrList& in, int k, int precision, const PtrList& outs, int nout,
-                          const PtrList& flags, int nflags, size_t n, int ctas, cudaStream_t s);
-// push/push mover: rows src[q] -> dst[q] (`bytes` each, a multiple of 16), a persistent grid of `ctas`
-void launch_scatter_push(const PtrList& src, const PtrList& dst, int nrow, size_t bytes, int ctas, cudaStream_t s);
+                          const PtrList& flags, int nflags, size_t n, int ctas, int threads, cudaStream_t s);
+// Fleet barrier over NVLink flags (DLC_MODE_P2P): one CTA stores the barrier's
+// signal into slot `me` of every peer's signal array (`remote`, after a system
+// fence), then waits until every peer's signal has landed in `local`.  A peer
+// silent for `timeout_ns` (globaltimer; NodeOptions::reduce_timeout_ms,
+// collective.hpp) sets *err and the kernel exits instead of hanging the GPU;
+// once *err is set (this round already failed) later barriers neither signal
+// nor wait.  A signal is (epoch << 1) | error bit.  `commit` (the last barrier
+// of a step): a failed rank still signals, with its error bit set, and a rank
+// that receives an error bit sets *err, so every rank's finish gate sees the
+// failure.  `stall` (fault injection, the reference's set_stage_hook) makes
+// this rank stop arriving: it sets *err without signalling its peers.
 void launch_flag_barrier(const PtrList& remote, const uint64_t* local, int k, int me, uint64_t epoch,
-                         int* err, uint64_t timeout_ns, bool stall, cudaStream_t s);
+                         int* err, uint64_t timeout_ns, bool stall, bool commit, cudaStream_t s);
 void launch_pseudo_grad_piece(Pair theta_t, Pair theta_local, const DevState* st, void* send,
                               int precision, int k, size_t S, size_t po, size_t plen, size_t n,
                               int ctas, cudaStream_t s);
-// K2 piece with the scatter fused in: the delta of owner q's slot is stored
-// straight into `rows.ptr[q]` (this rank's row of owner q's recv buffer, a
-// peer pointer for q != me), ending with a system fence per CTA.
-void launch_pseudo_grad_push_piece(Pair theta_t, Pair theta_local, const DevState* st,
-                                   const PtrList& rows, int precision, int k, size_t S, size_t po,
-                                   size_t plen, size_t n, cudaStream_t s);
 void launch_nesterov_p2p_piece(Pair theta_t, Pair buf, Pair theta_local, const PtrList& slots,
                                int k, size_t S, size_t po, size_t plen, int precision,
                                DevState* st, float lr, float mu, size_t n, int ctas, cudaStream_t s);

@@ -1,7 +1,7 @@
 // kernels_fold.cu — K3: the rank-ordered fold of the cross-worker average
 // (reduce.cpp:33-89, collective.cpp:1444-1489) on local rows, fused with the
-// push of the mean to every rank (per-thread and TMA bulk-copy versions), the
-// push/push scatter, and the NVLink flag barrier of the P2P step.
+// push of the mean to every rank (per-thread and TMA bulk-copy versions), and
+// the NVLink flag barrier of the P2P step.
 #include <algorithm>
 #include <atomic>
 #include <cstdlib>
@@ -401,49 +401,42 @@ __global__ void __launch_bounds__(NT) fold_push_tma_kernel(const __grid_constant
 
 size_t fold_push_tma_smem(int k) { return (size_t)kTmaStages * (k + 1) * kTmaTileBytes + kTmaStages * 8; }
 
-// Scatter half of the push/push P2P mover: row q of `src` (this rank's piece of
-// owner q's slot, in local HBM) is stored into row `me` of owner q's receive
-// buffer over NVLink.  Consecutive 16-byte vectors go to different owners so
-// every link carries traffic at once.
-__global__ void __launch_bounds__(kThreads) scatter_push_kernel(const __grid_constant__ PtrList src,
-                                                                const __grid_constant__ PtrList dst, int nrow,
-                                                                size_t bytes) {
-  const size_t n16 = bytes / 16, total = n16 * (size_t)nrow;
-  for (size_t i = gtid(); i < total; i += gstride()) {
-    const int q = (int)(i % (size_t)nrow);
-    const size_t j = i / (size_t)nrow;
-    const uint4 v = ld_stream(reinterpret_cast<const uint4*>(src.ptr[q]) + j);
-    st_stream(reinterpret_cast<uint4*>(const_cast<void*>(dst.ptr[q])) + j, v);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) __threadfence_system();  // the CTA's stores land before the barrier that follows
-}
-
 // ---- NVLink flag barrier ----------------------------------------------------
 __global__ void flag_barrier_kernel(const __grid_constant__ PtrList remote, const uint64_t* local, int k, int me,
-                                    uint64_t epoch, int* err, uint64_t timeout_ns, int stall) {
+                                    uint64_t epoch, int* err, uint64_t timeout_ns, int stall, int commit) {
   const int j = threadIdx.x;
   __shared__ int s_failed;
   if (j == 0) {
     s_failed = *reinterpret_cast<volatile int*>(err);
-    if (stall && !s_failed) {  // fault injection: stop arriving, fail this rank's round
+    if (stall) {  // fault injection: stop arriving, fail this rank's round
       atomicExch(err, 1);
-      s_failed = 1;
+      s_failed = 2;
     }
   }
   __syncthreads();
-  if (s_failed) return;  // the round already failed: no signal, no wait
+  const int failed = s_failed;
+  if (failed) {
+    // the round already failed here: no wait; at the commit barrier tell the
+    // peers (a stalled rank stays silent, as a dead peer would)
+    if (commit && failed == 1 && j < k && j != me) {
+      __threadfence_system();
+      *reinterpret_cast<volatile unsigned long long*>(const_cast<void*>(remote.ptr[j])) = (epoch << 1) | 1ull;
+    }
+    return;
+  }
   if (j < k && j != me) {
     __threadfence_system();  // everything this GPU wrote before the barrier is visible first
-    *reinterpret_cast<volatile unsigned long long*>(const_cast<void*>(remote.ptr[j])) = epoch;
+    *reinterpret_cast<volatile unsigned long long*>(const_cast<void*>(remote.ptr[j])) = epoch << 1;
     const uint64_t start = globaltimer_ns();
     const volatile unsigned long long* mine = reinterpret_cast<const volatile unsigned long long*>(local + j);
-    while (*mine < epoch) {
+    unsigned long long v;
+    while (((v = *mine) >> 1) < epoch) {
       if (globaltimer_ns() - start > timeout_ns) {  // a peer stopped participating
         atomicExch(err, 1);
         break;
       }
     }
+    if (commit && (v >> 1) == epoch && (v & 1ull)) atomicExch(err, 1);  // a peer's round failed
     __threadfence_system();
   }
   __syncthreads();
@@ -489,26 +482,11 @@ void launch_fold_push(const PtrList& in, int k, int precision, const PtrList& ou
 #undef DLC_FOLD_PUSH
 }
 
-// DLC_TMA_THREADS: 128, 256 or 512 threads per TMA fold CTA.  Default by K:
-// an owner decodes about N contributions per step whatever K is, but the CTA
-// count falls as 320 / K (the in-flight bytes rule), so the fold needs more
-// warps per CTA as K grows.  At K = 4 the 4-GPU A/B put the optimum at about
-// 80 "128-thread CTA equivalents" (80 x 128 or 48 x 512; 48 x 128 and 64 x 128
-// were 20% / 12% slower, profiles/r1_ab_tma_threads_ctas_4gpu.log); K >= 5 keeps
-// that capacity with 256 / 512 threads.  K >= 5 is extrapolated: this pool's
-// boxes have at most 4 GPUs.
-static int tma_threads(int k) {
-  if (const char* v = std::getenv("DLC_TMA_THREADS")) return (int)std::strtol(v, nullptr, 10);
-  return k <= 4 ? kTmaThreads : (k <= 6 ? 256 : 512);
-}
-
 bool launch_fold_push_tma(const PtrList& in, int k, int precision, const PtrList& outs, int nout,
-                          const PtrList& flags, int nflags, size_t n, int ctas, cudaStream_t s) {
+                          const PtrList& flags, int nflags, size_t n, int ctas, int threads, cudaStream_t s) {
   const size_t smem = fold_push_tma_smem(k);
-  const int nt = tma_threads(k);
-  // reduce.cpp:36, 43; DLC_FOLD_DIV=1 keeps the IEEE division for power-of-two K too (A/B knob)
-  MeanDiv md = mean_div(k);
-  if (const char* v = std::getenv("DLC_FOLD_DIV"); v && v[0] == '1') md.inv = 0.0f;
+  const int nt = threads;
+  const MeanDiv md = mean_div(k);  // reduce.cpp:36, 43
   const int W = precision == 1 ? 2 : 4;
   const size_t ntiles = (n + kTmaTileBytes / W - 1) / (kTmaTileBytes / W);
   const int grid = (int)std::max<size_t>(1, std::min<size_t>(ctas > 0 ? ctas : num_sms(), ntiles));
@@ -553,16 +531,9 @@ bool launch_fold_push_tma(const PtrList& in, int k, int precision, const PtrList
 #undef DLC_TMA_NT
 }
 
-void launch_scatter_push(const PtrList& src, const PtrList& dst, int nrow, size_t bytes, int ctas, cudaStream_t s) {
-  const size_t vecs = bytes / 16 * (size_t)nrow;
-  const int grid = (int)std::max<size_t>(1, std::min<size_t>(ctas > 0 ? ctas : 4 * num_sms(), (vecs + kThreads - 1) / kThreads));
-  scatter_push_kernel<<<grid, kThreads, 0, s>>>(src, dst, nrow, bytes);
-}
-
 void launch_flag_barrier(const PtrList& remote, const uint64_t* local, int k, int me, uint64_t epoch, int* err,
-                         uint64_t timeout_ns, bool stall,
-                         cudaStream_t s) {
-  flag_barrier_kernel<<<1, 32, 0, s>>>(remote, local, k, me, epoch, err, timeout_ns, stall ? 1 : 0);
+                         uint64_t timeout_ns, bool stall, bool commit, cudaStream_t s) {
+  flag_barrier_kernel<<<1, 32, 0, s>>>(remote, local, k, me, epoch, err, timeout_ns, stall ? 1 : 0, commit ? 1 : 0);
 }
 
 }  // namespace dlc

@@ -190,44 +190,6 @@ __global__ void __launch_bounds__(kThreads) pseudo_grad_piece_kernel(Pair ttp, P
 }
 
 template <int PREC>
-__global__ void __launch_bounds__(kThreads) pseudo_grad_push_piece_kernel(Pair ttp, Pair tl, const DevState* st,
-                                                                          const __grid_constant__ PtrList rows, int k,
-                                                                          size_t S, size_t po, size_t plen,
-                                                                          size_t n) {
-  const int q = (int)(blockIdx.x % (unsigned)k);
-  const size_t j = (size_t)(blockIdx.x / (unsigned)k) * kThreads + threadIdx.x;
-  const size_t e0 = (size_t)q * S + po + 4 * j;  // global element
-  const size_t o0 = po + 4 * j;                  // offset inside owner q's row
-  void* row = const_cast<void*>(rows.ptr[q]);
-  if (4 * j < plen && e0 < n) {
-    const float* T = sel(ttp, st->ocur);
-    const float* L = local_src(tl, ttp, st);
-    if (e0 + 3 < n) {
-      const float4 x = ld_stream(reinterpret_cast<const float4*>(T + e0));
-      const float4 y = ld_stream(reinterpret_cast<const float4*>(L + e0));
-      const float4 d = make_float4(delta_elem(x.x, y.x), delta_elem(x.y, y.y), delta_elem(x.z, y.z),
-                                   delta_elem(x.w, y.w));
-      if (PREC == 0) {
-        st_stream(reinterpret_cast<float4*>(static_cast<float*>(row) + o0), d);
-      } else {
-        st_stream(reinterpret_cast<uint2*>(static_cast<uint16_t*>(row) + o0),
-                  make_uint2(pack2(fp16_encode(d.x), fp16_encode(d.y)), pack2(fp16_encode(d.z), fp16_encode(d.w))));
-      }
-    } else {
-      for (size_t e = e0; e < n; ++e) {
-        const float d = delta_elem(T[e], L[e]);
-        if (PREC == 0)
-          static_cast<float*>(row)[o0 + (e - e0)] = d;
-        else
-          static_cast<uint16_t*>(row)[o0 + (e - e0)] = fp16_encode(d);
-      }
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) __threadfence_system();  // the CTA's stores land before the barrier that follows
-}
-
-template <int PREC>
 __device__ __forceinline__ void nesterov_p2p_piece_block(const float* T, const float* B, float* To, float* Bo, float* L,
                                                          const PtrList& slots, size_t blk, int k, size_t S, size_t po,
                                                          size_t plen, float lr, float mu, size_t n) {
@@ -407,15 +369,6 @@ void launch_pseudo_grad_piece(Pair tt, Pair tl, const DevState* st, void* send, 
     pseudo_grad_piece_kernel<0><<<grid, kThreads, 0, s>>>(tt, tl, st, send, k, S, po, plen, n, nblk);
   else
     pseudo_grad_piece_kernel<1><<<grid, kThreads, 0, s>>>(tt, tl, st, send, k, S, po, plen, n, nblk);
-}
-
-void launch_pseudo_grad_push_piece(Pair tt, Pair tl, const DevState* st, const PtrList& rows, int precision, int k,
-                                   size_t S, size_t po, size_t plen, size_t n, cudaStream_t s) {
-  const int grid = (int)(std::max<size_t>(1, (plen / 4 + kThreads - 1) / kThreads) * (size_t)k);
-  if (precision == 0)
-    pseudo_grad_push_piece_kernel<0><<<grid, kThreads, 0, s>>>(tt, tl, st, rows, k, S, po, plen, n);
-  else
-    pseudo_grad_push_piece_kernel<1><<<grid, kThreads, 0, s>>>(tt, tl, st, rows, k, S, po, plen, n);
 }
 
 void launch_nesterov_p2p_piece(Pair tt, Pair buf, Pair tl, const PtrList& slots, int k, size_t S, size_t po,

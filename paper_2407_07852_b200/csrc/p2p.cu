@@ -20,6 +20,10 @@ namespace dlc {
 void p2p_unbind(dlc_engine* e) {
   for (void* p : e->ipc_opened) cudaIpcCloseMemHandle(p);
   e->ipc_opened.clear();
+  if (e->p2p_bound) {
+    auto& b = const_cast<dlc_collective*>(e->p2p_bound)->bound;
+    b.erase(std::remove(b.begin(), b.end(), e), b.end());
+  }
   e->p2p_bound = nullptr;
 }
 
@@ -30,12 +34,11 @@ void p2p_bind(dlc_engine* e, dlc_collective* c) {
   p2p_unbind(e);
   const int K = (int)e->k, r = c->rank;
   struct Handles {
-    cudaIpcMemHandle_t send, gather, flags, sig, recv;
+    cudaIpcMemHandle_t send, gather, flags, sig;
     uint64_t sig_epoch;
   };
   Handles mine;
   mine.sig_epoch = e->sig_epoch;
-  DLC_CUDA(cudaIpcGetMemHandle(&mine.recv, e->recv));
   DLC_CUDA(cudaIpcGetMemHandle(&mine.send, e->send));
   DLC_CUDA(cudaIpcGetMemHandle(&mine.gather, e->gather));
   DLC_CUDA(cudaIpcGetMemHandle(&mine.flags, e->flags));
@@ -64,14 +67,8 @@ void p2p_bind(dlc_engine* e, dlc_collective* c) {
       e->peer_gather[j] = e->gather;
       e->peer_flags[j] = e->flags;
       e->peer_sig[j] = e->sig;
-      e->peer_recv[j] = e->recv;
       continue;
     }
-    void* precv = nullptr;
-    check_cuda(cudaIpcOpenMemHandle(&precv, all[j].recv, cudaIpcMemLazyEnablePeerAccess),
-               "cudaIpcOpenMemHandle (recv rows)");
-    e->ipc_opened.push_back(precv);
-    e->peer_recv[j] = precv;
     void* psig = nullptr;
     check_cuda(cudaIpcOpenMemHandle(&psig, all[j].sig, cudaIpcMemLazyEnablePeerAccess),
                "cudaIpcOpenMemHandle (signal slots)");
@@ -92,6 +89,7 @@ void p2p_bind(dlc_engine* e, dlc_collective* c) {
     e->peer_flags[j] = (int*)pf;
   }
   e->p2p_bound = c;
+  c->bound.push_back(e);
 }
 
 // Stream-ordered fleet barrier: a 4-byte NCCL all-reduce.
@@ -99,25 +97,18 @@ void fleet_barrier(dlc_engine* e, dlc_collective* c) {
   DLC_NCCL(ncclAllReduce(e->barrier_buf, e->barrier_buf, 1, ncclInt32, ncclSum, c->comm, e->stream));
 }
 
-// Phase barrier of the P2P step on stream `s`: NVLink flags by default
-// (one CTA, a few microseconds), DLC_P2P_BARRIER=nccl for the NCCL all-reduce.
-bool flag_barriers(const dlc_collective* c) {
-  const char* b = std::getenv("DLC_P2P_BARRIER");
-  return !(b && std::string(b) == "nccl" && !c->in_world);  // (one thread drives a world: flags only)
-}
-
-void p2p_barrier(dlc_engine* e, dlc_collective* c, cudaStream_t s) {
-  if (!flag_barriers(c)) {
-    DLC_NCCL(ncclAllReduce(e->barrier_buf, e->barrier_buf, 1, ncclInt32, ncclSum, c->comm, s));
-    return;
-  }
+// Phase barrier of the P2P step on stream `s`: NVLink flags (one CTA, a few
+// microseconds), also the failure detector.  `commit`: the last barrier of a
+// step, whose signals carry the ranks' error bits (every rank's finish gate
+// then aborts if any rank's round failed).
+void p2p_barrier(dlc_engine* e, dlc_collective* c, cudaStream_t s, bool commit) {
   PtrList remote{};
   for (size_t j = 0; j < e->k; ++j) remote.ptr[j] = e->peer_sig[j] + c->rank;
   e->sig_epoch += 1;
   const bool stall = c->stall_at >= 0 && c->barriers >= c->stall_at;
   c->barriers += 1;
   launch_flag_barrier(remote, e->sig, (int)e->k, c->rank, e->sig_epoch, e->sig_err, c->timeout_ms * 1000000ull, stall,
-                      s);
+                      commit, s);
   launched("flag_barrier");
 }
 
@@ -170,277 +161,241 @@ void outer_collective(dlc_engine* e, dlc_collective* c, dlc_reduce_report* rep) 
   }
 }
 
-// DLC_MODE_P2P: the rank-ordered owner fold fused with its own data movement
-// over NVLink peer memory (CUDA IPC), pipelined over the pieces of piece_plan()
-// (piece p = the same sub-range of every owner slot):
-//   main     K2(p) into my send buffer                                 -> evK2[p]
-//   cstream  wait evK2[p]; barrier A_p (every rank's K2(p) is done);
-//            fold_push(p): the owner pulls piece p of slot r from every rank,
-//            folds in rank order, pushes the mean + a non-finite mark into
-//            slot r of every rank's gather buffer; barrier B_p          -> evB[p]
-//   main     wait evB[p]; K4(p) speculative into the idle theta_t / momentum;
-//            ...; finish (flip ocur when every owner flag is clean)
-// The fold kernel keeps DLC_COMM_CTAS CTAs, so the NVLink time of piece p
-// overlaps the HBM-bound K2 / K4 pieces on the other SMs.  Other movers
-// (DLC_P2P_COPY): "ce" pulls / gathers with the copy engines around a local
-// fold; "push" stores K2's rows straight into the owners' receive buffers;
-// "push2" pushes them from a scatter kernel on the comm stream.  A_p orders
-// every rank's K2(p) (and, for p = 0, every rank's previous finish) before
-// anyone reads them; B_p orders every push of piece p before any K4(p).  With
-// host buffers (`hsrc` / `hdst`) piece p is also copied in before K2(p) and its
-// new theta_t copied out after K4(p).
-void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc_reduce_report* rep,
-                         const float* hsrc, float* hdst, int oc_host) {
-  p2p_bind(e, c);
-  const size_t K = e->k, S = e->S, w = elem_width(e->prec), n = e->n;
-  const int r = c->rank;
+// ---- DLC_MODE_P2P: the pipelined outer step, in stages ----------------------
+// The rank-ordered owner fold fused with its own data movement over NVLink peer
+// memory, pipelined over the pieces of piece_plan() (piece p = the same
+// sub-range of every owner slot):
+//   main     K2(p) into my send buffer                               -> evK2[p]
+//   cstream  [every rank's K2(p) done]; fold(p): the owner pulls piece p of
+//            slot r from every rank (TMA bulk copies over NVLink), folds in
+//            rank order, pushes the mean + a non-finite mark into slot r of
+//            every rank's gather buffer                              -> evB[p]
+//   main     [every rank's fold(p) done]; K4(p) speculative into the idle
+//            theta_t / momentum; ...; finish (flip ocur when every owner
+//            flag is clean)
+// The two "every rank" conditions are the only synchronisation.  One process
+// per GPU (outer_p2p_pipelined) makes them NVLink flag barriers on the comm
+// stream: barrier A_p before fold(p), B_p after it, B_p doubling as A_{p+1}
+// once our K2(p+1) is done, plus a commit barrier that exchanges the ranks'
+// error bits before the finish gate.  One thread driving every rank
+// (world.cu) makes them cudaEvent dependencies between the ranks' streams,
+// so any number of ranks may share a device.  The fold keeps a few dozen CTAs,
+// so its NVLink time overlaps the HBM-bound K2 / K4 pieces on the other SMs.
+// With host buffers (`hsrc` / `hdst`) piece p is also copied in before K2(p)
+// and its new theta_t copied out after K4(p).
+P2PStep p2p_begin(dlc_engine* e, int rank, const float* src, bool rep, const float* hsrc, float* hdst,
+                  int oc_host) {
+  P2PStep s;
+  s.e = e;
+  s.rank = rank;
+  s.K = e->k;
+  s.S = e->S;
+  s.w = elem_width(e->prec);
+  s.n = e->n;
+  s.hsrc = hsrc;
+  s.hdst = hdst;
+  s.oc_host = oc_host;
+  s.rep = rep;
   if (!e->cstream) {
     int lo = 0, hi = 0;
     DLC_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     DLC_CUDA(cudaStreamCreateWithPriority(&e->cstream, cudaStreamNonBlocking, hi));
-    DLC_CUDA(cudaStreamCreateWithPriority(&e->sstream, cudaStreamNonBlocking, hi));
   }
-  if (!p2p_mover_sm() && !e->pull[0]) {  // copy-engine mover: one pull and one gather stream per peer
-    for (size_t j = 0; j < K; ++j) {
-      DLC_CUDA(cudaStreamCreateWithFlags(&e->pull[j], cudaStreamNonBlocking));
-      DLC_CUDA(cudaStreamCreateWithFlags(&e->gath[j], cudaStreamNonBlocking));
-    }
-  }
-  const std::vector<size_t> pb = piece_plan(S, n, hsrc != nullptr);  // piece boundaries inside a slot
-  const size_t P = pb.size() - 1;
-  auto po = [&](size_t p) { return pb[p]; };
-  auto pl = [&](size_t p) { return pb[p + 1] - pb[p]; };
-  const size_t nev = 5 * P + 2 * K * P + 1;
+  s.pb = piece_plan(s.S, s.n, hsrc != nullptr);
+  s.P = s.pb.size() - 1;
+  const size_t nev = 4 * s.P + 2;
   while (e->piece_ev.size() < nev) {
     cudaEvent_t ev;
     DLC_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     e->piece_ev.push_back(ev);
   }
-  cudaEvent_t* evK2 = e->piece_ev.data();
-  cudaEvent_t* evA = evK2 + P;
-  cudaEvent_t* evB = evA + P;
-  cudaEvent_t* evH = evB + P;
-  cudaEvent_t* evK4 = evH + P;
-  cudaEvent_t* evPull = evK4 + P;       // [j * P + p]
-  cudaEvent_t* evGath = evPull + K * P;  // [q * P + p]
-  cudaEvent_t evStart = evGath[K * P];
-  float* s = const_cast<float*>(src);
-  const Pair tl = s ? Pair{{s, s}} : local_pair(e);
-  const float lr = e->hyper.outer_lr, mu = e->hyper.outer_momentum;
-  char* send = static_cast<char*>(e->send);
-  char* recv = static_cast<char*>(e->recv);
-  char* gather = static_cast<char*>(e->gather);
-  const bool push_mover = p2p_mover_push();
-  auto rows = [&](size_t p, auto&& fn) {  // piece p of every owner slot, clipped to n
-    for (size_t q = 0; q < K; ++q) {
-      const size_t lo = q * S + po(p);
-      if (lo >= n) break;
-      fn(lo, std::min(pl(p), n - lo));
-    }
-  };
+  s.evK2 = e->piece_ev.data();
+  s.evB = s.evK2 + s.P;
+  s.evH = s.evB + s.P;
+  s.evK4 = s.evH + s.P;
+  s.evStart = s.evK4[s.P];
+  s.evCommit = s.evK4[s.P + 1];
+  float* sp = const_cast<float*>(src);
+  s.tl = sp ? Pair{{sp, sp}} : local_pair(e);
+  for (size_t q = 0; q < s.K; ++q) {  // K4 reads the means from the local gather buffer
+    s.slots.ptr[q] = static_cast<char*>(e->gather) + q * s.S * s.w;
+    s.fl.ptr[q] = e->flags + q;  // owner q's non-finite mark, pushed here by owner q
+  }
   if (rep) DLC_CUDA(cudaEventRecord(e->ev0, e->stream));
-  // SM mover: owners push non-finite marks into this array after A_0, which
-  // every rank reaches only after this memset (it precedes our K2(0))
-  if (p2p_mover_sm()) DLC_CUDA(cudaMemsetAsync(e->flags, 0, kMaxK * sizeof(int), e->stream));
-  cudaEvent_t origin = trace_begin(e, e->stream);
-  DLC_CUDA(cudaEventRecord(evStart, e->stream));
+  // owners push their marks into this array after every rank's K2(0), which
+  // follows this memset on every rank
+  DLC_CUDA(cudaMemsetAsync(e->flags, 0, kMaxK * sizeof(int), e->stream));
+  s.origin = trace_begin(e, e->stream);
+  DLC_CUDA(cudaEventRecord(s.evStart, e->stream));
   if (hsrc) {
     ensure_copy_streams(e);
-    DLC_CUDA(cudaStreamWaitEvent(e->h2d, evStart, 0));  // staging buffer free
+    DLC_CUDA(cudaStreamWaitEvent(e->h2d, s.evStart, 0));  // staging buffer free
   }
-  const bool sm_mover = p2p_mover_sm();
-  const bool push2 = p2p_mover_push2();
-  const bool k4_pull = sm_mover && p2p_k4_pull();
-  const bool merge = p2p_merge_barriers();
-  cudaEvent_t* evS = evA;  // (evA is only used by the copy-engine mover)
-  auto k2_piece = [&](size_t p) {
-    if (hsrc) {
-      rows(p, [&](size_t lo, size_t len) {
-        DLC_CUDA(cudaMemcpyAsync(s + lo, hsrc + lo, len * sizeof(float), cudaMemcpyHostToDevice, e->h2d));
-      });
-      DLC_CUDA(cudaEventRecord(evH[p], e->h2d));
-      DLC_CUDA(cudaStreamWaitEvent(e->stream, evH[p], 0));
-    }
-    cudaEvent_t t0 = trace_begin(e, e->stream);
-    if (push_mover) {
-      PtrList rows{};  // my row in every owner's recv buffer
-      for (size_t q = 0; q < K; ++q) rows.ptr[q] = static_cast<char*>(e->peer_recv[q]) + r * S * w;
-      launch_pseudo_grad_push_piece(tt_pair(e), tl, e->st, rows, e->prec, (int)K, S, po(p), pl(p), n, e->stream);
-    } else {
-      launch_pseudo_grad_piece(tt_pair(e), tl, e->st, e->send, e->prec, (int)K, S, po(p), pl(p), n, piece_ctas(),
-                               e->stream);
-    }
-    trace_end(e, e->stream, "K2", (int)p, t0);
-    DLC_CUDA(cudaEventRecord(evK2[p], e->stream));
-  };
-  auto scatter_piece = [&](size_t p) {
-    // push/push: our piece of every foreign slot into its owner's recv row r, on
-    // its own stream so that scatter(p + 1) overlaps fold(p): every NVLink byte
-    // is a remote store and both link directions stay busy
-    DLC_CUDA(cudaStreamWaitEvent(e->sstream, evK2[p], 0));
-    PtrList src{}, dst{};
-    int nrow = 0;
-    for (size_t q = 0; q < K; ++q) {
-      if ((int)q == r) continue;
-      src.ptr[nrow] = send + (q * S + po(p)) * w;
-      dst.ptr[nrow] = static_cast<char*>(e->peer_recv[q]) + (r * S + po(p)) * w;
-      ++nrow;
-    }
-    cudaEvent_t ts = trace_begin(e, e->sstream);
-    launch_scatter_push(src, dst, nrow, pl(p) * w, comm_ctas(), e->sstream);
-    trace_end(e, e->sstream, "scatter", (int)p, ts);
-    DLC_CUDA(cudaEventRecord(evS[p], e->sstream));
-  };
+  return s;
+}
+
+// piece p of every owner slot, clipped to n
+template <typename F>
+static void piece_rows(const P2PStep& s, size_t p, F&& fn) {
+  for (size_t q = 0; q < s.K; ++q) {
+    const size_t lo = q * s.S + s.pb[p];
+    if (lo >= s.n) break;
+    fn(lo, std::min(s.pb[p + 1] - s.pb[p], s.n - lo));
+  }
+}
+
+void p2p_k2(P2PStep& s, size_t p) {
+  dlc_engine* e = s.e;
+  if (s.hsrc) {
+    float* stage = s.tl.ptr[0];
+    piece_rows(s, p, [&](size_t lo, size_t len) {
+      DLC_CUDA(cudaMemcpyAsync(stage + lo, s.hsrc + lo, len * sizeof(float), cudaMemcpyHostToDevice, e->h2d));
+    });
+    DLC_CUDA(cudaEventRecord(s.evH[p], e->h2d));
+    DLC_CUDA(cudaStreamWaitEvent(e->stream, s.evH[p], 0));
+  }
+  cudaEvent_t t0 = trace_begin(e, e->stream);
+  launch_pseudo_grad_piece(tt_pair(e), s.tl, e->st, e->send, e->prec, (int)s.K, s.S, s.pb[p], s.pb[p + 1] - s.pb[p],
+                           s.n, piece_ctas(), e->stream);
+  trace_end(e, e->stream, "K2", (int)p, t0);
+  DLC_CUDA(cudaEventRecord(s.evK2[p], e->stream));
+}
+
+void p2p_fold_begin(P2PStep& s) {
+  dlc_engine* e = s.e;
+  s.c0 = pooled_event(e);
+  s.c1 = pooled_event(e);
+  DLC_CUDA(cudaStreamWaitEvent(e->cstream, s.evStart, 0));
+  DLC_CUDA(cudaEventRecord(s.c0, e->cstream));
+}
+
+// The owner fold of piece p on the comm stream (the caller orders it after
+// every rank's K2(p)): slot r / piece p of every rank's delta in, the mean and
+// the non-finite mark out to every rank.
+void p2p_fold(P2PStep& s, size_t p) {
+  dlc_engine* e = s.e;
+  const size_t K = s.K, S = s.S, w = s.w, po = s.pb[p], plen = s.pb[p + 1] - s.pb[p];
+  const int r = s.rank;
+  PtrList in{}, outs{}, pfl{};
+  for (size_t j = 0; j < K; ++j) {
+    in.ptr[j] = static_cast<char*>(e->peer_send[j]) + (r * S + po) * w;
+    outs.ptr[j] = static_cast<char*>(e->peer_gather[j]) + (r * S + po) * w;
+    pfl.ptr[j] = e->peer_flags[j] + r;
+  }
+  cudaEvent_t tf = trace_begin(e, e->cstream);
+  if (!launch_fold_push_tma(in, (int)K, e->prec, outs, (int)K, pfl, (int)K, plen, tma_ctas(K), tma_threads(K),
+                            e->cstream))
+    launch_fold_push(in, (int)K, e->prec, outs, (int)K, pfl, (int)K, plen, kFoldCtas, e->cstream);
+  launched("fold_push");
+  trace_end(e, e->cstream, "fold_push", (int)p, tf);
+}
+
+void p2p_fold_end(P2PStep& s) {
+  dlc_engine* e = s.e;
+  DLC_CUDA(cudaEventRecord(s.c1, e->cstream));
+  if (e->timing) {
+    e->pending.push_back({DLC_PHASE_COLLECTIVE, s.c0, s.c1});
+  } else {
+    e->pool.push_back(s.c0);
+    e->pool.push_back(s.c1);
+  }
+  if (s.rep) DLC_CUDA(cudaEventRecord(e->ev1, e->cstream));
+}
+
+// K4 of piece p on the local gather buffer, speculative into the idle theta_t /
+// momentum; ordered after our own evB[p] (the caller adds the other ranks').
+void p2p_k4(P2PStep& s, size_t p) {
+  dlc_engine* e = s.e;
+  DLC_CUDA(cudaStreamWaitEvent(e->stream, s.evB[p], 0));
+  cudaEvent_t t4 = trace_begin(e, e->stream);
+  // device buffers: each piece is timed on its own (after its wait), so the
+  // OUTER phase sums K4's busy time, not the waits for the means
+  const bool piece_timing = e->timing && !s.hsrc;
+  if (piece_timing) phase_begin(e);
+  launch_nesterov_p2p_piece(tt_pair(e), buf_pair(e), local_pair(e), s.slots, (int)s.K, s.S, s.pb[p],
+                            s.pb[p + 1] - s.pb[p], e->prec, e->st, e->hyper.outer_lr, e->hyper.outer_momentum, s.n,
+                            piece_ctas(), e->stream);
+  launched("nesterov_p2p_piece");
+  if (piece_timing) phase_end(e, DLC_PHASE_OUTER);
+  trace_end(e, e->stream, "K4", (int)p, t4);
+  if (s.hdst) {
+    DLC_CUDA(cudaEventRecord(s.evK4[p], e->stream));
+    DLC_CUDA(cudaStreamWaitEvent(e->d2h, s.evK4[p], 0));
+    piece_rows(s, p, [&](size_t lo, size_t len) {
+      DLC_CUDA(cudaMemcpyAsync(s.hdst + lo, e->theta_t[s.oc_host ^ 1] + lo, len * sizeof(float),
+                               cudaMemcpyDeviceToHost, e->d2h));
+    });
+  }
+}
+
+// The finish gate: flip ocur when every owner's mark is clean; `abort`
+// (nullable) = the round failed on some rank, change nothing.
+void p2p_finish(P2PStep& s, const int* abort) {
+  dlc_engine* e = s.e;
+  if (!s.hsrc) phase_begin(e);
+  launch_p2p_finish(tt_pair(e), local_pair(e), s.fl, (int)s.K, e->st, s.n, abort, e->stream);
+  launched("p2p_finish");
+  phase_end(e, DLC_PHASE_OUTER);
+  trace_dump(e, s.origin);
+}
+
+// One process per GPU: the stages above ordered by NVLink flag barriers.
+void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc_reduce_report* rep,
+                         const float* hsrc, float* hdst, int oc_host) {
+  harvest_if_full(e);  // never inside the step: a host wait there could block on a peer's barrier
+  p2p_bind(e, c);
+  P2PStep s = p2p_begin(e, c->rank, src, rep != nullptr, hsrc, hdst, oc_host);
+  const size_t P = s.P;
+  // barrier B_p (= A_{p+1} once our K2(p+1) is done) after fold(p); the last
+  // one is followed by the commit barrier, which exchanges the error bits so
+  // that every rank's finish gate takes the same decision
   auto fold_piece = [&](size_t p) {
-    if (sm_mover) {
-      // SM mover: a persistent fold kernel on a few CTAs pulls slot r / piece p of
-      // every rank's delta and pushes the mean (and a non-finite mark) into slot r
-      // of every rank's gather buffer (flags reset by each rank before its K2(0)).
-      DLC_CUDA(cudaStreamWaitEvent(e->cstream, push2 ? evS[p] : evK2[p], 0));
-      if (!merge || p == 0) {
-        cudaEvent_t ta = trace_begin(e, e->cstream);
-        p2p_barrier(e, c, e->cstream);  // A_p
-        trace_end(e, e->cstream, "barrierA", (int)p, ta);
-      }
-      PtrList in{}, outs{}, pfl{};
-      for (size_t j = 0; j < K; ++j) {
-        in.ptr[j] = (int)j == r && push2 ? send + (r * S + po(p)) * w  // own row stays local
-                    : (push_mover || push2) ? recv + (j * S + po(p)) * w   // rows already pushed here
-                                            : static_cast<char*>(e->peer_send[j]) + (r * S + po(p)) * w;
-        outs.ptr[j] = static_cast<char*>(e->peer_gather[j]) + (r * S + po(p)) * w;
-        pfl.ptr[j] = e->peer_flags[j] + r;
-      }
-      cudaEvent_t tf = trace_begin(e, e->cstream);
-      // K4 pull: the mean stays in the owner's own gather slot; every rank's K4
-      // reads it from there over NVLink (no remote stores of means)
-      const int nout = k4_pull ? 1 : (int)K;
-      if (k4_pull) outs.ptr[0] = gather + (r * S + po(p)) * w;
-      if (!(fold_tma() && launch_fold_push_tma(in, (int)K, e->prec, outs, nout, pfl, (int)K, pl(p), tma_ctas(K),
-                                               e->cstream)))
-        launch_fold_push(in, (int)K, e->prec, outs, nout, pfl, (int)K, pl(p), comm_ctas(), e->cstream);
-      trace_end(e, e->cstream, "fold_push", (int)p, tf);
-      // merged barriers: B_p also serves as A_{p+1} once our K2(p+1) is done
-      // (it precedes K4(p) on the main stream anyway, so K4(p) waits no longer)
-      if (merge && p + 1 < P) DLC_CUDA(cudaStreamWaitEvent(e->cstream, push2 ? evS[p + 1] : evK2[p + 1], 0));
-      cudaEvent_t tb = trace_begin(e, e->cstream);
-      p2p_barrier(e, c, e->cstream);  // B_p
-      trace_end(e, e->cstream, "barrierB", (int)p, tb);
-      DLC_CUDA(cudaEventRecord(evB[p], e->cstream));
-      return;
+    DLC_CUDA(cudaStreamWaitEvent(e->cstream, s.evK2[p], 0));
+    if (p == 0) {
+      cudaEvent_t ta = trace_begin(e, e->cstream);
+      p2p_barrier(e, c, e->cstream, false);  // A_0
+      trace_end(e, e->cstream, "barrierA", 0, ta);
     }
-    DLC_CUDA(cudaStreamWaitEvent(e->cstream, evK2[p], 0));
-    p2p_barrier(e, c, e->cstream);  // A_p
-    if (p == 0) DLC_CUDA(cudaMemsetAsync(e->flags + r, 0, sizeof(int), e->cstream));
-    DLC_CUDA(cudaEventRecord(evA[p], e->cstream));
-    for (size_t j = 0; j < K; ++j) {  // scatter: pull slot r, piece p of every peer's delta
-      if ((int)j == r) continue;
-      DLC_CUDA(cudaStreamWaitEvent(e->pull[j], evA[p], 0));
-      DLC_CUDA(cudaMemcpyAsync(recv + (j * S + po(p)) * w, static_cast<char*>(e->peer_send[j]) + (r * S + po(p)) * w,
-                               pl(p) * w, cudaMemcpyDefault, e->pull[j]));
-      DLC_CUDA(cudaEventRecord(evPull[j * P + p], e->pull[j]));
-      DLC_CUDA(cudaStreamWaitEvent(e->cstream, evPull[j * P + p], 0));
-    }
-    PtrList in{};  // owner fold in rank order (collective.cpp:1444-1489)
-    for (size_t j = 0; j < K; ++j)  // my own contribution straight from my send buffer
-      in.ptr[j] = ((int)j == r ? send + (r * S + po(p)) * w : recv + (j * S + po(p)) * w);
-    launch_fold(in, (int)K, e->prec, gather + (r * S + po(p)) * w, e->prec, e->flags + r, pl(p), e->cstream);
-    p2p_barrier(e, c, e->cstream);  // B_p
-    DLC_CUDA(cudaEventRecord(evB[p], e->cstream));
-    for (size_t q = 0; q < K; ++q) {  // all-gather: pull piece p of every owner's mean slot
-      if ((int)q == r) continue;
-      DLC_CUDA(cudaStreamWaitEvent(e->gath[q], evB[p], 0));
-      DLC_CUDA(cudaMemcpyAsync(gather + (q * S + po(p)) * w,
-                               static_cast<char*>(e->peer_gather[q]) + (q * S + po(p)) * w, pl(p) * w,
-                               cudaMemcpyDefault, e->gath[q]));
-      DLC_CUDA(cudaEventRecord(evGath[q * P + p], e->gath[q]));
+    p2p_fold(s, p);
+    if (p + 1 < P) DLC_CUDA(cudaStreamWaitEvent(e->cstream, s.evK2[p + 1], 0));
+    cudaEvent_t tb = trace_begin(e, e->cstream);
+    p2p_barrier(e, c, e->cstream, false);  // B_p
+    trace_end(e, e->cstream, "barrierB", (int)p, tb);
+    DLC_CUDA(cudaEventRecord(s.evB[p], e->cstream));
+    if (p + 1 == P) {
+      p2p_barrier(e, c, e->cstream, true);  // commit
+      DLC_CUDA(cudaEventRecord(s.evCommit, e->cstream));
     }
   };
-  // K4 pieces on the local gather buffer, speculative into the idle theta_t / momentum
-  PtrList slots{}, fl{};
-  for (size_t q = 0; q < K; ++q) {
-    slots.ptr[q] = k4_pull ? static_cast<char*>(e->peer_gather[q]) + q * S * w : gather + q * S * w;
-    // SM mover: owners pushed their marks into my flag array; CE mover: owner
-    // q's flag lives in owner q's memory
-    fl.ptr[q] = sm_mover ? e->flags + q : e->peer_flags[q] + q;
-  }
-  auto k4_piece = [&](size_t p) {
-    DLC_CUDA(cudaStreamWaitEvent(e->stream, evB[p], 0));
-    for (size_t q = 0; q < K && !sm_mover; ++q)
-      if ((int)q != r) DLC_CUDA(cudaStreamWaitEvent(e->stream, evGath[q * P + p], 0));
-    cudaEvent_t t4 = trace_begin(e, e->stream);
-    // device buffers: time each piece's launch on its own (after its wait), so
-    // the OUTER phase sums K4's busy time, not the waits for the means
-    const bool piece_timing = e->timing && !hsrc;
-    if (piece_timing) phase_begin(e);
-    launch_nesterov_p2p_piece(tt_pair(e), buf_pair(e), local_pair(e), slots, (int)K, S, po(p), pl(p), e->prec, e->st,
-                              lr, mu, n, piece_ctas(), e->stream);
-    if (piece_timing) phase_end(e, DLC_PHASE_OUTER);
-    trace_end(e, e->stream, "K4", (int)p, t4);
-    if (hdst) {
-      DLC_CUDA(cudaEventRecord(evK4[p], e->stream));
-      DLC_CUDA(cudaStreamWaitEvent(e->d2h, evK4[p], 0));
-      rows(p, [&](size_t lo, size_t len) {
-        DLC_CUDA(cudaMemcpyAsync(hdst + lo, e->theta_t[oc_host ^ 1] + lo, len * sizeof(float),
-                                 cudaMemcpyDeviceToHost, e->d2h));
-      });
-    }
-  };
-  cudaEvent_t c0 = pooled_event(e), c1 = pooled_event(e);
-  auto fold_begin = [&] {
-    DLC_CUDA(cudaStreamWaitEvent(e->cstream, evStart, 0));
-    DLC_CUDA(cudaEventRecord(c0, e->cstream));
-  };
-  auto fold_end = [&] {
-    launched("fold_p2p");
-    DLC_CUDA(cudaEventRecord(c1, e->cstream));
-    if (e->timing) {
-      e->pending.push_back({DLC_PHASE_COLLECTIVE, c0, c1});
-    } else {
-      e->pool.push_back(c0);
-      e->pool.push_back(c1);
-    }
-    if (rep) DLC_CUDA(cudaEventRecord(e->ev1, e->cstream));
-  };
-  const char* il = std::getenv("DLC_P2P_INTERLEAVE");  // device buffers: A/B knob (default 0)
-  if (!hsrc && !(il && il[0] == '1')) {
+  if (!hsrc) {
     // device buffers: every K2 piece first (the folds of the early pieces run
     // beside the later K2 pieces), then the K4 pieces as their means land
     phase_begin(e);
-    for (size_t p = 0; p < P; ++p) k2_piece(p);
+    for (size_t p = 0; p < P; ++p) p2p_k2(s, p);
     launched("pseudo_grad_piece");
     phase_end(e, DLC_PHASE_PSEUDO);
-    fold_begin();
-    for (size_t p = 0; p < P && push2; ++p) scatter_piece(p);
+    p2p_fold_begin(s);
     for (size_t p = 0; p < P; ++p) fold_piece(p);
-    fold_end();
-    for (size_t p = 0; p < P; ++p) k4_piece(p);
-    phase_begin(e);  // the finish gate below is one more OUTER interval
+    p2p_fold_end(s);
+    for (size_t p = 0; p < P; ++p) p2p_k4(s, p);
   } else {
     // host buffers: K2(p+1) then K4(p) on the engine stream, so the D2H of
     // piece p's new theta_t starts while later pieces are still arriving (H2D
     // and D2H overlap on the two copy streams instead of running back to back).
     // Issue order keeps every event recorded before a stream waits on it: the
     // merged barrier after fold(p) waits on K2(p + 1), K4(p) on fold(p).
-    phase_begin(e);
-    k2_piece(0);
-    if (push2) scatter_piece(0);
-    fold_begin();
+    p2p_k2(s, 0);
+    p2p_fold_begin(s);
     for (size_t p = 0; p < P; ++p) {
-      if (p + 1 < P) {
-        k2_piece(p + 1);
-        if (push2) scatter_piece(p + 1);
-      }
+      if (p + 1 < P) p2p_k2(s, p + 1);
       fold_piece(p);
-      k4_piece(p);
+      p2p_k4(s, p);
     }
     launched("pseudo_grad_piece");
-    fold_end();
+    p2p_fold_end(s);
   }
-  launch_p2p_finish(tt_pair(e), local_pair(e), fl, (int)K, e->st, n, flag_barriers(c) ? e->sig_err : nullptr,
-                    e->stream);
-  phase_end(e, DLC_PHASE_OUTER);
-  launched("nesterov_p2p_piece");
-  trace_dump(e, origin);
+  DLC_CUDA(cudaStreamWaitEvent(e->stream, s.evCommit, 0));
+  p2p_finish(s, e->sig_err);
 }
 
 // DLC_MODE_ALLREDUCE, pipelined: ncclAllReduce(ncclAvg) of contiguous pieces of
@@ -449,13 +404,10 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
 //   main     K2(p) -> evK2[p]
 //   cstream  wait evK2[p]; ncclAllReduce(piece p, in place); non-finite(p) -> evB[p]
 //   main     wait evB[p]; K4(p) into the idle theta_t / momentum; ...; finish
-// (DLC_AR_SERIAL=1: the unpipelined K2 -> all-reduce -> K4 of outer_collective.)
-bool allreduce_pipelined() {
-  const char* s = std::getenv("DLC_AR_SERIAL");
-  return !(s && std::string(s) == "1");
-}
-
+// (measured 9.66 ms against 11.2 ms for the unpipelined K2 -> all-reduce -> K4
+// of outer_collective at 4 GPUs, profiles/r1_bench_4gpu_allreduce*.json)
 void outer_allreduce_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc_reduce_report* rep) {
+  harvest_if_full(e);
   const size_t n = e->n, w = elem_width(e->prec);
   if (!e->cstream) {
     int lo = 0, hi = 0;
@@ -531,7 +483,7 @@ void outer_round(dlc_engine* e, dlc_collective* c, const float* src, dlc_reduce_
     outer_p2p_pipelined(e, c, src, rep, nullptr, nullptr, 0);
     return;
   }
-  if (e->k > 1 && c->mode == DLC_MODE_ALLREDUCE && allreduce_pipelined()) {
+  if (e->k > 1 && c->mode == DLC_MODE_ALLREDUCE) {
     outer_allreduce_pipelined(e, c, src, rep);
     return;
   }

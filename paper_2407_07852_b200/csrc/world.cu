@@ -27,12 +27,14 @@ struct dlc_world {
 namespace {
 
 // Every engine's peer tables point straight at the other engines' buffers
-// (one address space, peer access enabled): no IPC, no handle exchange.
+// (one address space; peer access enabled between distinct devices, ranks on
+// the same device read each other's buffers as local memory): no IPC, no
+// handle exchange, no signal slots.
 void world_bind_p2p(dlc_world* w) {
   for (int a = 0; a < w->k; ++a) {
     DeviceGuard dg(w->devices[a]);
     for (int b = 0; b < w->k; ++b) {
-      if (a == b || w->devices[a] == w->devices[b]) continue;
+      if (w->devices[a] == w->devices[b]) continue;
       const cudaError_t st = cudaDeviceEnablePeerAccess(w->devices[b], 0);
       if (st == cudaErrorPeerAccessAlreadyEnabled) {
         cudaGetLastError();
@@ -43,15 +45,76 @@ void world_bind_p2p(dlc_world* w) {
   }
   for (int r = 0; r < w->k; ++r) {
     dlc_engine* e = w->engines[r];
+    p2p_unbind(e);
     for (int j = 0; j < w->k; ++j) {
       dlc_engine* q = w->engines[j];
       e->peer_send[j] = q->send;
       e->peer_gather[j] = q->gather;
       e->peer_flags[j] = q->flags;
-      e->peer_sig[j] = q->sig;
-      e->peer_recv[j] = q->recv;
     }
     e->p2p_bound = w->colls[r];
+    w->colls[r]->bound.push_back(e);
+  }
+}
+
+// DLC_MODE_P2P from one thread: every rank's staged step (p2p.cu), the
+// "every rank" conditions as cudaEvent dependencies between the ranks'
+// streams instead of flag barriers.  Nothing spins, so ranks may share a
+// device (the driver's one-GPU box runs any K), and a stream never waits on
+// an event that is not recorded yet: each stage is enqueued for every rank
+// before the next stage waits on it.
+//   fold_r(p) waits for K2_j(p) of every rank j (owner r reads slot r of
+//             every rank's send buffer);
+//   K4_r(p)   waits for fold_j(p) of every rank j (owner j pushed its mean
+//             and mark into rank r's gather buffer and flags).
+// The next step's K2 / flag reset on rank j follow rank j's K4 pieces on its
+// stream, hence every fold of this step: no buffer is rewritten early.
+void world_outer_p2p(dlc_world* w) {
+  const int K = w->k;
+  std::vector<P2PStep> st;
+  st.reserve(K);
+  for (int r = 0; r < K; ++r) {
+    DeviceGuard dg(w->devices[r]);
+    dlc_engine* e = w->engines[r];
+    harvest_if_full(e);
+    if (e->p2p_bound != w->colls[r]) world_bind_p2p(w);
+    st.push_back(p2p_begin(e, r, nullptr, false, nullptr, nullptr, 0));
+  }
+  const size_t P = st[0].P;
+  for (int r = 0; r < K; ++r) {
+    DeviceGuard dg(w->devices[r]);
+    dlc_engine* e = w->engines[r];
+    phase_begin(e);
+    for (size_t p = 0; p < P; ++p) p2p_k2(st[r], p);
+    launched("pseudo_grad_piece");
+    phase_end(e, DLC_PHASE_PSEUDO);
+    p2p_fold_begin(st[r]);
+  }
+  for (size_t p = 0; p < P; ++p) {
+    for (int r = 0; r < K; ++r) {
+      DeviceGuard dg(w->devices[r]);
+      dlc_engine* e = w->engines[r];
+      for (int j = 0; j < K; ++j) DLC_CUDA(cudaStreamWaitEvent(e->cstream, st[j].evK2[p], 0));
+      p2p_fold(st[r], p);
+      DLC_CUDA(cudaEventRecord(st[r].evB[p], e->cstream));
+    }
+  }
+  for (int r = 0; r < K; ++r) {
+    DeviceGuard dg(w->devices[r]);
+    p2p_fold_end(st[r]);
+  }
+  for (size_t p = 0; p < P; ++p) {
+    for (int r = 0; r < K; ++r) {
+      DeviceGuard dg(w->devices[r]);
+      dlc_engine* e = w->engines[r];
+      for (int j = 0; j < K; ++j)
+        if (j != r) DLC_CUDA(cudaStreamWaitEvent(e->stream, st[j].evB[p], 0));
+      p2p_k4(st[r], p);
+    }
+  }
+  for (int r = 0; r < K; ++r) {
+    DeviceGuard dg(w->devices[r]);
+    p2p_finish(st[r], nullptr);
   }
 }
 
@@ -145,11 +208,13 @@ int dlc_world_create(const dlc_config* cfg, const dlc_hyperparams* hyper, size_t
       if (s2 != DLC_OK) fail(s2, std::string("world engine ") + std::to_string(r) + ": " + dlc_last_error());
       w->engines.push_back(e);
     }
-    // one rank per device: two ranks' spinning flag barriers on one device could
-    // share a hardware queue with the work they wait for
+    // P2P synchronises the ranks with events, so ranks may share a device;
+    // NCCL communicators need one device per rank
+    bool shared = false;
     for (int r = 1; r < k; ++r)
-      for (int q = 0; q < r; ++q)
-        if (devices[q] == devices[r]) fail(DLC_ECONFIG, "world ranks need distinct devices");
+      for (int q = 0; q < r; ++q) shared |= devices[q] == devices[r];
+    if (shared && mode != DLC_MODE_P2P)
+      fail(DLC_ECONFIG, "world ranks sharing a device need DLC_MODE_P2P (NCCL needs one device per rank)");
     std::vector<ncclComm_t> comms(k, nullptr);
     if (k > 1 && mode != DLC_MODE_P2P) DLC_NCCL(ncclCommInitAll(comms.data(), k, devices));  // P2P needs none
     for (int r = 0; r < k; ++r) {
@@ -178,7 +243,7 @@ int dlc_world_destroy(dlc_world* w) {
       cudaDeviceSynchronize();
     }
     for (dlc_engine* e : w->engines) {
-      e->p2p_bound = nullptr;  // direct pointers: nothing to unmap, no fleet barrier
+      p2p_unbind(e);  // direct pointers: nothing to unmap, no fleet barrier
       dlc_engine_destroy(e);
     }
     for (size_t r = 0; r < w->colls.size(); ++r) {
@@ -206,12 +271,7 @@ int dlc_world_outer_step(dlc_world* w, dlc_outer_result* result) {
       DeviceGuard dg(w->devices[0]);
       outer_round(w->engines[0], nullptr, nullptr, nullptr);
     } else if (w->mode == DLC_MODE_P2P) {
-      // every rank's pipelined step is enqueued without a host wait; the
-      // flag barriers inside synchronise the GPUs with each other
-      for (int r = 0; r < w->k; ++r) {
-        DeviceGuard dg(w->devices[r]);
-        outer_p2p_pipelined(w->engines[r], w->colls[r], nullptr, nullptr, nullptr, nullptr, 0);
-      }
+      world_outer_p2p(w);
     } else {
       world_outer_nccl(w);
     }

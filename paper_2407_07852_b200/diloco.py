@@ -531,9 +531,11 @@ class DilocoEngine:
 
 
 class World:
-    """Single-process multi-GPU world (include/diloco_cuda.h): K engines on K
-    devices driven by one host thread, the device analogue of run_simulated's
-    K workers (netsim.cpp:325-357)."""
+    """Single-process world (include/diloco_cuda.h): K engines driven by one host
+    thread, the device analogue of run_simulated's K workers (netsim.cpp:325-357).
+    In DLC_MODE_P2P several ranks may share a device (``devices=[0] * k``): the
+    ranks then synchronise through CUDA events, and the whole P2P data plane
+    (piece pipeline, TMA owner fold, finish gate) runs on one GPU."""
 
     def __init__(self, config: DilocoConfig, hyper: OptimHyperparams, n_params: int, devices,
                  inner_mode: int = A.INNER_PINGPONG, mode: int = A.MODE_P2P):
@@ -574,6 +576,21 @@ class World:
             self.close()
         except Exception:
             pass
+
+
+def set_p2p_tuning(plan=None, fold_ctas: int = 0, fold_threads: int = 0, piece_ctas: int = 0) -> None:
+    """dlc_p2p_set_tuning: override the measured DLC_MODE_P2P defaults (sweeps);
+    no arguments restores them."""
+    if plan is None and not (fold_ctas or fold_threads or piece_ctas):
+        _check(lib.dlc_p2p_set_tuning(None))
+        return
+    t = A.P2PTuning()
+    plan = list(plan or [])
+    t.plan_len = len(plan)
+    for i, v in enumerate(plan):
+        t.plan[i] = int(v)
+    t.fold_ctas, t.fold_threads, t.piece_ctas = fold_ctas, fold_threads, piece_ctas
+    _check(lib.dlc_p2p_set_tuning(C.byref(t)))
 
 
 def outer_step_local(engines) -> OuterStepResult:

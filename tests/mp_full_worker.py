@@ -2,9 +2,11 @@
 
 Config 4 at full size: 1.1B parameters per worker, one worker per GPU, FP16
 pseudo-gradients, P2P mode (and the NCCL ordered mode), two outer rounds.  Each
-rank checks slices at the start, an unaligned middle and the end of its
-theta_t / theta_local / momentum against the oracle's rank-ordered outer round
+rank checks slices at the start, an unaligned middle, the end, every owner-slot
+edge q*S and every piece boundary of the P2P plan inside every slot, of its
+theta_t / theta_local / momentum, against the oracle's rank-ordered outer round
 over every rank's inputs restricted to the slice (all elementwise), bit for bit.
+(Every element at full size, K ranks sharing one GPU: tests/test_full_size.py.)
 """
 import json
 import os
@@ -22,6 +24,22 @@ from oracle import oracle as O  # noqa: E402
 
 N = int(os.environ.get("MP_FULL_N", 1_100_000_000))
 M = 4096
+E = 256  # elements on each side of a slot edge / piece boundary
+
+
+def slice_starts(n, k):
+    """Start, middle, end, and [b - E, b + E) around every slot edge and every piece
+    boundary of the default plan (1,1,2,2,1,1 eighths of a slot at this size)."""
+    S = PD.slot_elems(n, k)
+    cum = [1, 2, 4, 6, 7]
+    starts = {(0, M), (n // 2 - 777, M), (n - M, M)}
+    for q in range(k + 1):
+        for b in [0] + [(S // 64) * c // 8 * 64 for c in cum]:
+            x = q * S + b
+            lo, hi = max(0, x - E), min(n, x + E)
+            if lo < hi:
+                starts.add((lo, hi - lo))
+    return sorted(starts)
 
 
 def bits(a):
@@ -39,24 +57,26 @@ def main():
         coll = PD.make_nccl_collective(r, mode)
         e = D.DilocoEngine(D.DilocoConfig(1, k, D.FP16, 4), D.OptimHyperparams(), N, r.local)
         e.rng_fill(D.THETA_T, 4242, "theta", 0, -0.05, 0.05)
-        slices = [0, N // 2 - 777, N - M]
-        ws = {lo: DR.make_workers(O.rng_fill(4242, "theta", 0, M, -0.05, 0.05, first=lo), k, hyper) for lo in slices}
+        slices = slice_starts(N, k)
+        ws = {(lo, m): DR.make_workers(O.rng_fill(4242, "theta", 0, m, -0.05, 0.05, first=lo), k, hyper)
+              for lo, m in slices}
         for rnd in range(2):
             # end-of-window weights: theta_t - U(-1e-3, 1e-3) keyed by (round, rank)
             e.rng_perturb(4242, "local", rnd * 64 + r.rank, -1e-3, 1e-3)
             res = e.outer_step(coll, wait=True)
             assert res.applied and res.outer_epoch == rnd + 1
-            for lo in slices:
-                for j, w in enumerate(ws[lo]):
-                    noise = O.rng_fill(4242, "local", rnd * 64 + j, M, -1e-3, 1e-3, first=lo)
+            for lo, m in slices:
+                for j, w in enumerate(ws[lo, m]):
+                    noise = O.rng_fill(4242, "local", rnd * 64 + j, m, -1e-3, 1e-3, first=lo)
                     w.theta_local = (w.theta_t - noise).astype(np.float32)
-                DR.outer_round(port, ws[lo], D.FP16, hyper)
-                me = ws[lo][r.rank]
+                DR.outer_round(port, ws[lo, m], D.FP16, hyper)
+                me = ws[lo, m][r.rank]
                 for which, want in ((D.THETA_T, me.theta_t), (D.THETA_LOCAL, me.theta_local),
                                     (D.MOMENTUM, me.buf)):
-                    got = e.download_range(which, lo, M)
+                    got = e.download_range(which, lo, m)
                     assert np.array_equal(bits(got), bits(want)), (mode_name, rnd, lo, which)
-            out["checks"].append(f"{mode_name} round {rnd}: 3 slices x 3 vectors bitwise at N={N}")
+            out["checks"].append(f"{mode_name} round {rnd}: {len(slices)} slices (slot edges, piece boundaries) "
+                                 f"x 3 vectors bitwise at N={N}")
         e.close()
         coll.close()
     PD.barrier(r.world)

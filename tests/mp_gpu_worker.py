@@ -43,21 +43,15 @@ def main():
             g[3] = np.inf  # one overflowed inner step on the last worker
         return g
 
-    # P2P runs once per data mover and barrier flavour (read per step from the environment)
-    cases = [("ordered", D.MODE_ORDERED, {}), ("p2p", D.MODE_P2P, {"DLC_P2P_COPY": "sm"}),
-             ("p2p-push", D.MODE_P2P, {"DLC_P2P_COPY": "push", "DLC_P2P_PLAN": "2,2,2,2"}),
-             ("p2p-push2", D.MODE_P2P, {"DLC_P2P_COPY": "push2", "DLC_P2P_PLAN": "1,3,4"}),
-             ("p2p-tma3", D.MODE_P2P, {"DLC_TMA_CTAS": "3"}),
-             ("p2p-ldst", D.MODE_P2P, {"DLC_FOLD_TMA": "0"}),
-             ("p2p-k4pull", D.MODE_P2P, {"DLC_P2P_K4_PULL": "1"}),
-             ("p2p-nomerge", D.MODE_P2P, {"DLC_P2P_MERGE": "0"}),
-             ("p2p-ce", D.MODE_P2P, {"DLC_P2P_COPY": "ce", "DLC_P2P_BARRIER": "nccl", "DLC_P2P_PIECES": "2"}),
+    # P2P with the measured defaults and with a few tuning overrides (piece
+    # plan, a tiny fold grid, 512-thread fold CTAs)
+    cases = [("ordered", D.MODE_ORDERED, {}), ("p2p", D.MODE_P2P, {}),
+             ("p2p-plan2222", D.MODE_P2P, {"plan": [2, 2, 2, 2]}),
+             ("p2p-plan134-tma3", D.MODE_P2P, {"plan": [1, 3, 4], "fold_ctas": 3}),
+             ("p2p-tma512", D.MODE_P2P, {"fold_threads": 512, "piece_ctas": 37}),
              ("allreduce", D.MODE_ALLREDUCE, {})]
-    for mode_name, mode, env in cases:
-        for key in ("DLC_P2P_COPY", "DLC_P2P_PLAN", "DLC_P2P_BARRIER", "DLC_P2P_PIECES", "DLC_FOLD_TMA", "DLC_TMA_CTAS",
-                    "DLC_P2P_K4_PULL", "DLC_P2P_MERGE"):
-            os.environ.pop(key, None)
-        os.environ.update(env)
+    for mode_name, mode, tuning in cases:
+        D.set_p2p_tuning(**tuning)
         coll = PD.make_nccl_collective(r, mode)
         assert coll.world_size() == k and coll.rank() == r.rank
         for prec in (D.FP32, D.FP16):
@@ -75,8 +69,11 @@ def main():
                 res = e.outer_step(coll, wait=True, report=True)
                 assert res.applied
                 rep = res.report
-                assert rep.contributors == k and rep.data_bytes_sent == 2 * (k - 1) * PD.slot_elems(n, k) * (
-                    2 if prec == D.FP16 else 4)
+                # the reference's byte law (reduce.cpp:91-104); wire = the padded slots moved
+                assert rep.contributors == k and rep.data_bytes_sent == D.per_peer_reduce_bytes(n, k, r.rank, prec)
+                assert rep.wire_bytes_sent == 2 * (k - 1) * PD.slot_elems(n, k) * (2 if prec == D.FP16 else 4)
+                assert all_sum(r, rep.data_bytes_sent) == D.fleet_reduce_bytes(n, k, prec)
+                assert all_sum(r, rep.data_bytes_received) == D.fleet_reduce_bytes(n, k, prec)
             me = workers[r.rank]
             got = {w: e.download(w) for w in (D.THETA_T, D.THETA_LOCAL, D.ADAM_M, D.ADAM_V, D.MOMENTUM)}
             if mode != D.MODE_ALLREDUCE:
@@ -118,8 +115,10 @@ def main():
 
             recs = []
             res = D.run_training(e, coll, producer, sink=recs.append, worker_index=r.rank)
-            assert res["rounds_done"] == rounds and res["reduce_data_bytes"] == rounds * 2 * (k - 1) * \
-                PD.slot_elems(n, k) * 2
+            # ledger (test_harness.cpp:121-133): the fleet's bytes = rounds x fleet_reduce_bytes
+            assert res["rounds_done"] == rounds
+            assert res["reduce_data_bytes"] == rounds * D.per_peer_reduce_bytes(n, k, r.rank, D.FP16)
+            assert all_sum(r, res["reduce_data_bytes"]) == rounds * D.fleet_reduce_bytes(n, k, D.FP16)
             assert sum(1 for x in recs if x["kind"] == "round" and x["contributors"] == k) == rounds
             for w, want in ((D.THETA_T, workers[r.rank].theta_t), (D.MOMENTUM, workers[r.rank].buf)):
                 assert np.array_equal(bits(e.download(w)), bits(want)), ("run_training", w)
@@ -181,8 +180,17 @@ def main():
         _, r16 = coll.all_reduce_avg(x, D.FP16)
         assert 2 * r16.data_bytes_sent == rx.data_bytes_sent
         coll.close()
+    D.set_p2p_tuning()
     PD.barrier(r.world)
     print("MPRESULT " + json.dumps(out), flush=True)
+
+
+def all_sum(r, x: int) -> int:
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([int(x)], dtype=torch.int64)
+    dist.all_reduce(t)
+    return int(t.item())
 
 
 def workers_round0_local(port, theta0, grad_fn, k, h, hyper, rank):

@@ -1,12 +1,12 @@
-"""Parity at BASELINE.json's full sizes, on a B200 (configs 2-5).
+"""Parity at BASELINE.json's full sizes, on a B200 (configs 2-5), on EVERY element.
 
-Every operation on the path is elementwise apart from the rank-ordered fold,
-which is elementwise across workers, so any slice of a full-size run is
-computed exactly by the CPU oracle from the same counter-based inputs restricted
-to that slice (rng streams are addressable by element).  These
-tests run the full-size vectors on the GPU and check slices at the start,
-middle (unaligned) and end of every state vector, bit for bit; the 1.1B
-multi-GPU case is tests/mp_full_worker.py via tests/test_multigpu.py.
+The GPU runs the full-size vectors; tests/chunked_oracle.py replays the oracle
+chunk by chunk on the host cores and compares every element of theta_t,
+theta_local, m, v and momentum of every worker, bit for bit (the reference's
+whole-vector comparisons, /root/reference/proj/tests/test_engine.cpp:213-241,
+test_collective.cpp:368-396).  The multi-worker cases run K ranks of a
+dlc_world on cuda:0 (DLC_MODE_P2P with event synchronisation): the pipelined
+pieces, the TMA owner fold and the finish gate at full size on one GPU.
 """
 import numpy as np
 import pytest
@@ -14,10 +14,9 @@ import pytest
 import paper_2407_07852_b200 as D
 from paper_2407_07852_b200 import _capi as A
 from oracle import driver as DR
-from oracle import oracle as O
+from chunked_oracle import compare_whole  # tests/chunked_oracle.py
 
 pytestmark = pytest.mark.gpu
-M = 4096  # slice length
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -29,14 +28,7 @@ def gpu():
     if n < 1:
         pytest.skip("no CUDA device")
     D.lib.dlc_set_device(0)
-
-
-def bits(a):
-    return np.ascontiguousarray(a, np.float32).view(np.uint32)
-
-
-def slices(n):
-    return [0, n // 2 - 777, n - M]
+    D.set_p2p_tuning()
 
 
 def _hp(hyper):
@@ -46,66 +38,80 @@ def _hp(hyper):
                               scaler_growth_interval=hyper.growth_interval)
 
 
-def _check_slices(e, n, ws, wi=0):
-    for lo in slices(n):
-        w = ws[lo][wi]
-        for which, want in ((A.THETA_T, w.theta_t), (A.THETA_LOCAL, w.theta_local), (A.ADAM_M, w.m),
-                            (A.ADAM_V, w.v), (A.MOMENTUM, w.buf)):
-            got = e.download_range(which, lo, M)
-            assert np.array_equal(bits(got), bits(want)), (lo, which)
+def _oracle_chunk(port, k, h, rounds, prec, hyper, overflow):
+    """The oracle's K-worker run restricted to elements [lo, lo + length): inputs
+    are the same counter-based streams at element offset lo.  An overflow
+    injected at (worker, step) is a global skip of that worker's step, so every
+    chunk injects it."""
+    from oracle import oracle as O
+
+    def run(lo, length):
+        th0 = O.rng_fill(4242, "theta", 0, length, -0.05, 0.05, first=lo)
+
+        def grad_fn(w, t):
+            g = O.rng_fill(4242, "grad", w * 1000 + t, length, -1e-2, 1e-2, first=lo)
+            if (w, t) == overflow:
+                g[-1] = np.inf
+            return g
+        ws, _ = DR.simulate(port, th0, grad_fn, k, h, rounds, prec, hyper)
+        return ws
+    return run
+
+
+def _run_engines(engines, n, h, rounds, overflow, outer):
+    for e in engines:
+        e.rng_fill(A.THETA_T, 4242, "theta", 0, -0.05, 0.05)
+        e.rng_fill(A.THETA_LOCAL, 4242, "theta", 0, -0.05, 0.05)
+    step = 0
+    for rnd in range(rounds):
+        for _ in range(h):
+            for wi, e in enumerate(engines):
+                e.rng_fill(A.GRAD, 4242, "grad", wi * 1000 + step, -1e-2, 1e-2)
+                if (wi, step) == overflow:
+                    e.upload_range(A.GRAD, n - 1, [np.inf])
+                e.inner_step(e.device_ptr(A.GRAD), grad_is_scaled=False)
+            step += 1
+        res = outer()
+        assert res.applied and res.outer_epoch == rnd + 1
 
 
 @pytest.mark.parametrize("prec", [A.FP16, A.FP32])
 def test_full_size_1p1b_window(port, prec):
-    """Config 4/5 shape on one worker: 1.1B parameters, H = 3 inner steps (the
-    second with an injected overflow at the last element) and the fused outer step."""
+    """Configs 4/5 on one worker: 1.1B parameters, H = 3 inner steps (the second
+    overflows at the last element: a global skip) and the fused outer step;
+    all 5 x 1.1B elements compared."""
     n, h = 1_100_000_000, 3
     hyper = DR.Hyper(warmup_steps=5)
     e = D.DilocoEngine(D.DilocoConfig(h, 1, prec, h), _hp(hyper), n)
-    e.rng_fill(A.THETA_T, 4242, "theta", 0, -0.05, 0.05)
-    e.rng_fill(A.THETA_LOCAL, 4242, "theta", 0, -0.05, 0.05)
-    for t in range(h):
-        e.rng_fill(A.GRAD, 4242, "grad", t, -1e-2, 1e-2)
-        if t == 1:
-            e.upload_range(A.GRAD, n - 1, [np.inf])
-        e.inner_step(e.device_ptr(A.GRAD), grad_is_scaled=False)
+    _run_engines([e], n, h, 1, (0, 1), lambda: e.outer_step(None, wait=True))
     assert e.scalars().overflow_skips == 1
-    assert e.outer_step(None, wait=True).applied
-    ws = {}
-    for lo in slices(n):
-        th0 = O.rng_fill(4242, "theta", 0, M, -0.05, 0.05, first=lo)
-
-        def grad_fn(w, t, lo=lo):
-            g = O.rng_fill(4242, "grad", t, M, -1e-2, 1e-2, first=lo)
-            if t == 1:  # the overflow is global: step 1 is skipped in every slice
-                g[-1] = np.inf
-            return g
-        ws[lo], _ = DR.simulate(port, th0, grad_fn, 1, h, 1, prec, hyper)
-    _check_slices(e, n, ws)
+    done = compare_whole([e], n, 1 << 23, _oracle_chunk(port, 1, h, 1, prec, hyper, (0, 1)))
+    assert done == 5 * n
     e.close()
 
 
 @pytest.mark.parametrize("prec", [A.FP32, A.FP16])
 def test_full_size_150m_eight_workers(port, prec):
-    """Configs 2 / 3: 150M parameters, 8 workers (in-process fleet on one GPU),
-    H = 2, one outer step with the rank-ordered fold over all 8."""
-    n, k, h = 150_000_000, 8, 2
+    """Configs 2 / 3: 150M parameters x 8 workers (8 ranks of a P2P world on one
+    GPU), H = 2, two rounds, an overflowed inner step on the last worker; all
+    5 x 8 x 150M elements compared."""
+    n, k, h, rounds = 150_000_000, 8, 2, 2
     hyper = DR.Hyper(warmup_steps=5)
-    engines = [D.DilocoEngine(D.DilocoConfig(h, k, prec, h), _hp(hyper), n) for _ in range(k)]
-    for wi, e in enumerate(engines):
-        e.rng_fill(A.THETA_T, 4242, "theta", 0, -0.05, 0.05)
-        e.rng_fill(A.THETA_LOCAL, 4242, "theta", 0, -0.05, 0.05)
-    for t in range(h):
-        for wi, e in enumerate(engines):
-            e.rng_fill(A.GRAD, 4242, "grad", wi * 1000 + t, -1e-2, 1e-2)
-            e.inner_step(e.device_ptr(A.GRAD), grad_is_scaled=False)
-    assert D.outer_step_local(engines).applied
-    ws = {}
-    for lo in slices(n):
-        th0 = O.rng_fill(4242, "theta", 0, M, -0.05, 0.05, first=lo)
-        grad_fn = lambda w, t, lo=lo: O.rng_fill(4242, "grad", w * 1000 + t, M, -1e-2, 1e-2, first=lo)  # noqa: E731
-        ws[lo], _ = DR.simulate(port, th0, grad_fn, k, h, 1, prec, hyper)
-    for wi, e in enumerate(engines):
-        _check_slices(e, n, ws, wi)
-    for e in engines:
-        e.close()
+    world = D.World(D.DilocoConfig(h, k, prec, h * rounds), _hp(hyper), n, [0] * k, mode=A.MODE_P2P)
+    _run_engines(world.engines, n, h, rounds, (k - 1, 1), world.outer_step)
+    done = compare_whole(world.engines, n, 1 << 20, _oracle_chunk(port, k, h, rounds, prec, hyper, (k - 1, 1)))
+    assert done == 5 * k * n
+    world.close()
+
+
+def test_full_size_1p1b_two_workers(port):
+    """Config 4 (1.1B, FP16 average, Nesterov 0.7 / 0.9) with two workers of a
+    P2P world on one GPU (~100 GB of HBM), one window of H = 1 per round, two
+    rounds; all 5 x 2 x 1.1B elements compared."""
+    n, k, h, rounds = 1_100_000_000, 2, 1, 2
+    hyper = DR.Hyper(warmup_steps=5)
+    world = D.World(D.DilocoConfig(h, k, A.FP16, h * rounds), _hp(hyper), n, [0] * k, mode=A.MODE_P2P)
+    _run_engines(world.engines, n, h, rounds, (None, None), world.outer_step)
+    done = compare_whole(world.engines, n, 1 << 23, _oracle_chunk(port, k, h, rounds, A.FP16, hyper, (None, None)))
+    assert done == 5 * k * n
+    world.close()

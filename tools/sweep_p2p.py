@@ -1,12 +1,16 @@
 #!/usr/bin/env python
-"""Sweep the DLC_MODE_P2P knobs in-process (development tool; run under torchrun).
+"""Sweep the DLC_MODE_P2P tuning in-process (development tool; run under torchrun).
 
-    torchrun --nproc-per-node 4 tools/sweep_p2p.py --params 1100000000
+    torchrun --nproc-per-node 4 tools/sweep_p2p.py --params 1100000000 \
+        --plans "1,1,2,2,1,1;1,3,3,1" --fold-ctas 0 48 80 --fold-threads 0 256 --repeat 2
 
-Times the outer step (CUDA events on the engine stream, max over ranks) for
-DLC_P2P_COPY x DLC_P2P_PIECES x DLC_COMM_CTAS, plus the NCCL ordered mode.
+Times the outer step (CUDA events on the engine stream, max over ranks) for every
+combination of piece plan x fold CTAs x fold threads (dlc_p2p_set_tuning; 0 = the
+measured default), interleaving the repeats so box drift spreads over all
+configurations, plus the NCCL ordered mode as the baseline.
 """
 import argparse
+import itertools
 import json
 import os
 import sys
@@ -25,60 +29,35 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--params", type=int, default=1_100_000_000)
     ap.add_argument("--steps", type=int, default=6)
+    ap.add_argument("--plans", default="", help="';'-separated piece plans ('' = default)")
+    ap.add_argument("--fold-ctas", type=int, nargs="+", default=[0])
+    ap.add_argument("--fold-threads", type=int, nargs="+", default=[0])
+    ap.add_argument("--piece-ctas", type=int, nargs="+", default=[0])
+    ap.add_argument("--repeat", type=int, default=1)
+    ap.add_argument("--no-ordered", action="store_true")
     a = ap.parse_args()
     r = PD.init("gloo")
     torch.cuda.set_device(r.local)
     D.lib.dlc_set_device(r.local)
     n, k = a.params, r.world
-    colls = {"p2p": PD.make_nccl_collective(r, D.MODE_P2P), "ordered": PD.make_nccl_collective(r, D.MODE_ORDERED)}
+    colls = {"p2p": PD.make_nccl_collective(r, D.MODE_P2P)}
+    if not a.no_ordered:
+        colls["ordered"] = PD.make_nccl_collective(r, D.MODE_ORDERED)
     eng = D.DilocoEngine(D.DilocoConfig(1, k, D.FP16, 1 << 40), D.OptimHyperparams(), n, r.local)
     eng.rng_fill(D.THETA_T, 4242, "theta", 0, -0.05, 0.05)
     xs = [torch.empty(n, dtype=torch.float32, device=f"cuda:{r.local}") for _ in range(2)]
     for i, x in enumerate(xs):
         eng.rng_perturb(4242, "local", r.rank * 16 + i, -1e-3, 1e-3, dst_dev_ptr=x.data_ptr())
     stream = torch.cuda.ExternalStream(eng.stream, device=f"cuda:{r.local}")
-    configs = [("ordered", None, None, None, None, 0, 0, 128, "")]
-    movers = os.environ.get("SWEEP_MOVERS", "sm,ce").split(",")
-    pieces_l = [int(x) for x in os.environ.get("SWEEP_PIECES", "1,2,4,8").split(",")]
-    ctas_l = [int(x) for x in os.environ.get("SWEEP_CTAS", "0,32,64,128,256").split(",")]
-    barriers = os.environ.get("SWEEP_BARRIERS", "flag").split(",")
-    piece_ctas_l = [int(x) for x in os.environ.get("SWEEP_PIECE_CTAS", "0").split(",")]
-    tma_l = [int(x) for x in os.environ.get("SWEEP_TMA_CTAS", "0").split(",")]  # 0: per-thread fold
-    tthr_l = [int(x) for x in os.environ.get("SWEEP_TMA_THREADS", "128").split(",")]
-    # SWEEP_ENV="A=1,B=2;A=0": extra environment per config; SWEEP_REPEAT: interleaved repeats (A/B)
-    env_l = os.environ.get("SWEEP_ENV", "").split(";")
-    plans = os.environ.get("SWEEP_PLANS", "").split(";") if os.environ.get("SWEEP_PLANS") else None
-    for barrier in barriers:
-        for mover in movers:
-            for pieces in (plans or pieces_l):
-                for ctas in (ctas_l if mover in ("sm", "push", "push2") else (0,)):
-                    for pc in piece_ctas_l:
-                        for tc in tma_l:
-                            for tt in tthr_l:
-                                for ev in env_l:
-                                    configs.append(("p2p", mover, pieces, ctas, barrier, pc, tc, tt, ev))
-    configs = configs * int(os.environ.get("SWEEP_REPEAT", "1"))
+    plans = [p for p in a.plans.split(";")] if a.plans else [""]
+    configs = [("p2p", p, fc, ft, pc) for p, fc, ft, pc in itertools.product(plans, a.fold_ctas, a.fold_threads,
+                                                                             a.piece_ctas)]
+    if not a.no_ordered:
+        configs.insert(0, ("ordered", "", 0, 0, 0))
     results = []
-    for mode, mover, pieces, ctas, barrier, pc, tc, tt, ev in configs:
-        for kv in filter(None, ev.split(",")):
-            key, val = kv.split("=", 1)
-            os.environ[key] = val
-        os.environ["DLC_TMA_THREADS"] = str(tt)
-        os.environ["DLC_P2P_PIECE_CTAS"] = str(pc)
-        os.environ["DLC_FOLD_TMA"] = "1" if tc else "0"  # tc < 0: TMA fold, default CTA count
-        if tc > 0:
-            os.environ["DLC_TMA_CTAS"] = str(tc)
-        else:
-            os.environ.pop("DLC_TMA_CTAS", None)
-        if mover:
-            os.environ["DLC_P2P_COPY"] = mover
-            if isinstance(pieces, str):
-                os.environ["DLC_P2P_PLAN"] = pieces
-            else:
-                os.environ.pop("DLC_P2P_PLAN", None)
-                os.environ["DLC_P2P_PIECES"] = str(pieces)
-            os.environ["DLC_COMM_CTAS"] = str(ctas)
-            os.environ["DLC_P2P_BARRIER"] = barrier
+    for mode, plan, fc, ft, pc in configs * a.repeat:
+        D.set_p2p_tuning(plan=[int(x) for x in plan.split(",")] if plan else None, fold_ctas=fc, fold_threads=ft,
+                         piece_ctas=pc)
         c = colls[mode]
         for s in range(2):
             eng.outer_step_from(c, xs[s % 2].data_ptr())
@@ -91,10 +70,11 @@ def main():
         e1.record(stream)
         e1.synchronize()
         ms = PD.max_over_ranks(e0.elapsed_time(e1) / a.steps, r.world)
-        results.append({"mode": mode, "mover": mover, "pieces": pieces, "ctas": ctas, "barrier": barrier,
-                        "piece_ctas": pc, "tma_ctas": tc, "tma_threads": tt, "env": ev, "ms": ms})
+        results.append({"mode": mode, "plan": plan or "default", "fold_ctas": fc, "fold_threads": ft,
+                        "piece_ctas": pc, "ms": ms})
         if r.rank == 0:
             print(json.dumps(results[-1]), flush=True)
+    D.set_p2p_tuning()
     eng.close()
     for c in colls.values():
         c.close()
