@@ -155,26 +155,110 @@ class Clocks:
                 "power_w_max": max(s[1] for s in self.samples) if sm else None, "source": "nvml"}
 
 
+class NvlinkCounters:
+    """NVML's cumulative NVLink data counters of this GPU (all links), read before
+    and after the timed region: NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX / _RX
+    (fields 138 / 139, aggregate scope), in KiB (calibrated with a known peer
+    copy by tools/nvlink_probe.py, profiles/r2_nvlink_probe_*.json)."""
+
+    TX, RX, ALL = 138, 139, 0xFFFFFFFF
+
+    def __init__(self, device: int):
+        self.err = None
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            phys = int(vis.split(",")[device]) if vis and vis.split(",")[device].isdigit() else device
+            self.N, self.h = N, N.nvmlDeviceGetHandleByIndex(phys)
+            self.t0 = self._read()
+        except Exception as e:  # noqa: BLE001
+            self.err = f"nvml unavailable: {e}"
+
+    def _read(self):
+        vals = self.N.nvmlDeviceGetFieldValues(self.h, [(self.TX, self.ALL), (self.RX, self.ALL)])
+        for v in vals:
+            if v.nvmlReturn != 0:
+                raise RuntimeError(f"field {v.fieldId}: nvml status {v.nvmlReturn}")
+        return [int(v.value.ullVal) for v in vals]
+
+    def stop(self, seconds: float, expected_bytes_per_direction: float):
+        if self.err:
+            return {"source": self.err}
+        try:
+            t1 = self._read()
+        except Exception as e:  # noqa: BLE001
+            return {"source": f"nvml read failed: {e}"}
+        tx, rx = ((b - a) * 1024 for a, b in zip(self.t0, t1))
+        return {"source": "nvml NVLINK_THROUGHPUT_DATA_TX/RX (KiB, all links)", "tx_bytes": tx, "rx_bytes": rx,
+                "tx_gbs": tx / seconds / 1e9, "rx_gbs": rx / seconds / 1e9, "peak_gbs_per_direction": 900.0,
+                "tx_frac_of_900": tx / seconds / 900e9, "rx_frac_of_900": rx / seconds / 900e9,
+                "expected_bytes_per_direction": expected_bytes_per_direction,
+                "tx_over_expected": tx / expected_bytes_per_direction if expected_bytes_per_direction else None}
+
+
 # ---- CPU baseline: the reference's own functions on host threads --------------------------
 
-def cpu_reference_outer(k: int, prec: int, iters: int, warmup: int = 0, budget_gb: float = 8.0):
-    """Returns (params_per_s, seconds/iter list, dict describing the sample)."""
+def host_mem_available():
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable:"):
+                    return int(line.split()[1]) * 1024
+    except Exception:
+        pass
+    return 0
+
+
+def cpu_reference_outer(n: int, k: int, prec: int, iters: int, warmup: int = 0, full_ok: bool = True):
+    """The reference's own outer round (oracle/_ref, run_simulated's K x axpy +
+    reduce_average + K x outer_step, netsim.cpp:325-357) on every host core, each
+    thread on a disjoint slice.  At the full workload (n params x k workers) when
+    it fits in half the host's available memory (~4 (5k + 3) B/param live),
+    else on a bounded sample whose per-step time is extrapolated linearly in
+    params (the work is elementwise) and labelled so.
+    Returns (params_per_s, per-step seconds, dict describing the run)."""
     from oracle import oracle as O
     lib = O.reference()
-    kind = "reference"
     if lib is None:
         return None
     threads = os.cpu_count() or 1
-    per_thread = int(budget_gb * 1e9 / (threads * k * 20))
-    slice_len = max(1 << 16, min((16 << 20) // k, per_thread))
-    if warmup:
-        lib.bench_outer(threads, slice_len, k, prec, warmup)
-    secs = [lib.bench_outer(threads, slice_len, k, prec, 1) for _ in range(iters)]
-    units = k * threads * slice_len
-    sample = (f"{threads} threads x {slice_len} params/thread x {k} workers "
-              f"({'fp16' if prec else 'fp32'}), per step: K x axpy + reduce_average + K x nesterov/outer_step "
-              f"(netsim.cpp:325-357), {iters} steps")
-    return units / statistics.mean(secs), secs, {"kind": kind, "cores": threads, "sample": sample}
+    need = 4 * (5 * k + 3) * n
+    full = full_ok and need <= 0.5 * host_mem_available()
+    sample = n if full else max(threads << 16, min(n, (16 << 20) * threads // k))
+    secs = lib.bench_outer(threads, sample, k, prec, warmup, iters)
+    units = k * sample
+    desc = {"kind": "reference", "cores": threads,
+            "sample": (f"{'the full workload' if full else 'a bounded sample'}: {sample} params x {k} workers "
+                       f"({'fp16' if prec else 'fp32'}) split over {threads} threads, per step K x axpy + "
+                       f"reduce_average + K x (all_finite, nesterov_step, theta_local = theta_t) "
+                       f"(netsim.cpp:325-357); the reference's math is single-threaded per call, "
+                       f"here every core takes a slice (reduce_average included), {iters} steps"),
+            "sample_params_per_worker": sample, "sample_ms_per_step": statistics.mean(secs) * 1e3,
+            "extrapolated": not full}
+    if not full:
+        desc["full_step_ms_extrapolated"] = statistics.mean(secs) * 1e3 * n / sample
+    return units / statistics.mean(secs), secs, desc
+
+
+def cpu_reference_inner(n: int, iters: int = 3):
+    """The reference's apply_inner_step (engine.cpp:50-69: scale_gradient,
+    scaler_unscale_and_check, lr_at, adamw_step, scaler_update) on every host
+    core over a bounded sample of the parameter vector."""
+    from oracle import oracle as O
+    lib = O.reference()
+    if lib is None:
+        return None
+    threads = os.cpu_count() or 1
+    sample = max(threads << 16, min(n, (16 << 20) * threads))
+    secs = lib.bench_inner(threads, sample, 1, iters)
+    v = sample / statistics.mean(secs)
+    return {"value": v, "unit": "params/s", "cores": threads, "kind": "reference",
+            "sample": f"a bounded sample: {sample} params split over {threads} threads, apply_inner_step "
+                      f"(scale + unscale/check + AdamW + scaler update), {iters} steps",
+            "sample_ms_per_step": statistics.mean(secs) * 1e3,
+            "full_step_ms_extrapolated": statistics.mean(secs) * 1e3 * n / sample, "extrapolated": sample != n,
+            "hbm_equivalent_gbs": 28 * v / 1e9}
 
 
 def run_reference(args):
@@ -183,11 +267,13 @@ def run_reference(args):
         return 0
     k = args.gpus if world == 1 else world
     prec = 1 if args.precision == "fp16" else 0
-    res = cpu_reference_outer(k, prec, args.steps, args.warmup)
+    res = cpu_reference_outer(args.params, k, prec, args.steps, args.warmup)
     if res is None:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
         return 0
     value, secs, desc = res
+    # ms_per_step is the measured step: the full workload, or the bounded sample
+    # (then desc carries the extrapolated full-size step time, labelled)
     ms = statistics.mean(secs) * 1e3
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "params/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -333,7 +419,14 @@ def run_ours(args):
     clocks = Clocks(local, enabled=not args.no_clocks)
     eng.set_timing(True)
     eng.phase_times()
+    nvl = NvlinkCounters(local) if k > 1 else None
     outer_ms = timed(outer, args.steps)
+    nvl_res = nvl.stop(outer_ms * 1e-3, 2 * (k - 1) * (-(-n // k)) * (2 if prec == D.FP16 else 4) * args.steps) \
+        if nvl else None
+    if world > 1:  # every rank's own counters
+        allv = [None] * world
+        dist.all_gather_object(allv, nvl_res)
+        nvl_res = allv
     ph_ms, ph_n = eng.phase_times()
     inner_total = timed(inner, args.steps)
     ph2_ms, ph2_n = eng.phase_times()
@@ -415,8 +508,12 @@ def run_ours(args):
                              "hbm_peak_gbs": peak, "hbm_bytes_incl_exchange": hbm_bpp * n + hbm_coll,
                              "frac_of_bound_incl_exchange": max(hbm_all_ms, nvl_ms) / ms_step}
     if k > 1:
-        line["nvlink_gbs_over_step"] = wire_bytes / (ms_step * 1e-3) / 1e9
-        line["nccl_bus_gbs"] = wire_bytes / (coll_ms * 1e-3) / 1e9 if coll_ms else None
+        # algorithmic NVLink bytes per direction (the padded owner slots each GPU
+        # serves and receives) over the whole step and over the exchange's busy time
+        line["exchange_gbs_per_direction_over_step"] = wire_bytes / (ms_step * 1e-3) / 1e9
+        key = "exchange_gbs_per_direction_over_collective" if mode == D.MODE_P2P else "nccl_bus_gbs"
+        line[key] = wire_bytes / (coll_ms * 1e-3) / 1e9 if coll_ms else None
+        line["nvlink_counters"] = nvl_res  # per rank, measured by each GPU itself
     ir = roof(b_k1, k1_ms)
     ir["kernel"] = "adamw_kernel (K1, %s)" % args.inner_mode
     ir["traffic"] = ncu_traffic("adamw_kernel", n)
@@ -459,10 +556,14 @@ def run_ours(args):
         del hx, ht
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        res = cpu_reference_outer(k, 1 if prec == D.FP16 else 0, iters=2)
+        # a bounded sample (~10 s of CPU work); the --impl reference arm times the full workload
+        res = cpu_reference_outer(n, k, 1 if prec == D.FP16 else 0, iters=2, full_ok=False)
         if res is not None:
             v, secs, desc = res
             line["cpu_baseline"] = dict(desc, value=v, unit="params/s")
+        ci = cpu_reference_inner(n)
+        if ci is not None:
+            line["inner_adamw"]["cpu_baseline"] = ci
     if world == 1 and not args.no_wire:
         line["wire"] = measure_wire(D, eng, n, prec, cpu=not args.no_cpu_baseline)
     if rank == 0:

@@ -95,9 +95,10 @@ class _Lib:
                              P(C.c_uint8), P(_sz), P(_sz), P(_u64), P(_u64), P(_sz), P(_sz))
         else:
             self._reduce = fn("reduce_average", C.c_int, C.POINTER(C.c_void_p), _sz, _sz, C.c_int, _f32p)
-            self._bench_outer = fn("bench_outer", C.c_int, C.c_int, _sz, _sz, C.c_int, C.c_int,
-                                   C.c_float, C.c_float, C.POINTER(C.c_double))
-            self._bench_inner = fn("bench_inner", C.c_int, C.c_int, _sz, C.c_int, C.POINTER(C.c_double))
+            _dp = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+            self._bench_outer = fn("bench_outer", C.c_int, C.c_int, _sz, _sz, C.c_int, C.c_int, C.c_int,
+                                   C.c_float, C.c_float, _dp)
+            self._bench_inner = fn("bench_inner", C.c_int, C.c_int, _sz, C.c_int, C.c_int, _dp)
             vp = C.c_void_p
             self._ck_read = fn("checkpoint_read", C.c_int, C.c_char_p, _sz, _sz, vp, vp, vp, vp, vp,
                                C.POINTER(_u64), C.POINTER(C.c_double), C.POINTER(_u64))
@@ -314,12 +315,14 @@ class _Lib:
                  "precision": int(pr[i]), "ok": bool(ok[i])} for i in range(k)]
 
     # -- CPU baseline harness (reference only) -----------------------------------
-    def bench_outer(self, threads, slice_len, k, precision, iters, lr=0.7, mu=0.9):
-        t = C.c_double(0)
-        st = self._bench_outer(threads, slice_len, k, precision, iters, lr, mu, C.byref(t))
+    def bench_outer(self, threads, n, k, precision, warmup, iters, lr=0.7, mu=0.9):
+        """Wall seconds of each timed iteration of run_simulated's outer round over
+        n parameters x k workers, split across `threads` host threads."""
+        t = np.zeros(iters, np.float64)
+        st = self._bench_outer(threads, n, k, precision, warmup, iters, lr, mu, t)
         if st:
             raise RuntimeError(f"ref_bench_outer failed with status {st}")
-        return float(t.value)
+        return [float(x) for x in t]
 
     def bench_wire(self, threads, slice_len, precision, chunk_bytes, iters):
         """(seconds per iteration, frame bytes per iteration) of the reference's scatter-side framing."""
@@ -329,12 +332,13 @@ class _Lib:
             raise RuntimeError(f"ref_bench_wire failed with status {st}")
         return float(t.value), int(b.value)
 
-    def bench_inner(self, threads, slice_len, iters):
-        t = C.c_double(0)
-        st = self._bench_inner(threads, slice_len, iters, C.byref(t))
+    def bench_inner(self, threads, n, warmup, iters):
+        """Wall seconds of each timed apply_inner_step over n parameters."""
+        t = np.zeros(iters, np.float64)
+        st = self._bench_inner(threads, n, warmup, iters, t)
         if st:
             raise RuntimeError(f"ref_bench_inner failed with status {st}")
-        return float(t.value)
+        return [float(x) for x in t]
 
 
 _port = None

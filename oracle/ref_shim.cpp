@@ -213,7 +213,13 @@ namespace {
 std::vector<float> fill(uint64_t seed, const char* purpose, uint64_t stream, size_t first,
                         size_t n, float lo, float hi) {
   CounterRng rng(seed, purpose, stream);
-  for (size_t i = 0; i < first; ++i) rng.next_u64();
+  // skip `first` draws: each draw advances the (only) state word by the
+  // splitmix64 increment (rng.hpp:43-46), so add first x increment directly
+  static_assert(sizeof(CounterRng) == sizeof(uint64_t), "CounterRng holds one state word");
+  uint64_t state;
+  std::memcpy(&state, &rng, sizeof state);
+  state += 0x9E3779B97F4A7C15ull * (uint64_t)first;
+  std::memcpy(static_cast<void*>(&rng), &state, sizeof state);
   std::vector<float> out(n);
   for (float& f : out) f = rng.next_uniform(lo, hi);
   return out;
@@ -221,109 +227,144 @@ std::vector<float> fill(uint64_t seed, const char* purpose, uint64_t stream, siz
 
 }  // namespace
 
-REF_API int ref_bench_outer(int threads, size_t slice, size_t k, int precision, int iters,
-                            float lr, float mu, double* sec_per_iter) {
-  if (threads < 1 || k < 1 || iters < 1 || slice < 1) return kConfig;
-  const Precision prec = precision ? Precision::fp16 : Precision::fp32;
-  std::barrier sync(threads + 1);
-  std::vector<double> t_thread(threads, 0.0);
-  std::atomic<int> err{0};
-  auto work = [&](int tid) {
-    try {
-      auto layout = Layout::single("p", slice);
-      const std::vector<float> theta0 = fill(4242, "theta", 0, tid * slice, slice, -0.05f, 0.05f);
-      std::vector<ParamVector> theta_t, local, pristine;
-      std::vector<NesterovState> outer;
-      for (size_t w = 0; w < k; ++w) {
-        std::vector<float> noise = fill(4242, "local", w, tid * slice, slice, -1e-3f, 1e-3f);
-        std::vector<float> loc(slice);
-        for (size_t i = 0; i < slice; ++i) loc[i] = theta0[i] - noise[i];
-        theta_t.emplace_back(layout, theta0);
-        pristine.emplace_back(layout, std::move(loc));
-        local.push_back(pristine.back());
-        outer.push_back(NesterovState::init(layout, lr, mu));
-      }
-      for (int it = 0; it < iters; ++it) {
-        for (size_t w = 0; w < k; ++w) local[w] = pristine[w];  // untimed: fresh window
-        sync.arrive_and_wait();
-        const auto t0 = std::chrono::steady_clock::now();
-        // run_simulated's outer round (netsim.cpp:325-357) on this slice.
-        std::vector<ParamVector> deltas;
-        deltas.reserve(k);
-        for (size_t w = 0; w < k; ++w) deltas.push_back(axpy(-1.0f, local[w], theta_t[w]));
-        std::vector<const ParamVector*> ptrs;
-        for (const auto& d : deltas) ptrs.push_back(&d);
-        const ParamVector dbar = reduce_average(ptrs, prec);
-        for (size_t w = 0; w < k; ++w) {  // DilocoEngine::outer_step, engine.cpp:136-144
-          if (dbar.all_finite()) theta_t[w] = nesterov_step(outer[w], theta_t[w], dbar);
-          local[w] = theta_t[w];
-        }
-        t_thread[tid] += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-        sync.arrive_and_wait();
-      }
-    } catch (...) {
-      err = 1;
-    }
-  };
-  std::vector<std::thread> pool;
-  for (int t = 0; t < threads; ++t) pool.emplace_back(work, t);
-  for (int it = 0; it < iters; ++it) {
-    sync.arrive_and_wait();
-    sync.arrive_and_wait();
-  }
-  for (auto& th : pool) th.join();
-  if (err) return kOther;
-  double worst = 0.0;
-  for (double t : t_thread) worst = t > worst ? t : worst;
-  *sec_per_iter = worst / iters;
-  return kOk;
+// Thread t takes elements [lo_t, lo_t + len_t) of an n-element vector
+// (balanced split).  `warmup` untimed iterations, then `iters` timed ones;
+// per_iter[i] = wall seconds of timed iteration i, from the moment every
+// thread starts it until the last one finishes (main-thread clock between
+// the two barriers).
+namespace {
+
+struct Split {
+  size_t lo, len;
+};
+Split split(size_t n, int threads, int t) {
+  const size_t base = n / threads, extra = n % threads;
+  return Split{t * base + std::min<size_t>(t, extra), base + ((size_t)t < extra ? 1 : 0)};
 }
 
-// Inner step per thread: scale_gradient (engine.cpp:20-27) +
-// scaler_unscale_and_check + adamw_step (engine.cpp:50-69) on a slice.
-REF_API int ref_bench_inner(int threads, size_t slice, int iters, double* sec_per_iter) {
-  if (threads < 1 || iters < 1 || slice < 1) return kConfig;
+template <typename Body>
+int run_timed(int threads, int warmup, int iters, double* per_iter, Body&& body) {
   std::barrier sync(threads + 1);
-  std::vector<double> t_thread(threads, 0.0);
   std::atomic<int> err{0};
   auto work = [&](int tid) {
     try {
-      auto layout = Layout::single("p", slice);
-      ParamVector params(layout, fill(4242, "theta", 0, tid * slice, slice, -0.05f, 0.05f));
-      const ParamVector grad(layout, fill(4242, "grad", 0, tid * slice, slice, -1e-2f, 1e-2f));
-      AdamWState adam = AdamWState::init(layout, 0.9f, 0.95f, 1e-8f, 0.1f);
-      LossScaler scaler;
-      LrSchedule sched;
-      for (int it = 0; it < iters; ++it) {
-        sync.arrive_and_wait();
-        const auto t0 = std::chrono::steady_clock::now();
-        std::vector<float> scaled(slice);
-        const auto g = grad.values();
-        for (size_t i = 0; i < slice; ++i) scaled[i] = g[i] * scaler.scale;
-        UnscaleResult un = scaler_unscale_and_check(scaler, ParamVector(layout, std::move(scaled)));
-        if (!un.overflow) {
-          params = adamw_step(adam, params, un.grad, lr_at(sched, adam.step_count + 1));
-        }
-        scaler_update(scaler, un.overflow);
-        t_thread[tid] += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-        sync.arrive_and_wait();
-      }
+      body.setup(tid);
     } catch (...) {
       err = 1;
+    }
+    for (int it = 0; it < warmup + iters; ++it) {
+      body.prepare(tid);  // untimed
+      sync.arrive_and_wait();
+      try {
+        if (!err) body.step(tid);
+      } catch (...) {
+        err = 1;
+      }
+      sync.arrive_and_wait();
     }
   };
   std::vector<std::thread> pool;
   for (int t = 0; t < threads; ++t) pool.emplace_back(work, t);
-  for (int it = 0; it < iters; ++it) {
+  for (int it = 0; it < warmup + iters; ++it) {
     sync.arrive_and_wait();
+    const auto t0 = std::chrono::steady_clock::now();
     sync.arrive_and_wait();
+    if (it >= warmup) per_iter[it - warmup] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   }
   for (auto& th : pool) th.join();
-  if (err) return kOther;
-  double worst = 0.0;
-  for (double t : t_thread) worst = t > worst ? t : worst;
-  *sec_per_iter = worst / iters;
-  return kOk;
+  return err ? kOther : kOk;
+}
+
+}  // namespace
+
+// run_simulated's outer round (netsim.cpp:325-357) over n parameters per
+// worker, K workers: K x axpy pseudo-gradients, one reduce_average, K x
+// (all_finite, nesterov_step, theta_local = theta_t).
+REF_API int ref_bench_outer(int threads, size_t n, size_t k, int precision, int warmup, int iters, float lr,
+                            float mu, double* per_iter) {
+  if (threads < 1 || k < 1 || iters < 1 || warmup < 0 || n < (size_t)threads || !per_iter) return kConfig;
+  const Precision prec = precision ? Precision::fp16 : Precision::fp32;
+  struct Body {
+    size_t n, k;
+    Precision prec;
+    float lr, mu;
+    struct Slice {
+      std::vector<ParamVector> theta_t, local, pristine;
+      std::vector<NesterovState> outer;
+    };
+    std::vector<Slice> sl;
+    int threads;
+    void setup(int tid) {
+      const Split sp = split(n, threads, tid);
+      auto layout = Layout::single("p", sp.len);
+      const std::vector<float> theta0 = fill(4242, "theta", 0, sp.lo, sp.len, -0.05f, 0.05f);
+      Slice& s = sl[tid];
+      for (size_t w = 0; w < k; ++w) {
+        std::vector<float> noise = fill(4242, "local", w, sp.lo, sp.len, -1e-3f, 1e-3f);
+        std::vector<float> loc(sp.len);
+        for (size_t i = 0; i < sp.len; ++i) loc[i] = theta0[i] - noise[i];
+        s.theta_t.emplace_back(layout, theta0);
+        s.pristine.emplace_back(layout, std::move(loc));
+        s.local.push_back(s.pristine.back());
+        s.outer.push_back(NesterovState::init(layout, lr, mu));
+      }
+    }
+    void prepare(int tid) {  // a fresh end-of-window theta_local
+      Slice& s = sl[tid];
+      for (size_t w = 0; w < k; ++w) s.local[w] = s.pristine[w];
+    }
+    void step(int tid) {
+      Slice& s = sl[tid];
+      std::vector<ParamVector> deltas;
+      deltas.reserve(k);
+      for (size_t w = 0; w < k; ++w) deltas.push_back(axpy(-1.0f, s.local[w], s.theta_t[w]));  // engine.cpp:122
+      std::vector<const ParamVector*> ptrs;
+      for (const auto& d : deltas) ptrs.push_back(&d);
+      const ParamVector dbar = reduce_average(ptrs, prec);
+      for (size_t w = 0; w < k; ++w) {  // DilocoEngine::outer_step, engine.cpp:136-144
+        if (dbar.all_finite()) s.theta_t[w] = nesterov_step(s.outer[w], s.theta_t[w], dbar);
+        s.local[w] = s.theta_t[w];
+      }
+    }
+  } body{n, k, prec, lr, mu, std::vector<Body::Slice>(threads), threads};
+  return run_timed(threads, warmup, iters, per_iter, body);
+}
+
+// apply_inner_step (engine.cpp:50-69) over n parameters: scale_gradient
+// (engine.cpp:20-27), scaler_unscale_and_check, lr_at, adamw_step,
+// scaler_update.
+REF_API int ref_bench_inner(int threads, size_t n, int warmup, int iters, double* per_iter) {
+  if (threads < 1 || iters < 1 || warmup < 0 || n < (size_t)threads || !per_iter) return kConfig;
+  struct Body {
+    size_t n;
+    int threads;
+    struct Slice {
+      std::vector<ParamVector> params, grad;
+      std::vector<AdamWState> adam;
+      LossScaler scaler;
+      LrSchedule sched;
+    };
+    std::vector<Slice> sl;
+    void setup(int tid) {
+      const Split sp = split(n, threads, tid);
+      auto layout = Layout::single("p", sp.len);
+      Slice& s = sl[tid];
+      s.params.emplace_back(layout, fill(4242, "theta", 0, sp.lo, sp.len, -0.05f, 0.05f));
+      s.grad.emplace_back(layout, fill(4242, "grad", 0, sp.lo, sp.len, -1e-2f, 1e-2f));
+      s.adam.push_back(AdamWState::init(layout, 0.9f, 0.95f, 1e-8f, 0.1f));
+    }
+    void prepare(int) {}
+    void step(int tid) {
+      Slice& s = sl[tid];
+      const auto g = s.grad[0].values();
+      std::vector<float> scaled(g.size());
+      for (size_t i = 0; i < g.size(); ++i) scaled[i] = g[i] * s.scaler.scale;
+      UnscaleResult un = scaler_unscale_and_check(s.scaler, ParamVector(s.grad[0].layout(), std::move(scaled)));
+      if (!un.overflow) s.params[0] = adamw_step(s.adam[0], s.params[0], un.grad, lr_at(s.sched, s.adam[0].step_count + 1));
+      scaler_update(s.scaler, un.overflow);
+    }
+  } body{n, threads, std::vector<Body::Slice>(threads)};
+  return run_timed(threads, warmup, iters, per_iter, body);
 }
 
 // ---------------------------------------------------------------------------

@@ -51,7 +51,7 @@ class ReduceReport(C.Structure):
 
 class P2PTuning(C.Structure):
     _fields_ = [("plan", C.c_uint32 * 32), ("plan_len", C.c_uint32), ("fold_ctas", C.c_int32),
-                ("fold_threads", C.c_int32), ("piece_ctas", C.c_int32)]
+                ("fold_threads", C.c_int32), ("piece_ctas", C.c_int32), ("fold_kernel", C.c_int32)]
 
 
 class WireTags(C.Structure):

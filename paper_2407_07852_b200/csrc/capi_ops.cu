@@ -402,6 +402,7 @@ int dlc_fold_push_probe(const void* const* contribs, int k, size_t n, int precis
                         int* nonfinite) {
   return guard([&] {
     if (k < 1 || k > kMaxK) fail(DLC_EINVAL, "fold_push_probe: k must be 1..32");
+    if (tma < 0 || tma > 2) fail(DLC_EINVAL, "fold_push_probe: tma must be 0, 1 or 2");
     if (precision != DLC_FP32 && precision != DLC_FP16) fail(DLC_ECONFIG, "unknown precision");
     if (n % 64) fail(DLC_ESHAPE, "fold_push_probe: n must be a multiple of 64");
     if (!contribs || !nonfinite) fail(DLC_EINVAL, "fold_push_probe: null argument");
@@ -421,7 +422,8 @@ int dlc_fold_push_probe(const void* const* contribs, int k, size_t n, int precis
     DLC_CUDA(cudaMemsetAsync(d_flag, 0, sizeof(int), c.stream));
     outs.ptr[0] = d_out;
     flags.ptr[0] = d_flag;
-    if (!(tma && launch_fold_push_tma(in, k, precision, outs, 1, flags, 1, n, tma_ctas(k), tma_threads(k), c.stream)))
+    if (!(tma && launch_fold_push_tma(in, k, precision, outs, 1, flags, 1, n, tma_ctas(k), tma_threads(k), tma - 1,
+                                      c.stream)))
       launch_fold_push(in, k, precision, outs, 1, flags, 1, n, 0, c.stream);
     d2h(out, d_out, n * w, c.stream);
     d2h(nonfinite, d_flag, sizeof(int), c.stream);
@@ -493,7 +495,8 @@ int dlc_p2p_overlap_probe(int k, size_t n, int precision, int reps, int fold_cta
         launch_pseudo_grad_piece(ttp, src, st, send, precision, k, S, 0, S, n, 0, c.stream);
       });
       ms3[1] = timed([&] {
-        if (!launch_fold_push_tma(in, k, precision, outs, k, fl, k, S, tma_ctas(k), tma_threads(k), c.stream))
+        if (!launch_fold_push_tma(in, k, precision, outs, k, fl, k, S, tma_ctas(k), tma_threads(k), fold_kernel(),
+                                  c.stream))
           launch_fold_push(in, k, precision, outs, k, fl, k, S, kFoldCtas, c.stream);
       });
       ms3[2] = timed([&] {
@@ -513,7 +516,7 @@ int dlc_p2p_overlap_probe(int k, size_t n, int precision, int reps, int fold_cta
         DLC_CUDA(cudaEventRecord(f0, s2));
         for (int i = 0; i < freps; ++i)
           if (!launch_fold_push_tma(in, k, precision, outs, k, fl, k, S, fold_ctas > 0 ? fold_ctas : tma_ctas(k),
-                                    tma_threads(k), s2))
+                                    tma_threads(k), fold_kernel(), s2))
             launch_fold_push(in, k, precision, outs, k, fl, k, S, fold_ctas > 0 ? fold_ctas : kFoldCtas, s2);
         DLC_CUDA(cudaEventRecord(f1, s2));
         DLC_CUDA(cudaEventRecord(ev[0], c.stream));

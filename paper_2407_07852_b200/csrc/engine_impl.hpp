@@ -147,6 +147,7 @@ std::vector<size_t> piece_plan(size_t S, size_t n, bool host_path = false);
 int tma_ctas(size_t k);
 int tma_threads(size_t k);
 int piece_ctas();
+int fold_kernel();
 void ensure_copy_streams(dlc_engine* e);
 void ensure_chunk_events(dlc_engine* e, size_t count);
 void harvest(dlc_engine* e);

@@ -82,6 +82,9 @@ int tma_threads(size_t k) {
 // CTAs of the K2 / K4 piece kernels running beside the fold (0: one per window)
 int piece_ctas() { return tuning().piece_ctas; }
 
+// TMA fold kernel: 0 warp-specialised (default), 1 single leader thread (A/B)
+int fold_kernel() { return tuning().fold_kernel; }
+
 void ensure_copy_streams(dlc_engine* e) {
   if (!e->h2d) DLC_CUDA(cudaStreamCreateWithFlags(&e->h2d, cudaStreamNonBlocking));
   if (!e->d2h) DLC_CUDA(cudaStreamCreateWithFlags(&e->d2h, cudaStreamNonBlocking));
@@ -424,6 +427,7 @@ int dlc_p2p_set_tuning(const dlc_p2p_tuning* t) {
       if (v.fold_threads != 0 && v.fold_threads != 128 && v.fold_threads != 256 && v.fold_threads != 512)
         fail(DLC_ECONFIG, "p2p tuning: fold_threads must be 128, 256 or 512");
       if (v.fold_ctas < 0 || v.piece_ctas < 0) fail(DLC_ECONFIG, "p2p tuning: negative CTA count");
+      if (v.fold_kernel != 0 && v.fold_kernel != 1) fail(DLC_ECONFIG, "p2p tuning: fold_kernel must be 0 or 1");
     }
     std::lock_guard<std::mutex> lock(g_tuning_mu);
     g_tuning = v;

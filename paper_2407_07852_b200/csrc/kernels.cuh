@@ -124,11 +124,14 @@ void launch_nesterov_outer(Pair theta_t, Pair buf, Pair theta_local,
 // `ctas` > 0 runs a persistent grid of that many CTAs (0: one CTA per window).
 void launch_fold_push(const PtrList& in, int k, int precision, const PtrList& outs, int nout,
                       const PtrList& flags, int nflags, size_t n, int ctas, cudaStream_t s);
-// fold_push with the bulk-copy engine (TMA) moving the tiles, `threads` per CTA
-// (128 / 256 / 512); false when k is outside 2..8 (the caller then uses
-// launch_fold_push)
+// fold_push with the bulk-copy engine (TMA) moving the tiles, `threads`
+// folding threads per CTA (128 / 256 / 512); kernel 0: warp-specialised (a
+// producer warp + the folding warps), 1: one leader thread issues the copies
+// between its share of the fold.  False when k is outside 2..8 (the caller then
+// uses launch_fold_push).
 bool launch_fold_push_tma(const PtrList& in, int k, int precision, const PtrList& outs, int nout,
-                          const PtrList& flags, int nflags, size_t n, int ctas, int threads, cudaStream_t s);
+                          const PtrList& flags, int nflags, size_t n, int ctas, int threads, int kernel,
+                          cudaStream_t s);
 // Fleet barrier over NVLink flags (DLC_MODE_P2P): one CTA stores the barrier's
 // signal into slot `me` of every peer's signal array (`remote`, after a system
 // fence), then waits until every peer's signal has landed in `local`.  A peer

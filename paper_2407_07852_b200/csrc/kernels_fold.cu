@@ -401,6 +401,177 @@ __global__ void __launch_bounds__(NT) fold_push_tma_kernel(const __grid_constant
 
 size_t fold_push_tma_smem(int k) { return (size_t)kTmaStages * (k + 1) * kTmaTileBytes + kTmaStages * 8; }
 
+// ---- K3 fused with the all-gather, warp-specialised TMA version --------------
+// The same fold again, with the roles split across warps so no thread both
+// issues copies and computes:
+//   warp 0 (one elected lane): producer.  Streams 8 KB tiles of the KK inputs
+//     into a kWsStages-deep ring (bulk copies, mbarrier full[s] with the
+//     expected bytes); reuses stage s once the consumers release it (empty[s]).
+//   warps 1..NC: consumers.  Wait full[s], fold the tile 16 B per thread and
+//     step (decode 2 codes per conversion, rank-ordered FP32 adds, the mean,
+//     encode 2 per conversion), release in_buf[s] (empty[s]), write the mean
+//     tile into one of two output buffers; one elected consumer bulk-stores it
+//     to every destination (the owner's slot in every rank's gather buffer).
+// Only the consumers meet at a named barrier, once per tile.  FP16 decode is
+// the plain hardware widening (exact for every finite and infinite code; a NaN
+// contribution makes the mean NaN whatever its payload, and NaNs compare by
+// class); encode is cvt.rn.f16x2.f32 (RNE with overflow to inf,
+// fp16.cpp:25-63) with the reference's NaN code sign|0x7E00 patched on the
+// rare path where a code is non-finite.
+constexpr int kWsStages = 3;
+constexpr int kWsOutStages = 2;
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void consumer_sync(int nthreads) {
+  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+
+__device__ __forceinline__ float2 h2_to_f2(uint32_t w) {
+  return __half22float2(*reinterpret_cast<const __half2*>(&w));
+}
+
+__device__ __forceinline__ uint32_t f2_to_h2(float lo, float hi) {
+  const __half2 h = __floats2half2_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+__device__ __forceinline__ bool h2_nonfinite(uint32_t w) {
+  return ((w & 0x7C00u) == 0x7C00u) | ((w & 0x7C000000u) == 0x7C000000u);
+}
+
+template <int PREC, int KK, int NC>
+__global__ void __launch_bounds__(32 * (NC + 1)) fold_push_ws_kernel(const __grid_constant__ PtrList in,
+                                                                     const __grid_constant__ PtrList outs, int nout,
+                                                                     const __grid_constant__ PtrList flags,
+                                                                     int nflags, size_t n, MeanDiv divisor) {
+  constexpr int W = PREC == 1 ? 2 : 4;
+  constexpr int TILE = kTmaTileBytes / W;  // elements per tile
+  constexpr int NCT = NC * 32;             // consumer threads
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* in_buf = smem;                                       // [kWsStages][KK][8 KB]
+  uint8_t* out_buf = smem + kWsStages * KK * kTmaTileBytes;     // [kWsOutStages][8 KB]
+  uint64_t* full = reinterpret_cast<uint64_t*>(out_buf + kWsOutStages * kTmaTileBytes);  // [kWsStages]
+  uint64_t* empty = full + kWsStages;                                                     // [kWsStages]
+  __shared__ int s_bad;
+  const size_t ntiles = (n + TILE - 1) / TILE;
+  const size_t mine = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  auto tile_bytes = [&](size_t t) {
+    const size_t e = t * (size_t)TILE;
+    return (uint32_t)((n - e < (size_t)TILE ? n - e : (size_t)TILE) * W);
+  };
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kWsStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NC);  // one arrival per consumer warp
+    }
+    s_bad = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 0) {  // ---- producer ----
+    if (lane == 0) {
+      for (size_t i = 0; i < mine; ++i) {
+        const int s = (int)(i % kWsStages);
+        if (i >= (size_t)kWsStages) mbar_wait(&empty[s], (uint32_t)(((i / kWsStages) + 1) & 1));
+        const size_t t = blockIdx.x + i * gridDim.x;
+        const uint32_t bytes = tile_bytes(t);
+        mbar_expect_tx(&full[s], bytes * KK);
+#pragma unroll
+        for (int j = 0; j < KK; ++j)
+          bulk_load(in_buf + ((size_t)s * KK + j) * kTmaTileBytes,
+                    static_cast<const uint8_t*>(in.ptr[j]) + t * (size_t)kTmaTileBytes, bytes, &full[s]);
+      }
+    }
+    return;
+  }
+  // ---- consumers ----
+  const int ct = threadIdx.x - 32;
+  const bool storer = ct == 0;
+  bool bad = false;
+  for (size_t i = 0; i < mine; ++i) {
+    const int s = (int)(i % kWsStages);
+    const size_t t = blockIdx.x + i * gridDim.x;
+    const uint32_t bytes = tile_bytes(t);
+    uint8_t* dst = out_buf + (size_t)(i % kWsOutStages) * kTmaTileBytes;  // free: see the wait below
+    mbar_wait(&full[s], (uint32_t)((i / kWsStages) & 1));
+    const uint8_t* src = in_buf + (size_t)s * KK * kTmaTileBytes;
+    for (uint32_t off = ct * 16; off < bytes; off += NCT * 16) {
+      uint4 o;
+      if constexpr (PREC == 1) {
+        float a[8];
+#pragma unroll
+        for (int j = 0; j < KK; ++j) {  // rank order (reduce.cpp:37-43)
+          const uint4 v = *reinterpret_cast<const uint4*>(src + (size_t)j * kTmaTileBytes + off);
+          const float2 x0 = h2_to_f2(v.x), x1 = h2_to_f2(v.y), x2 = h2_to_f2(v.z), x3 = h2_to_f2(v.w);
+          if (j == 0) {
+            a[0] = x0.x; a[1] = x0.y; a[2] = x1.x; a[3] = x1.y;
+            a[4] = x2.x; a[5] = x2.y; a[6] = x3.x; a[7] = x3.y;
+          } else {
+            a[0] = __fadd_rn(a[0], x0.x); a[1] = __fadd_rn(a[1], x0.y);
+            a[2] = __fadd_rn(a[2], x1.x); a[3] = __fadd_rn(a[3], x1.y);
+            a[4] = __fadd_rn(a[4], x2.x); a[5] = __fadd_rn(a[5], x2.y);
+            a[6] = __fadd_rn(a[6], x3.x); a[7] = __fadd_rn(a[7], x3.y);
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) a[q] = div_mean(a[q], divisor);
+        o = make_uint4(f2_to_h2(a[0], a[1]), f2_to_h2(a[2], a[3]), f2_to_h2(a[4], a[5]), f2_to_h2(a[6], a[7]));
+        if (h2_nonfinite(o.x) | h2_nonfinite(o.y) | h2_nonfinite(o.z) | h2_nonfinite(o.w)) {
+          bad = true;  // rare: the reference's exact codes (NaN -> sign|0x7E00)
+          o = make_uint4(pack2(fp16_encode(a[0]), fp16_encode(a[1])), pack2(fp16_encode(a[2]), fp16_encode(a[3])),
+                         pack2(fp16_encode(a[4]), fp16_encode(a[5])), pack2(fp16_encode(a[6]), fp16_encode(a[7])));
+        }
+      } else {
+        float a[4];
+#pragma unroll
+        for (int j = 0; j < KK; ++j) {
+          const uint4 v = *reinterpret_cast<const uint4*>(src + (size_t)j * kTmaTileBytes + off);
+          const float x[4] = {__uint_as_float(v.x), __uint_as_float(v.y), __uint_as_float(v.z), __uint_as_float(v.w)};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) a[q] = j == 0 ? x[q] : __fadd_rn(a[q], x[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          a[q] = div_mean(a[q], divisor);
+          bad |= !finite_f(a[q]);
+        }
+        o = make_uint4(__float_as_uint(a[0]), __float_as_uint(a[1]), __float_as_uint(a[2]), __float_as_uint(a[3]));
+      }
+      *reinterpret_cast<uint4*>(dst + off) = o;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);  // in_buf[s] is read: the producer may refill it
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // our smem writes -> the bulk store's reads
+    // before the next tile overwrites the other output buffer, the store that
+    // read it (issued one tile ago) must be done reading
+    if (storer) bulk_wait_read<kWsOutStages - 2>();
+    consumer_sync(NCT);  // every consumer's share of dst is written
+    if (storer) {
+      for (int o = 0; o < nout; ++o)
+        bulk_store(static_cast<uint8_t*>(const_cast<void*>(outs.ptr[o])) + t * (size_t)kTmaTileBytes, dst, bytes);
+      bulk_commit();
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&s_bad, 1);
+  consumer_sync(NCT);
+  if (storer) {
+    if (s_bad)
+      for (int o = 0; o < nflags; ++o) *reinterpret_cast<volatile int*>(const_cast<void*>(flags.ptr[o])) = 1;
+    bulk_wait_all();  // every bulk store of this CTA has landed
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    __threadfence_system();  // ... and is visible system-wide before the barrier that follows
+  }
+}
+
+size_t fold_push_ws_smem(int k) {
+  return (size_t)kWsStages * k * kTmaTileBytes + kWsOutStages * kTmaTileBytes + 2 * kWsStages * 8;
+}
+
+
 // ---- NVLink flag barrier ----------------------------------------------------
 __global__ void flag_barrier_kernel(const __grid_constant__ PtrList remote, const uint64_t* local, int k, int me,
                                     uint64_t epoch, int* err, uint64_t timeout_ns, int stall, int commit) {
@@ -482,53 +653,68 @@ void launch_fold_push(const PtrList& in, int k, int precision, const PtrList& ou
 #undef DLC_FOLD_PUSH
 }
 
+namespace {
+
+// One instance of the TMA fold: WS = the warp-specialised kernel (NT consumer
+// threads + a producer warp), else the single-leader one (NT threads).
+template <int P, int KK, int NT, bool WS>
+void launch_tma_inst(int grid, cudaStream_t s, const PtrList& in, const PtrList& outs, int nout, const PtrList& flags,
+                     int nflags, size_t n, MeanDiv md) {
+  auto* kern = WS ? fold_push_ws_kernel<P, KK, NT / 32> : fold_push_tma_kernel<P, KK, NT>;
+  const size_t smem = WS ? fold_push_ws_smem(KK) : fold_push_tma_smem(KK);
+  // per-device function attribute, set once (rank threads may launch concurrently)
+  static std::atomic<unsigned> attr_devices{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!(attr_devices.load() & (1u << (dev & 31)))) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  // failures surface at launch
+    attr_devices.fetch_or(1u << (dev & 31));
+  }
+  kern<<<grid, WS ? NT + 32 : NT, smem, s>>>(in, outs, nout, flags, nflags, n, md);
+}
+
+template <int P, int KK>
+void launch_tma_k(int nt, bool ws, int grid, cudaStream_t s, const PtrList& in, const PtrList& outs, int nout,
+                  const PtrList& flags, int nflags, size_t n, MeanDiv md) {
+#define DLC_TMA_NT(NT)                                                                     \
+  (ws ? launch_tma_inst<P, KK, NT, true>(grid, s, in, outs, nout, flags, nflags, n, md)    \
+      : launch_tma_inst<P, KK, NT, false>(grid, s, in, outs, nout, flags, nflags, n, md))
+  if (nt >= 512)
+    DLC_TMA_NT(512);
+  else if (nt >= 256)
+    DLC_TMA_NT(256);
+  else
+    DLC_TMA_NT(128);
+#undef DLC_TMA_NT
+}
+
+template <int P>
+bool launch_tma_p(int k, int nt, bool ws, int grid, cudaStream_t s, const PtrList& in, const PtrList& outs, int nout,
+                  const PtrList& flags, int nflags, size_t n, MeanDiv md) {
+  switch (k) {
+    case 2: launch_tma_k<P, 2>(nt, ws, grid, s, in, outs, nout, flags, nflags, n, md); return true;
+    case 3: launch_tma_k<P, 3>(nt, ws, grid, s, in, outs, nout, flags, nflags, n, md); return true;
+    case 4: launch_tma_k<P, 4>(nt, ws, grid, s, in, outs, nout, flags, nflags, n, md); return true;
+    case 5: launch_tma_k<P, 5>(nt, ws, grid, s, in, outs, nout, flags, nflags, n, md); return true;
+    case 6: launch_tma_k<P, 6>(nt, ws, grid, s, in, outs, nout, flags, nflags, n, md); return true;
+    case 7: launch_tma_k<P, 7>(nt, ws, grid, s, in, outs, nout, flags, nflags, n, md); return true;
+    case 8: launch_tma_k<P, 8>(nt, ws, grid, s, in, outs, nout, flags, nflags, n, md); return true;
+    default: return false;
+  }
+}
+
+}  // namespace
+
 bool launch_fold_push_tma(const PtrList& in, int k, int precision, const PtrList& outs, int nout,
-                          const PtrList& flags, int nflags, size_t n, int ctas, int threads, cudaStream_t s) {
-  const size_t smem = fold_push_tma_smem(k);
-  const int nt = threads;
+                          const PtrList& flags, int nflags, size_t n, int ctas, int threads, int kernel,
+                          cudaStream_t s) {
   const MeanDiv md = mean_div(k);  // reduce.cpp:36, 43
   const int W = precision == 1 ? 2 : 4;
   const size_t ntiles = (n + kTmaTileBytes / W - 1) / (kTmaTileBytes / W);
   const int grid = (int)std::max<size_t>(1, std::min<size_t>(ctas > 0 ? ctas : num_sms(), ntiles));
-#define DLC_TMA_NT(P, KK, NT)                                                                            \
-  {                                                                                                      \
-    /* per-device function attribute, set once (rank threads may launch concurrently) */                \
-    static std::atomic<unsigned> attr_devices{0};                                                        \
-    int dev = 0;                                                                                         \
-    cudaGetDevice(&dev);                                                                                 \
-    if (!(attr_devices.load() & (1u << (dev & 31)))) {                                                   \
-      cudaFuncSetAttribute(fold_push_tma_kernel<P, KK, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                           (int)fold_push_tma_smem(KK)); /* a failure surfaces as the launch error */    \
-      attr_devices.fetch_or(1u << (dev & 31));                                                           \
-    }                                                                                                    \
-    fold_push_tma_kernel<P, KK, NT><<<grid, NT, smem, s>>>(in, outs, nout, flags, nflags, n, md);        \
-    return true;                                                                                         \
-  }
-#define DLC_TMA(P, KK)                          \
-  {                                             \
-    if (nt >= 512) DLC_TMA_NT(P, KK, 512)       \
-    if (nt >= 256) DLC_TMA_NT(P, KK, 256)       \
-    DLC_TMA_NT(P, KK, 128)                      \
-  }
-#define DLC_TMA_K(P)             \
-  switch (k) {                   \
-    case 2: DLC_TMA(P, 2)        \
-    case 3: DLC_TMA(P, 3)        \
-    case 4: DLC_TMA(P, 4)        \
-    case 5: DLC_TMA(P, 5)        \
-    case 6: DLC_TMA(P, 6)        \
-    case 7: DLC_TMA(P, 7)        \
-    case 8: DLC_TMA(P, 8)        \
-    default: return false;       \
-  }
-  if (precision == 0) {
-    DLC_TMA_K(0)
-  } else {
-    DLC_TMA_K(1)
-  }
-#undef DLC_TMA_K
-#undef DLC_TMA
-#undef DLC_TMA_NT
+  const bool ws = kernel == 0;
+  return precision == 0 ? launch_tma_p<0>(k, threads, ws, grid, s, in, outs, nout, flags, nflags, n, md)
+                        : launch_tma_p<1>(k, threads, ws, grid, s, in, outs, nout, flags, nflags, n, md);
 }
 
 void launch_flag_barrier(const PtrList& remote, const uint64_t* local, int k, int me, uint64_t epoch, int* err,

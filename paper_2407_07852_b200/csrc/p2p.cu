@@ -284,7 +284,7 @@ void p2p_fold(P2PStep& s, size_t p) {
   }
   cudaEvent_t tf = trace_begin(e, e->cstream);
   if (!launch_fold_push_tma(in, (int)K, e->prec, outs, (int)K, pfl, (int)K, plen, tma_ctas(K), tma_threads(K),
-                            e->cstream))
+                            fold_kernel(), e->cstream))
     launch_fold_push(in, (int)K, e->prec, outs, (int)K, pfl, (int)K, plen, kFoldCtas, e->cstream);
   launched("fold_push");
   trace_end(e, e->cstream, "fold_push", (int)p, tf);

@@ -578,10 +578,11 @@ class World:
             pass
 
 
-def set_p2p_tuning(plan=None, fold_ctas: int = 0, fold_threads: int = 0, piece_ctas: int = 0) -> None:
+def set_p2p_tuning(plan=None, fold_ctas: int = 0, fold_threads: int = 0, piece_ctas: int = 0,
+                   fold_kernel: int = 0) -> None:
     """dlc_p2p_set_tuning: override the measured DLC_MODE_P2P defaults (sweeps);
     no arguments restores them."""
-    if plan is None and not (fold_ctas or fold_threads or piece_ctas):
+    if plan is None and not (fold_ctas or fold_threads or piece_ctas or fold_kernel):
         _check(lib.dlc_p2p_set_tuning(None))
         return
     t = A.P2PTuning()
@@ -589,7 +590,7 @@ def set_p2p_tuning(plan=None, fold_ctas: int = 0, fold_threads: int = 0, piece_c
     t.plan_len = len(plan)
     for i, v in enumerate(plan):
         t.plan[i] = int(v)
-    t.fold_ctas, t.fold_threads, t.piece_ctas = fold_ctas, fold_threads, piece_ctas
+    t.fold_ctas, t.fold_threads, t.piece_ctas, t.fold_kernel = fold_ctas, fold_threads, piece_ctas, fold_kernel
     _check(lib.dlc_p2p_set_tuning(C.byref(t)))
 
 

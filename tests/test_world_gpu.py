@@ -130,7 +130,8 @@ def test_world_shared_device_nonfinite_skip(port, prec):
 
 
 @pytest.mark.parametrize("tuning", [dict(plan=[2, 2, 2, 2]), dict(plan=[1, 3, 4], fold_ctas=3),
-                                    dict(fold_threads=512, piece_ctas=37), dict(plan=[1] * 16, fold_ctas=1)])
+                                    dict(fold_threads=512, piece_ctas=37), dict(plan=[1] * 16, fold_ctas=1),
+                                    dict(fold_kernel=1), dict(fold_kernel=1, fold_threads=256, fold_ctas=5)])
 def test_world_shared_device_tuning(port, tuning):
     """The tuning overrides change the schedule, never the bits."""
     D.set_p2p_tuning(**tuning)
