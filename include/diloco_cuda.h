@@ -457,9 +457,17 @@ DLC_API int dlc_checkpoint_save(dlc_engine* const* engines, size_t count, const 
                                 const dlc_checkpoint_meta* meta, const char* const* seg_names,
                                 const uint64_t* seg_lengths, size_t nseg);
 /* Restores `count` engines (sizes must match, ShapeError otherwise);
- * meta_out (may be NULL) receives the header fields (ledger = NULL). */
+ * meta_out (may be NULL) receives the header fields (ledger = NULL).  All or
+ * nothing: the whole file is parsed and validated first (SerializationError
+ * for a truncated file, a missing key or a bad number; ShapeError for a
+ * layout or length mismatch), and no engine changes unless every engine
+ * restores.  The _layout variant also checks every vector's segment names and
+ * lengths against the caller's Layout (restore_state, engine.cpp:148-155). */
 DLC_API int dlc_checkpoint_load(dlc_engine* const* engines, size_t count, const char* path,
                                 dlc_checkpoint_meta* meta_out);
+DLC_API int dlc_checkpoint_load_layout(dlc_engine* const* engines, size_t count, const char* path,
+                                       const char* const* seg_names, const uint64_t* seg_lengths, size_t nseg,
+                                       dlc_checkpoint_meta* meta_out);
 
 /* Per-phase device timing with CUDA events on the engine stream (ncu-free
  * evidence for the roofline): phase 0 = K1 inner AdamW, 1 = K2 pseudo-grad,

@@ -184,6 +184,8 @@ _SIGS = {
     "dlc_checkpoint_save": (I, [PP, SZ, C.c_char_p, C.POINTER(CheckpointMeta), C.POINTER(C.c_char_p),
                                 C.POINTER(C.c_uint64), SZ]),
     "dlc_checkpoint_load": (I, [PP, SZ, C.c_char_p, C.POINTER(CheckpointMeta)]),
+    "dlc_checkpoint_load_layout": (I, [PP, SZ, C.c_char_p, C.POINTER(C.c_char_p), C.POINTER(C.c_uint64), SZ,
+                                       C.POINTER(CheckpointMeta)]),
     "dlc_optimizer_step": (I, [P, P, P, I, C.POINTER(I)]),
     "dlc_rng_key": (U64, [U64, C.c_char_p, U64]),
     "dlc_rng_fill_device": (I, [P, I, U64, U64, F, F]),

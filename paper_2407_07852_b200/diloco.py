@@ -621,11 +621,19 @@ def checkpoint_save(engines, path: str, config_hash: int = 0, completed_rounds: 
     _check(lib.dlc_checkpoint_save(arr, len(engines), path.encode(), C.byref(meta), names, lens, nseg))
 
 
-def checkpoint_load(engines, path: str) -> dict:
-    """load_checkpoint (checkpoint.cpp:162-198) into device engines; returns the header fields."""
+def checkpoint_load(engines, path: str, segments=None) -> dict:
+    """load_checkpoint (checkpoint.cpp:162-198) into device engines, all or nothing;
+    returns the header fields.  segments: optional [(name, length), ...] Layout
+    every vector must carry (restore_state, engine.cpp:148-155)."""
     arr = (C.c_void_p * len(engines))(*[e.handle.value for e in engines])
     meta = A.CheckpointMeta()
-    _check(lib.dlc_checkpoint_load(arr, len(engines), path.encode(), C.byref(meta)))
+    if segments:
+        nseg = len(segments)
+        names = (C.c_char_p * nseg)(*[s[0].encode() for s in segments])
+        lens = (C.c_uint64 * nseg)(*[int(s[1]) for s in segments])
+        _check(lib.dlc_checkpoint_load_layout(arr, len(engines), path.encode(), names, lens, nseg, C.byref(meta)))
+    else:
+        _check(lib.dlc_checkpoint_load(arr, len(engines), path.encode(), C.byref(meta)))
     return {"config_hash": int(meta.config_hash), "completed_rounds": int(meta.completed_rounds),
             "clock_seconds": float(meta.clock_seconds), "reduce_data_bytes": int(meta.reduce_data_bytes),
             "ledger_workers": int(meta.ledger_workers)}

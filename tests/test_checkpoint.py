@@ -110,3 +110,65 @@ def test_resume_is_bitwise(gpu, tmp_path, segments):
             D.checkpoint_load([D.DilocoEngine(cfg, hyper, n)], bad)
     a.close()
     b.close()
+
+
+@pytest.mark.gpu
+def test_failed_load_changes_nothing(gpu, tmp_path):
+    """load is all or nothing (the reference parses the whole file before any
+    restore_state, checkpoint.cpp:162-198): a file whose SECOND engine is
+    truncated, one with a bad number in a header, and one whose layout differs
+    from the caller's all fail, and both engines keep their state, counters
+    and hyperparameters bit for bit (checked by continuing them against twins
+    that never saw the failed loads)."""
+    D = gpu
+    n = 30_011
+    hyper = D.OptimHyperparams(inner_lr=1e-3, warmup_steps=3)
+    cfg = D.DilocoConfig(2, 1, D.FP16, 8)
+
+    def make(seed):
+        e = D.DilocoEngine(cfg, hyper, n)
+        th = O.rng_fill(seed, "theta", 0, n, -0.1, 0.1)
+        e.upload(D.THETA_T, th)
+        e.upload(D.THETA_LOCAL, th)
+        for t in range(2):
+            e.inner_step_host(O.rng_fill(seed, "grad", t, n, -1e-2, 1e-2))
+        e.outer_step(None)
+        return e
+
+    # a valid 2-engine file with other state and other hyperparameters
+    other = [D.DilocoEngine(cfg, D.OptimHyperparams(outer_lr=0.3, weight_decay=0.0), n) for _ in range(2)]
+    for j, e in enumerate(other):
+        e.upload(D.THETA_T, O.rng_fill(50 + j, "theta", 0, n, -1, 1))
+    good = str(tmp_path / "two.ckpt")
+    D.checkpoint_save(other, good, segments=[("w", n - 11), ("b", 11)])
+    raw = open(good, "rb").read()
+    bad_files = {"truncated_second": raw[: len(raw) - 4 * n // 2]}
+    txt = raw.replace(b"scale=", b"scale=x", 1)
+    bad_files["bad_number"] = txt
+    engines, twins = [make(1), make(2)], [make(1), make(2)]
+    for name, blob in bad_files.items():
+        p = str(tmp_path / name)
+        with open(p, "wb") as f:
+            f.write(blob)
+        with pytest.raises(D.SerializationError):
+            D.checkpoint_load(engines, p)
+    with pytest.raises(D.ShapeError):  # restore_state's layout check against the caller's Layout
+        D.checkpoint_load(engines, good, segments=[("w", n - 12), ("b", 12)])
+    for e, t in zip(engines, twins):
+        for step in range(2, 4):
+            for x in (e, t):
+                x.inner_step_host(O.rng_fill(9, "grad", step, n, -1e-2, 1e-2))
+        for x in (e, t):
+            x.outer_step(None)
+        for w in (D.THETA_T, D.THETA_LOCAL, D.ADAM_M, D.ADAM_V, D.MOMENTUM):
+            assert np.array_equal(bits(e.download(w)), bits(t.download(w))), w
+        a, b = e.scalars(), t.scalars()
+        assert (a.step_count, a.inner_step, a.outer_epoch, a.scale) == (b.step_count, b.inner_step, b.outer_epoch,
+                                                                          b.scale)
+    # and the good file with the right layout restores both engines
+    D.checkpoint_load(engines, good, segments=[("w", n - 11), ("b", 11)])
+    for e, o in zip(engines, other):
+        for w in (D.THETA_T, D.THETA_LOCAL, D.ADAM_M, D.ADAM_V, D.MOMENTUM):
+            assert np.array_equal(bits(e.download(w)), bits(o.download(w))), w
+    for e in engines + twins + other:
+        e.close()

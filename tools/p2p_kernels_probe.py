@@ -29,6 +29,9 @@ def main():
     ap.add_argument("--k", type=int, nargs="+", default=[2, 4, 8])
     ap.add_argument("--precision", choices=["fp16", "fp32"], default="fp16")
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--fold-kernel", type=int, nargs="+", default=[0], help="0 warp-specialised, 1 single-leader")
+    ap.add_argument("--fold-threads", type=int, nargs="+", default=[0], help="0 = default by K")
+    ap.add_argument("--fold-ctas", type=int, nargs="+", default=[0], help="0 = default max(16, 320 / K)")
     ap.add_argument("--overlap", action="store_true",
                     help="also time K4 while the fold (320/k CTAs, as in the step) runs on a second stream")
     a = ap.parse_args()
@@ -36,19 +39,22 @@ def main():
     prec = D.FP16 if a.precision == "fp16" else D.FP32
     w = 2 if prec == D.FP16 else 4
     n = a.params
-    for k in a.k:
+    import itertools
+    for k, fk, ft, fc in itertools.product(a.k, a.fold_kernel, a.fold_threads, a.fold_ctas):
+        D.set_p2p_tuning(fold_kernel=fk, fold_threads=ft, fold_ctas=fc)
         ms = (C.c_float * 3)()
         ov = (C.c_float * 2)()
-        st = D.lib.dlc_p2p_overlap_probe(k, n, prec, a.reps, max(16, 320 // k), ms, ov if a.overlap else None)
+        st = D.lib.dlc_p2p_overlap_probe(k, n, prec, a.reps, 0, ms, ov if a.overlap else None)
         if st != 0:
             raise RuntimeError(D.lib.dlc_last_error().decode())
-        out = {"k": k, "params": n, "precision": a.precision}
+        out = {"k": k, "params": n, "precision": a.precision, "fold_kernel": fk, "fold_threads": ft,
+               "fold_ctas": fc}
         for name, bpp, t in (("K2_pseudo_grad_piece", 8 + w, ms[0]), ("fold_push", 2 * w, ms[1]),
                              ("K4_nesterov_p2p_piece", 16 + w, ms[2])):
             out[name] = {"ms": round(t, 4), "bytes_per_param": bpp, "gbs": round(bpp * n / (t * 1e-3) / 1e9, 1)}
         if a.overlap:
             out["K4_while_fold_runs"] = {"ms": round(ov[0], 4), "gbs": round((16 + w) * n / (ov[0] * 1e-3) / 1e9, 1),
-                                         "fold_ms": round(ov[1], 4), "fold_ctas": max(16, 320 // k)}
+                                         "fold_ms": round(ov[1], 4)}
         print(json.dumps(out), flush=True)
 
 

@@ -33,6 +33,7 @@ def main():
     ap.add_argument("--fold-ctas", type=int, nargs="+", default=[0])
     ap.add_argument("--fold-threads", type=int, nargs="+", default=[0])
     ap.add_argument("--piece-ctas", type=int, nargs="+", default=[0])
+    ap.add_argument("--fold-kernel", type=int, nargs="+", default=[0], help="0 warp-specialised, 1 single-leader")
     ap.add_argument("--repeat", type=int, default=1)
     ap.add_argument("--no-ordered", action="store_true")
     a = ap.parse_args()
@@ -50,14 +51,14 @@ def main():
         eng.rng_perturb(4242, "local", r.rank * 16 + i, -1e-3, 1e-3, dst_dev_ptr=x.data_ptr())
     stream = torch.cuda.ExternalStream(eng.stream, device=f"cuda:{r.local}")
     plans = [p for p in a.plans.split(";")] if a.plans else [""]
-    configs = [("p2p", p, fc, ft, pc) for p, fc, ft, pc in itertools.product(plans, a.fold_ctas, a.fold_threads,
-                                                                             a.piece_ctas)]
+    configs = [("p2p", p, fc, ft, pc, fk) for p, fc, ft, pc, fk in
+               itertools.product(plans, a.fold_ctas, a.fold_threads, a.piece_ctas, a.fold_kernel)]
     if not a.no_ordered:
-        configs.insert(0, ("ordered", "", 0, 0, 0))
+        configs.insert(0, ("ordered", "", 0, 0, 0, 0))
     results = []
-    for mode, plan, fc, ft, pc in configs * a.repeat:
+    for mode, plan, fc, ft, pc, fk in configs * a.repeat:
         D.set_p2p_tuning(plan=[int(x) for x in plan.split(",")] if plan else None, fold_ctas=fc, fold_threads=ft,
-                         piece_ctas=pc)
+                         piece_ctas=pc, fold_kernel=fk)
         c = colls[mode]
         for s in range(2):
             eng.outer_step_from(c, xs[s % 2].data_ptr())
@@ -71,7 +72,7 @@ def main():
         e1.synchronize()
         ms = PD.max_over_ranks(e0.elapsed_time(e1) / a.steps, r.world)
         results.append({"mode": mode, "plan": plan or "default", "fold_ctas": fc, "fold_threads": ft,
-                        "piece_ctas": pc, "ms": ms})
+                        "piece_ctas": pc, "fold_kernel": fk, "ms": ms})
         if r.rank == 0:
             print(json.dumps(results[-1]), flush=True)
     D.set_p2p_tuning()
