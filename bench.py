@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--no-wire", action="store_true")
+    ap.add_argument("--no-training", action="store_true")
     ap.add_argument("--plan", default=None, help="P2P piece plan override, e.g. 1,1,2,2,1,1 (dlc_p2p_set_tuning)")
     ap.add_argument("--fold-ctas", type=int, default=0)
     ap.add_argument("--fold-threads", type=int, default=0)
@@ -344,6 +345,36 @@ def measure_wire(D, eng, n, prec, steps=3, cpu=True):
     return out
 
 
+# ---- run_training (engine.cpp:176-240) through the C ABI -------------------------------------
+
+def measure_training_loop(D, coll, n, k, prec, local, max_over_ranks, barrier, h=4, rounds=3):
+    """dlc_run_training for `rounds` windows of H inner steps with a device-side
+    gradient producer (a resident loss-scaled gradient): host wall time per step
+    against the device time of the steps themselves (CUDA events inside the
+    loop).  The loop enqueues each step without waiting for the previous one, so
+    `gpu_busy` near 1 means the host never starves the GPU."""
+    cfg = D.DilocoConfig(local_steps_h=h, num_workers_k=k, reduce_precision=prec, total_inner_steps=h * rounds)
+    e = D.DilocoEngine(cfg, D.OptimHyperparams(), n, local)
+    e.rng_fill(D.THETA_T, 4242, "theta", 0, -0.05, 0.05)
+    e.rng_fill(D.THETA_LOCAL, 4242, "theta", 0, -0.05, 0.05)
+    e.rng_fill(D.GRAD, 4242, "grad", 0, -1e-2 * 65536.0, 1e-2 * 65536.0)
+    gptr = e.device_ptr(D.GRAD)
+    e.synchronize()
+    recs = []
+    barrier()
+    t0 = time.perf_counter()
+    res = D.run_training(e, coll, lambda step: (gptr, True, 0.0), sink=recs.append)
+    wall = time.perf_counter() - t0
+    dev_ms = res["compute_ms"] + res["comm_ms"]
+    e.close()
+    steps = int(res["steps_done"])
+    return {"steps": steps, "local_steps_h": h, "rounds": int(res["rounds_done"]),
+            "wall_ms_per_step": max_over_ranks(wall * 1e3 / steps), "device_ms_per_step": dev_ms / steps,
+            "gpu_busy": dev_ms / (wall * 1e3), "records": len(recs),
+            "producer": "device-resident loss-scaled gradient (no host copy)",
+            "note": "dlc_run_training: steps enqueued back to back, records emitted one step behind"}
+
+
 # ---- our arm -----------------------------------------------------------------------------
 
 def run_ours(args):
@@ -566,9 +597,11 @@ def run_ours(args):
             line["inner_adamw"]["cpu_baseline"] = ci
     if world == 1 and not args.no_wire:
         line["wire"] = measure_wire(D, eng, n, prec, cpu=not args.no_cpu_baseline)
+    eng.close()
+    if not args.no_training:
+        line["training_loop"] = measure_training_loop(D, coll, n, k, prec, local, max_over_ranks, barrier)
     if rank == 0:
         print(json.dumps(line))
-    eng.close()
     if coll:
         coll.close()
     if world > 1:

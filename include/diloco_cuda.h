@@ -237,7 +237,7 @@ typedef struct {
   int32_t fold_ctas;    /* TMA fold CTAs, 0 = default */
   int32_t fold_threads; /* 128, 256 or 512; 0 = default by K */
   int32_t piece_ctas;   /* K2 / K4 piece kernels' grid, 0 = one CTA per window */
-  int32_t fold_kernel;  /* 0 = warp-specialised TMA fold (default), 1 = single-leader TMA fold */
+  int32_t fold_kernel;  /* 0 = single-leader TMA fold (default), 1 = warp-specialised TMA fold */
 } dlc_p2p_tuning;
 DLC_API int dlc_p2p_set_tuning(const dlc_p2p_tuning* t);
 DLC_API int dlc_p2p_get_tuning(dlc_p2p_tuning* t);
@@ -495,8 +495,8 @@ DLC_API int dlc_fp16_encode_bits(uint32_t start, size_t n, uint16_t* out);
 /* The P2P owner fold (K3 + push) on HOST buffers staged through the current
  * device: k contributions of n elements (FP32 values or FP16 codes per
  * `precision`, n a multiple of 64) folded in order into `out` by the
- * per-thread kernel (tma = 0), the warp-specialised TMA kernel (tma = 1) or
- * the single-leader TMA kernel (tma = 2; TMA needs k in 2..8, else the
+ * per-thread kernel (tma = 0), the single-leader TMA kernel (tma = 1) or the
+ * warp-specialised TMA kernel (tma = 2; TMA needs k in 2..8, else the
  * per-thread kernel runs); *nonfinite = the mark the owner pushes.  Probe for
  * the kernels every world size uses. */
 DLC_API int dlc_fold_push_probe(const void* const* contribs, int k, size_t n, int precision, int tma, void* out,

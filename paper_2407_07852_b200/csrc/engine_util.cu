@@ -82,7 +82,8 @@ int tma_threads(size_t k) {
 // CTAs of the K2 / K4 piece kernels running beside the fold (0: one per window)
 int piece_ctas() { return tuning().piece_ctas; }
 
-// TMA fold kernel: 0 warp-specialised (default), 1 single leader thread (A/B)
+// TMA fold kernel: 0 single leader thread (default: fastest inside the 4-GPU
+// step, profiles/r2_ab_fold_kernel_*.log), 1 warp-specialised (fastest alone)
 int fold_kernel() { return tuning().fold_kernel; }
 
 void ensure_copy_streams(dlc_engine* e) {
@@ -216,6 +217,7 @@ DevState read_state(dlc_engine* e) {
 }
 
 float* live(dlc_engine* e, int which) {
+  if (which == DLC_GRAD) return e->grad;  // not part of a ping-pong pair: no host wait
   const DevState s = read_state(e);
   const int cur = s.cur, oc = s.ocur;
   switch (which) {

@@ -125,9 +125,9 @@ void launch_nesterov_outer(Pair theta_t, Pair buf, Pair theta_local,
 void launch_fold_push(const PtrList& in, int k, int precision, const PtrList& outs, int nout,
                       const PtrList& flags, int nflags, size_t n, int ctas, cudaStream_t s);
 // fold_push with the bulk-copy engine (TMA) moving the tiles, `threads`
-// folding threads per CTA (128 / 256 / 512); kernel 0: warp-specialised (a
-// producer warp + the folding warps), 1: one leader thread issues the copies
-// between its share of the fold.  False when k is outside 2..8 (the caller then
+// folding threads per CTA (128 / 256 / 512); kernel 0: one leader thread
+// issues the copies between its share of the fold, 1: warp-specialised (a
+// producer warp + the folding warps).  False when k is outside 2..8 (the caller then
 // uses launch_fold_push).
 bool launch_fold_push_tma(const PtrList& in, int k, int precision, const PtrList& outs, int nout,
                           const PtrList& flags, int nflags, size_t n, int ctas, int threads, int kernel,

@@ -712,7 +712,7 @@ bool launch_fold_push_tma(const PtrList& in, int k, int precision, const PtrList
   const int W = precision == 1 ? 2 : 4;
   const size_t ntiles = (n + kTmaTileBytes / W - 1) / (kTmaTileBytes / W);
   const int grid = (int)std::max<size_t>(1, std::min<size_t>(ctas > 0 ? ctas : num_sms(), ntiles));
-  const bool ws = kernel == 0;
+  const bool ws = kernel == 1;
   return precision == 0 ? launch_tma_p<0>(k, threads, ws, grid, s, in, outs, nout, flags, nflags, n, md)
                         : launch_tma_p<1>(k, threads, ws, grid, s, in, outs, nout, flags, nflags, n, md);
 }

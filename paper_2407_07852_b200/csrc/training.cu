@@ -1,26 +1,28 @@
 // training.cu — run_training (engine.cpp:176-240) around the device engine:
 // the reference's training loop with its metrics records, the gradient
 // producer (task.cpp, out of scope) supplied by the caller.
-#include <chrono>
 #include <cmath>
+#include <deque>
 #include <string>
 
 #include "engine_impl.hpp"
 
 using namespace dlc;
 
-namespace {
-
-using Clock = std::chrono::steady_clock;
-
-double ms_since(Clock::time_point t0) {
-  return std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
-}
-
-}  // namespace
 
 extern "C" {
 
+// The loop never waits for the GPU between inner steps: each step's K1 (and,
+// at a window boundary, the outer round) is enqueued, followed by an
+// asynchronous copy of the engine's device scalars into a pinned ring slot and
+// a timing event.  A step's records are emitted one step behind, once its event
+// has completed, so the GPU always has the next step queued while the host
+// formats records and calls the producer.  At a window boundary the loop drains
+// (the round's report, the barrier check and the on_round hook need the final
+// state).  The record stream is the reference's (engine.cpp:181-238); only the
+// interleaving of producer calls and sink calls differs (producer(t + 1) runs
+// before step t's records are emitted).  compute_ms / comm_ms are CUDA-event
+// times of the step and of its collective on the device, not host wall time.
 int dlc_run_training(dlc_engine* e, dlc_collective* c, dlc_grad_producer producer, dlc_metrics_sink sink,
                      dlc_round_hook on_round, void* user, int worker_index, dlc_run_result* out) {
   return guard([&] {
@@ -28,42 +30,50 @@ int dlc_run_training(dlc_engine* e, dlc_collective* c, dlc_grad_producer produce
     if (c && c->kind == 0) c = nullptr;
     DeviceGuard dg(e->device);
     *out = dlc_run_result{};
-    while (e->issued_inner < e->cfg.total_inner_steps) {  // !engine.finished()
-      const auto compute_start = Clock::now();
-      const float* grad = nullptr;
-      int grad_is_scaled = 1;
-      float loss = 0.0f;
-      if (producer(user, e->issued_inner, &grad, &grad_is_scaled, &loss) != 0)
-        fail(DLC_EINVAL, "run_training: the gradient producer failed at inner step " +
-                             std::to_string(e->issued_inner));
-      if (e->n && !grad) fail(DLC_EINVAL, "run_training: the gradient producer returned no gradient");
-      // DilocoOptimizer::step (engine.cpp:162-174)
-      engine_inner(e, grad, grad_is_scaled);
-      const bool boundary = e->issued_inner % e->cfg.local_steps_h == 0;
+    constexpr int kRing = 4;
+    struct Ring {
+      DevState* host = nullptr;
+      cudaEvent_t a[kRing] = {}, b[kRing] = {};
+      ~Ring() {
+        if (host) cudaFreeHost(host);
+        for (int i = 0; i < kRing; ++i) {
+          if (a[i]) cudaEventDestroy(a[i]);
+          if (b[i]) cudaEventDestroy(b[i]);
+        }
+      }
+    } ring;
+    DLC_CUDA(cudaMallocHost(&ring.host, kRing * sizeof(DevState)));
+    for (int i = 0; i < kRing; ++i) {
+      DLC_CUDA(cudaEventCreate(&ring.a[i]));
+      DLC_CUDA(cudaEventCreate(&ring.b[i]));
+    }
+    struct Pending {
+      int slot;
+      float loss;
+      bool boundary;
+    };
+    std::deque<Pending> pending;
+    auto emit = [&](const Pending& p) {
+      DLC_CUDA(cudaEventSynchronize(ring.b[p.slot]));
+      const DevState s = ring.host[p.slot];
+      float step_ms = 0.0f;
+      DLC_CUDA(cudaEventElapsedTime(&step_ms, ring.a[p.slot], ring.b[p.slot]));
       dlc_reduce_report report{};
       bool applied = false;
-      if (boundary) {
-        check_collective(e, c);
-        const uint64_t epoch = read_state(e).outer_epoch;
-        outer_round(e, c, nullptr, &report);
-        fill_report(e, c, &report, epoch);
-      }
-      const DevState s = read_state(e);  // synchronises: the step's result is final
-      if (boundary) {
-        check_barrier(e);
+      if (p.boundary) {
+        check_barrier(e);  // a failed round raises CollectiveError here
+        fill_report(e, c, &report, s.outer_epoch - 1);
         applied = s.last_applied != 0;
       }
-      const double total_ms = ms_since(compute_start);
       out->steps_done += 1;
-      out->final_train_loss = loss;
-
+      out->final_train_loss = p.loss;
       dlc_metrics_record record{};
       record.kind = DLC_RECORD_STEP;
       record.worker = worker_index;
       record.inner_step = s.inner_step;
       record.outer_epoch = s.outer_epoch;
-      record.loss = loss;
-      record.perplexity = std::exp(loss);  // task.cpp:544-546
+      record.loss = p.loss;
+      record.perplexity = std::exp(p.loss);  // task.cpp:544-546
       record.lr = s.last_lr;
       if (s.last_overflow && sink) {
         dlc_metrics_record event = record;
@@ -71,12 +81,12 @@ int dlc_run_training(dlc_engine* e, dlc_collective* c, dlc_grad_producer produce
         event.event = "inner_overflow_skip";
         sink(user, &event);
       }
-      if (boundary) {
+      if (p.boundary) {
         out->rounds_done += 1;
         out->reduce_data_bytes += report.data_bytes_sent;
         out->reduce_wire_bytes += report.wire_bytes_sent;
         out->comm_ms += report.wall_ms;
-        record.compute_ms = total_ms - report.wall_ms;
+        record.compute_ms = step_ms - report.wall_ms;
         out->compute_ms += record.compute_ms;
         if (sink) {
           sink(user, &record);
@@ -95,10 +105,42 @@ int dlc_run_training(dlc_engine* e, dlc_collective* c, dlc_grad_producer produce
         }
         if (on_round) on_round(user, out->rounds_done);
       } else {
-        record.compute_ms = total_ms;
-        out->compute_ms += total_ms;
+        record.compute_ms = step_ms;
+        out->compute_ms += step_ms;
         if (sink) sink(user, &record);
       }
+    };
+    while (e->issued_inner < e->cfg.total_inner_steps) {  // !engine.finished()
+      const uint64_t t = e->issued_inner;
+      const float* grad = nullptr;
+      int grad_is_scaled = 1;
+      float loss = 0.0f;
+      if (producer(user, t, &grad, &grad_is_scaled, &loss) != 0)
+        fail(DLC_EINVAL, "run_training: the gradient producer failed at inner step " + std::to_string(t));
+      if (e->n && !grad) fail(DLC_EINVAL, "run_training: the gradient producer returned no gradient");
+      const int slot = (int)(t % kRing);
+      DLC_CUDA(cudaEventRecord(ring.a[slot], e->stream));
+      // DilocoOptimizer::step (engine.cpp:162-174)
+      engine_inner(e, grad, grad_is_scaled);
+      const bool boundary = e->issued_inner % e->cfg.local_steps_h == 0;
+      dlc_reduce_report rep{};
+      if (boundary) {
+        check_collective(e, c);
+        outer_round(e, c, nullptr, &rep);  // records the collective's events for fill_report
+      }
+      DLC_CUDA(cudaMemcpyAsync(&ring.host[slot], e->st, sizeof(DevState), cudaMemcpyDeviceToHost, e->stream));
+      DLC_CUDA(cudaEventRecord(ring.b[slot], e->stream));
+      pending.push_back({slot, loss, boundary});
+      while (!pending.empty() && (boundary || pending.size() > 1)) {  // one step behind; drain at a boundary
+        const Pending p = pending.front();
+        pending.pop_front();
+        emit(p);
+      }
+    }
+    while (!pending.empty()) {
+      const Pending p = pending.front();
+      pending.pop_front();
+      emit(p);
     }
   });
 }

@@ -618,7 +618,7 @@ def test_tiny_and_empty_vectors(port, n, prec):
 @pytest.mark.parametrize("prec", [0, 1])
 def test_fold_push_kernels_every_world_size(port, prec, tma):
     """The P2P owner fold for K = 1..9 and 16 (the compile-time-K TMA kernels,
-    warp-specialised and single-leader, the per-thread kernels and the generic
+    single-leader and warp-specialised, the per-thread kernels and the generic
     one), bit for bit against reduce_average in rank order, with the non-finite
     mark."""
     n = 64 * 301

@@ -18,10 +18,14 @@ import torch
 FIELDS = {"DATA_TX": 138, "DATA_RX": 139, "RAW_TX": 140, "RAW_RX": 141, "XMIT_BYTES": 202, "RCV_BYTES": 204}
 
 
+STATUS = {}
+
+
 def read(h, fid, scope):
     try:
         v = N.nvmlDeviceGetFieldValues(h, [(fid, scope)])[0]
         if v.nvmlReturn != 0:
+            STATUS[(fid, scope)] = int(v.nvmlReturn)
             return None
         return int(v.value.ullVal)
     except Exception as e:  # noqa: BLE001
@@ -61,7 +65,21 @@ def main():
         v1 = s1[key]
         if isinstance(v0, int) and isinstance(v1, int) and v1 != v0:
             res["deltas"][f"gpu{key[0]}.{key[1]}.{key[2]}"] = {"delta": v1 - v0, "ratio_to_bytes": (v1 - v0) / moved}
-    res["unsupported"] = sorted({f"{k[1]}.{k[2]}" for k, v in s0.items() if v is None})[:40]
+    res["unsupported"] = sorted({f"{k[1]}.{k[2]}" for k, v in s0.items() if v is None})
+    res["nvml_status"] = {f"{fid}.{sc}": st for (fid, sc), st in list(STATUS.items())[:16]}
+    links = {}
+    for link in range(18):
+        try:
+            links[link] = int(N.nvmlDeviceGetNvLinkState(handles[0], link))
+        except Exception as e:  # noqa: BLE001
+            links[link] = str(e)[:40]
+    res["nvlink_state_gpu0"] = links
+    import subprocess
+    for cmd in (["nvidia-smi", "nvlink", "-s", "-i", "0"], ["nvidia-smi", "nvlink", "-gt", "d", "-i", "0"]):
+        try:
+            res[" ".join(cmd)] = subprocess.run(cmd, capture_output=True, text=True, timeout=30).stdout[-1500:]
+        except Exception as e:  # noqa: BLE001
+            res[" ".join(cmd)] = str(e)
     print(json.dumps(res, indent=1))
 
 

@@ -29,7 +29,7 @@ def main():
     ap.add_argument("--k", type=int, nargs="+", default=[2, 4, 8])
     ap.add_argument("--precision", choices=["fp16", "fp32"], default="fp16")
     ap.add_argument("--reps", type=int, default=5)
-    ap.add_argument("--fold-kernel", type=int, nargs="+", default=[0], help="0 warp-specialised, 1 single-leader")
+    ap.add_argument("--fold-kernel", type=int, nargs="+", default=[0], help="0 single-leader, 1 warp-specialised")
     ap.add_argument("--fold-threads", type=int, nargs="+", default=[0], help="0 = default by K")
     ap.add_argument("--fold-ctas", type=int, nargs="+", default=[0], help="0 = default max(16, 320 / K)")
     ap.add_argument("--overlap", action="store_true",

@@ -33,7 +33,7 @@ def main():
     ap.add_argument("--fold-ctas", type=int, nargs="+", default=[0])
     ap.add_argument("--fold-threads", type=int, nargs="+", default=[0])
     ap.add_argument("--piece-ctas", type=int, nargs="+", default=[0])
-    ap.add_argument("--fold-kernel", type=int, nargs="+", default=[0], help="0 warp-specialised, 1 single-leader")
+    ap.add_argument("--fold-kernel", type=int, nargs="+", default=[0], help="0 single-leader, 1 warp-specialised")
     ap.add_argument("--repeat", type=int, default=1)
     ap.add_argument("--no-ordered", action="store_true")
     a = ap.parse_args()
