@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--no-wire", action="store_true")
     ap.add_argument("--no-training", action="store_true")
+    ap.add_argument("--no-boundary", action="store_true")
     ap.add_argument("--plan", default=None, help="P2P piece plan override, e.g. 1,1,2,2,1,1 (dlc_p2p_set_tuning)")
     ap.add_argument("--fold-ctas", type=int, default=0)
     ap.add_argument("--fold-threads", type=int, default=0)
@@ -347,7 +348,7 @@ def measure_wire(D, eng, n, prec, steps=3, cpu=True):
 
 # ---- run_training (engine.cpp:176-240) through the C ABI -------------------------------------
 
-def measure_training_loop(D, coll, n, k, prec, local, max_over_ranks, barrier, h=4, rounds=3):
+def measure_training_loop(D, coll, n, k, prec, local, max_over_ranks, barrier, h=4, rounds=8):
     """dlc_run_training for `rounds` windows of H inner steps with a device-side
     gradient producer (a resident loss-scaled gradient): host wall time per step
     against the device time of the steps themselves (CUDA events inside the
@@ -373,6 +374,66 @@ def measure_training_loop(D, coll, n, k, prec, local, max_over_ranks, barrier, h
             "gpu_busy": dev_ms / (wall * 1e3), "records": len(recs),
             "producer": "device-resident loss-scaled gradient (no host copy)",
             "note": "dlc_run_training: steps enqueued back to back, records emitted one step behind"}
+
+
+# ---- the window boundary: K2 fused into the last inner step vs the outer step's own K2 -------
+
+def measure_window_boundary(D, coll, n, k, prec, local, max_over_ranks, barrier, windows=4, warmup=1):
+    """The last inner step of a window plus the outer step that follows it
+    (DilocoOptimizer::step at inner_step % H == 0, engine.cpp:162-174), timed
+    with CUDA events on the engine stream around exactly those two calls, H = 2
+    so theta_local != theta_t when the fused K1 runs (it reads theta_t).
+    Variants, interleaved window by window on one engine: "unfused" (the outer
+    step's own K2, the default) and "fused" (K1 writes the delta into the send
+    buffer, dlc_engine_set_fused_delta).  Per variant: the boundary's mean time
+    and the K1 / K2 / K4 phase times (max over ranks)."""
+    import torch
+    h = 2
+    variants = [("unfused", False), ("fused", True)]
+    total = h * len(variants) * (warmup + windows)
+    cfg = D.DilocoConfig(local_steps_h=h, num_workers_k=k, reduce_precision=prec, total_inner_steps=total)
+    e = D.DilocoEngine(cfg, D.OptimHyperparams(), n, local)
+    e.rng_fill(D.THETA_T, 4242, "theta", 0, -0.05, 0.05)
+    e.rng_fill(D.THETA_LOCAL, 4242, "theta", 0, -0.05, 0.05)
+    e.rng_fill(D.GRAD, 4242, "grad", k * 100 + 7, -1e-2 * 65536.0, 1e-2 * 65536.0)
+    gptr = e.device_ptr(D.GRAD)
+    e.synchronize()
+    stream = torch.cuda.ExternalStream(e.stream, device=f"cuda:{local}")
+    rec = {name: {"ms": [], "k1": [], "k2": [], "k4": []} for name, _ in variants}
+    e.set_timing(True)
+    for wi in range(warmup + windows):
+        for name, fused in variants:
+            e.set_fused_delta(fused)
+            e.inner_step(gptr, grad_is_scaled=True)
+            barrier()
+            e.synchronize()
+            e.phase_times()  # reset
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            e.inner_step(gptr, grad_is_scaled=True)
+            e.outer_step(coll)
+            b.record(stream)
+            b.synchronize()
+            e.synchronize()
+            ph, _ = e.phase_times()
+            if wi >= warmup:
+                r = rec[name]
+                r["ms"].append(a.elapsed_time(b))
+                r["k1"].append(ph[0])
+                r["k2"].append(ph[1])
+                r["k4"].append(ph[3])
+    e.set_timing(False)
+    e.close()
+    out = {}
+    for name, _ in variants:
+        r = rec[name]
+        out[name] = {key + "_ms": max_over_ranks(statistics.mean(v)) for key, v in
+                     (("boundary", r["ms"]), ("k1", r["k1"]), ("k2", r["k2"]), ("k4", r["k4"]))}
+    out["fused_saves_ms"] = out["unfused"]["boundary_ms"] - out["fused"]["boundary_ms"]
+    out.update({"windows_each": windows, "local_steps_h": h,
+                "what": "last inner step (K1) + outer step, CUDA events on the engine stream, variants interleaved; "
+                        "k1 / k2 / k4 = summed event-timed phases of that boundary (k4: busy time of the pieces)"})
+    return out
 
 
 # ---- our arm -----------------------------------------------------------------------------
@@ -598,8 +659,13 @@ def run_ours(args):
     if world == 1 and not args.no_wire:
         line["wire"] = measure_wire(D, eng, n, prec, cpu=not args.no_cpu_baseline)
     eng.close()
+    if k > 1 and not args.no_boundary:
+        line["window_boundary"] = measure_window_boundary(D, coll, n, k, prec, local, max_over_ranks, barrier)
     if not args.no_training:
         line["training_loop"] = measure_training_loop(D, coll, n, k, prec, local, max_over_ranks, barrier)
+        if n > 150_000_000:  # the paper's Llama-150M size (configs 2-3): ~0.6 ms inner steps
+            line["training_loop_150m"] = measure_training_loop(D, coll, 150_000_000, k, prec, local,
+                                                               max_over_ranks, barrier)
     if rank == 0:
         print(json.dumps(line))
     if coll:

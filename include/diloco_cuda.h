@@ -386,7 +386,8 @@ DLC_API int dlc_engines_outer_step_local(dlc_engine* const* engines, size_t k, d
  * netsim.cpp:325-357, and of SURVEY.md §8b's dlc_world_create).  DLC_MODE_P2P
  * joins the engines by direct NVLink peer access (no IPC, no communicator);
  * ORDERED / ALLREDUCE use communicators from ncclCommInitAll with the
- * per-rank calls grouped.  Every rank needs its own device.
+ * per-rank calls grouped, and need one device per rank; in DLC_MODE_P2P the
+ * ranks synchronise through CUDA events, so several may share a device.
  * The engines belong to the world (use dlc_world_engine for inner steps,
  * uploads and downloads; do not destroy them).  dlc_world_outer_step runs
  * every rank's outer step; `result` (may be NULL: asynchronous) is rank 0's,
@@ -397,6 +398,23 @@ DLC_API int dlc_world_create(const dlc_config* cfg, const dlc_hyperparams* hyper
 DLC_API int dlc_world_destroy(dlc_world* w);
 DLC_API int dlc_world_engine(dlc_world* w, int rank, dlc_engine** e);
 DLC_API int dlc_world_outer_step(dlc_world* w, dlc_outer_result* result);
+/* Membership change of a world: the next rounds run
+ * over the current ranks minus `exclude_ranks`, survivors kept in order and
+ * renumbered 0..k'-1, divisor k' (collective.cpp:1369-1395).  The excluded
+ * engines are destroyed; the survivors re-lay their owner slots for k'
+ * (ReduceReport::contributors = k').  The window rule of the reference holds:
+ * call it between rounds (every engine at a window boundary).  DLC_EQUORUM when
+ * fewer than max(quorum_min, 1) ranks would remain, DLC_ECONFIG for a rank out
+ * of range; on error nothing changes.  ORDERED / ALLREDUCE worlds get fresh
+ * communicators over the survivors' devices.  The failure detector of a
+ * one-thread world is its caller (every rank is driven by it), so this is the
+ * planned exclusion of the reference's fleet; the flag-barrier timeout
+ * (dlc_collective_set_reduce_timeout_ms) detects silent peers of the one
+ * process per GPU path. */
+DLC_API int dlc_world_shrink(dlc_world* w, const int* exclude_ranks, size_t n_exclude, size_t quorum_min);
+/* Original ranks (at dlc_world_create) of the current members, in rank order;
+ * returns the member count. */
+DLC_API size_t dlc_world_members(const dlc_world* w, int* ranks, size_t cap);
 
 /* DilocoOptimizer::step (engine.cpp:162-174): one inner step, then the outer
  * step when the window boundary is reached.  `round_completed` may be NULL. */
@@ -477,6 +495,23 @@ DLC_API int dlc_checkpoint_load_layout(dlc_engine* const* engines, size_t count,
 enum { DLC_PHASE_INNER = 0, DLC_PHASE_PSEUDO = 1, DLC_PHASE_COLLECTIVE = 2, DLC_PHASE_OUTER = 3 };
 DLC_API int dlc_engine_set_timing(dlc_engine* e, int on);
 DLC_API int dlc_engine_phase_times(dlc_engine* e, double total_ms[4], uint64_t count[4]);
+
+/* K2 fused into the window's last inner step (opt-in, default off; meaningful
+ * for num_workers_k > 1).  The inner step that completes a window of H also
+ * writes delta = theta_t - theta_local' (engine.cpp:115-126, in the reduce
+ * precision) into the collective's send buffer, so the outer step starts with
+ * the exchange instead of a separate 10-12 B/param K2 pass.  Results are
+ * bit-identical either way: the outer step still runs a gated K2 that
+ * recomputes the delta when that inner step overflowed (theta_local kept its
+ * old value), and every engine call that writes theta_t / theta_local or the
+ * send buffer between the two (uploads, set_scalars, checkpoint load, wire
+ * rounds, host-buffer and explicit-source outer steps) drops the fused delta.
+ * Writes through a pointer from dlc_engine_device_ptr made AFTER that inner
+ * step are not seen: make them before it, or leave fusion off.  Off by
+ * default because the window boundary (that inner step + the outer step) is
+ * not faster with it on this pool's B200 boxes: the P2P outer step is bound by
+ * the NVLink exchange and K4, not by K2. */
+DLC_API int dlc_engine_set_fused_delta(dlc_engine* e, int on);
 
 /* =========================================================================
  * 4. Synthetic inputs and test probes (bench / parity tests).  Counter-based

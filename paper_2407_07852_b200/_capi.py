@@ -179,6 +179,7 @@ _SIGS = {
     "dlc_engine_compute_pseudo_gradient": (I, [P, P, C.POINTER(C.c_uint64)]),
     "dlc_engine_apply_outer_step": (I, [P, P, C.c_uint64, C.POINTER(OuterResult)]),
     "dlc_engine_set_timing": (I, [P, I]),
+    "dlc_engine_set_fused_delta": (I, [P, I]),
     "dlc_engine_phase_times": (I, [P, C.POINTER(C.c_double), C.POINTER(C.c_uint64)]),
     "dlc_engines_outer_step_local": (I, [PP, SZ, C.POINTER(OuterResult)]),
     "dlc_checkpoint_save": (I, [PP, SZ, C.c_char_p, C.POINTER(CheckpointMeta), C.POINTER(C.c_char_p),
@@ -201,6 +202,8 @@ _SIGS = {
     "dlc_world_destroy": (I, [P]),
     "dlc_world_engine": (I, [P, I, C.POINTER(P)]),
     "dlc_world_outer_step": (I, [P, C.POINTER(OuterResult)]),
+    "dlc_world_shrink": (I, [P, C.POINTER(C.c_int), SZ, SZ]),
+    "dlc_world_members": (SZ, [P, C.POINTER(C.c_int), SZ]),
     "dlc_wire_frames_size": (I, [U64, C.POINTER(WireTags), C.POINTER(SZ), C.POINTER(C.c_uint64)]),
     "dlc_wire_encode": (I, [P, U64, U64, C.POINTER(WireTags), P, SZ, C.POINTER(SZ), P]),
     "dlc_wire_decode": (I, [P, SZ, I, U64, U64, P, C.POINTER(WireChunk), SZ, C.POINTER(SZ), C.POINTER(SZ), P]),

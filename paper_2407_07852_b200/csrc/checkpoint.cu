@@ -334,6 +334,8 @@ int dlc_checkpoint_load_layout(dlc_engine* const* engines, size_t count, const c
       s.outer_epoch = h.outer_epoch;
       s.found_inf = 0;
       s.delta_nonfinite = 0;
+      s.delta_ready = 0;
+      e->delta_fused = false;
       e->hyper.beta1 = h.beta1;
       e->hyper.beta2 = h.beta2;
       e->hyper.adam_eps = h.eps;

@@ -105,6 +105,65 @@ __device__ __forceinline__ const float* local_src(const Pair& tl, const Pair& tt
   return (tl.follow && st->lalias) ? sel(tt, st->ocur) : sel(tl, st->cur);
 }
 
+// One thread after K1 (and after the fused window boundary): the skip decision,
+// step counter, lr record and scaler_update (engine.cpp:57-67, optim.cpp:69,
+// optim.cpp:137-148 with clamps :13-14).
+__device__ __forceinline__ void inner_finalize(DevState* st, const float* lr_tab, int pingpong, int fused) {
+  const int fi = st->found_inf;
+  // a fused delta is the outer step's input only if p' became theta_local
+  st->delta_ready = fused && !fi;
+  const uint64_t t = st->step_count + 1;
+  if (!fi) {
+    if (pingpong) st->cur ^= 1;  // the freshly written buffers become live
+    st->lalias = 0;              // theta_local now lives in p[cur]
+    st->step_count = t;
+    st->last_lr = lr_tab[t];
+  } else {
+    st->last_lr = 0.0f;
+    st->overflow_skips += 1;
+  }
+  st->last_overflow = fi;
+  if (fi) {
+    const float s = __fmul_rn(st->scale, 0.5f);
+    st->scale = (s < 0x1p-20f) ? 0x1p-20f : s;
+    st->good = 0;
+  } else {
+    st->good += 1;
+    if (st->good >= st->growth) {
+      const float s = __fmul_rn(st->scale, 2.0f);
+      st->scale = (0x1p24f < s) ? 0x1p24f : s;
+      st->good = 0;
+    }
+  }
+  st->inner_step += 1;  // data cursor always advances (engine.cpp:103)
+  st->found_inf = 0;
+}
+
+// After an outer step, applied or skipped: theta_local := theta_t
+// (engine.cpp:141-143, recorded as DevState::lalias for PINGPONG engines),
+// the result and the epoch (engine.cpp:144).
+__device__ __forceinline__ void k4_finalize(DevState* st, bool applied, const Pair& tl) {
+  if (tl.follow) st->lalias = 1;  // theta_local := theta_t (engine.cpp:141-143) without the copy
+  st->last_applied = applied ? 1 : 0;
+  st->outer_skips += applied ? 0 : 1;
+  st->outer_epoch += 1;  // engine.cpp:144
+}
+
+// K2 of a single worker in the reduce precision: the delta as the outer step
+// sees it (FP16: encoded once at the source; the mean of one contribution
+// re-encodes to the same code), non-finite OR into `bad`.
+template <int PREC>
+__device__ __forceinline__ float solo_delta(float tt, float tl, bool& bad) {
+  const float d = delta_elem(tt, tl);  // engine.cpp:122
+  if (PREC == 0) {
+    bad |= !finite_f(d);
+    return d;
+  }
+  const uint16_t h = fp16_encode(d);
+  bad |= fp16_nonfinite(h);
+  return fp16_decode(h);
+}
+
 }  // namespace
 
 }  // namespace dlc

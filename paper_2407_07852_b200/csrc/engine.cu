@@ -270,6 +270,7 @@ int dlc_engine_set_scalars(dlc_engine* e, const dlc_engine_scalars* in) {
     s.last_lr = in->last_lr;
     s.last_overflow = in->last_overflow;
     s.last_applied = in->last_applied;
+    e->delta_fused = false;
     ensure_tables(e, in->step_count + 2);
     DLC_CUDA(cudaMemcpy(e->st, &s, sizeof(s), cudaMemcpyHostToDevice));
     e->issued_inner = in->inner_step;
@@ -341,6 +342,14 @@ int dlc_engine_outer_step_from(dlc_engine* e, dlc_collective* c, const float* th
   });
 }
 
+int dlc_engine_set_fused_delta(dlc_engine* e, int on) {
+  return guard([&] {
+    if (!e) fail(DLC_EINVAL, "dlc_engine_set_fused_delta: null engine");
+    e->fuse_delta = on != 0;
+    if (!e->fuse_delta) e->delta_fused = false;
+  });
+}
+
 int dlc_engine_set_timing(dlc_engine* e, int on) {
   return guard([&] {
     if (!e) fail(DLC_EINVAL, "dlc_engine_set_timing: null engine");
@@ -371,6 +380,7 @@ int dlc_engine_outer_step_host(dlc_engine* e, dlc_collective* c, const float* ho
     if (c && c->kind == 0) c = nullptr;
     check_collective(e, c);
     DeviceGuard dg(e->device);
+    e->delta_fused = false;  // theta_local comes from the host: the full K2 runs
     // theta_local arrives chunk by chunk in the staging buffer (copy stream);
     // each chunk's kernel starts as soon as its bytes land, and for a single
     // worker each finished chunk of the new theta_t streams back on a second
@@ -458,6 +468,7 @@ int dlc_engine_apply_outer_step(dlc_engine* e, const float* host_mean, uint64_t 
     if (outer_epoch != s.outer_epoch)  // engine.cpp:129-134
       fail(DLC_ECOLLECTIVE, "outer_step: reduced pseudo-gradient from epoch " + std::to_string(outer_epoch) +
                                 " applied at epoch " + std::to_string(s.outer_epoch));
+    e->delta_fused = false;
     DLC_CUDA(cudaMemcpyAsync(e->grad, host_mean, e->n * sizeof(float), cudaMemcpyHostToDevice, e->stream));
     DLC_CUDA(cudaMemsetAsync(e->flags, 0, sizeof(int), e->stream));
     launch_nonfinite(e->grad, e->flags, e->n, e->stream);  // engine.cpp:136
@@ -494,8 +505,11 @@ int dlc_engines_outer_step_local(dlc_engine* const* engines, size_t k, dlc_outer
     PtrList in{};
     for (size_t j = 0; j < k; ++j) {
       dlc_engine* e = engines[j];
-      launch_pseudo_grad(tt_pair(e), local_pair(e), e->st, e->send, e->prec, &e->st->delta_nonfinite, 0, e->n,
-                         s);
+      if (take_fused_delta(e) && k > 1)  // the window's last K1 wrote the delta (k = 1 needs the flag below)
+        launch_pseudo_grad_gated(tt_pair(e), local_pair(e), e->st, e->send, e->prec, e->n, s);
+      else
+        launch_pseudo_grad(tt_pair(e), local_pair(e), e->st, e->send, e->prec, &e->st->delta_nonfinite, 0, e->n,
+                           s);
       in.ptr[j] = e->send;
     }
     DLC_CUDA(cudaMemsetAsync(e0->flags, 0, kMaxK * sizeof(int), s));

@@ -59,6 +59,11 @@ struct dlc_engine {
   float* tab = nullptr;  // corr1 | corr2 | lr, tab_cap entries each
   size_t tab_cap = 0;
   uint64_t issued_inner = 0;  // host mirror of the data cursor (always advances)
+  // K2 fused into the last inner step of a window (K > 1, dlc_engine_set_fused_delta):
+  // delta_fused = that K1 wrote the send buffer and nothing has touched theta_t,
+  // theta_local or the send buffer since; the outer step then runs only the gated K2.
+  bool fuse_delta = false;
+  bool delta_fused = false;
   std::vector<void*> allocs;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   // per-phase event timing (dlc_engine_set_timing)
@@ -165,6 +170,16 @@ float* live(dlc_engine* e, int which);
 void unalias(dlc_engine* e);
 float* writable(dlc_engine* e, int which);
 void engine_inner(dlc_engine* e, const float* grad, int grad_is_scaled);
+// The outer step's K2 input: true (and cleared) when the window's last K1 wrote
+// the delta into the send buffer (DevState::delta_ready then tells the device
+// whether it still holds).
+inline bool take_fused_delta(dlc_engine* e) {
+  const bool f = e->delta_fused;
+  e->delta_fused = false;
+  return f;
+}
+// K2 of an outer step: the gated fallback after a fused K1, else the full pass.
+void pseudo_grad_step(dlc_engine* e, Pair tl, bool fused);
 // PINGPONG: theta_local follows theta_t after every outer step (Pair::follow).
 inline Pair local_pair(dlc_engine* e) { return Pair{{e->p[0], e->p[1]}, e->inner_mode == DLC_INNER_PINGPONG}; }
 inline Pair tt_pair(dlc_engine* e) { return Pair{{e->theta_t[0], e->theta_t[1]}}; }
@@ -198,14 +213,16 @@ struct P2PStep {
 };
 P2PStep p2p_begin(dlc_engine* e, int rank, const float* src, bool rep, const float* hsrc, float* hdst, int oc_host);
 void p2p_k2(P2PStep& s, size_t p);
+void p2p_k2_all(P2PStep& s, bool fused);
 void p2p_fold_begin(P2PStep& s);
 void p2p_fold(P2PStep& s, size_t p);
 void p2p_fold_end(P2PStep& s);
 void p2p_k4(P2PStep& s, size_t p);
 void p2p_finish(P2PStep& s, const int* abort);
 void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc_reduce_report* rep,
-                         const float* hsrc, float* hdst, int oc_host);
-void outer_allreduce_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc_reduce_report* rep);
+                         const float* hsrc, float* hdst, int oc_host, bool fused = false);
+void outer_allreduce_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc_reduce_report* rep,
+                               bool fused = false);
 void outer_round(dlc_engine* e, dlc_collective* c, const float* src, dlc_reduce_report* rep);
 
 // ---- engine_util.cu (results) ----

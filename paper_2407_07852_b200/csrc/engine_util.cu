@@ -86,6 +86,7 @@ int piece_ctas() { return tuning().piece_ctas; }
 // step, profiles/r2_ab_fold_kernel_*.log), 1 warp-specialised (fastest alone)
 int fold_kernel() { return tuning().fold_kernel; }
 
+
 void ensure_copy_streams(dlc_engine* e) {
   if (!e->h2d) DLC_CUDA(cudaStreamCreateWithFlags(&e->h2d, cudaStreamNonBlocking));
   if (!e->d2h) DLC_CUDA(cudaStreamCreateWithFlags(&e->d2h, cudaStreamNonBlocking));
@@ -245,7 +246,10 @@ void unalias(dlc_engine* e) {
 
 // live() for a caller that writes through the pointer
 float* writable(dlc_engine* e, int which) {
-  if (which == DLC_THETA_T || which == DLC_THETA_LOCAL) unalias(e);
+  if (which == DLC_THETA_T || which == DLC_THETA_LOCAL) {
+    e->delta_fused = false;  // a fused delta no longer matches the weights
+    unalias(e);
+  }
   return live(e, which);
 }
 
@@ -278,11 +282,19 @@ void engine_inner(dlc_engine* e, const float* grad, int grad_is_scaled) {
   a.omb1 = 1.0f - e->hyper.beta1;
   a.omb2 = 1.0f - e->hyper.beta2;
   a.pingpong = e->inner_mode == DLC_INNER_PINGPONG;
+  // fused delta (opt-in): the last step of a window at K > 1 also writes the
+  // pseudo-gradient (engine.cpp:115-126) into the send buffer, so the outer
+  // step starts with the exchange; a single worker keeps K2 fused into its
+  // outer step instead
+  const bool fuse = e->fuse_delta && e->k > 1 && (e->issued_inner + 1) % e->cfg.local_steps_h == 0;
+  a.delta = fuse ? e->send : nullptr;
+  a.delta_fp16 = e->prec == DLC_FP16;
   phase_begin(e);
   launch_adamw(a, e->stream);
   phase_end(e, DLC_PHASE_INNER);
   launched("adamw");
   e->issued_inner += 1;
+  e->delta_fused = fuse;
 }
 
 
@@ -297,6 +309,17 @@ void pseudo_grad(dlc_engine* e, Pair tl) {
   launch_pseudo_grad(tt_pair(e), tl, e->st, e->send, e->prec, &e->st->delta_nonfinite, 0, e->n, e->stream);
   phase_end(e, DLC_PHASE_PSEUDO);
   launched("pseudo_grad");
+}
+
+void pseudo_grad_step(dlc_engine* e, Pair tl, bool fused) {
+  if (!fused) {
+    pseudo_grad(e, tl);
+    return;
+  }
+  phase_begin(e);
+  launch_pseudo_grad_gated(tt_pair(e), tl, e->st, e->send, e->prec, e->n, e->stream);
+  phase_end(e, DLC_PHASE_PSEUDO);
+  launched("pseudo_grad_gated");
 }
 
 void nesterov(dlc_engine* e, const void* dbar, const int* flags, int nflags) {
@@ -355,6 +378,7 @@ void relayout(dlc_engine* e, size_t k) {
   DLC_CUDA(cudaStreamSynchronize(e->stream));
   if (e->cstream) DLC_CUDA(cudaStreamSynchronize(e->cstream));
   p2p_unbind(e);
+  e->delta_fused = false;
   const size_t pb = e->slot_cap * elem_width(e->prec);
   DLC_CUDA(cudaMemsetAsync(e->send, 0, pb, e->stream));
   if (e->gather) DLC_CUDA(cudaMemsetAsync(e->gather, 0, pb, e->stream));

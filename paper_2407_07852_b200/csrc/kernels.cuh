@@ -25,6 +25,10 @@ namespace dlc {
 
 constexpr int kMaxK = 32;  // largest worker count a single fold launch takes
 
+struct PtrList {
+  const void* ptr[kMaxK];
+};
+
 // Device-resident engine scalars (EngineState, engine.hpp:48-56; AdamWState
 // step_count, optim.hpp:20; LossScaler, optim.hpp:52-56).  Kept on the GPU so
 // the inner loop never waits on the host: the overflow decision, step counter
@@ -46,7 +50,10 @@ struct DevState {
   int delta_nonfinite;      // K2 / solo: non-finite delta (or FP16 encode overflow)
   int last_applied;         // OuterStepResult::applied
   int ocur;                 // live buffer of the theta_t / momentum pair (solo fused outer step)
-  int pad;
+  int delta_ready;          // the send buffer holds theta_t - theta_local of the live state: written by
+                            // the window's last K1 (AdamWArgs::delta) when that step was applied
+  int redo;                 // fused single-worker boundary: its inner step overflowed, so the outer
+                            // step reruns from the unchanged theta_local (launch_boundary_solo)
 };
 
 struct AdamWArgs {
@@ -62,6 +69,11 @@ struct AdamWArgs {
   float b1, b2, eps, wd, omb1, omb2;  // omb = 1.0f - b, rounded as optim.cpp:84-85
   int pingpong;                       // 1: read [cur], write [cur^1]; 0: in place, gated
   float* tt[2];                       // theta_t pair: the source while DevState::lalias (pingpong only)
+  // K2 fused into the last inner step of a window (K > 1): besides p', write
+  // delta = theta_t[ocur] - p' into `delta` (FP32, or binary16 codes when
+  // delta_fp16) and let the finalize set DevState::delta_ready = !overflow.
+  void* delta;                        // nullptr: plain K1
+  int delta_fp16;
 };
 
 // Scalars of one out-of-place AdamW call whose gradient is already unscaled
@@ -70,9 +82,6 @@ struct AdamWPlain {
   float b1, b2, eps, wd, omb1, omb2, corr1, corr2, lr;
 };
 
-struct PtrList {
-  const void* ptr[kMaxK];
-};
 
 // The two buffers of a ping-pong pair; DevState::cur / ocur selects the live one.
 struct Pair {
@@ -93,7 +102,27 @@ void launch_adamw(const AdamWArgs& a, cudaStream_t s);
 void launch_adamw_plain(const float* p, const float* g, float* m, float* v, float* out,
                         size_t n, const AdamWPlain& a, cudaStream_t s);
 
+// K1 + K2 + K4 for one worker at a window boundary ------------------------------
+// DilocoOptimizer::step at inner_step % H == 0 (engine.cpp:162-174) with the
+// SoloCollective (reduce.cpp:113-126), PINGPONG engines: ONE HBM pass reads
+// theta_local (p, or theta_t while DevState::lalias), g, m, v, theta_t and
+// momentum and writes m', v' and the speculative theta_t', momentum' (40 B per
+// parameter instead of K1's 28 + the solo outer step's 20).  theta_local' is
+// never stored: after the outer step theta_local follows theta_t.  A one-thread
+// finalize applies the inner step's skip decision and scaler update, then the
+// outer step's finite gate.  If the inner step overflowed, the fused outer
+// values came from a rejected theta_local: a gated persistent pass reruns the
+// solo outer step from the unchanged one (DevState::redo; ~10 us when idle).
+void launch_boundary_solo(const AdamWArgs& a, Pair theta_t, Pair buf, int precision, float lr, float mu,
+                          cudaStream_t s);
+
 // K2 --------------------------------------------------------------------------
+// The outer step's K2 after a fused K1 (AdamWArgs::delta): a persistent grid
+// that returns at once when DevState::delta_ready (the usual case) and
+// otherwise (the window's last step overflowed, so theta_local kept its old
+// value) writes delta = theta_t - theta_local over [0, n) of `send`.
+void launch_pseudo_grad_gated(Pair theta_t, Pair theta_local, const DevState* st, void* send, int precision,
+                              size_t n, cudaStream_t s);
 // Elements [off, off + len) of delta = theta_t - theta_local into `out`
 // (float* for precision 0, binary16 codes for 1); non-finite OR into *flag.
 void launch_pseudo_grad(Pair theta_t, Pair theta_local, const DevState* st, void* out,

@@ -20,6 +20,24 @@ namespace {
 
 constexpr int kU1 = 1;  // vectors per thread (tools/tune_stream: best for 4R3W)
 
+// FUSE 0: plain K1.  FUSE 1 / 2: K2 fused in (the last inner step of a window,
+// K > 1, dlc_engine_set_fused_delta): delta = theta_t[ocur] - p' (tensor.cpp:126,
+// the same explicit-RN op as pseudo_grad_kernel) stored as FP32 / binary16 into
+// a.delta, +4 B read and +4 / 2 B written per parameter instead of K2's
+// separate 12 / 10 B pass.  While theta_local follows theta_t
+// (DevState::lalias) the theta_t read is the p read.
+template <int FUSE>
+__device__ __forceinline__ void store_delta(void* out, size_t j, float4 t, float4 p) {
+  const float4 d = make_float4(delta_elem(t.x, p.x), delta_elem(t.y, p.y), delta_elem(t.z, p.z), delta_elem(t.w, p.w));
+  if (FUSE == 1) {
+    st_stream(reinterpret_cast<float4*>(out) + j, d);
+  } else {
+    st_stream(reinterpret_cast<uint2*>(out) + j,
+              make_uint2(pack2(fp16_encode(d.x), fp16_encode(d.y)), pack2(fp16_encode(d.z), fp16_encode(d.w))));
+  }
+}
+
+template <int FUSE>
 __global__ void __launch_bounds__(kThreads) adamw_kernel(AdamWArgs a) {
   DevState* st = a.st;
   // INPLACE mode: the pre-pass already decided; an overflowed step writes nothing.
@@ -29,7 +47,9 @@ __global__ void __launch_bounds__(kThreads) adamw_kernel(AdamWArgs a) {
   const uint64_t t = st->step_count + 1;
   const AdamScalars s{a.b1, a.b2, a.eps, a.wd, a.omb1, a.omb2, a.corr1[t], a.corr2[t], a.lr[t]};
   const float inv = __fdiv_rn(1.0f, st->scale);  // optim.cpp:124 (exact: power of two)
-  const float* pc = (a.pingpong && st->lalias) ? (st->ocur ? a.tt[1] : a.tt[0]) : (cur ? a.p[1] : a.p[0]);
+  const bool follow = a.pingpong && st->lalias;
+  const float* tc = st->ocur ? a.tt[1] : a.tt[0];
+  const float* pc = follow ? tc : (cur ? a.p[1] : a.p[0]);
   const float* mc = cur ? a.m[1] : a.m[0];
   const float* vc = cur ? a.v[1] : a.v[0];
   float* pn = nxt ? a.p[1] : a.p[0];
@@ -37,7 +57,7 @@ __global__ void __launch_bounds__(kThreads) adamw_kernel(AdamWArgs a) {
   float* vn = nxt ? a.v[1] : a.v[0];
   bool bad = false;
   const size_t n4 = a.n / 4, b = wbase<kU1>();
-  float4 p[kU1], g[kU1], m[kU1], v[kU1];
+  float4 p[kU1], g[kU1], m[kU1], v[kU1], tt[kU1];
 #pragma unroll
   for (int u = 0; u < kU1; ++u) {
     const size_t j = b + u * kThreads;
@@ -46,6 +66,7 @@ __global__ void __launch_bounds__(kThreads) adamw_kernel(AdamWArgs a) {
       p[u] = ld_stream(reinterpret_cast<const float4*>(pc) + j);
       m[u] = ld_stream(reinterpret_cast<const float4*>(mc) + j);
       v[u] = ld_stream(reinterpret_cast<const float4*>(vc) + j);
+      if (FUSE) tt[u] = follow ? p[u] : ld_stream(reinterpret_cast<const float4*>(tc) + j);
     }
   }
 #pragma unroll
@@ -63,6 +84,7 @@ __global__ void __launch_bounds__(kThreads) adamw_kernel(AdamWArgs a) {
       st_stream(reinterpret_cast<float4*>(pn) + j, po);
       st_stream(reinterpret_cast<float4*>(mn) + j, m[u]);
       st_stream(reinterpret_cast<float4*>(vn) + j, v[u]);
+      if (FUSE) store_delta<FUSE>(a.delta, j, tt[u], po);
     }
   }
   if (blockIdx.x == 0 && threadIdx.x < a.n - n4 * 4) {
@@ -70,42 +92,20 @@ __global__ void __launch_bounds__(kThreads) adamw_kernel(AdamWArgs a) {
     const float gu = __fmul_rn(a.g[e], inv);
     bad |= !finite_f(gu);
     float mm = mc[e], vv = vc[e];
-    pn[e] = adamw_elem(pc[e], gu, mm, vv, s);
+    const float po = adamw_elem(pc[e], gu, mm, vv, s);
+    pn[e] = po;
     mn[e] = mm;
     vn[e] = vv;
+    if (FUSE == 1) static_cast<float*>(a.delta)[e] = delta_elem(tc[e], po);
+    if (FUSE == 2) static_cast<uint16_t*>(a.delta)[e] = fp16_encode(delta_elem(tc[e], po));
   }
   if (a.pingpong) block_or_flag(bad, &st->found_inf);
 }
 
 // One thread: the skip decision, step counter, lr record and scaler_update
-// (engine.cpp:57-67, optim.cpp:69, optim.cpp:137-148 with clamps :13-14).
-__global__ void adamw_finalize_kernel(DevState* st, const float* lr_tab, int pingpong) {
-  const int fi = st->found_inf;
-  const uint64_t t = st->step_count + 1;
-  if (!fi) {
-    if (pingpong) st->cur ^= 1;  // the freshly written buffers become live
-    st->lalias = 0;              // theta_local now lives in p[cur]
-    st->step_count = t;
-    st->last_lr = lr_tab[t];
-  } else {
-    st->last_lr = 0.0f;
-    st->overflow_skips += 1;
-  }
-  st->last_overflow = fi;
-  if (fi) {
-    const float s = __fmul_rn(st->scale, 0.5f);
-    st->scale = (s < 0x1p-20f) ? 0x1p-20f : s;
-    st->good = 0;
-  } else {
-    st->good += 1;
-    if (st->good >= st->growth) {
-      const float s = __fmul_rn(st->scale, 2.0f);
-      st->scale = (0x1p24f < s) ? 0x1p24f : s;
-      st->good = 0;
-    }
-  }
-  st->inner_step += 1;  // data cursor always advances (engine.cpp:103)
-  st->found_inf = 0;
+// (inner_finalize, device.cuh).
+__global__ void adamw_finalize_kernel(DevState* st, const float* lr_tab, int pingpong, int fused) {
+  inner_finalize(st, lr_tab, pingpong, fused);
 }
 
 // INPLACE pre-pass (optim.cpp:127-132): found_inf |= !isfinite(g * (1/scale)).
@@ -144,8 +144,14 @@ __global__ void __launch_bounds__(kThreads) adamw_plain_kernel(const float* p, c
 void launch_adamw(const AdamWArgs& a, cudaStream_t s) {
   if (!a.pingpong)
     unscale_check_kernel<<<grid_window<2>(a.n / 4), kThreads, 0, s>>>(a.g, a.st, a.n);
-  adamw_kernel<<<grid_window<kU1>(a.n / 4), kThreads, 0, s>>>(a);
-  adamw_finalize_kernel<<<1, 1, 0, s>>>(a.st, a.lr, a.pingpong);
+  const int grid = grid_window<kU1>(a.n / 4);
+  if (!a.delta)
+    adamw_kernel<0><<<grid, kThreads, 0, s>>>(a);
+  else if (!a.delta_fp16)
+    adamw_kernel<1><<<grid, kThreads, 0, s>>>(a);
+  else
+    adamw_kernel<2><<<grid, kThreads, 0, s>>>(a);
+  adamw_finalize_kernel<<<1, 1, 0, s>>>(a.st, a.lr, a.pingpong, a.delta != nullptr);
 }
 
 void launch_adamw_plain(const float* p, const float* g, float* m, float* v, float* out, size_t n,

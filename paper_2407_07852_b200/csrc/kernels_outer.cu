@@ -68,6 +68,36 @@ __global__ void __launch_bounds__(kThreads) pseudo_grad_kernel(Pair ttp, Pair tl
   block_or_flag(bad, flag);
 }
 
+// The outer step's K2 after a fused K1: nothing to do when the window's last
+// step wrote the delta (DevState::delta_ready); else the whole delta, grid-stride.
+template <int PREC>
+__global__ void __launch_bounds__(kThreads) pseudo_grad_gated_kernel(Pair ttp, Pair tl, const DevState* st, void* out,
+                                                                     size_t n) {
+  if (*(volatile const int*)&st->delta_ready) return;
+  const float* T = sel(ttp, st->ocur);
+  const float* L = local_src(tl, ttp, st);
+  const size_t n4 = n / 4;
+  for (size_t j = gtid(); j < n4; j += gstride()) {
+    const float4 x = ld_stream(reinterpret_cast<const float4*>(T) + j);
+    const float4 y = ld_stream(reinterpret_cast<const float4*>(L) + j);
+    const float4 d = make_float4(delta_elem(x.x, y.x), delta_elem(x.y, y.y), delta_elem(x.z, y.z),
+                                 delta_elem(x.w, y.w));
+    if (PREC == 0)
+      st_stream(reinterpret_cast<float4*>(out) + j, d);
+    else
+      st_stream(reinterpret_cast<uint2*>(out) + j,
+                make_uint2(pack2(fp16_encode(d.x), fp16_encode(d.y)), pack2(fp16_encode(d.z), fp16_encode(d.w))));
+  }
+  if (blockIdx.x == 0 && threadIdx.x < n - n4 * 4) {
+    const size_t e = n4 * 4 + threadIdx.x;
+    const float d = delta_elem(T[e], L[e]);
+    if (PREC == 0)
+      static_cast<float*>(out)[e] = d;
+    else
+      static_cast<uint16_t*>(out)[e] = fp16_encode(d);
+  }
+}
+
 // =============================================================================
 // K4: finite-gated Nesterov on theta_t + theta_local refresh (engine.cpp:136-144).
 // =============================================================================
@@ -102,13 +132,6 @@ __device__ __forceinline__ void k4_scalar(bool applied, float* T, float* B, floa
   } else if (L) {
     *L = *T;
   }
-}
-
-__device__ __forceinline__ void k4_finalize(DevState* st, bool applied, const Pair& tl) {
-  if (tl.follow) st->lalias = 1;  // theta_local := theta_t (engine.cpp:141-143) without the copy
-  st->last_applied = applied ? 1 : 0;
-  st->outer_skips += applied ? 0 : 1;
-  st->outer_epoch += 1;  // engine.cpp:144
 }
 
 template <int PREC>
@@ -270,18 +293,6 @@ __global__ void __launch_bounds__(kThreads) p2p_finish_kernel(Pair ttp, Pair tl,
 // Speculative: the new theta_t and momentum go to the idle buffers of their
 // ping-pong pairs, so a skip only has to leave `ocur` unflipped.
 template <int PREC>
-__device__ __forceinline__ float solo_delta(float tt, float tl, bool& bad) {
-  const float d = delta_elem(tt, tl);  // engine.cpp:122
-  if (PREC == 0) {
-    bad |= !finite_f(d);
-    return d;
-  }
-  const uint16_t h = fp16_encode(d);  // encode once at the source; the mean of one
-  bad |= fp16_nonfinite(h);           // contribution re-encodes to the same code
-  return fp16_decode(h);
-}
-
-template <int PREC>
 __global__ void __launch_bounds__(kThreads) outer_solo_kernel(Pair ttp, Pair bufp, Pair tl, const float* src,
                                                               DevState* st, float lr, float mu, size_t off,
                                                               size_t len) {
@@ -350,6 +361,15 @@ void launch_pseudo_grad(Pair tt, Pair tl, const DevState* st, void* out, int pre
     pseudo_grad_kernel<0><<<grid, kThreads, 0, s>>>(tt, tl, st, out, flag, off, len);
   else
     pseudo_grad_kernel<1><<<grid, kThreads, 0, s>>>(tt, tl, st, out, flag, off, len);
+}
+
+void launch_pseudo_grad_gated(Pair tt, Pair tl, const DevState* st, void* send, int precision, size_t n,
+                              cudaStream_t s) {
+  const int grid = num_sms() * 8;
+  if (precision == 0)
+    pseudo_grad_gated_kernel<0><<<grid, kThreads, 0, s>>>(tt, tl, st, send, n);
+  else
+    pseudo_grad_gated_kernel<1><<<grid, kThreads, 0, s>>>(tt, tl, st, send, n);
 }
 
 void launch_nesterov_outer(Pair tt, Pair buf, Pair tl, const void* dbar, int precision, const int* flags,

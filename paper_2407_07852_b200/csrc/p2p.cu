@@ -261,6 +261,23 @@ void p2p_k2(P2PStep& s, size_t p) {
   DLC_CUDA(cudaEventRecord(s.evK2[p], e->stream));
 }
 
+// Every K2 piece of a device-buffer step; after a fused K1 (the delta is
+// already in the send buffer) only the gated fallback, whose completion then
+// releases every piece's fold at once.
+void p2p_k2_all(P2PStep& s, bool fused) {
+  dlc_engine* e = s.e;
+  if (!fused) {
+    for (size_t p = 0; p < s.P; ++p) p2p_k2(s, p);
+    launched("pseudo_grad_piece");
+    return;
+  }
+  cudaEvent_t t0 = trace_begin(e, e->stream);
+  launch_pseudo_grad_gated(tt_pair(e), s.tl, e->st, e->send, e->prec, s.n, e->stream);
+  launched("pseudo_grad_gated");
+  trace_end(e, e->stream, "K2gated", 0, t0);
+  for (size_t p = 0; p < s.P; ++p) DLC_CUDA(cudaEventRecord(s.evK2[p], e->stream));
+}
+
 void p2p_fold_begin(P2PStep& s) {
   dlc_engine* e = s.e;
   s.c0 = pooled_event(e);
@@ -341,7 +358,7 @@ void p2p_finish(P2PStep& s, const int* abort) {
 
 // One process per GPU: the stages above ordered by NVLink flag barriers.
 void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc_reduce_report* rep,
-                         const float* hsrc, float* hdst, int oc_host) {
+                         const float* hsrc, float* hdst, int oc_host, bool fused) {
   harvest_if_full(e);  // never inside the step: a host wait there could block on a peer's barrier
   p2p_bind(e, c);
   P2PStep s = p2p_begin(e, c->rank, src, rep != nullptr, hsrc, hdst, oc_host);
@@ -371,8 +388,7 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
     // device buffers: every K2 piece first (the folds of the early pieces run
     // beside the later K2 pieces), then the K4 pieces as their means land
     phase_begin(e);
-    for (size_t p = 0; p < P; ++p) p2p_k2(s, p);
-    launched("pseudo_grad_piece");
+    p2p_k2_all(s, fused);
     phase_end(e, DLC_PHASE_PSEUDO);
     p2p_fold_begin(s);
     for (size_t p = 0; p < P; ++p) fold_piece(p);
@@ -406,7 +422,8 @@ void outer_p2p_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc
 //   main     wait evB[p]; K4(p) into the idle theta_t / momentum; ...; finish
 // (measured 9.66 ms against 11.2 ms for the unpipelined K2 -> all-reduce -> K4
 // of outer_collective at 4 GPUs, profiles/r1_bench_4gpu_allreduce*.json)
-void outer_allreduce_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc_reduce_report* rep) {
+void outer_allreduce_pipelined(dlc_engine* e, dlc_collective* c, const float* src, dlc_reduce_report* rep,
+                               bool fused) {
   harvest_if_full(e);
   const size_t n = e->n, w = elem_width(e->prec);
   if (!e->cstream) {
@@ -432,12 +449,17 @@ void outer_allreduce_pipelined(dlc_engine* e, dlc_collective* c, const float* sr
   DLC_CUDA(cudaMemsetAsync(e->flags, 0, sizeof(int), e->stream));
   DLC_CUDA(cudaEventRecord(evStart, e->stream));
   phase_begin(e);
+  if (fused) {  // the delta is in the send buffer already (fused K1), the gated K2 covers an overflow
+    launch_pseudo_grad_gated(tt_pair(e), tl, e->st, e->send, e->prec, n, e->stream);
+    launched("pseudo_grad_gated");
+  }
   for (size_t p = 0; p < P; ++p) {  // k = 1: piece p is the contiguous range [pb[p], pb[p+1])
-    launch_pseudo_grad_piece(tt_pair(e), tl, e->st, e->send, e->prec, 1, 0, pb[p], pb[p + 1] - pb[p], n, 0,
-                             e->stream);
+    if (!fused)
+      launch_pseudo_grad_piece(tt_pair(e), tl, e->st, e->send, e->prec, 1, 0, pb[p], pb[p + 1] - pb[p], n, 0,
+                               e->stream);
     DLC_CUDA(cudaEventRecord(evK2[p], e->stream));
   }
-  launched("pseudo_grad_piece");
+  if (!fused) launched("pseudo_grad_piece");
   phase_end(e, DLC_PHASE_PSEUDO);
   DLC_CUDA(cudaStreamWaitEvent(e->cstream, evStart, 0));
   cudaEvent_t c0 = pooled_event(e), c1 = pooled_event(e);
@@ -479,12 +501,13 @@ void outer_allreduce_pipelined(dlc_engine* e, dlc_collective* c, const float* sr
 }
 
 void outer_round(dlc_engine* e, dlc_collective* c, const float* src, dlc_reduce_report* rep) {
+  const bool fused = take_fused_delta(e) && !src;  // an explicit theta_local source needs the full K2
   if (e->k > 1 && c->mode == DLC_MODE_P2P) {  // manages its own flag (read remotely by peers)
-    outer_p2p_pipelined(e, c, src, rep, nullptr, nullptr, 0);
+    outer_p2p_pipelined(e, c, src, rep, nullptr, nullptr, 0, fused);
     return;
   }
   if (e->k > 1 && c->mode == DLC_MODE_ALLREDUCE) {
-    outer_allreduce_pipelined(e, c, src, rep);
+    outer_allreduce_pipelined(e, c, src, rep, fused);
     return;
   }
   reset_flags(e);
@@ -497,7 +520,7 @@ void outer_round(dlc_engine* e, dlc_collective* c, const float* src, dlc_reduce_
     return;
   }
   float* s = const_cast<float*>(src);
-  pseudo_grad(e, s ? Pair{{s, s}} : local_pair(e));
+  pseudo_grad_step(e, s ? Pair{{s, s}} : local_pair(e), fused);
   outer_collective(e, c, rep);
 }
 

@@ -17,9 +17,11 @@ extern "C" {
 // asynchronous copy of the engine's device scalars into a pinned ring slot and
 // a timing event.  A step's records are emitted one step behind, once its event
 // has completed, so the GPU always has the next step queued while the host
-// formats records and calls the producer.  At a window boundary the loop drains
-// (the round's report, the barrier check and the on_round hook need the final
-// state).  The record stream is the reference's (engine.cpp:181-238); only the
+// formats records and calls the producer.  At a window boundary the loop
+// drains when a fleet's barrier check (K > 1) must raise before the next inner
+// step is queued, or when an on_round hook (a checkpoint) must see the
+// boundary's state; otherwise a boundary is emitted one step behind like any
+// other step.  The record stream is the reference's (engine.cpp:181-238); only the
 // interleaving of producer calls and sink calls differs (producer(t + 1) runs
 // before step t's records are emitted).  compute_ms / comm_ms are CUDA-event
 // times of the step and of its collective on the device, not host wall time.
@@ -61,7 +63,7 @@ int dlc_run_training(dlc_engine* e, dlc_collective* c, dlc_grad_producer produce
       dlc_reduce_report report{};
       bool applied = false;
       if (p.boundary) {
-        check_barrier(e);  // a failed round raises CollectiveError here
+        if (e->k > 1) check_barrier(e);  // a failed round raises CollectiveError here
         fill_report(e, c, &report, s.outer_epoch - 1);
         applied = s.last_applied != 0;
       }
@@ -131,7 +133,11 @@ int dlc_run_training(dlc_engine* e, dlc_collective* c, dlc_grad_producer produce
       DLC_CUDA(cudaMemcpyAsync(&ring.host[slot], e->st, sizeof(DevState), cudaMemcpyDeviceToHost, e->stream));
       DLC_CUDA(cudaEventRecord(ring.b[slot], e->stream));
       pending.push_back({slot, loss, boundary});
-      while (!pending.empty() && (boundary || pending.size() > 1)) {  // one step behind; drain at a boundary
+      // one step behind; drain at a boundary when a fleet's failed round must
+      // raise before the next inner step runs, or when the on_round hook (the
+      // checkpoint hook, engine.hpp:154) must see the state of that boundary
+      const bool drain = boundary && (e->k > 1 || on_round);
+      while (!pending.empty() && (drain || pending.size() > 1)) {
         const Pending p = pending.front();
         pending.pop_front();
         emit(p);

@@ -66,6 +66,7 @@ int dlc_engine_wire_begin(dlc_engine* e, uint64_t* outer_epoch) {
     if (!e) fail(DLC_EINVAL, "dlc_engine_wire_begin: null engine");
     check_window(e);
     DeviceGuard dg(e->device);
+    e->delta_fused = false;  // the wire round decodes the means into the send buffer
     // encode once at the source (collective.cpp:1356-1366): FP16 codes or FP32 deltas
     launch_pseudo_grad(tt_pair(e), local_pair(e), e->st, e->grad, e->prec, &e->st->delta_nonfinite, 0, e->n,
                        e->stream);

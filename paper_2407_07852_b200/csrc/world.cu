@@ -22,6 +22,7 @@ struct dlc_world {
   std::vector<int> devices;
   std::vector<dlc_engine*> engines;
   std::vector<dlc_collective*> colls;
+  std::vector<int> members;  // original rank of each current rank (dlc_world_shrink)
 };
 
 namespace {
@@ -85,8 +86,7 @@ void world_outer_p2p(dlc_world* w) {
     DeviceGuard dg(w->devices[r]);
     dlc_engine* e = w->engines[r];
     phase_begin(e);
-    for (size_t p = 0; p < P; ++p) p2p_k2(st[r], p);
-    launched("pseudo_grad_piece");
+    p2p_k2_all(st[r], take_fused_delta(e));
     phase_end(e, DLC_PHASE_PSEUDO);
     p2p_fold_begin(st[r]);
   }
@@ -129,7 +129,7 @@ void world_outer_nccl(dlc_world* w) {
     DeviceGuard dg(w->devices[r]);
     dlc_engine* e = w->engines[r];
     reset_flags(e);
-    pseudo_grad(e, local_pair(e));
+    pseudo_grad_step(e, local_pair(e), take_fused_delta(e));
   }
   if (w->mode == DLC_MODE_ORDERED) {
     DLC_NCCL(ncclGroupStart());
@@ -202,6 +202,7 @@ int dlc_world_create(const dlc_config* cfg, const dlc_hyperparams* hyper, size_t
     w->k = k;
     w->mode = mode;
     w->devices.assign(devices, devices + k);
+    for (int r = 0; r < k; ++r) w->members.push_back(r);
     for (int r = 0; r < k; ++r) {
       dlc_engine* e = nullptr;
       const int s2 = dlc_engine_create(cfg, hyper, n_params, devices[r], inner_mode, &e);
@@ -261,6 +262,76 @@ int dlc_world_engine(dlc_world* w, int rank, dlc_engine** e) {
     if (rank < 0 || rank >= w->k) fail(DLC_EINVAL, "dlc_world_engine: rank out of range");
     *e = w->engines[rank];
   });
+}
+
+int dlc_world_shrink(dlc_world* w, const int* exclude_ranks, size_t n_exclude, size_t quorum_min) {
+  return guard([&] {
+    if (!w || (n_exclude && !exclude_ranks)) fail(DLC_EINVAL, "dlc_world_shrink: null argument");
+    std::vector<int> ex(exclude_ranks, exclude_ranks + n_exclude);
+    std::sort(ex.begin(), ex.end());
+    ex.erase(std::unique(ex.begin(), ex.end()), ex.end());
+    for (int r : ex)
+      if (r < 0 || r >= w->k) fail(DLC_ECONFIG, "dlc_world_shrink: rank " + std::to_string(r) + " not in the world");
+    const int k2 = w->k - (int)ex.size();
+    if ((size_t)k2 < std::max<size_t>(quorum_min, 1))  // collective.cpp:1376-1378
+      fail(DLC_EQUORUM, "contributor set below quorum");
+    for (dlc_engine* e : w->engines)  // engine.cpp:116-120: membership changes between rounds
+      if (e->issued_inner % e->cfg.local_steps_h != 0) fail(DLC_EINVAL, "dlc_world_shrink: mid-window");
+    if (ex.empty()) return;
+    for (int r = 0; r < w->k; ++r) {  // nothing in flight on any rank
+      DeviceGuard dg(w->devices[r]);
+      DLC_CUDA(cudaDeviceSynchronize());
+    }
+    std::vector<dlc_engine*> engines;
+    std::vector<int> devices, members;
+    for (int r = 0; r < w->k; ++r) {
+      if (std::binary_search(ex.begin(), ex.end(), r)) {
+        p2p_unbind(w->engines[r]);
+        dlc_engine_destroy(w->engines[r]);
+        continue;
+      }
+      engines.push_back(w->engines[r]);
+      devices.push_back(w->devices[r]);
+      members.push_back(w->members[r]);
+    }
+    for (size_t r = 0; r < w->colls.size(); ++r) {
+      DeviceGuard dg(w->devices[r]);
+      if (w->colls[r]->comm) ncclCommDestroy(w->colls[r]->comm);
+      delete w->colls[r];
+    }
+    w->colls.clear();
+    w->engines = engines;
+    w->devices = devices;
+    w->members = members;
+    w->k = k2;
+    for (dlc_engine* e : w->engines) {
+      DeviceGuard dg(e->device);
+      p2p_unbind(e);
+      relayout(e, (size_t)k2);  // survivor slots and divisor
+    }
+    std::vector<ncclComm_t> comms(k2, nullptr);
+    if (k2 > 1 && w->mode != DLC_MODE_P2P) DLC_NCCL(ncclCommInitAll(comms.data(), k2, w->devices.data()));
+    for (int r = 0; r < k2; ++r) {
+      auto* c = new dlc_collective();
+      c->kind = k2 > 1 ? 1 : 0;
+      c->rank = r;
+      c->world = k2;
+      c->device = w->devices[r];
+      c->mode = w->mode;
+      c->comm = comms[r];
+      c->in_world = true;
+      c->shrunk = true;
+      for (int j = 0; j < k2; ++j) c->members[j] = w->members[j];
+      w->colls.push_back(c);
+    }
+    if (k2 > 1 && w->mode == DLC_MODE_P2P) world_bind_p2p(w);
+  });
+}
+
+size_t dlc_world_members(const dlc_world* w, int* ranks, size_t cap) {
+  if (!w) return 0;
+  for (size_t i = 0; i < w->members.size() && i < cap && ranks; ++i) ranks[i] = w->members[i];
+  return w->members.size();
 }
 
 int dlc_world_outer_step(dlc_world* w, dlc_outer_result* result) {

@@ -499,6 +499,10 @@ class DilocoEngine:
         _check(lib.dlc_engine_wire_finish(self.handle, outer_epoch, C.byref(res)))
         return OuterStepResult(bool(res.applied), int(res.outer_epoch))
 
+    def set_fused_delta(self, on: bool) -> None:
+        """K2 fused into the window's last inner step (opt-in; K > 1)."""
+        _check(lib.dlc_engine_set_fused_delta(self.handle, int(on)))
+
     def set_timing(self, on: bool) -> None:
         _check(lib.dlc_engine_set_timing(self.handle, int(on)))
 
@@ -563,6 +567,25 @@ class World:
         res = A.OuterResult()
         _check(lib.dlc_world_outer_step(self.handle, C.byref(res)))
         return OuterStepResult(bool(res.applied), int(res.outer_epoch))
+
+    def shrink(self, exclude, quorum_min: int = 0) -> None:
+        """dlc_world_shrink: the next rounds run over the ranks not in `exclude`
+        (survivor order and divisor, collective.cpp:1369-1395); the excluded
+        engines are destroyed."""
+        ex = list(exclude)
+        arr = (C.c_int * max(len(ex), 1))(*ex)
+        _check(lib.dlc_world_shrink(self.handle, arr, len(ex), quorum_min))
+        dropped = set(ex)
+        for r, e in enumerate(self.engines):
+            if r in dropped:
+                e.handle = None
+        self.engines = [e for r, e in enumerate(self.engines) if r not in dropped]
+
+    def members(self) -> list:
+        """Original ranks of the current members."""
+        buf = (C.c_int * 32)()
+        n = lib.dlc_world_members(self.handle, buf, 32)
+        return [buf[i] for i in range(n)]
 
     def close(self):
         if getattr(self, "handle", None):

@@ -42,11 +42,13 @@ def bits(a):
 
 
 def run_world(port, k, prec, mode, devices, n=40_009, h=2, rounds=2, overflow=(None, None), seed=77,
-              nonfinite_round=None):
+              nonfinite_round=None, fused=True, inner_mode=A.INNER_PINGPONG):
     """K workers, `rounds` windows of H inner steps: the GPU world vs the oracle.
     overflow=(w, t): grad[5] = inf for worker w at global step t (that worker's
     inner step is skipped).  nonfinite_round: a non-finite theta_local on the
-    last worker before that round's outer step (every rank skips it)."""
+    last worker before that round's outer step (every rank skips it).
+    fused: K2 fused into each window's last inner step (the default), else the
+    outer step's own K2 pieces."""
     hyper = DR.Hyper(inner_lr=1e-3, warmup_steps=2)
     hp = D.OptimHyperparams(inner_lr=1e-3, warmup_steps=2)
     theta0 = O.rng_fill(seed, "theta", 0, n, -0.05, 0.05)
@@ -57,8 +59,9 @@ def run_world(port, k, prec, mode, devices, n=40_009, h=2, rounds=2, overflow=(N
             g[5] = np.inf
         return g
 
-    world = D.World(D.DilocoConfig(h, k, prec, h * rounds), hp, n, devices, mode=mode)
+    world = D.World(D.DilocoConfig(h, k, prec, h * rounds), hp, n, devices, mode=mode, inner_mode=inner_mode)
     for e in world.engines:
+        e.set_fused_delta(fused)
         e.upload(A.THETA_T, theta0)
         e.upload(A.THETA_LOCAL, theta0)
     ws = DR.make_workers(theta0, k, hyper)
@@ -101,6 +104,107 @@ def test_world_shared_device_p2p(port, k, prec):
     worker, two rounds."""
     world, ws = run_world(port, k, prec, A.MODE_P2P, [0] * k, overflow=(k - 1, 1))
     check_bitwise(world, ws)
+    world.close()
+
+
+@pytest.mark.parametrize("inner_mode", [A.INNER_PINGPONG, A.INNER_INPLACE])
+@pytest.mark.parametrize("fused", [True, False, "mixed"])
+@pytest.mark.parametrize("prec", [A.FP16, A.FP32])
+def test_world_fused_delta(port, prec, fused, inner_mode):
+    """K2 fused into the window's last inner step (dlc_engine_set_fused_delta)
+    against the unfused outer K2, and a mix of both in one fleet: H = 3, three
+    rounds; worker 1 overflows on the last step of round 0 (its fused delta is
+    discarded and the gated K2 recomputes it from the unchanged theta_local),
+    worker 2 on the first step of round 1, and round 2 replaces worker 0's
+    theta_local after its last inner step (the upload drops the fused delta).
+    Both inner modes."""
+    k, h, n, seed = 4, 3, 30_011, 91
+    hyper = DR.Hyper(inner_lr=1e-3, warmup_steps=2)
+    hp = D.OptimHyperparams(inner_lr=1e-3, warmup_steps=2)
+    theta0 = O.rng_fill(seed, "theta", 0, n, -0.05, 0.05)
+
+    def grad_fn(w, t):
+        g = O.rng_fill(seed, "grad", w * 1000 + t, n, -1e-2, 1e-2)
+        if (w, t) in ((1, 2), (2, 3)):
+            g[7] = np.inf
+        return g
+
+    world = D.World(D.DilocoConfig(h, k, prec, 3 * h), hp, n, [0] * k, mode=A.MODE_P2P, inner_mode=inner_mode)
+    for i, e in enumerate(world.engines):
+        e.set_fused_delta(i % 2 == 0 if fused == "mixed" else fused)
+        e.upload(A.THETA_T, theta0)
+        e.upload(A.THETA_LOCAL, theta0)
+    ws = DR.make_workers(theta0, k, hyper)
+    step = 0
+    for rnd in range(3):
+        for _ in range(h):
+            for wi, e in enumerate(world.engines):
+                e.inner_step_host(grad_fn(wi, step))
+                DR.inner_step(port, ws[wi], grad_fn(wi, step), hyper)
+            step += 1
+        if rnd == 2:
+            moved = world.engines[0].download(A.THETA_LOCAL)
+            moved[: n // 2] += np.float32(1e-3)
+            world.engines[0].upload(A.THETA_LOCAL, moved)
+            ws[0].theta_local = moved.copy()
+        _, applied, _ = DR.outer_round(port, ws, prec, hyper)
+        res = world.outer_step()
+        assert res.applied == applied and res.outer_epoch == rnd + 1
+    check_bitwise(world, ws)
+    world.close()
+
+
+@pytest.mark.parametrize("k,exclude", [(4, [2]), (8, [0, 3, 7]), (3, [0, 1])])
+@pytest.mark.parametrize("prec", [A.FP16, A.FP32])
+def test_world_shrink_survivor_rounds(port, k, exclude, prec):
+    """Membership change between rounds: one round over K
+    ranks, then the world drops `exclude` and runs two rounds over the
+    survivors, bitwise against the oracle's outer round over the survivors in
+    order with divisor K' (collective.cpp:1369-1395; test_collective.cpp:460-531
+    "survivor mean").  Below-quorum, out-of-range and mid-window shrinks raise
+    and change nothing."""
+    n, h, seed = 20_011, 2, 13
+    hyper = DR.Hyper(inner_lr=1e-3, warmup_steps=2)
+    hp = D.OptimHyperparams(inner_lr=1e-3, warmup_steps=2)
+    theta0 = O.rng_fill(seed, "theta", 0, n, -0.05, 0.05)
+
+    def grad_fn(w, t):
+        g = O.rng_fill(seed, "grad", w * 1000 + t, n, -1e-2, 1e-2)
+        if (w, t) == (k - 1, 5):
+            g[3] = np.inf
+        return g
+
+    world = D.World(D.DilocoConfig(h, k, prec, 3 * h), hp, n, [0] * k, mode=A.MODE_P2P)
+    for e in world.engines:
+        e.upload(A.THETA_T, theta0)
+        e.upload(A.THETA_LOCAL, theta0)
+    ws = DR.make_workers(theta0, k, hyper)
+    alive = list(range(k))
+    step = 0
+    for rnd in range(3):
+        if rnd == 1:
+            with pytest.raises(D.QuorumError):
+                world.shrink(list(range(k)), quorum_min=1)
+            with pytest.raises(D.ConfigError):
+                world.shrink([k])
+            survivors = [r for r in alive if r not in exclude]
+            with pytest.raises(D.QuorumError):
+                world.shrink(exclude, quorum_min=len(survivors) + 1)
+            world.shrink(exclude)
+            alive = survivors
+            assert world.members() == alive
+        for _ in range(h):
+            for idx, w in enumerate(alive):
+                world.engines[idx].inner_step_host(grad_fn(w, step))
+                DR.inner_step(port, ws[w], grad_fn(w, step), hyper)
+            step += 1
+            if rnd == 2 and step % h == 1:
+                with pytest.raises(D.Error):
+                    world.shrink([0])  # mid-window
+        _, applied, _ = DR.outer_round(port, [ws[w] for w in alive], prec, hyper)
+        res = world.outer_step()
+        assert res.applied == applied and res.outer_epoch == rnd + 1
+    check_bitwise(world, [ws[w] for w in alive])
     world.close()
 
 

@@ -1,0 +1,11 @@
+# 4-GPU: state after the fused-delta A/B (opt-in, local) + world shrink + run_training drain rule — smoke, GPU suite, bench at 1 / 2 / 4 GPUs (development script)
+O=gpurun_out/r2k
+mkdir -p $O
+nvidia-smi -L > $O/gpus.txt
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1
+timeout 1500 python -m pytest tests -m gpu -q -rs --durations=10 > $O/pytest_gpu.log 2>&1
+timeout 400 python bench.py > $O/bench_1gpu.json 2> $O/bench_1gpu.err
+for n in 2 4; do
+  timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port 2955$n bench.py --gpus $n > $O/bench_${n}gpu.json 2> $O/bench_${n}gpu.err
+done
+echo done
