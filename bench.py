@@ -383,16 +383,19 @@ def measure_window_boundary(D, coll, n, k, prec, local, max_over_ranks, barrier,
     (DilocoOptimizer::step at inner_step % H == 0, engine.cpp:162-174), timed
     with CUDA events on the engine stream around exactly those two calls, H = 2
     so theta_local != theta_t when the fused K1 runs (it reads theta_t).
-    Variants, interleaved window by window on one engine: "unfused" (the outer
-    step's own K2, the default) and "fused" (K1 writes the delta into the send
-    buffer, dlc_engine_set_fused_delta).  Per variant: the boundary's mean time
-    and the K1 / K2 / K4 phase times (max over ranks)."""
+    Variants, interleaved window by window on one engine: "unfused" (inner
+    step, then the outer step with its own K2) and "fused": at K = 1
+    DilocoOptimizer::step's single pass (K1 + K2 + K4, launch_boundary_solo,
+    the default there), at K > 1 the opt-in K1 that also writes the delta
+    (dlc_engine_set_fused_delta).  Per variant: the boundary's mean time and
+    the K1 / K2 / K4 phase times (max over ranks)."""
     import torch
     h = 2
     variants = [("unfused", False), ("fused", True)]
     total = h * len(variants) * (warmup + windows)
     cfg = D.DilocoConfig(local_steps_h=h, num_workers_k=k, reduce_precision=prec, total_inner_steps=total)
     e = D.DilocoEngine(cfg, D.OptimHyperparams(), n, local)
+    opt = D.DilocoOptimizer(e, coll)
     e.rng_fill(D.THETA_T, 4242, "theta", 0, -0.05, 0.05)
     e.rng_fill(D.THETA_LOCAL, 4242, "theta", 0, -0.05, 0.05)
     e.rng_fill(D.GRAD, 4242, "grad", k * 100 + 7, -1e-2 * 65536.0, 1e-2 * 65536.0)
@@ -410,8 +413,11 @@ def measure_window_boundary(D, coll, n, k, prec, local, max_over_ranks, barrier,
             e.phase_times()  # reset
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            e.inner_step(gptr, grad_is_scaled=True)
-            e.outer_step(coll)
+            if fused and k == 1:
+                opt.step(gptr, grad_is_scaled=True)
+            else:
+                e.inner_step(gptr, grad_is_scaled=True)
+                e.outer_step(coll)
             b.record(stream)
             b.synchronize()
             e.synchronize()
@@ -430,6 +436,12 @@ def measure_window_boundary(D, coll, n, k, prec, local, max_over_ranks, barrier,
         out[name] = {key + "_ms": max_over_ranks(statistics.mean(v)) for key, v in
                      (("boundary", r["ms"]), ("k1", r["k1"]), ("k2", r["k2"]), ("k4", r["k4"]))}
     out["fused_saves_ms"] = out["unfused"]["boundary_ms"] - out["fused"]["boundary_ms"]
+    if k == 1:  # the fused pass is one kernel: 40 B/param (theta_local, g, m, v, theta_t, momentum in; m, v, theta_t, momentum out)
+        peak, kind = measured_peak()
+        ach = 40 * n / (out["fused"]["k1_ms"] * 1e-3) / 1e9
+        out["fused"]["roofline"] = {"kernel": "boundary_solo_kernel (K1+K2+K4)", "bytes_per_param": 40,
+                                    "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                                    "peak_source": kind}
     out.update({"windows_each": windows, "local_steps_h": h,
                 "what": "last inner step (K1) + outer step, CUDA events on the engine stream, variants interleaved; "
                         "k1 / k2 / k4 = summed event-timed phases of that boundary (k4: busy time of the pieces)"})
@@ -659,13 +671,13 @@ def run_ours(args):
     if world == 1 and not args.no_wire:
         line["wire"] = measure_wire(D, eng, n, prec, cpu=not args.no_cpu_baseline)
     eng.close()
-    if k > 1 and not args.no_boundary:
+    if not args.no_boundary:
         line["window_boundary"] = measure_window_boundary(D, coll, n, k, prec, local, max_over_ranks, barrier)
     if not args.no_training:
         line["training_loop"] = measure_training_loop(D, coll, n, k, prec, local, max_over_ranks, barrier)
         if n > 150_000_000:  # the paper's Llama-150M size (configs 2-3): ~0.6 ms inner steps
             line["training_loop_150m"] = measure_training_loop(D, coll, 150_000_000, k, prec, local,
-                                                               max_over_ranks, barrier)
+                                                               max_over_ranks, barrier, rounds=32)
     if rank == 0:
         print(json.dumps(line))
     if coll:

@@ -496,8 +496,14 @@ enum { DLC_PHASE_INNER = 0, DLC_PHASE_PSEUDO = 1, DLC_PHASE_COLLECTIVE = 2, DLC_
 DLC_API int dlc_engine_set_timing(dlc_engine* e, int on);
 DLC_API int dlc_engine_phase_times(dlc_engine* e, double total_ms[4], uint64_t count[4]);
 
-/* K2 fused into the window's last inner step (opt-in, default off; meaningful
- * for num_workers_k > 1).  The inner step that completes a window of H also
+/* One worker (num_workers_k = 1, PINGPONG, solo collective): dlc_optimizer_step
+ * and dlc_run_training run the window's last inner step and the outer step as
+ * ONE fused pass (K1 + K2 + K4, 40 B/param instead of 28 + 20; the outer
+ * step's result is bit-identical, and an overflow on that inner step reruns
+ * the outer step from the unchanged theta_local).  On by default; `on` = 0
+ * runs them as two steps.
+ * num_workers_k > 1: K2 fused into the window's last inner step (opt-in,
+ * default off).  The inner step that completes a window of H also
  * writes delta = theta_t - theta_local' (engine.cpp:115-126, in the reduce
  * precision) into the collective's send buffer, so the outer step starts with
  * the exchange instead of a separate 10-12 B/param K2 pass.  Results are

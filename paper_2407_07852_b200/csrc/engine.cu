@@ -73,6 +73,7 @@ int dlc_engine_create(const dlc_config* cfg, const dlc_hyperparams* hyper, size_
     e->n = n;
     e->k = cfg->num_workers_k;
     e->prec = cfg->reduce_precision;
+    e->fuse_delta = e->k == 1;  // K = 1: the fused window boundary; K > 1: opt-in
     e->S = slot_elems(n, e->k);
     // the collective buffers also fit every smaller fleet a membership change
     // (dlc_collective_shrink) can leave behind
@@ -159,6 +160,11 @@ int dlc_engine_destroy(dlc_engine* e) {
     }
     for (cudaEvent_t ev : e->pool) cudaEventDestroy(ev);
     if (e->tab) cudaFree(e->tab);
+    if (e->ring_host) cudaFreeHost(e->ring_host);
+    for (int i = 0; i < dlc_engine::kRing; ++i) {
+      if (e->ring_a[i]) cudaEventDestroy(e->ring_a[i]);
+      if (e->ring_b[i]) cudaEventDestroy(e->ring_b[i]);
+    }
     if (e->ev0) cudaEventDestroy(e->ev0);
     if (e->ev1) cudaEventDestroy(e->ev1);
     for (cudaEvent_t ev : e->chunk_ev) cudaEventDestroy(ev);
@@ -537,6 +543,11 @@ int dlc_optimizer_step(dlc_engine* e, dlc_collective* c, const float* grad, int 
     if (!e || (e->n && !grad)) fail(DLC_EINVAL, "dlc_optimizer_step: null argument");
     if (c && c->kind == 0) c = nullptr;
     DeviceGuard dg(e->device);
+    if (boundary_solo_ok(e, c)) {  // K = 1: the window's last inner step and the outer step in one pass
+      engine_boundary_solo(e, grad, grad_is_scaled);
+      if (round_completed) *round_completed = 1;
+      return;
+    }
     engine_inner(e, grad, grad_is_scaled);  // engine.cpp:163
     const bool boundary = e->issued_inner % e->cfg.local_steps_h == 0;
     if (round_completed) *round_completed = boundary ? 1 : 0;

@@ -59,7 +59,9 @@ struct dlc_engine {
   float* tab = nullptr;  // corr1 | corr2 | lr, tab_cap entries each
   size_t tab_cap = 0;
   uint64_t issued_inner = 0;  // host mirror of the data cursor (always advances)
-  // K2 fused into the last inner step of a window (K > 1, dlc_engine_set_fused_delta):
+  // K2 fused into the last inner step of a window (dlc_engine_set_fused_delta;
+  // K = 1: the whole solo outer step fused into it by dlc_optimizer_step /
+  // dlc_run_training, on by default; K > 1:
   // delta_fused = that K1 wrote the send buffer and nothing has touched theta_t,
   // theta_local or the send buffer since; the outer step then runs only the gated K2.
   bool fuse_delta = false;
@@ -105,6 +107,11 @@ struct dlc_engine {
   };
   std::vector<TraceMark> trace;  // DLC_TRACE=1: per-op timeline of the P2P step
   std::vector<cudaEvent_t> piece_ev;
+  // dlc_run_training: pinned ring of device-scalar snapshots + per-step events,
+  // made on the first call and kept (no allocation inside a training loop)
+  static constexpr int kRing = 4;
+  dlc::DevState* ring_host = nullptr;
+  cudaEvent_t ring_a[kRing] = {}, ring_b[kRing] = {};
   // wire rounds (dlc_engine_wire_*): fold rows of the owned range, `wire_stride` elements each
   void* wire_rows = nullptr;
   size_t wire_rows_bytes = 0;
@@ -170,6 +177,12 @@ float* live(dlc_engine* e, int which);
 void unalias(dlc_engine* e);
 float* writable(dlc_engine* e, int which);
 void engine_inner(dlc_engine* e, const float* grad, int grad_is_scaled);
+// The window boundary of a single worker as one fused pass (launch_boundary_solo):
+// usable when the next inner step completes a window, K = 1, PINGPONG, and the
+// collective is the solo one.  engine_boundary_solo = that inner step + the
+// outer step (engine.cpp:162-174).
+bool boundary_solo_ok(const dlc_engine* e, const dlc_collective* c);
+void engine_boundary_solo(dlc_engine* e, const float* grad, int grad_is_scaled);
 // The outer step's K2 input: true (and cleared) when the window's last K1 wrote
 // the delta into the send buffer (DevState::delta_ready then tells the device
 // whether it still holds).

@@ -253,7 +253,9 @@ float* writable(dlc_engine* e, int which) {
   return live(e, which);
 }
 
-void engine_inner(dlc_engine* e, const float* grad, int grad_is_scaled) {
+// K1's arguments for the engine's live state; the gradient is scaled on the
+// device first when the caller passes a raw one (engine.cpp:56).
+static AdamWArgs inner_args(dlc_engine* e, const float* grad, int grad_is_scaled) {
   harvest_if_full(e);
   if (e->issued_inner >= e->cfg.total_inner_steps) fail(DLC_EINVAL, "inner_step called after total_inner_steps");
   ensure_tables(e, e->issued_inner + 2);
@@ -282,10 +284,15 @@ void engine_inner(dlc_engine* e, const float* grad, int grad_is_scaled) {
   a.omb1 = 1.0f - e->hyper.beta1;
   a.omb2 = 1.0f - e->hyper.beta2;
   a.pingpong = e->inner_mode == DLC_INNER_PINGPONG;
+  return a;
+}
+
+void engine_inner(dlc_engine* e, const float* grad, int grad_is_scaled) {
+  AdamWArgs a = inner_args(e, grad, grad_is_scaled);
   // fused delta (opt-in): the last step of a window at K > 1 also writes the
   // pseudo-gradient (engine.cpp:115-126) into the send buffer, so the outer
-  // step starts with the exchange; a single worker keeps K2 fused into its
-  // outer step instead
+  // step starts with the exchange; a single worker fuses its whole outer step
+  // into the boundary instead (engine_boundary_solo)
   const bool fuse = e->fuse_delta && e->k > 1 && (e->issued_inner + 1) % e->cfg.local_steps_h == 0;
   a.delta = fuse ? e->send : nullptr;
   a.delta_fp16 = e->prec == DLC_FP16;
@@ -295,6 +302,22 @@ void engine_inner(dlc_engine* e, const float* grad, int grad_is_scaled) {
   launched("adamw");
   e->issued_inner += 1;
   e->delta_fused = fuse;
+}
+
+bool boundary_solo_ok(const dlc_engine* e, const dlc_collective* c) {
+  return e->fuse_delta && e->k == 1 && e->inner_mode == DLC_INNER_PINGPONG && (!c || c->kind == 0) &&
+         (e->issued_inner + 1) % e->cfg.local_steps_h == 0 && e->issued_inner < e->cfg.total_inner_steps;
+}
+
+void engine_boundary_solo(dlc_engine* e, const float* grad, int grad_is_scaled) {
+  const AdamWArgs a = inner_args(e, grad, grad_is_scaled);
+  e->delta_fused = false;
+  DLC_CUDA(cudaMemsetAsync(&e->st->delta_nonfinite, 0, sizeof(int), e->stream));
+  phase_begin(e);
+  launch_boundary_solo(a, tt_pair(e), buf_pair(e), e->prec, e->hyper.outer_lr, e->hyper.outer_momentum, e->stream);
+  phase_end(e, DLC_PHASE_INNER);
+  launched("boundary_solo");
+  e->issued_inner += 1;
 }
 
 

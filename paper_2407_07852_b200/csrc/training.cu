@@ -32,23 +32,18 @@ int dlc_run_training(dlc_engine* e, dlc_collective* c, dlc_grad_producer produce
     if (c && c->kind == 0) c = nullptr;
     DeviceGuard dg(e->device);
     *out = dlc_run_result{};
-    constexpr int kRing = 4;
-    struct Ring {
-      DevState* host = nullptr;
-      cudaEvent_t a[kRing] = {}, b[kRing] = {};
-      ~Ring() {
-        if (host) cudaFreeHost(host);
-        for (int i = 0; i < kRing; ++i) {
-          if (a[i]) cudaEventDestroy(a[i]);
-          if (b[i]) cudaEventDestroy(b[i]);
-        }
+    constexpr int kRing = dlc_engine::kRing;
+    if (!e->ring_host) {
+      DLC_CUDA(cudaMallocHost(&e->ring_host, kRing * sizeof(DevState)));
+      for (int i = 0; i < kRing; ++i) {
+        DLC_CUDA(cudaEventCreate(&e->ring_a[i]));
+        DLC_CUDA(cudaEventCreate(&e->ring_b[i]));
       }
-    } ring;
-    DLC_CUDA(cudaMallocHost(&ring.host, kRing * sizeof(DevState)));
-    for (int i = 0; i < kRing; ++i) {
-      DLC_CUDA(cudaEventCreate(&ring.a[i]));
-      DLC_CUDA(cudaEventCreate(&ring.b[i]));
     }
+    struct {
+      DevState* host;
+      cudaEvent_t *a, *b;
+    } ring{e->ring_host, e->ring_a, e->ring_b};
     struct Pending {
       int slot;
       float loss;
@@ -122,11 +117,16 @@ int dlc_run_training(dlc_engine* e, dlc_collective* c, dlc_grad_producer produce
       if (e->n && !grad) fail(DLC_EINVAL, "run_training: the gradient producer returned no gradient");
       const int slot = (int)(t % kRing);
       DLC_CUDA(cudaEventRecord(ring.a[slot], e->stream));
-      // DilocoOptimizer::step (engine.cpp:162-174)
-      engine_inner(e, grad, grad_is_scaled);
+      // DilocoOptimizer::step (engine.cpp:162-174); a single worker's window
+      // boundary runs as one fused pass (engine_boundary_solo)
+      const bool fused = boundary_solo_ok(e, c);
+      if (fused)
+        engine_boundary_solo(e, grad, grad_is_scaled);
+      else
+        engine_inner(e, grad, grad_is_scaled);
       const bool boundary = e->issued_inner % e->cfg.local_steps_h == 0;
       dlc_reduce_report rep{};
-      if (boundary) {
+      if (boundary && !fused) {
         check_collective(e, c);
         outer_round(e, c, nullptr, &rep);  // records the collective's events for fill_report
       }

@@ -716,3 +716,65 @@ def test_run_training_records_and_state(port):
         e2 = D.DilocoEngine(D.DilocoConfig(h, 1, A.FP16, total), hp, n)
         D.run_training(e2, None, lambda step: 1 / 0)
     e.close()
+
+
+@pytest.mark.parametrize("fused", [True, False])
+@pytest.mark.parametrize("prec", [A.FP16, A.FP32])
+def test_optimizer_step_fused_solo_boundary(port, prec, fused):
+    """DilocoOptimizer::step (engine.cpp:162-174) for one worker: the window's
+    last inner step and the SoloCollective outer step as ONE pass
+    (launch_boundary_solo, the default) or as two steps, bitwise against the
+    oracle over four windows of H = 3: an overflow on a window's last step
+    (round 0: the outer step reruns from the unchanged theta_local), one
+    mid-window (round 1), a non-finite delta (round 2: theta_t / theta_local
+    uploaded at +-3e38 so the delta overflows; the outer step is skipped and
+    theta_local := theta_t), and an ordinary round last.  Ragged N."""
+    n, h, rounds, seed = 70_003, 3, 4, 57
+    hyper = DR.Hyper(inner_lr=1e-3, warmup_steps=2)
+    hp = D.OptimHyperparams(inner_lr=1e-3, warmup_steps=2)
+    theta0 = O.rng_fill(seed, "theta", 0, n, -0.05, 0.05)
+
+    def grad_np(t):
+        g = O.rng_fill(seed, "grad", t, n, -1e-2, 1e-2)
+        if t in (2, 4):
+            g[n - 2] = np.inf
+        return g
+
+    e = D.DilocoEngine(D.DilocoConfig(h, 1, prec, h * rounds), hp, n)
+    e.set_fused_delta(fused)
+    e.upload(A.THETA_T, theta0)
+    e.upload(A.THETA_LOCAL, theta0)
+    gptr = e.device_ptr(A.GRAD)
+    opt = D.DilocoOptimizer(e)
+    (w,) = DR.make_workers(theta0, 1, hyper)
+    t = 0
+    for rnd in range(rounds):
+        if rnd == 2:  # a non-finite delta at this window's end
+            tt = e.download(A.THETA_T)
+            tt[11] = np.float32(3e38)
+            e.upload(A.THETA_T, tt)
+            tl = e.download(A.THETA_LOCAL)
+            tl[11] = np.float32(-3e38)
+            e.upload(A.THETA_LOCAL, tl)
+            w.theta_t, w.theta_local = tt.copy(), tl.copy()
+        if rnd == 3:  # back to an ordinary element
+            tt = e.download(A.THETA_T)
+            tt[11] = np.float32(0.01)
+            e.upload(A.THETA_T, tt)
+            e.upload(A.THETA_LOCAL, tt)
+            w.theta_t, w.theta_local = tt.copy(), tt.copy()
+        for _ in range(h):
+            e.upload(A.GRAD, grad_np(t))
+            opt.step(gptr, grad_is_scaled=False)
+            DR.inner_step(port, w, grad_np(t), hyper)
+            t += 1
+        assert opt.round_just_completed
+        _, applied, _ = DR.outer_round(port, [w], prec, hyper)
+        sc = e.scalars()
+        assert sc.outer_epoch == rnd + 1 and bool(sc.last_applied) == applied, (rnd, applied)
+        assert applied == (rnd != 2)
+        for which, want in ((A.THETA_T, w.theta_t), (A.THETA_LOCAL, w.theta_local), (A.ADAM_M, w.m),
+                            (A.ADAM_V, w.v), (A.MOMENTUM, w.buf)):
+            assert np.array_equal(bits(e.download(which)), bits(want)), (rnd, which)
+        assert sc.step_count == w.step_count
+    e.close()
