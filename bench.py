@@ -441,7 +441,7 @@ def measure_window_boundary(D, coll, n, k, prec, local, max_over_ranks, barrier,
         ach = 40 * n / (out["fused"]["k1_ms"] * 1e-3) / 1e9
         out["fused"]["roofline"] = {"kernel": "boundary_solo_kernel (K1+K2+K4)", "bytes_per_param": 40,
                                     "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                                    "peak_source": kind}
+                                    "peak_source": kind, "traffic": ncu_traffic("boundary_solo_kernel", n)}
     out.update({"windows_each": windows, "local_steps_h": h,
                 "what": "last inner step (K1) + outer step, CUDA events on the engine stream, variants interleaved; "
                         "k1 / k2 / k4 = summed event-timed phases of that boundary (k4: busy time of the pieces)"})
