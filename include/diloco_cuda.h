@@ -210,8 +210,21 @@ DLC_API int dlc_collective_all_reduce_avg(dlc_collective* c, const float* local_
  *   dlc_collective_members  original ranks of the current members, sorted;
  *                           returns the member count.
  *   dlc_collective_set_reduce_timeout_ms
- *                           NodeOptions::reduce_timeout_ms: how long a DLC_MODE_P2P
- *                           barrier waits for a peer (default 20000).
+ *                           NodeOptions::reduce_timeout_ms (default 20000):
+ *                           how long a DLC_MODE_P2P barrier waits for a peer
+ *                           (on the device; the round then fails on every
+ *                           rank with the state unchanged), and how long after
+ *                           it was enqueued an ORDERED / ALLREDUCE round may
+ *                           take before a host wait on the engine (a result,
+ *                           a download, dlc_engine_synchronize) declares it
+ *                           failed: DLC_ECOLLECTIVE "timed out".  NCCL never
+ *                           times out, so that round's device work stays
+ *                           blocked until the survivors call
+ *                           dlc_collective_shrink with DLC_SHRINK_ABORT; it
+ *                           then finishes without changing the engine state
+ *                           (speculative K4, error-gated finish), and the
+ *                           same epoch is retried on the shrunk collective
+ *                           (ReduceReport::attempts = 2).
  *   dlc_collective_inject_stall
  *                           fault injection (SocketCollective::set_stage_hook,
  *                           test_collective.cpp:485-492): this rank stops

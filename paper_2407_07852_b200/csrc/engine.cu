@@ -193,7 +193,7 @@ int dlc_engine_upload(dlc_engine* e, int which, const float* host, size_t n) {
     DeviceGuard dg(e->device);
     float* d = writable(e, which);
     DLC_CUDA(cudaMemcpyAsync(d, host, n * sizeof(float), cudaMemcpyHostToDevice, e->stream));
-    DLC_CUDA(cudaStreamSynchronize(e->stream));
+    stream_wait(e);
   });
 }
 
@@ -204,7 +204,7 @@ int dlc_engine_download(dlc_engine* e, int which, float* host, size_t n) {
     DeviceGuard dg(e->device);
     float* d = live(e, which);
     DLC_CUDA(cudaMemcpyAsync(host, d, n * sizeof(float), cudaMemcpyDeviceToHost, e->stream));
-    DLC_CUDA(cudaStreamSynchronize(e->stream));
+    stream_wait(e);
   });
 }
 
@@ -217,7 +217,7 @@ int dlc_engine_download_range(dlc_engine* e, int which, size_t offset, float* ho
     DeviceGuard dg(e->device);
     const float* d = live(e, which);
     DLC_CUDA(cudaMemcpyAsync(host, d + offset, count * sizeof(float), cudaMemcpyDeviceToHost, e->stream));
-    DLC_CUDA(cudaStreamSynchronize(e->stream));
+    stream_wait(e);
   });
 }
 
@@ -230,7 +230,7 @@ int dlc_engine_upload_range(dlc_engine* e, int which, size_t offset, const float
     DeviceGuard dg(e->device);
     float* d = writable(e, which);
     DLC_CUDA(cudaMemcpyAsync(d + offset, host, count * sizeof(float), cudaMemcpyHostToDevice, e->stream));
-    DLC_CUDA(cudaStreamSynchronize(e->stream));
+    stream_wait(e);
   });
 }
 
@@ -287,7 +287,7 @@ int dlc_engine_synchronize(dlc_engine* e) {
   return guard([&] {
     if (!e) fail(DLC_EINVAL, "dlc_engine_synchronize: null engine");
     DeviceGuard dg(e->device);
-    DLC_CUDA(cudaStreamSynchronize(e->stream));
+    stream_wait(e);
     check_barrier(e);
   });
 }
@@ -435,14 +435,14 @@ int dlc_engine_outer_step_host(dlc_engine* e, dlc_collective* c, const float* ho
       launch_outer_solo_finish(tt_pair(e), local_pair(e), e->st, n, e->stream);
       launched("outer_solo_finish");
     } else {
-      outer_collective(e, c, nullptr);  // ORDERED / ALLREDUCE: K4 in place on theta_t[ocur]
-      DLC_CUDA(cudaMemcpyAsync(host_theta_t, e->theta_t[s0.ocur], n * sizeof(float), cudaMemcpyDeviceToHost,
+      outer_collective(e, c, nullptr);  // ORDERED / ALLREDUCE: K4 speculative into theta_t[ocur ^ 1]
+      DLC_CUDA(cudaMemcpyAsync(host_theta_t, e->theta_t[s0.ocur ^ 1], n * sizeof(float), cudaMemcpyDeviceToHost,
                                e->stream));
     }
     DLC_CUDA(cudaStreamSynchronize(e->h2d));
     DLC_CUDA(cudaStreamSynchronize(e->d2h));
     const DevState s1 = read_state(e);
-    if (e->k == 1 && !s1.last_applied)  // skipped: theta_t did not move
+    if (!s1.last_applied)  // skipped: theta_t did not move
       DLC_CUDA(cudaMemcpy(host_theta_t, e->theta_t[s1.ocur], n * sizeof(float), cudaMemcpyDeviceToHost));
     outer_result(e, result);
   });

@@ -6,6 +6,7 @@
 #pragma once
 
 #include <algorithm>
+#include <chrono>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -94,6 +95,15 @@ struct dlc_engine {
   size_t k_cap = 1;      // collective buffers hold any layout k' <= k_cap (membership changes)
   size_t slot_cap = 0;   // elements per collective buffer: max over k' <= k_cap of k' * S(k')
   uint64_t failed_tries = 0;  // consecutive failed rounds at the current epoch (ReduceReport::attempts - 1)
+  // Failure detector of the NCCL modes (ORDERED / ALLREDUCE, one process per
+  // GPU; NCCL itself never times out): the round's device work is watched
+  // through an event until reduce_timeout_ms after it was enqueued; a host wait
+  // past that deadline declares the round failed (stream_wait).
+  bool watched = false;
+  std::chrono::steady_clock::time_point deadline{};
+  uint64_t watch_ms = 0;
+  cudaEvent_t watch_ev = nullptr;
+  bool nccl_failed = false;  // reported; drained and reset at the next outer step
   std::vector<void*> ipc_opened;
   // host-buffer path: copy streams and per-chunk events
   cudaStream_t h2d = nullptr, d2h = nullptr;
@@ -173,6 +183,15 @@ void trace_end(dlc_engine* e, cudaStream_t s, const char* label, int piece, cuda
 void trace_dump(dlc_engine* e, cudaEvent_t origin);
 void ensure_tables(dlc_engine* e, uint64_t t_max);
 DevState read_state(dlc_engine* e);
+// cudaStreamSynchronize of the engine stream that raises CollectiveError when a
+// watched NCCL round passes its deadline (the stream may then stay blocked
+// until the caller shrinks the collective with DLC_SHRINK_ABORT).
+void stream_wait(dlc_engine* e);
+void watch_round(dlc_engine* e, const dlc_collective* c);
+// The failed round's commit gate: ncclAllReduce(MAX) of the error word, so
+// every rank's finish takes the same decision, then the speculative K4 of
+// the whole vector and the finish (abort = the error word).
+void drain_failed_round(dlc_engine* e);
 float* live(dlc_engine* e, int which);
 void unalias(dlc_engine* e);
 float* writable(dlc_engine* e, int which);

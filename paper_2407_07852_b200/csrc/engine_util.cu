@@ -11,6 +11,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "engine_impl.hpp"
@@ -102,7 +103,7 @@ void ensure_chunk_events(dlc_engine* e, size_t count) {
 
 void harvest(dlc_engine* e) {
   if (e->pending.empty()) return;
-  DLC_CUDA(cudaStreamSynchronize(e->stream));
+  stream_wait(e);
   for (const auto& mk : e->pending) {
     float ms = 0.0f;
     DLC_CUDA(cudaEventElapsedTime(&ms, mk.a, mk.b));
@@ -204,15 +205,59 @@ void ensure_tables(dlc_engine* e, uint64_t t_max) {
   float* fresh = nullptr;
   DLC_CUDA(cudaMalloc(&fresh, 3 * cap * sizeof(float)));
   DLC_CUDA(cudaMemcpyAsync(fresh, h.data(), 3 * cap * sizeof(float), cudaMemcpyHostToDevice, e->stream));
-  DLC_CUDA(cudaStreamSynchronize(e->stream));  // in-flight K1 launches still read the old table
+  stream_wait(e);  // in-flight K1 launches still read the old table
   if (e->tab) cudaFree(e->tab);
   e->tab = fresh;
   e->tab_cap = cap;
 }
 
+void watch_round(dlc_engine* e, const dlc_collective* c) {
+  if (!e->watch_ev) DLC_CUDA(cudaEventCreateWithFlags(&e->watch_ev, cudaEventDisableTiming));
+  DLC_CUDA(cudaEventRecord(e->watch_ev, e->stream));
+  e->watched = true;
+  e->watch_ms = c->timeout_ms;
+  e->deadline = std::chrono::steady_clock::now() + std::chrono::milliseconds(c->timeout_ms);
+}
+
+void stream_wait(dlc_engine* e) {
+  while (e->watched) {
+    const cudaError_t q = cudaEventQuery(e->watch_ev);
+    if (q == cudaSuccess) {
+      e->watched = false;
+      break;
+    }
+    if (q != cudaErrorNotReady) check_cuda(q, "cudaEventQuery (watched NCCL round)");
+    if (std::chrono::steady_clock::now() > e->deadline) {
+      // a peer stopped participating: mark the round failed on the device (a
+      // side stream; the engine stream is blocked inside NCCL), so its commit
+      // gate changes nothing once the caller's shrink with DLC_SHRINK_ABORT
+      // releases it (collective.cpp:1368-1440 restarts over the survivors)
+      e->watched = false;
+      e->nccl_failed = true;
+      e->failed_tries += 1;
+      ensure_copy_streams(e);
+      DLC_CUDA(cudaMemsetAsync(e->sig_err, 1, 1, e->h2d));
+      DLC_CUDA(cudaStreamSynchronize(e->h2d));
+      fail(DLC_ECOLLECTIVE, "outer round timed out after " + std::to_string(e->watch_ms) +
+                                " ms: a peer rank stopped participating; the state is unchanged once the round is "
+                                "released: shrink the collective with DLC_SHRINK_ABORT and retry");
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+  DLC_CUDA(cudaStreamSynchronize(e->stream));
+}
+
+void drain_failed_round(dlc_engine* e) {
+  if (!e->nccl_failed) return;
+  DLC_CUDA(cudaStreamSynchronize(e->stream));
+  if (e->cstream) DLC_CUDA(cudaStreamSynchronize(e->cstream));
+  DLC_CUDA(cudaMemset(e->sig_err, 0, sizeof(int)));
+  e->nccl_failed = false;
+}
+
 DevState read_state(dlc_engine* e) {
   DevState s;
-  DLC_CUDA(cudaStreamSynchronize(e->stream));
+  stream_wait(e);
   DLC_CUDA(cudaMemcpy(&s, e->st, sizeof(DevState), cudaMemcpyDeviceToHost));
   return s;
 }
@@ -367,6 +412,7 @@ void fill_report(dlc_engine* e, dlc_collective* c, dlc_reduce_report* rep, uint6
     rep->data_bytes_sent = dlc_per_peer_reduce_bytes(e->n, e->k, (size_t)rank, e->prec);
     rep->data_bytes_received = per_peer_reduce_bytes_received(e->n, e->k, (size_t)rank, e->prec);
     rep->wire_bytes_sent = rep->wire_bytes_received = 2ull * (e->k - 1) * e->S * elem_width(e->prec);
+    stream_wait(e);  // raises when a watched NCCL round timed out (its events never complete)
     DLC_CUDA(cudaEventSynchronize(e->ev1));
     float ms = 0;
     DLC_CUDA(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
@@ -398,7 +444,7 @@ void relayout(dlc_engine* e, size_t k) {
   if (k == e->k) return;
   if (k < 1 || k > e->k_cap) fail(DLC_ECOLLECTIVE, "membership of " + std::to_string(k) + " workers exceeds the " +
                                                        std::to_string(e->k_cap) + " this engine was made for");
-  DLC_CUDA(cudaStreamSynchronize(e->stream));
+  stream_wait(e);
   if (e->cstream) DLC_CUDA(cudaStreamSynchronize(e->cstream));
   p2p_unbind(e);
   e->delta_fused = false;
@@ -413,6 +459,7 @@ void relayout(dlc_engine* e, size_t k) {
 }
 
 void check_collective(dlc_engine* e, dlc_collective* c) {
+  drain_failed_round(e);  // a timed-out NCCL round, released by the caller's shrink
   const size_t world = c ? (size_t)c->world : 1;
   if (world != e->k && c && c->shrunk && c->kind == 1 && world <= e->k_cap &&
       e->issued_inner % e->cfg.local_steps_h == 0)
@@ -433,9 +480,9 @@ void check_collective(dlc_engine* e, dlc_collective* c) {
 // (collective.cpp:1369-1440).  The barrier epochs of the failed round are
 // abandoned: the next bind (over the new communicator) agrees on fresh ones.
 void check_barrier(dlc_engine* e) {
-  if (!e->sig_err) return;
+  if (!e->sig_err || e->nccl_failed) return;  // (a timed-out NCCL round was reported already)
   int err = 0;
-  DLC_CUDA(cudaStreamSynchronize(e->stream));
+  stream_wait(e);
   if (e->cstream) DLC_CUDA(cudaStreamSynchronize(e->cstream));
   DLC_CUDA(cudaMemcpy(&err, e->sig_err, sizeof(int), cudaMemcpyDeviceToHost));
   if (!err) return;
@@ -444,9 +491,9 @@ void check_barrier(dlc_engine* e) {
   p2p_unbind(e);
   e->failed_tries += 1;
   if (e->inner_mode != DLC_INNER_PINGPONG)
-    fail(DLC_ECOLLECTIVE, "P2P barrier timed out: a peer rank stopped participating (DLC_INNER_INPLACE: theta_local "
+    fail(DLC_ECOLLECTIVE, "outer round failed: a peer rank stopped participating (DLC_INNER_INPLACE: theta_local "
                           "was overwritten, restore it before retrying)");
-  fail(DLC_ECOLLECTIVE, "P2P barrier timed out: a peer rank stopped participating; state unchanged, shrink the "
+  fail(DLC_ECOLLECTIVE, "outer round failed: a peer rank stopped participating; state unchanged, shrink the "
                         "collective and retry");
 }
 

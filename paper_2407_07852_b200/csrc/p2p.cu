@@ -112,6 +112,31 @@ void p2p_barrier(dlc_engine* e, dlc_collective* c, cudaStream_t s, bool commit) 
   launched("flag_barrier");
 }
 
+// The end of an NCCL-mode round (ORDERED / ALLREDUCE, one process per GPU):
+// the ranks' error words are OR-ed (ncclAllReduce MAX) so every finish gate
+// takes the same decision, K4 runs speculatively into the idle theta_t /
+// momentum over `nslots` mean slots (`slots`, `S` elements apart) and the finish
+// flips them in only when every mark is clean and no rank's round failed; the
+// round is watched by the NCCL-mode failure detector (stream_wait).
+static void nccl_round_commit(dlc_engine* e, dlc_collective* c, const PtrList& slots, int nslots, size_t S,
+                              const PtrList& marks, int nmarks, cudaStream_t err_stream) {
+  DLC_NCCL(ncclAllReduce(e->sig_err, e->sig_err, 1, ncclInt32, ncclMax, c->comm, err_stream));
+  if (err_stream != e->stream) {
+    cudaEvent_t ev = pooled_event(e);
+    DLC_CUDA(cudaEventRecord(ev, err_stream));
+    DLC_CUDA(cudaStreamWaitEvent(e->stream, ev, 0));
+    e->pool.push_back(ev);
+  }
+  phase_begin(e);
+  if (nslots > 0)
+    launch_nesterov_p2p_piece(tt_pair(e), buf_pair(e), local_pair(e), slots, nslots, S, 0, nslots > 1 ? S : e->n,
+                              e->prec, e->st, e->hyper.outer_lr, e->hyper.outer_momentum, e->n, 0, e->stream);
+  launch_p2p_finish(tt_pair(e), local_pair(e), marks, nmarks, e->st, e->n, e->sig_err, e->stream);
+  phase_end(e, DLC_PHASE_OUTER);
+  launched("nesterov_p2p_piece");
+  if (c->kind == 1 && !c->in_world) watch_round(e, c);
+}
+
 // C1 + K3 on the engine's send buffer, then K4.  Everything is enqueued on the
 // engine stream; NCCL calls are stream-ordered with the kernels around them.
 void outer_collective(dlc_engine* e, dlc_collective* c, dlc_reduce_report* rep) {
@@ -124,6 +149,7 @@ void outer_collective(dlc_engine* e, dlc_collective* c, dlc_reduce_report* rep) 
   const int r = c->rank;
   if (rep) DLC_CUDA(cudaEventRecord(e->ev0, e->stream));
   phase_begin(e);
+  PtrList slots{}, marks{};
   if (c->mode == DLC_MODE_ORDERED) {
     char* recv = static_cast<char*>(e->recv);
     char* gather = static_cast<char*>(e->gather);
@@ -147,7 +173,11 @@ void outer_collective(dlc_engine* e, dlc_collective* c, dlc_reduce_report* rep) 
     DLC_NCCL(ncclGroupEnd());
     phase_end(e, DLC_PHASE_COLLECTIVE);
     if (rep) DLC_CUDA(cudaEventRecord(e->ev1, e->stream));
-    nesterov(e, e->gather, e->flags, (int)K);
+    for (size_t q = 0; q < K; ++q) {
+      slots.ptr[q] = gather + q * S * w;
+      marks.ptr[q] = e->flags + q;
+    }
+    nccl_round_commit(e, c, slots, (int)K, S, marks, (int)K, e->stream);
   } else {
     DLC_NCCL(ncclAllReduce(send, send, K * S, nccl_type(e->prec), ncclAvg, c->comm, e->stream));
     if (e->prec == DLC_FP16)
@@ -157,7 +187,9 @@ void outer_collective(dlc_engine* e, dlc_collective* c, dlc_reduce_report* rep) 
     launched("nonfinite");
     phase_end(e, DLC_PHASE_COLLECTIVE);
     if (rep) DLC_CUDA(cudaEventRecord(e->ev1, e->stream));
-    nesterov(e, e->send, e->flags, 1);
+    slots.ptr[0] = send;
+    marks.ptr[0] = e->flags;
+    nccl_round_commit(e, c, slots, 1, 0, marks, 1, e->stream);
   }
 }
 
@@ -489,15 +521,23 @@ void outer_allreduce_pipelined(dlc_engine* e, dlc_collective* c, const float* sr
   PtrList slots{}, fl{};
   slots.ptr[0] = send;
   fl.ptr[0] = e->flags;
+  // the commit gate's error OR on the comm stream after the last piece, then
+  // K4 of every piece as its mean lands, the finish and the watch
+  DLC_NCCL(ncclAllReduce(e->sig_err, e->sig_err, 1, ncclInt32, ncclMax, c->comm, e->cstream));
+  cudaEvent_t evErr = pooled_event(e);
+  DLC_CUDA(cudaEventRecord(evErr, e->cstream));
   phase_begin(e);
   for (size_t p = 0; p < P; ++p) {
     DLC_CUDA(cudaStreamWaitEvent(e->stream, evB[p], 0));
     launch_nesterov_p2p_piece(tt_pair(e), buf_pair(e), local_pair(e), slots, 1, 0, pb[p], pb[p + 1] - pb[p],
                               e->prec, e->st, e->hyper.outer_lr, e->hyper.outer_momentum, n, 0, e->stream);
   }
-  launch_p2p_finish(tt_pair(e), local_pair(e), fl, 1, e->st, n, nullptr, e->stream);
+  DLC_CUDA(cudaStreamWaitEvent(e->stream, evErr, 0));
+  e->pool.push_back(evErr);
+  launch_p2p_finish(tt_pair(e), local_pair(e), fl, 1, e->st, n, e->sig_err, e->stream);
   phase_end(e, DLC_PHASE_OUTER);
   launched("nesterov_p2p_piece");
+  if (!c->in_world) watch_round(e, c);
 }
 
 void outer_round(dlc_engine* e, dlc_collective* c, const float* src, dlc_reduce_report* rep) {

@@ -51,6 +51,7 @@ int dlc_run_training(dlc_engine* e, dlc_collective* c, dlc_grad_producer produce
     };
     std::deque<Pending> pending;
     auto emit = [&](const Pending& p) {
+      if (p.boundary && e->k > 1) stream_wait(e);  // a timed-out NCCL round raises instead of blocking
       DLC_CUDA(cudaEventSynchronize(ring.b[p.slot]));
       const DevState s = ring.host[p.slot];
       float step_ms = 0.0f;

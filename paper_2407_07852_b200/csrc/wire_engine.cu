@@ -40,7 +40,7 @@ uint64_t row_stride(uint64_t capacity) { return (capacity + 7) / 8 * 8; }
 char* wire_rows(dlc_engine* e, size_t rows) {
   const size_t need = std::max<size_t>(rows * row_stride(e->wire_stride) * elem_width(e->prec), 256);
   if (need > e->wire_rows_bytes) {
-    DLC_CUDA(cudaStreamSynchronize(e->stream));
+    stream_wait(e);
     void* fresh = nullptr;
     DLC_CUDA(cudaMalloc(&fresh, need));
     if (e->wire_rows) {
@@ -140,7 +140,7 @@ int dlc_engine_wire_fold(dlc_engine* e, int rank, int k, uint64_t offset, uint64
       launched("fold");
       if (!aligned) DLC_CUDA(cudaMemcpyAsync(out, dst, length * w, cudaMemcpyDeviceToDevice, e->stream));
     }
-    DLC_CUDA(cudaStreamSynchronize(e->stream));
+    stream_wait(e);
   });
 }
 

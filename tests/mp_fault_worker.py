@@ -15,7 +15,14 @@ mean" (test_collective.cpp:460-531) on the device path:
 * DLC_MODE_ORDERED / DLC_MODE_ALLREDUCE: a planned exclusion after a full
   round; survivors run the next round on the shrunk NCCL communicator
   (ordered bitwise, allreduce within SPEC.md:325's tolerance).
+* DLC_MODE_ORDERED / DLC_MODE_ALLREDUCE with a stalled peer (round 2): the
+  victim never enters the round; NCCL does not time out, so the engine's
+  failure detector does (reduce_timeout_ms after the round was enqueued): the
+  survivors' outer step raises CollectiveError, they shrink with
+  DLC_SHRINK_ABORT (which releases their blocked NCCL work), find the engine
+  state unchanged, and retry the same epoch over the survivors (attempts = 2).
 """
+import time
 import json
 import os
 import sys
@@ -73,7 +80,8 @@ def main():
         return O.rng_fill(77, "grad", w * 1000 + t, n, -1e-2, 1e-2)
 
     cases = [("p2p-stall", D.MODE_P2P, D.FP16), ("p2p-stall", D.MODE_P2P, D.FP32),
-             ("ordered-planned", D.MODE_ORDERED, D.FP16), ("allreduce-planned", D.MODE_ALLREDUCE, D.FP32)]
+             ("ordered-planned", D.MODE_ORDERED, D.FP16), ("allreduce-planned", D.MODE_ALLREDUCE, D.FP32),
+             ("ordered-stall", D.MODE_ORDERED, D.FP32), ("allreduce-stall", D.MODE_ALLREDUCE, D.FP16)]
     for name, mode, prec in cases:
         tag = f"{name}/{'fp16' if prec else 'fp32'}"
         coll = PD.make_nccl_collective(r, mode)
@@ -100,8 +108,38 @@ def main():
         DR.outer_round(port, ws, prec, hyper)
         assert res.applied and res.report.contributors == k and res.report.attempts == 1, tag
         close(e, ws[r.rank], mode, (tag, "round 1"))
-        inner(list(range(k)) if mode == D.MODE_P2P else survivors)
+        stall = name.endswith("stall")
+        inner(list(range(k)) if stall else survivors)
 
+        if stall and mode != D.MODE_P2P:
+            # round 2: the victim never arrives; the survivors' round times out
+            if not me_alive:
+                time.sleep(4.0)  # past the survivors' 1.5 s deadline: it stopped participating
+            else:
+                before = state(e)
+                epoch0 = e.scalars().outer_epoch
+                t0 = time.time()
+                try:
+                    e.outer_step(coll, wait=True, report=True)
+                    raise AssertionError(f"{tag}: the round with a stalled peer succeeded")
+                except D.CollectiveError as x:
+                    assert "timed out" in str(x), (tag, str(x))
+                assert time.time() - t0 < 15.0, tag
+                sub = coll.shrink([victim], quorum_min=k - 1, abort=True)  # releases the blocked round
+                assert e.scalars().outer_epoch == epoch0, tag
+                assert same(state(e), before), (tag, "a failed round changed the engine state")
+                out["checks"].append(f"{tag}: timed-out round leaves state unchanged")
+                res = e.outer_step(sub, wait=True, report=True)
+                sw = [ws[j] for j in survivors]
+                DR.outer_round(port, sw, prec, hyper)
+                assert res.applied and res.report.contributors == k - 1 and res.report.attempts == 2, (
+                    tag, res.report.attempts)
+                close(e, ws[r.rank], mode, (tag, "survivor retry"))
+                out["checks"].append(f"{tag}: survivors {survivors} after the timeout")
+                e.close()
+                sub.close()
+                coll.close()
+                continue
         if mode == D.MODE_P2P:
             # round 2: the victim stops arriving after its first barrier (mid-reduce)
             before = state(e)
