@@ -251,7 +251,7 @@ void drain_failed_round(dlc_engine* e) {
   if (!e->nccl_failed) return;
   DLC_CUDA(cudaStreamSynchronize(e->stream));
   if (e->cstream) DLC_CUDA(cudaStreamSynchronize(e->cstream));
-  DLC_CUDA(cudaMemset(e->sig_err, 0, sizeof(int)));
+  DLC_CUDA(cudaMemset(e->sig_err, 0, 2 * sizeof(int)));
   e->nccl_failed = false;
 }
 

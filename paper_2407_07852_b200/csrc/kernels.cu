@@ -190,4 +190,10 @@ void launch_copy(const float* src, float* dst, size_t n, cudaStream_t s) {
   copy_kernel<<<grid_window<1>(n / 4), kThreads, 0, s>>>(src, dst, n);
 }
 
+namespace {
+__global__ void or_word_kernel(int* dst, const int* src) { *dst |= *src; }
+}  // namespace
+
+void launch_or_word(int* dst, const int* src, cudaStream_t s) { or_word_kernel<<<1, 1, 0, s>>>(dst, src); }
+
 }  // namespace dlc

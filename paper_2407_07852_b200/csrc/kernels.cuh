@@ -225,5 +225,7 @@ void launch_rng_perturb(const float* theta_t, uint64_t key, float lo, float hi, 
 // codes for the consecutive FP32 bit patterns [start, start + n)
 void launch_encode_bits_range(uint32_t start, uint16_t* out, size_t n, cudaStream_t s);
 void launch_copy(const float* src, float* dst, size_t n, cudaStream_t s);
+// *dst |= *src (one thread)
+void launch_or_word(int* dst, const int* src, cudaStream_t s);
 
 }  // namespace dlc

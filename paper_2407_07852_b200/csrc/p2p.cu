@@ -118,9 +118,18 @@ void p2p_barrier(dlc_engine* e, dlc_collective* c, cudaStream_t s, bool commit) 
 // momentum over `nslots` mean slots (`slots`, `S` elements apart) and the finish
 // flips them in only when every mark is clean and no rank's round failed; the
 // round is watched by the NCCL-mode failure detector (stream_wait).
+// The OR lands in a second word (sig_err[1]) and is folded into the local one
+// after the all-reduce: a round released by an abort leaves that buffer
+// undefined, and the local word (set by the failure detector) must survive.
+static void nccl_error_or(dlc_engine* e, dlc_collective* c, cudaStream_t s) {
+  DLC_NCCL(ncclAllReduce(e->sig_err, e->sig_err + 1, 1, ncclInt32, ncclMax, c->comm, s));
+  launch_or_word(e->sig_err, e->sig_err + 1, s);
+  launched("or_word");
+}
+
 static void nccl_round_commit(dlc_engine* e, dlc_collective* c, const PtrList& slots, int nslots, size_t S,
                               const PtrList& marks, int nmarks, cudaStream_t err_stream) {
-  DLC_NCCL(ncclAllReduce(e->sig_err, e->sig_err, 1, ncclInt32, ncclMax, c->comm, err_stream));
+  nccl_error_or(e, c, err_stream);
   if (err_stream != e->stream) {
     cudaEvent_t ev = pooled_event(e);
     DLC_CUDA(cudaEventRecord(ev, err_stream));
@@ -523,7 +532,7 @@ void outer_allreduce_pipelined(dlc_engine* e, dlc_collective* c, const float* sr
   fl.ptr[0] = e->flags;
   // the commit gate's error OR on the comm stream after the last piece, then
   // K4 of every piece as its mean lands, the finish and the watch
-  DLC_NCCL(ncclAllReduce(e->sig_err, e->sig_err, 1, ncclInt32, ncclMax, c->comm, e->cstream));
+  nccl_error_or(e, c, e->cstream);
   cudaEvent_t evErr = pooled_event(e);
   DLC_CUDA(cudaEventRecord(evErr, e->cstream));
   phase_begin(e);
