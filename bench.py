@@ -88,6 +88,40 @@ def ncu_traffic(kernel_prefix: str, n: int, launches: int = 1):
     return None
 
 
+def nvlink_from_profile(k, n, fp16):
+    """The owner fold's NVLink bytes per step from the committed ncu capture of a
+    one-process world (profiles/r2_ncu_nvlink_fold_world.json: every fold launch
+    with nvl{rx,tx}__bytes{,_data_user}.sum, the kernels serialised by ncu), when
+    it was taken at this K and size: per GPU and step, its own fold's pulls and
+    pushes, counted twice for the peers' folds that read from and write into it."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r2_ncu_nvlink_fold_world.json")) as f:
+            d = json.load(f)
+    except Exception:
+        return None
+    launches = d.get(f"k{k}")
+    if not launches or n != 1_100_000_000 or not fp16:
+        return None
+    dev0 = [x for x in launches if x["device"] == 0]
+    w = [1, 1, 2, 2, 1, 1]  # the default piece plan at this size: one step's fold launches per GPU
+    step = dev0[:len(w)]
+    if not step:
+        return None
+    scale = sum(w) / sum(w[:len(step)])  # a capture cut short (ncu -c) covers the first pieces only
+    user_rx = scale * sum(x["nvl_rx_user_bytes"] for x in step)
+    user_tx = scale * sum(x["nvl_tx_user_bytes"] for x in step)
+    link_tx = scale * sum(x["nvl_tx_bytes"] for x in step)
+    alone_ms = scale * sum(x["ms"] for x in step)
+    return {"source": "profiles/r2_ncu_nvlink_fold_world.json (ncu, fold launches of GPU 0, one step)",
+            "pieces_captured": len(step),
+            "own_fold_user_bytes_rx": user_rx, "own_fold_user_bytes_tx": user_tx,
+            "user_bytes_per_direction_per_step": user_rx + user_tx,
+            "algorithmic_bytes_per_direction": 2 * (k - 1) * (-(-n // k)) * 2,
+            "own_fold_link_bytes_tx": link_tx, "fold_alone_ms": alone_ms,
+            "fold_alone_user_gbs_per_direction": user_rx / (alone_ms * 1e-3) / 1e9,
+            "fold_alone_link_tx_gbs": link_tx / (alone_ms * 1e-3) / 1e9}
+
+
 def measured_peak():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -618,6 +652,8 @@ def run_ours(args):
         key = "exchange_gbs_per_direction_over_collective" if mode == D.MODE_P2P else "nccl_bus_gbs"
         line[key] = wire_bytes / (coll_ms * 1e-3) / 1e9 if coll_ms else None
         line["nvlink_counters"] = nvl_res  # per rank, measured by each GPU itself
+        if mode == D.MODE_P2P:
+            line["nvlink_ncu"] = nvlink_from_profile(k, n, prec == D.FP16)
     ir = roof(b_k1, k1_ms)
     ir["kernel"] = "adamw_kernel (K1, %s)" % args.inner_mode
     ir["traffic"] = ncu_traffic("adamw_kernel", n)
