@@ -302,6 +302,43 @@ class DeviceEngine {
   dlc_engine* e_ = nullptr;
 };
 
+/// DilocoOptimizer (engine.hpp:122-140, engine.cpp:162-174) on a DeviceEngine:
+/// step() runs one inner step and, after every H-th, the outer round; for a
+/// single worker the window's last inner step and the outer step run as one
+/// fused pass (dlc_optimizer_step).  The producer (task.cpp) stays with the
+/// caller, so step() takes the raw gradient of one batch instead of a Batch.
+class DeviceOptimizer {
+ public:
+  explicit DeviceOptimizer(DeviceEngine& engine, NcclCollective* collective = nullptr)
+      : engine_(engine), collective_(collective) {
+    throw_status(dlc_engine_device_ptr(engine_.handle(), DLC_GRAD, &grad_));
+  }
+
+  /// InnerStepResult's lr and overflow_skipped (engine.hpp:58-62).
+  dlc_inner_result step(const ParamVector& grad) {
+    throw_status(dlc_engine_upload(engine_.handle(), DLC_GRAD, grad.values().data(), grad.size()));
+    int done = 0;
+    throw_status(dlc_optimizer_step(engine_.handle(), collective_ ? collective_->handle() : nullptr, grad_, 0, &done));
+    const dlc_engine_scalars s = engine_.scalars();
+    round_completed_ = done != 0;
+    if (round_completed_) last_applied_ = s.last_applied != 0;
+    dlc_inner_result r{};
+    r.lr = s.last_lr;
+    r.overflow_skipped = s.last_overflow;
+    return r;
+  }
+  void zero_grad() {}
+  bool round_just_completed() const { return round_completed_; }
+  bool last_round_applied() const { return last_applied_; }
+
+ private:
+  DeviceEngine& engine_;
+  NcclCollective* collective_ = nullptr;
+  float* grad_ = nullptr;
+  bool round_completed_ = false;
+  bool last_applied_ = false;
+};
+
 /// One sample of the gradient producer (task.cpp's loss_and_grad, out of
 /// scope here): a DEVICE gradient on the engine's device and its loss.
 struct GradSample {

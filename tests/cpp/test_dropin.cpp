@@ -183,6 +183,58 @@ int main() {
     const dlc_engine_scalars s = eng.scalars();
     CHECK(s.step_count == adam.step_count && s.scale == scaler.scale && s.overflow_skips == 1);
   }
+  // DeviceOptimizer (DilocoOptimizer::step, engine.cpp:162-174): one worker's
+  // window boundary as one fused pass, against the same reference sequence,
+  // with overflows on a window's last step (the gated rerun) and mid-window
+  for (Precision prec : {Precision::fp32, Precision::fp16}) {
+    const ParamVector theta0 = random_vec(layout, 9, "theta", -0.05f, 0.05f);
+    dlc_config cfg{3, 1, cuda::to_c(prec), 9};
+    dlc_hyperparams hp;
+    dlc_hyperparams_default(&hp);
+    hp.warmup_steps = 2;
+    cuda::DeviceEngine eng(cfg, hp, theta0, 0);
+    cuda::DeviceOptimizer opt(eng);
+    ParamVector theta_t = theta0, theta_local = theta0;
+    AdamWState adam = AdamWState::init(layout, hp.beta1, hp.beta2, hp.adam_eps, hp.weight_decay);
+    NesterovState outer = NesterovState::init(layout, hp.outer_lr, hp.outer_momentum);
+    LossScaler scaler;
+    LrSchedule sched;
+    sched.warmup_steps = hp.warmup_steps;
+    sched.total_steps = cfg.total_inner_steps;
+    sched.base_lr = hp.inner_lr;
+    SoloCollective solo;
+    for (int round = 0; round < 3; ++round) {
+      for (int t = 0; t < 3; ++t) {
+        ParamVector g = random_vec(layout, 2000 + round * 10 + t, "grad", -1e-2f, 1e-2f);
+        if ((round == 0 && t == 2) || (round == 1 && t == 0)) {
+          std::vector<float> d(g.values().begin(), g.values().end());
+          d[5] = INFINITY;
+          g = ParamVector(layout, d);
+        }
+        std::vector<float> scaled(n);
+        for (size_t i = 0; i < n; ++i) scaled[i] = g.values()[i] * scaler.scale;  // engine.cpp:20-27
+        const UnscaleResult un = scaler_unscale_and_check(scaler, ParamVector(layout, scaled));
+        if (!un.overflow) theta_local = adamw_step(adam, theta_local, un.grad, lr_at(sched, adam.step_count + 1));
+        scaler_update(scaler, un.overflow);
+        const dlc_inner_result r = opt.step(g);
+        CHECK((r.overflow_skipped != 0) == un.overflow);
+        CHECK(opt.round_just_completed() == (t == 2));
+      }
+      PseudoGradient pg;
+      pg.delta = axpy(-1.0f, theta_local, theta_t);
+      pg.precision = prec;
+      const PseudoGradient red = solo.all_reduce_avg(pg, nullptr);
+      const bool applied = red.delta.all_finite();
+      if (applied) theta_t = nesterov_step(outer, theta_t, red.delta);
+      theta_local = theta_t;
+      CHECK(opt.last_round_applied() == applied);
+      CHECK(eng.download(DLC_THETA_T) == theta_t && eng.download(DLC_THETA_LOCAL) == theta_local);
+    }
+    CHECK(eng.download(DLC_ADAM_M) == adam.m && eng.download(DLC_ADAM_V) == adam.v);
+    CHECK(eng.download(DLC_MOMENTUM) == outer.momentum_buf);
+    const dlc_engine_scalars s = eng.scalars();
+    CHECK(s.step_count == adam.step_count && s.scale == scaler.scale && s.overflow_skips == 2 && s.outer_epoch == 3);
+  }
   // DeviceEngine's outer round through the reference's own Collective class
   // (SoloCollective here; SocketCollective plugs in the same way across boxes),
   // with an epoch-guard violation and a non-finite skip.
