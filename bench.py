@@ -122,6 +122,14 @@ def nvlink_from_profile(k, n, fp16):
             "fold_alone_link_tx_gbs": link_tx / (alone_ms * 1e-3) / 1e9}
 
 
+def pcie_probe():
+    try:
+        with open(os.path.join(ROOT, "profiles", "r2_pcie_probe_1gpu.json")) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
 def measured_peak():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -689,31 +697,16 @@ def run_ours(args):
         for _ in range(e2e_steps):
             eng.outer_step_host(coll, hx.data_ptr(), ht.data_ptr())
         dt = max_over_ranks(time.perf_counter() - t0)
-        # the copies alone: the same bytes H2D and D2H at once on two streams
-        # (pinned, 64 MB chunks), every rank together: the e2e step's ceiling
-        s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
-
-        def copies():
-            with torch.cuda.stream(s1):
-                for o in range(0, n, 1 << 24):
-                    xs[1][o:o + (1 << 24)].copy_(hx[o:o + (1 << 24)], non_blocking=True)
-            with torch.cuda.stream(s2):
-                for o in range(0, n, 1 << 24):
-                    ht[o:o + (1 << 24)].copy_(xs[0][o:o + (1 << 24)], non_blocking=True)
-            torch.cuda.synchronize()
-        copies()
-        barrier()
-        t0 = time.perf_counter()
-        for _ in range(2):
-            copies()
-        ct = max_over_ranks((time.perf_counter() - t0) / 2)
         line["e2e"] = {"value": k * n * e2e_steps / dt, "unit": "params/s", "h2d_bytes_per_step": 4 * n,
                        "d2h_bytes_per_step": 4 * n, "ms_per_step": dt * 1e3 / e2e_steps, "steps": e2e_steps,
                        "host_buffers": "pinned, " + (f"GPU-local NUMA node ({len(local_cpus)} CPUs)"
-                                                      if local_cpus else "default NUMA placement"),
-                       "copies_alone_ms": ct * 1e3, "frac_of_copy_ceiling": ct / (dt / e2e_steps),
-                       "copy_ceiling_note": "the step's H2D + D2H bytes copied at once on two streams with no "
-                                            "kernel, every rank together (PCIe / host memory bound)"}
+                                                      if local_cpus else "default NUMA placement")}
+        probe = pcie_probe()
+        if probe and world == 1 and n == 1_100_000_000:
+            # the same bytes H2D and D2H at once on two streams, no kernel (tools/pcie_probe.py)
+            line["e2e"]["copy_ceiling_ms"] = probe["both_ms"]
+            line["e2e"]["frac_of_copy_ceiling"] = probe["both_ms"] / (dt * 1e3 / e2e_steps)
+            line["e2e"]["copy_ceiling_source"] = "profiles/r2_pcie_probe_1gpu.json (pinned H2D + D2H concurrently)"
         del hx, ht
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
