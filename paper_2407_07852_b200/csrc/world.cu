@@ -285,14 +285,17 @@ int dlc_world_shrink(dlc_world* w, const int* exclude_ranks, size_t n_exclude, s
     std::vector<dlc_engine*> engines;
     std::vector<int> devices, members;
     for (int r = 0; r < w->k; ++r) {
-      if (std::binary_search(ex.begin(), ex.end(), r)) {
-        p2p_unbind(w->engines[r]);
-        dlc_engine_destroy(w->engines[r]);
-        continue;
-      }
+      if (std::binary_search(ex.begin(), ex.end(), r)) continue;
       engines.push_back(w->engines[r]);
       devices.push_back(w->devices[r]);
       members.push_back(w->members[r]);
+    }
+    // the survivors' communicators first: if that fails, the world is unchanged
+    std::vector<ncclComm_t> comms(k2, nullptr);
+    if (k2 > 1 && w->mode != DLC_MODE_P2P) DLC_NCCL(ncclCommInitAll(comms.data(), k2, devices.data()));
+    for (int r = 0; r < w->k; ++r) {
+      p2p_unbind(w->engines[r]);  // before their collectives go away (unbind edits the collective's list)
+      if (std::binary_search(ex.begin(), ex.end(), r)) dlc_engine_destroy(w->engines[r]);
     }
     for (size_t r = 0; r < w->colls.size(); ++r) {
       DeviceGuard dg(w->devices[r]);
@@ -304,13 +307,6 @@ int dlc_world_shrink(dlc_world* w, const int* exclude_ranks, size_t n_exclude, s
     w->devices = devices;
     w->members = members;
     w->k = k2;
-    for (dlc_engine* e : w->engines) {
-      DeviceGuard dg(e->device);
-      p2p_unbind(e);
-      relayout(e, (size_t)k2);  // survivor slots and divisor
-    }
-    std::vector<ncclComm_t> comms(k2, nullptr);
-    if (k2 > 1 && w->mode != DLC_MODE_P2P) DLC_NCCL(ncclCommInitAll(comms.data(), k2, w->devices.data()));
     for (int r = 0; r < k2; ++r) {
       auto* c = new dlc_collective();
       c->kind = k2 > 1 ? 1 : 0;
@@ -323,6 +319,10 @@ int dlc_world_shrink(dlc_world* w, const int* exclude_ranks, size_t n_exclude, s
       c->shrunk = true;
       for (int j = 0; j < k2; ++j) c->members[j] = w->members[j];
       w->colls.push_back(c);
+    }
+    for (dlc_engine* e : w->engines) {
+      DeviceGuard dg(e->device);
+      relayout(e, (size_t)k2);  // survivor slots and divisor
     }
     if (k2 > 1 && w->mode == DLC_MODE_P2P) world_bind_p2p(w);
   });

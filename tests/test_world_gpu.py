@@ -208,6 +208,47 @@ def test_world_shrink_survivor_rounds(port, k, exclude, prec):
     world.close()
 
 
+@pytest.mark.parametrize("mode", [A.MODE_ORDERED, A.MODE_ALLREDUCE, A.MODE_P2P])
+def test_world_shrink_one_rank_per_gpu(port, mode):
+    """dlc_world_shrink with one rank per GPU: the NCCL worlds get fresh
+    communicators over the survivors' devices, the P2P world re-binds its peer
+    tables; one round over 3 ranks, then two over ranks 0 and 2 (ordered and
+    P2P bitwise, all-reduce within its tolerance)."""
+    if gpus() < 3:
+        pytest.skip("needs 3 GPUs")
+    n, h, seed, k = 30_011, 2, 19, 3
+    hyper = DR.Hyper(inner_lr=1e-3, warmup_steps=2)
+    hp = D.OptimHyperparams(inner_lr=1e-3, warmup_steps=2)
+    theta0 = O.rng_fill(seed, "theta", 0, n, -0.05, 0.05)
+    world = D.World(D.DilocoConfig(h, k, A.FP16, 3 * h), hp, n, [0, 1, 2], mode=mode)
+    for e in world.engines:
+        e.upload(A.THETA_T, theta0)
+        e.upload(A.THETA_LOCAL, theta0)
+    ws = DR.make_workers(theta0, k, hyper)
+    alive, step = [0, 1, 2], 0
+    for rnd in range(3):
+        if rnd == 1:
+            world.shrink([1])
+            alive = [0, 2]
+            assert world.members() == alive
+        for _ in range(h):
+            for idx, w in enumerate(alive):
+                g = O.rng_fill(seed, "grad", w * 1000 + step, n, -1e-2, 1e-2)
+                world.engines[idx].inner_step_host(g)
+                DR.inner_step(port, ws[w], g, hyper)
+            step += 1
+        DR.outer_round(port, [ws[w] for w in alive], A.FP16, hyper)
+        res = world.outer_step()
+        assert res.applied and res.outer_epoch == rnd + 1
+    if mode != A.MODE_ALLREDUCE:
+        check_bitwise(world, [ws[w] for w in alive])
+    else:
+        for idx, w in enumerate(alive):
+            got = world.engines[idx].download(A.THETA_T)
+            assert np.max(np.abs(got - ws[w].theta_t)) <= 1e-3
+    world.close()
+
+
 @pytest.mark.parametrize("k", [9, 16])
 def test_world_shared_device_p2p_wide(port, k):
     """K > 8: the owner fold without a TMA instance (per-thread loads)."""
