@@ -224,7 +224,10 @@ DLC_API int dlc_collective_all_reduce_avg(dlc_collective* c, const float* local_
  *                           then finishes without changing the engine state
  *                           (speculative K4, error-gated finish), and the
  *                           same epoch is retried on the shrunk collective
- *                           (ReduceReport::attempts = 2).
+ *                           (ReduceReport::attempts = 2).  A timed-out
+ *                           collective is marked broken: destroying it aborts
+ *                           the blocked work too (do that before destroying
+ *                           the engine, whose destroy waits for its stream).
  *   dlc_collective_inject_stall
  *                           fault injection (SocketCollective::set_stage_hook,
  *                           test_collective.cpp:485-492): this rank stops

@@ -159,6 +159,7 @@ int dlc_collective_destroy(dlc_collective* c) {
       if (e->cstream) cudaStreamSynchronize(e->cstream);
       p2p_unbind(e);  // removes e from c->bound
     }
+    while (!c->watchers.empty()) unwatch(c->watchers.back());
     if (c->kind == 1) {
       DeviceGuard dg(c->device);
       if (c->stream) cudaStreamDestroy(c->stream);

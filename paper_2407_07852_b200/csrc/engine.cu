@@ -152,6 +152,8 @@ int dlc_engine_destroy(dlc_engine* e) {
       cudaStreamSynchronize(e->stream);
     }
     p2p_unbind(e);
+    unwatch(e);
+    if (e->watch_ev) cudaEventDestroy(e->watch_ev);
     for (void* p : e->allocs) cudaFree(p);
     if (e->wire_rows) cudaFree(e->wire_rows);
     for (const auto& mk : e->pending) {

@@ -34,6 +34,7 @@ struct dlc_collective {
   int64_t stall_at = -1;               // fault injection: stop arriving from this barrier on (-1 off)
   int64_t barriers = 0;                // P2P barriers issued on this collective
   std::vector<dlc_engine*> bound;      // engines whose peer tables map this collective's members
+  std::vector<dlc_engine*> watchers;   // engines whose last NCCL round on it is watched (engine::watch_coll)
 };
 
 struct dlc_engine {
@@ -103,6 +104,7 @@ struct dlc_engine {
   std::chrono::steady_clock::time_point deadline{};
   uint64_t watch_ms = 0;
   cudaEvent_t watch_ev = nullptr;
+  dlc_collective* watch_coll = nullptr;  // marked broken on a timeout (its destroy then aborts, not waits)
   bool nccl_failed = false;  // reported; drained and reset at the next outer step
   std::vector<void*> ipc_opened;
   // host-buffer path: copy streams and per-chunk events
@@ -187,7 +189,8 @@ DevState read_state(dlc_engine* e);
 // watched NCCL round passes its deadline (the stream may then stay blocked
 // until the caller shrinks the collective with DLC_SHRINK_ABORT).
 void stream_wait(dlc_engine* e);
-void watch_round(dlc_engine* e, const dlc_collective* c);
+void watch_round(dlc_engine* e, dlc_collective* c);
+void unwatch(dlc_engine* e);
 // The failed round's commit gate: ncclAllReduce(MAX) of the error word, so
 // every rank's finish takes the same decision, then the speculative K4 of
 // the whole vector and the finish (abort = the error word).

@@ -211,9 +211,21 @@ void ensure_tables(dlc_engine* e, uint64_t t_max) {
   e->tab_cap = cap;
 }
 
-void watch_round(dlc_engine* e, const dlc_collective* c) {
+void unwatch(dlc_engine* e) {
+  if (!e->watch_coll) return;
+  auto& v = e->watch_coll->watchers;
+  v.erase(std::remove(v.begin(), v.end(), e), v.end());
+  e->watch_coll = nullptr;
+}
+
+void watch_round(dlc_engine* e, dlc_collective* c) {
   if (!e->watch_ev) DLC_CUDA(cudaEventCreateWithFlags(&e->watch_ev, cudaEventDisableTiming));
   DLC_CUDA(cudaEventRecord(e->watch_ev, e->stream));
+  if (e->watch_coll != c) {
+    unwatch(e);
+    e->watch_coll = c;
+    c->watchers.push_back(e);
+  }
   e->watched = true;
   e->watch_ms = c->timeout_ms;
   e->deadline = std::chrono::steady_clock::now() + std::chrono::milliseconds(c->timeout_ms);
@@ -235,6 +247,7 @@ void stream_wait(dlc_engine* e) {
       e->watched = false;
       e->nccl_failed = true;
       e->failed_tries += 1;
+      if (e->watch_coll) e->watch_coll->broken = true;  // its peers are gone: destroy aborts it
       ensure_copy_streams(e);
       DLC_CUDA(cudaMemsetAsync(e->sig_err, 1, 1, e->h2d));
       DLC_CUDA(cudaStreamSynchronize(e->h2d));
