@@ -100,3 +100,15 @@ def test_null_arguments_are_einval():
     assert A.lib.dlc_engine_destroy(None) == A.OK
     assert A.lib.dlc_collective_world_size(None) == 1
     assert A.lib.dlc_engine_size(C.c_void_p()) == 0
+
+
+def test_round2_entry_points_validate_without_gpu():
+    # round-2 entry points: argument checks come before any device work
+    assert A.lib.dlc_world_shrink(None, None, 0, 0) == A.EINVAL
+    assert A.lib.dlc_world_members(None, None, 0) == 0
+    assert A.lib.dlc_engine_set_fused_delta(None, 1) == A.EINVAL
+    assert b"null" in A.lib.dlc_last_error()
+    t = A.P2PTuning()
+    t.fold_kernel = 2
+    assert A.lib.dlc_p2p_set_tuning(C.byref(t)) == A.ECONFIG
+    assert A.lib.dlc_p2p_set_tuning(None) == A.OK
