@@ -26,6 +26,21 @@ __device__ __forceinline__ void st_stream(uint2* p, uint2 v) { __stcs(p, v); }
 __device__ __forceinline__ uint4 ld_stream(const uint4* p) { return __ldcs(p); }
 __device__ __forceinline__ void st_stream(uint4* p, uint4 v) { __stcs(p, v); }
 
+// The exchange's FP16 / FP32 delta stores (K2 pieces) and the mean loads (K4
+// pieces).  DLC_EXCHANGE_L2 (an A/B build, tools/): default caching, so a
+// piece may still sit in L2 when the owners pull it / after the owners pushed it.
+#ifdef DLC_EXCHANGE_L2
+__device__ __forceinline__ void st_exchange(float4* p, float4 v) { *p = v; }
+__device__ __forceinline__ void st_exchange(uint2* p, uint2 v) { *p = v; }
+__device__ __forceinline__ float4 ld_exchange(const float4* p) { return *p; }
+__device__ __forceinline__ uint2 ld_exchange(const uint2* p) { return *p; }
+#else
+__device__ __forceinline__ void st_exchange(float4* p, float4 v) { st_stream(p, v); }
+__device__ __forceinline__ void st_exchange(uint2* p, uint2 v) { st_stream(p, v); }
+__device__ __forceinline__ float4 ld_exchange(const float4* p) { return ld_stream(p); }
+__device__ __forceinline__ uint2 ld_exchange(const uint2* p) { return ld_stream(p); }
+#endif
+
 __device__ __forceinline__ bool finite_f(float x) {
   return (__float_as_uint(x) & 0x7F800000u) != 0x7F800000u;
 }

@@ -185,9 +185,9 @@ __device__ __forceinline__ void pseudo_grad_piece_block(const float* T, const fl
     const float4 d = make_float4(delta_elem(x.x, y.x), delta_elem(x.y, y.y), delta_elem(x.z, y.z),
                                  delta_elem(x.w, y.w));
     if (PREC == 0) {
-      st_stream(reinterpret_cast<float4*>(static_cast<float*>(send) + e0), d);
+      st_exchange(reinterpret_cast<float4*>(static_cast<float*>(send) + e0), d);
     } else {
-      st_stream(reinterpret_cast<uint2*>(static_cast<uint16_t*>(send) + e0),
+      st_exchange(reinterpret_cast<uint2*>(static_cast<uint16_t*>(send) + e0),
                 make_uint2(pack2(fp16_encode(d.x), fp16_encode(d.y)), pack2(fp16_encode(d.z), fp16_encode(d.w))));
     }
   } else {
@@ -223,8 +223,8 @@ __device__ __forceinline__ void nesterov_p2p_piece_block(const float* T, const f
   const void* dbar = slots.ptr[q];
   const size_t o0 = po + 4 * j;  // offset inside owner q's mean slot
   if (e0 + 3 < n) {
-    const float4 d = PREC == 0 ? ld_stream(reinterpret_cast<const float4*>(static_cast<const float*>(dbar) + o0))
-                               : decode4(ld_stream(reinterpret_cast<const uint2*>(
+    const float4 d = PREC == 0 ? ld_exchange(reinterpret_cast<const float4*>(static_cast<const float*>(dbar) + o0))
+                               : decode4(ld_exchange(reinterpret_cast<const uint2*>(
                                      static_cast<const uint16_t*>(dbar) + o0)));
     const float4 t = ld_stream(reinterpret_cast<const float4*>(T + e0));
     float4 b = ld_stream(reinterpret_cast<const float4*>(B + e0)), o;
