@@ -1,4 +1,5 @@
 # 2/4-GPU A/B: exchange stores / loads with default caching (variants/l2) vs streaming hints (product), alternating builds (development script)
+# builds the variant first: make -C paper_2407_07852_b200/csrc EXTRA=-DDLC_EXCHANGE_L2 BUILD=/tmp/build_l2 OUT=$PWD/paper_2407_07852_b200/variants/l2/libdiloco_cuda.so
 O=gpurun_out/r2v
 mkdir -p $O
 L=paper_2407_07852_b200/libdiloco_cuda.so
