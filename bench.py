@@ -119,7 +119,10 @@ def nvlink_from_profile(k, n, fp16):
             "algorithmic_bytes_per_direction": 2 * (k - 1) * (-(-n // k)) * 2,
             "own_fold_link_bytes_tx": link_tx, "fold_alone_ms": alone_ms,
             "fold_alone_user_gbs_per_direction": user_rx / (alone_ms * 1e-3) / 1e9,
-            "fold_alone_link_tx_gbs": link_tx / (alone_ms * 1e-3) / 1e9}
+            "fold_alone_link_tx_gbs": link_tx / (alone_ms * 1e-3) / 1e9,
+            "fold_alone_link_frac_of_900": link_tx / (alone_ms * 1e-3) / 1e9 / 900.0,
+            "note": "the fold's bound is NVLink, not HBM: kernels_alone.fold_push runs it over local rows on one "
+                    "GPU (no links), this is the same kernel moving its bytes over NVLink"}
 
 
 def pcie_probe():
