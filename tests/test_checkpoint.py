@@ -172,3 +172,60 @@ def test_failed_load_changes_nothing(gpu, tmp_path):
             assert np.array_equal(bits(e.download(w)), bits(o.download(w))), w
     for e in engines + twins + other:
         e.close()
+
+
+@pytest.mark.gpu
+def test_checkpoint_hook_after_fused_boundary(gpu, tmp_path):
+    """run_training's on_round hook (the reference's checkpoint hook,
+    engine.hpp:154) after one worker's FUSED window boundary: the file holds
+    the boundary's state (theta_local following theta_t, the new moments), and
+    an engine resumed from it continues bit-identically to the uninterrupted
+    run and to the two-step path."""
+    D = gpu
+    n, h, rounds = 40_009, 3, 4
+    hyper = D.OptimHyperparams(inner_lr=1e-3, warmup_steps=2)
+    th = O.rng_fill(3, "theta", 0, n, -0.1, 0.1)
+    grads = [O.rng_fill(3, "grad", t, n, -1e-2, 1e-2) for t in range(h * rounds)]
+    grads[5][7] = np.inf  # an overflow on a window's last step (the gated rerun)
+
+    def engine(fused):
+        e = D.DilocoEngine(D.DilocoConfig(h, 1, D.FP16, h * rounds), hyper, n)
+        e.set_fused_delta(fused)
+        e.upload(D.THETA_T, th)
+        e.upload(D.THETA_LOCAL, th)
+        return e
+
+    paths = []
+
+    def run(e, hook):
+        gptr = e.device_ptr(D.GRAD)
+
+        def producer(step):
+            e.upload(D.GRAD, grads[step])
+            return gptr, False, 0.0
+        return D.run_training(e, None, producer, on_round=hook)
+
+    a = engine(True)
+
+    def save(rounds_done):
+        if rounds_done == 2:
+            p = str(tmp_path / "r2.ckpt")
+            D.checkpoint_save([a], p, completed_rounds=rounds_done)
+            paths.append(p)
+    run(a, save)
+    twostep = engine(False)
+    run(twostep, None)
+    for w in (D.THETA_T, D.THETA_LOCAL, D.ADAM_M, D.ADAM_V, D.MOMENTUM):
+        assert np.array_equal(bits(a.download(w)), bits(twostep.download(w))), w
+    b = engine(True)
+    D.checkpoint_load([b], paths[0])
+    assert b.scalars().inner_step == 2 * h and b.scalars().outer_epoch == 2
+    gptr = b.device_ptr(D.GRAD)
+    opt = D.DilocoOptimizer(b)
+    for t in range(2 * h, h * rounds):
+        b.upload(D.GRAD, grads[t])
+        opt.step(gptr, grad_is_scaled=False)
+    for w in (D.THETA_T, D.THETA_LOCAL, D.ADAM_M, D.ADAM_V, D.MOMENTUM):
+        assert np.array_equal(bits(a.download(w)), bits(b.download(w))), w
+    for e in (a, b, twostep):
+        e.close()
