@@ -64,7 +64,7 @@ def plan_of(args, n):
     """The piece plan of the P2P / pipelined all-reduce step (engine_util.cu piece_plan)."""
     if args.plan:
         return [int(x) for x in args.plan.split(",")]
-    return [1, 3, 3, 1] if n < 400_000_000 else [1, 1, 2, 2, 1, 1]
+    return [1, 2, 2, 1] if n < 400_000_000 else [1, 1, 2, 2, 1, 1]
 
 
 def dist_env():

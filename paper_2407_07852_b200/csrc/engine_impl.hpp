@@ -161,9 +161,10 @@ constexpr int kFoldCtas = 256;
 void* dalloc(dlc_engine* e, size_t bytes);
 // Piece boundaries inside an owner slot of S elements, for a vector of n
 // elements per worker.  Measured defaults (dlc_p2p_set_tuning overrides):
-// 1,1,2,2,1,1 eighths, or 1,3,3,1 below 400M elements per worker, where the
+// 1,1,2,2,1,1 eighths, or 1,2,2,1 below 400M elements per worker, where the
 // step is ~1 ms and per-piece costs outweigh a shorter fill / drain (150M:
-// 1.00 vs 1.07 ms at 4 GPUs, 0.89 vs 0.95 ms at 2, profiles/r1_sweep_150m_*).
+// 0.99 vs 1.07 ms at 4 GPUs, 0.88 vs 0.95 ms at 2 against the 1.1B plan;
+// 1,3,3,1 1.00 / 0.90 ms; profiles/r1_sweep_150m_*, r2_sweep_150m_*).
 // host_path: the e2e call with host buffers, where the step is PCIe-bound and
 // the pipeline fill / drain is one piece of H2D / D2H: 16 equal pieces.
 constexpr size_t kSmallStepElems = 400000000;

@@ -45,7 +45,7 @@ std::vector<size_t> piece_plan(size_t S, size_t n, bool host_path) {
   } else if (host_path) {
     w.assign(16, 1);
   } else if (n < kSmallStepElems) {
-    w = {1, 3, 3, 1};
+    w = {1, 2, 2, 1};
   } else {
     w = {1, 1, 2, 2, 1, 1};  // short first and last pieces shrink the pipeline's fill and drain
   }
