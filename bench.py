@@ -54,7 +54,7 @@ def parse():
     ap.add_argument("--no-wire", action="store_true")
     ap.add_argument("--no-training", action="store_true")
     ap.add_argument("--no-boundary", action="store_true")
-    ap.add_argument("--plan", default=None, help="P2P piece plan override, e.g. 1,1,2,2,1,1 (dlc_p2p_set_tuning)")
+    ap.add_argument("--plan", default=None, help="P2P piece plan override, e.g. 1,2,3,2,1 (dlc_p2p_set_tuning)")
     ap.add_argument("--fold-ctas", type=int, default=0)
     ap.add_argument("--fold-threads", type=int, default=0)
     return ap.parse_args()
@@ -64,7 +64,7 @@ def plan_of(args, n):
     """The piece plan of the P2P / pipelined all-reduce step (engine_util.cu piece_plan)."""
     if args.plan:
         return [int(x) for x in args.plan.split(",")]
-    return [1, 2, 2, 1] if n < 400_000_000 else [1, 1, 2, 2, 1, 1]
+    return [1, 2, 2, 1] if n < 400_000_000 else [1, 2, 3, 2, 1]
 
 
 def dist_env():
@@ -103,7 +103,7 @@ def nvlink_from_profile(k, n, fp16):
     if not launches or n != 1_100_000_000 or not fp16:
         return None
     dev0 = [x for x in launches if x["device"] == 0]
-    w = [1, 1, 2, 2, 1, 1]  # the default piece plan at this size: one step's fold launches per GPU
+    w = [1, 1, 2, 2, 1, 1]  # the piece plan of that capture: one step's fold launches per GPU
     step = dev0[:len(w)]
     if not step:
         return None

@@ -242,7 +242,7 @@ DLC_API int dlc_collective_set_reduce_timeout_ms(dlc_collective* c, uint64_t ms)
 DLC_API int dlc_collective_inject_stall(dlc_collective* c, int64_t barrier_index);
 
 /* DLC_MODE_P2P tuning (development sweeps; no reference counterpart).  All
- * fields zero = the measured defaults: piece plan 1,1,2,2,1,1
+ * fields zero = the measured defaults: piece plan 1,2,3,2,1
  * (1,2,2,1 below 400M params per worker, 16 equal pieces on the host-buffer
  * path), max(16, 320 / K) fold CTAs, 128 / 256 / 512 fold threads for
  * K <= 4 / <= 6 / <= 8, one piece-kernel CTA per 256-vector window.

@@ -161,7 +161,9 @@ constexpr int kFoldCtas = 256;
 void* dalloc(dlc_engine* e, size_t bytes);
 // Piece boundaries inside an owner slot of S elements, for a vector of n
 // elements per worker.  Measured defaults (dlc_p2p_set_tuning overrides):
-// 1,1,2,2,1,1 eighths, or 1,2,2,1 below 400M elements per worker, where the
+// 1,2,3,2,1 ninths (r2: 6.22 vs 6.27 ms at 4 GPUs, 5.88 vs 5.96 at 2 against
+// round 1's 1,1,2,2,1,1, profiles/r2_ab_plan_1p1b_*), or 1,2,2,1 below 400M
+// elements per worker, where the
 // step is ~1 ms and per-piece costs outweigh a shorter fill / drain (150M:
 // 0.99 vs 1.07 ms at 4 GPUs, 0.88 vs 0.95 ms at 2 against the 1.1B plan;
 // 1,3,3,1 1.00 / 0.90 ms; profiles/r1_sweep_150m_*, r2_sweep_150m_*).

@@ -47,7 +47,7 @@ std::vector<size_t> piece_plan(size_t S, size_t n, bool host_path) {
   } else if (n < kSmallStepElems) {
     w = {1, 2, 2, 1};
   } else {
-    w = {1, 1, 2, 2, 1, 1};  // short first and last pieces shrink the pipeline's fill and drain
+    w = {1, 2, 3, 2, 1};  // short first and last pieces shrink the pipeline's fill and drain
   }
   size_t sum = 0;
   for (size_t x : w) sum += x;
