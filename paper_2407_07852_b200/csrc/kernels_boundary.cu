@@ -19,9 +19,16 @@ namespace {
 // in by the finalize when the inner step applies), theta_t' and momentum' to
 // the idle outer pair (flipped in when the inner step applied and every delta
 // was finite).
+#ifndef DLC_BOUNDARY_MINB  // min resident CTAs per SM (6: 40 registers; r2 A/B: 6.28 vs 6.49 ms at 1.1B)
+#define DLC_BOUNDARY_MINB 6
+#endif
+#if DLC_BOUNDARY_MINB > 0
+#define DLC_BOUNDARY_BOUNDS __launch_bounds__(kThreads, DLC_BOUNDARY_MINB)
+#else
+#define DLC_BOUNDARY_BOUNDS __launch_bounds__(kThreads)
+#endif
 template <int PREC>
-__global__ void __launch_bounds__(kThreads) boundary_solo_kernel(AdamWArgs a, Pair ttp, Pair bufp, float lr,
-                                                                 float mu) {
+__global__ void DLC_BOUNDARY_BOUNDS boundary_solo_kernel(AdamWArgs a, Pair ttp, Pair bufp, float lr, float mu) {
   DevState* st = a.st;
   const int cur = st->cur, nxt = cur ^ 1, oc = st->ocur;
   const uint64_t t = st->step_count + 1;

@@ -18,7 +18,10 @@ namespace {
 // K1: fused unscale + overflow OR + AdamW.
 // =============================================================================
 
-constexpr int kU1 = 1;  // vectors per thread (tools/tune_stream: best for 4R3W)
+// vectors per thread (tools/tune_stream: best for 4R3W).  Round 2 A/B of
+// builds (profiles/r2_ab_k1_builds.jsonl): 2 vectors with >= 4 CTAs per SM,
+// or 1 vector with >= 8 CTAs per SM (32 registers), run within 1% of this one.
+constexpr int kU1 = 1;
 
 // FUSE 0: plain K1.  FUSE 1 / 2: K2 fused in (the last inner step of a window,
 // K > 1, dlc_engine_set_fused_delta): delta = theta_t[ocur] - p' (tensor.cpp:126,
