@@ -423,7 +423,8 @@ def measure_training_loop(D, coll, n, k, prec, local, max_over_ranks, barrier, h
 
 # ---- the window boundary: K2 fused into the last inner step vs the outer step's own K2 -------
 
-def measure_window_boundary(D, coll, n, k, prec, local, max_over_ranks, barrier, windows=4, warmup=1):
+def measure_window_boundary(D, coll, n, k, prec, local, max_over_ranks, barrier, windows=4, warmup=1,
+                            inner_mode=0):
     """The last inner step of a window plus the outer step that follows it
     (DilocoOptimizer::step at inner_step % H == 0, engine.cpp:162-174), timed
     with CUDA events on the engine stream around exactly those two calls, H = 2
@@ -439,7 +440,7 @@ def measure_window_boundary(D, coll, n, k, prec, local, max_over_ranks, barrier,
     variants = [("unfused", False), ("fused", True)]
     total = h * len(variants) * (warmup + windows)
     cfg = D.DilocoConfig(local_steps_h=h, num_workers_k=k, reduce_precision=prec, total_inner_steps=total)
-    e = D.DilocoEngine(cfg, D.OptimHyperparams(), n, local)
+    e = D.DilocoEngine(cfg, D.OptimHyperparams(), n, local, inner_mode)
     opt = D.DilocoOptimizer(e, coll)
     e.rng_fill(D.THETA_T, 4242, "theta", 0, -0.05, 0.05)
     e.rng_fill(D.THETA_LOCAL, 4242, "theta", 0, -0.05, 0.05)
@@ -481,12 +482,15 @@ def measure_window_boundary(D, coll, n, k, prec, local, max_over_ranks, barrier,
         out[name] = {key + "_ms": max_over_ranks(statistics.mean(v)) for key, v in
                      (("boundary", r["ms"]), ("k1", r["k1"]), ("k2", r["k2"]), ("k4", r["k4"]))}
     out["fused_saves_ms"] = out["unfused"]["boundary_ms"] - out["fused"]["boundary_ms"]
-    if k == 1:  # the fused pass is one kernel: 40 B/param (theta_local, g, m, v, theta_t, momentum in; m, v, theta_t, momentum out)
+    if k == 1:  # the fused pass: 40 B/param (theta_local, g, m, v, theta_t, momentum in; m, v, theta_t, momentum out);
+        # INPLACE engines: + the 4 B/param overflow pre-pass and the theta_local store = 48
         peak, kind = measured_peak()
-        ach = 40 * n / (out["fused"]["k1_ms"] * 1e-3) / 1e9
-        out["fused"]["roofline"] = {"kernel": "boundary_solo_kernel (K1+K2+K4)", "bytes_per_param": 40,
+        bpp = 40 if inner_mode == 0 else 48
+        ach = bpp * n / (out["fused"]["k1_ms"] * 1e-3) / 1e9
+        out["fused"]["roofline"] = {"kernel": "boundary_solo_kernel (K1+K2+K4)" if inner_mode == 0 else
+                                    "unscale_check + boundary_solo_inplace_kernel (K1+K2+K4)", "bytes_per_param": bpp,
                                     "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                                    "peak_source": kind, "traffic": ncu_traffic("boundary_solo_kernel", n)}
+                                    "peak_source": kind, "traffic": ncu_traffic("boundary_solo_kernel", n) if inner_mode == 0 else None}
     out.update({"windows_each": windows, "local_steps_h": h,
                 "what": "last inner step (K1) + outer step, CUDA events on the engine stream, variants interleaved; "
                         "k1 / k2 / k4 = summed event-timed phases of that boundary (k4: busy time of the pieces)"})
@@ -725,7 +729,8 @@ def run_ours(args):
         line["wire"] = measure_wire(D, eng, n, prec, cpu=not args.no_cpu_baseline)
     eng.close()
     if not args.no_boundary:
-        line["window_boundary"] = measure_window_boundary(D, coll, n, k, prec, local, max_over_ranks, barrier)
+        line["window_boundary"] = measure_window_boundary(D, coll, n, k, prec, local, max_over_ranks, barrier,
+                                                          inner_mode=inner_mode)
     if not args.no_training:
         line["training_loop"] = measure_training_loop(D, coll, n, k, prec, local, max_over_ranks, barrier)
         if n > 150_000_000:  # the paper's Llama-150M size (configs 2-3): ~0.6 ms inner steps

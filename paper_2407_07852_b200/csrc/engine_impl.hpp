@@ -203,7 +203,7 @@ void unalias(dlc_engine* e);
 float* writable(dlc_engine* e, int which);
 void engine_inner(dlc_engine* e, const float* grad, int grad_is_scaled);
 // The window boundary of a single worker as one fused pass (launch_boundary_solo):
-// usable when the next inner step completes a window, K = 1, PINGPONG, and the
+// usable when the next inner step completes a window, K = 1 (either inner mode), and the
 // collective is the solo one.  engine_boundary_solo = that inner step + the
 // outer step (engine.cpp:162-174).
 bool boundary_solo_ok(const dlc_engine* e, const dlc_collective* c);

@@ -363,7 +363,7 @@ void engine_inner(dlc_engine* e, const float* grad, int grad_is_scaled) {
 }
 
 bool boundary_solo_ok(const dlc_engine* e, const dlc_collective* c) {
-  return e->fuse_delta && e->k == 1 && e->inner_mode == DLC_INNER_PINGPONG && (!c || c->kind == 0) &&
+  return e->fuse_delta && e->k == 1 && (!c || c->kind == 0) &&
          (e->issued_inner + 1) % e->cfg.local_steps_h == 0 && e->issued_inner < e->cfg.total_inner_steps;
 }
 
@@ -372,7 +372,11 @@ void engine_boundary_solo(dlc_engine* e, const float* grad, int grad_is_scaled) 
   e->delta_fused = false;
   DLC_CUDA(cudaMemsetAsync(&e->st->delta_nonfinite, 0, sizeof(int), e->stream));
   phase_begin(e);
-  launch_boundary_solo(a, tt_pair(e), buf_pair(e), e->prec, e->hyper.outer_lr, e->hyper.outer_momentum, e->stream);
+  if (e->inner_mode == DLC_INNER_PINGPONG)
+    launch_boundary_solo(a, tt_pair(e), buf_pair(e), e->prec, e->hyper.outer_lr, e->hyper.outer_momentum, e->stream);
+  else
+    launch_boundary_solo_inplace(a, tt_pair(e), buf_pair(e), e->prec, e->hyper.outer_lr, e->hyper.outer_momentum,
+                                 e->stream);
   phase_end(e, DLC_PHASE_INNER);
   launched("boundary_solo");
   e->issued_inner += 1;

@@ -115,6 +115,16 @@ void launch_adamw_plain(const float* p, const float* g, float* m, float* v, floa
 // solo outer step from the unchanged one (DevState::redo; ~10 us when idle).
 void launch_boundary_solo(const AdamWArgs& a, Pair theta_t, Pair buf, int precision, float lr, float mu,
                           cudaStream_t s);
+// The same for DLC_INNER_INPLACE engines (fixed theta_local / m / v addresses):
+// the overflow pre-pass first (4 B/param), then ONE in-place pass that applies
+// the inner step unless it overflowed and the outer step from the resulting
+// theta_local, storing theta_t' into theta_local as well (44 B/param; 48 with
+// the pre-pass, against 32 + 24 as two steps); a skipped outer step restores
+// theta_local := theta_t in the finish (outer_solo_finish_kernel).
+void launch_boundary_solo_inplace(const AdamWArgs& a, Pair theta_t, Pair buf, int precision, float lr, float mu,
+                                  cudaStream_t s);
+// INPLACE K1's pre-pass: found_inf |= !isfinite(g * (1 / scale)).
+void launch_unscale_check(const float* g, DevState* st, size_t n, cudaStream_t s);
 
 // K2 --------------------------------------------------------------------------
 // The outer step's K2 after a fused K1 (AdamWArgs::delta): a persistent grid

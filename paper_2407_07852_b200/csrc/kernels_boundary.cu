@@ -129,6 +129,73 @@ __global__ void boundary_solo_redo_finish_kernel(DevState* st) {
   st->redo = 0;
 }
 
+// DLC_INNER_INPLACE: the pre-pass has decided the overflow (found_inf), so one
+// pass applies the inner step or not, then the outer step from the resulting
+// theta_local, and stores theta_t' speculatively into the idle outer pair AND
+// into theta_local (its fixed address; the finish restores it on a skip).
+template <int PREC>
+__global__ void __launch_bounds__(kThreads) boundary_solo_inplace_kernel(AdamWArgs a, Pair ttp, Pair bufp, float lr,
+                                                                 float mu) {
+  DevState* st = a.st;
+  const bool skip_inner = *(volatile int*)&st->found_inf != 0;
+  const int oc = st->ocur;
+  const uint64_t t = st->step_count + 1;
+  const AdamScalars s{a.b1, a.b2, a.eps, a.wd, a.omb1, a.omb2, a.corr1[t], a.corr2[t], a.lr[t]};
+  const float inv = __fdiv_rn(1.0f, st->scale);
+  const float* T = sel(ttp, oc);
+  const float* B = sel(bufp, oc);
+  float* To = sel(ttp, oc ^ 1);
+  float* Bo = sel(bufp, oc ^ 1);
+  float* P = a.p[0];
+  float* M = a.m[0];
+  float* V = a.v[0];
+  bool bad_out = false;
+  const size_t n4 = a.n / 4, j = gtid();
+  if (j < n4) {
+    const float4 tt = ld_stream(reinterpret_cast<const float4*>(T) + j);
+    float4 p = ld_stream(reinterpret_cast<const float4*>(P) + j);
+    float4 b = ld_stream(reinterpret_cast<const float4*>(B) + j), o;
+    if (!skip_inner) {
+      const float4 g = ld_stream(reinterpret_cast<const float4*>(a.g) + j);
+      float4 m = ld_stream(reinterpret_cast<const float4*>(M) + j);
+      float4 v = ld_stream(reinterpret_cast<const float4*>(V) + j);
+      p.x = adamw_elem(p.x, __fmul_rn(g.x, inv), m.x, v.x, s);
+      p.y = adamw_elem(p.y, __fmul_rn(g.y, inv), m.y, v.y, s);
+      p.z = adamw_elem(p.z, __fmul_rn(g.z, inv), m.z, v.z, s);
+      p.w = adamw_elem(p.w, __fmul_rn(g.w, inv), m.w, v.w, s);
+      st_stream(reinterpret_cast<float4*>(M) + j, m);
+      st_stream(reinterpret_cast<float4*>(V) + j, v);
+    }
+    o.x = nesterov_elem(tt.x, solo_delta<PREC>(tt.x, p.x, bad_out), b.x, lr, mu);
+    o.y = nesterov_elem(tt.y, solo_delta<PREC>(tt.y, p.y, bad_out), b.y, lr, mu);
+    o.z = nesterov_elem(tt.z, solo_delta<PREC>(tt.z, p.z, bad_out), b.z, lr, mu);
+    o.w = nesterov_elem(tt.w, solo_delta<PREC>(tt.w, p.w, bad_out), b.w, lr, mu);
+    st_stream(reinterpret_cast<float4*>(To) + j, o);
+    st_stream(reinterpret_cast<float4*>(Bo) + j, b);
+    st_stream(reinterpret_cast<float4*>(P) + j, o);
+  }
+  if (blockIdx.x == 0 && threadIdx.x < a.n - n4 * 4) {
+    const size_t e = n4 * 4 + threadIdx.x;
+    float pp = P[e], bb = B[e];
+    if (!skip_inner) {
+      float mm = M[e], vv = V[e];
+      pp = adamw_elem(pp, __fmul_rn(a.g[e], inv), mm, vv, s);
+      M[e] = mm;
+      V[e] = vv;
+    }
+    const float o = nesterov_elem(T[e], solo_delta<PREC>(T[e], pp, bad_out), bb, lr, mu);
+    To[e] = o;
+    Bo[e] = bb;
+    P[e] = o;
+  }
+  block_or_flag(bad_out, &st->delta_nonfinite);
+}
+
+// One thread: the inner step's finalize (the pre-pass decided the skip)
+__global__ void boundary_inplace_finalize_kernel(DevState* st, const float* lr_tab) {
+  inner_finalize(st, lr_tab, 0, 0);
+}
+
 }  // namespace
 
 void launch_boundary_solo(const AdamWArgs& a, Pair tt, Pair buf, int precision, float lr, float mu,
@@ -145,6 +212,19 @@ void launch_boundary_solo(const AdamWArgs& a, Pair tt, Pair buf, int precision, 
   else
     boundary_solo_redo_kernel<1><<<num_sms() * 4, kThreads, 0, s>>>(tt, buf, tl, a.st, lr, mu, a.n);
   boundary_solo_redo_finish_kernel<<<1, 1, 0, s>>>(a.st);
+}
+
+void launch_boundary_solo_inplace(const AdamWArgs& a, Pair tt, Pair buf, int precision, float lr, float mu,
+                                  cudaStream_t s) {
+  launch_unscale_check(a.g, a.st, a.n, s);
+  const int grid = grid_window<1>(a.n / 4);
+  if (precision == 0)
+    boundary_solo_inplace_kernel<0><<<grid, kThreads, 0, s>>>(a, tt, buf, lr, mu);
+  else
+    boundary_solo_inplace_kernel<1><<<grid, kThreads, 0, s>>>(a, tt, buf, lr, mu);
+  boundary_inplace_finalize_kernel<<<1, 1, 0, s>>>(a.st, a.lr);
+  // the outer gate: flip theta_t / momentum in, or restore theta_local := theta_t
+  launch_outer_solo_finish(tt, Pair{{a.p[0], a.p[1]}, 0}, a.st, a.n, s);
 }
 
 }  // namespace dlc

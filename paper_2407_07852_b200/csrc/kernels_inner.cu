@@ -157,6 +157,10 @@ void launch_adamw(const AdamWArgs& a, cudaStream_t s) {
   adamw_finalize_kernel<<<1, 1, 0, s>>>(a.st, a.lr, a.pingpong, a.delta != nullptr);
 }
 
+void launch_unscale_check(const float* g, DevState* st, size_t n, cudaStream_t s) {
+  unscale_check_kernel<<<grid_window<2>(n / 4), kThreads, 0, s>>>(g, st, n);
+}
+
 void launch_adamw_plain(const float* p, const float* g, float* m, float* v, float* out, size_t n,
                         const AdamWPlain& a, cudaStream_t s) {
   if (n == 0) return;

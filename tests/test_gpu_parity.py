@@ -718,9 +718,10 @@ def test_run_training_records_and_state(port):
     e.close()
 
 
+@pytest.mark.parametrize("inner_mode", [A.INNER_PINGPONG, A.INNER_INPLACE])
 @pytest.mark.parametrize("fused", [True, False])
 @pytest.mark.parametrize("prec", [A.FP16, A.FP32])
-def test_optimizer_step_fused_solo_boundary(port, prec, fused):
+def test_optimizer_step_fused_solo_boundary(port, prec, fused, inner_mode):
     """DilocoOptimizer::step (engine.cpp:162-174) for one worker: the window's
     last inner step and the SoloCollective outer step as ONE pass
     (launch_boundary_solo, the default) or as two steps, bitwise against the
@@ -740,7 +741,7 @@ def test_optimizer_step_fused_solo_boundary(port, prec, fused):
             g[n - 2] = np.inf
         return g
 
-    e = D.DilocoEngine(D.DilocoConfig(h, 1, prec, h * rounds), hp, n)
+    e = D.DilocoEngine(D.DilocoConfig(h, 1, prec, h * rounds), hp, n, 0, inner_mode)
     e.set_fused_delta(fused)
     e.upload(A.THETA_T, theta0)
     e.upload(A.THETA_LOCAL, theta0)
