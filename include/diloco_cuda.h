@@ -512,7 +512,7 @@ enum { DLC_PHASE_INNER = 0, DLC_PHASE_PSEUDO = 1, DLC_PHASE_COLLECTIVE = 2, DLC_
 DLC_API int dlc_engine_set_timing(dlc_engine* e, int on);
 DLC_API int dlc_engine_phase_times(dlc_engine* e, double total_ms[4], uint64_t count[4]);
 
-/* One worker (num_workers_k = 1, PINGPONG, solo collective): dlc_optimizer_step
+/* One worker (num_workers_k = 1, solo collective, either inner mode): dlc_optimizer_step
  * and dlc_run_training run the window's last inner step and the outer step as
  * ONE fused pass (K1 + K2 + K4, 40 B/param instead of 28 + 20; the outer
  * step's result is bit-identical, and an overflow on that inner step reruns

@@ -134,7 +134,12 @@ __global__ void boundary_solo_redo_finish_kernel(DevState* st) {
 // theta_local, and stores theta_t' speculatively into the idle outer pair AND
 // into theta_local (its fixed address; the finish restores it on a skip).
 template <int PREC>
-__global__ void __launch_bounds__(kThreads) boundary_solo_inplace_kernel(AdamWArgs a, Pair ttp, Pair bufp, float lr,
+#ifdef DLC_INPLACE_MINB  // A/B build knob (tools/): min resident CTAs per SM of the in-place pass
+#define DLC_INPLACE_BOUNDS __launch_bounds__(kThreads, DLC_INPLACE_MINB)
+#else
+#define DLC_INPLACE_BOUNDS __launch_bounds__(kThreads)
+#endif
+__global__ void DLC_INPLACE_BOUNDS boundary_solo_inplace_kernel(AdamWArgs a, Pair ttp, Pair bufp, float lr,
                                                                  float mu) {
   DevState* st = a.st;
   const bool skip_inner = *(volatile int*)&st->found_inf != 0;
