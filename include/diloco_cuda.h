@@ -514,10 +514,10 @@ DLC_API int dlc_engine_phase_times(dlc_engine* e, double total_ms[4], uint64_t c
 
 /* One worker (num_workers_k = 1, solo collective, either inner mode): dlc_optimizer_step
  * and dlc_run_training run the window's last inner step and the outer step as
- * ONE fused pass (K1 + K2 + K4, 40 B/param instead of 28 + 20; the outer
- * step's result is bit-identical, and an overflow on that inner step reruns
- * the outer step from the unchanged theta_local).  On by default; `on` = 0
- * runs them as two steps.
+ * ONE fused pass (K1 + K2 + K4, 40 B/param instead of 28 + 20; INPLACE
+ * engines 48 instead of 32 + 24; the result is bit-identical, and an overflow
+ * on that inner step reruns the outer step from the unchanged theta_local).
+ * On by default; `on` = 0 runs them as two steps.
  * num_workers_k > 1: K2 fused into the window's last inner step (opt-in,
  * default off).  The inner step that completes a window of H also
  * writes delta = theta_t - theta_local' (engine.cpp:115-126, in the reduce
