@@ -418,7 +418,7 @@ def measure_training_loop(D, coll, n, k, prec, local, max_over_ranks, barrier, h
             "wall_ms_per_step": max_over_ranks(wall * 1e3 / steps), "device_ms_per_step": dev_ms / steps,
             "gpu_busy": dev_ms / (wall * 1e3), "records": len(recs),
             "producer": "device-resident loss-scaled gradient (no host copy)",
-            "note": "dlc_run_training: steps enqueued back to back, records emitted one step behind"}
+            "note": "dlc_run_training: steps enqueued back to back, records emitted two steps behind"}
 
 
 # ---- the window boundary: K2 fused into the last inner step vs the outer step's own K2 -------

@@ -15,14 +15,15 @@ extern "C" {
 // The loop never waits for the GPU between inner steps: each step's K1 (and,
 // at a window boundary, the outer round) is enqueued, followed by an
 // asynchronous copy of the engine's device scalars into a pinned ring slot and
-// a timing event.  A step's records are emitted one step behind, once its event
-// has completed, so the GPU always has the next step queued while the host
-// formats records and calls the producer.  At a window boundary the loop
+// a timing event.  A step's records are emitted two steps behind, once its
+// event has completed, so the GPU always has the next two steps queued while
+// the host formats records and calls the producer (one step of slack was not
+// enough to hide the Python callbacks of 0.7 ms steps).  At a window boundary the loop
 // drains when a fleet's barrier check (K > 1) must raise before the next inner
 // step is queued, or when an on_round hook (a checkpoint) must see the
-// boundary's state; otherwise a boundary is emitted one step behind like any
+// boundary's state; otherwise a boundary is emitted two steps behind like any
 // other step.  The record stream is the reference's (engine.cpp:181-238); only the
-// interleaving of producer calls and sink calls differs (producer(t + 1) runs
+// interleaving of producer calls and sink calls differs (producer(t + 2) runs
 // before step t's records are emitted).  compute_ms / comm_ms are CUDA-event
 // times of the step and of its collective on the device, not host wall time.
 int dlc_run_training(dlc_engine* e, dlc_collective* c, dlc_grad_producer producer, dlc_metrics_sink sink,
@@ -134,11 +135,11 @@ int dlc_run_training(dlc_engine* e, dlc_collective* c, dlc_grad_producer produce
       DLC_CUDA(cudaMemcpyAsync(&ring.host[slot], e->st, sizeof(DevState), cudaMemcpyDeviceToHost, e->stream));
       DLC_CUDA(cudaEventRecord(ring.b[slot], e->stream));
       pending.push_back({slot, loss, boundary});
-      // one step behind; drain at a boundary when a fleet's failed round must
+      // two steps behind (kRing = 4 slots: at most 3 in flight); drain at a boundary when a fleet's failed round must
       // raise before the next inner step runs, or when the on_round hook (the
       // checkpoint hook, engine.hpp:154) must see the state of that boundary
       const bool drain = boundary && (e->k > 1 || on_round);
-      while (!pending.empty() && (drain || pending.size() > 1)) {
+      while (!pending.empty() && (drain || pending.size() > 2)) {
         const Pending p = pending.front();
         pending.pop_front();
         emit(p);
