@@ -661,6 +661,12 @@ def run_ours(args):
                              "hbm_peak_gbs": peak, "hbm_bytes_incl_exchange": hbm_bpp * n + hbm_coll,
                              "frac_of_bound_incl_exchange": max(hbm_all_ms, nvl_ms) / ms_step}
     if k > 1:
+        # weak-scaling ceiling: one worker's outer step needs b_solo B/param and no
+        # exchange; K workers each need (K2 + K4 + exchange) HBM bytes or the NVLink
+        # time, whichever is longer, so value(K) / (K value(1)) cannot exceed this
+        solo_ms = b_solo * n / (peak * 1e9) * 1e3
+        line["step_roofline"]["weak_scaling_ceiling"] = solo_ms / max(hbm_all_ms, nvl_ms)
+    if k > 1:
         # algorithmic NVLink bytes per direction (the padded owner slots each GPU
         # serves and receives) over the whole step and over the exchange's busy time
         line["exchange_gbs_per_direction_over_step"] = wire_bytes / (ms_step * 1e-3) / 1e9
