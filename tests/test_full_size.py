@@ -90,6 +90,32 @@ def test_full_size_1p1b_window(port, prec):
     e.close()
 
 
+@pytest.mark.parametrize("overflow_step", [1, 2])
+def test_full_size_1p1b_fused_boundary(port, overflow_step):
+    """One worker's window boundary as ONE pass (DilocoOptimizer::step,
+    boundary_solo_kernel) at 1.1B: H = 3 with the overflow mid-window (1) or on
+    the window's last step (2: the fused outer values are discarded and the
+    gated pass reruns the outer step from the unchanged theta_local); all
+    5 x 1.1B elements compared."""
+    n, h = 1_100_000_000, 3
+    hyper = DR.Hyper(warmup_steps=5)
+    e = D.DilocoEngine(D.DilocoConfig(h, 1, A.FP16, h), _hp(hyper), n)
+    e.rng_fill(A.THETA_T, 4242, "theta", 0, -0.05, 0.05)
+    e.rng_fill(A.THETA_LOCAL, 4242, "theta", 0, -0.05, 0.05)
+    opt = D.DilocoOptimizer(e)
+    for step in range(h):
+        e.rng_fill(A.GRAD, 4242, "grad", step, -1e-2, 1e-2)
+        if step == overflow_step:
+            e.upload_range(A.GRAD, n - 1, [np.inf])
+        opt.step(e.device_ptr(A.GRAD), grad_is_scaled=False)
+    assert opt.round_just_completed
+    sc = e.scalars()
+    assert sc.overflow_skips == 1 and sc.outer_epoch == 1 and sc.last_applied == 1
+    done = compare_whole([e], n, 1 << 23, _oracle_chunk(port, 1, h, 1, A.FP16, hyper, (0, overflow_step)))
+    assert done == 5 * n
+    e.close()
+
+
 @pytest.mark.parametrize("prec", [A.FP32, A.FP16])
 def test_full_size_150m_eight_workers(port, prec):
     """Configs 2 / 3: 150M parameters x 8 workers (8 ranks of a P2P world on one
