@@ -249,10 +249,11 @@ def test_world_shrink_one_rank_per_gpu(port, mode):
     world.close()
 
 
+@pytest.mark.parametrize("prec", [A.FP16, A.FP32])
 @pytest.mark.parametrize("k", [9, 16])
-def test_world_shared_device_p2p_wide(port, k):
+def test_world_shared_device_p2p_wide(port, k, prec):
     """K > 8: the owner fold without a TMA instance (per-thread loads)."""
-    world, ws = run_world(port, k, A.FP16, A.MODE_P2P, [0] * k, n=10_007, overflow=(0, 0))
+    world, ws = run_world(port, k, prec, A.MODE_P2P, [0] * k, n=10_007, overflow=(0, 0))
     check_bitwise(world, ws)
     world.close()
 
