@@ -445,11 +445,12 @@ DLC_API int dlc_optimizer_step(dlc_engine* e, dlc_collective* c, const float* gr
  * inner step, it returns a DEVICE gradient on the engine's device (loss-scaled
  * when *grad_is_scaled), the step's loss, and 0 (non-zero aborts with
  * DLC_EINVAL).  `sink` / `on_round` may be NULL.  Result: RunResult
- * (engine.hpp:142-150).  The loop keeps two steps queued on the GPU: the
- * producer is called for step t + 2 before step t's records reach the sink,
- * so a producer must enqueue its work on the engine's stream (or wait for it)
- * rather than read engine state on the host.  It drains at a window boundary
- * when K > 1 or `on_round` is set, so the hook sees the boundary's state. */
+ * (engine.hpp:142-150).  The loop keeps up to two steps queued on the GPU:
+ * the producer is called for step t + 2 before step t's records reach the
+ * sink.  Every step the producer depends on is enqueued by then, and engine
+ * reads (downloads) synchronize the stream, so a producer sees theta_local
+ * after step t + 1.  It drains at a window boundary when K > 1 or `on_round`
+ * is set, so the hook sees the boundary's state. */
 enum dlc_record_kind { DLC_RECORD_STEP = 0, DLC_RECORD_ROUND = 1, DLC_RECORD_EVENT = 2 };
 typedef struct {
   int kind;
