@@ -642,6 +642,21 @@ def run_ours(args):
                 name: {"ms": t, "bytes_per_param": bpp, "frac": roof(bpp, t)["frac"]}
                 for name, bpp, t in (("pseudo_grad_K2", b_k2, ms3[0]), ("fold_push", 2 * wire, ms3[1]),
                                      ("nesterov_K4", 16 + wire, ms3[2]))}
+            # the warp-specialised fold alone too (the step uses the single-leader one:
+            # tied inside the step, where the fold is NVLink-bound; see nvlink_ncu)
+            from paper_2407_07852_b200 import _capi as A
+            t0 = A.P2PTuning()
+            D.lib.dlc_p2p_get_tuning(ctypes.byref(t0))
+            t1 = A.P2PTuning()
+            ctypes.memmove(ctypes.byref(t1), ctypes.byref(t0), ctypes.sizeof(t0))
+            t1.fold_kernel = 1
+            D.lib.dlc_p2p_set_tuning(ctypes.byref(t1))
+            if D.lib.dlc_p2p_kernels_probe(k, n, prec, 3, ms3) == 0:
+                line["kernels_alone"]["fold_push_warp_specialised"] = {
+                    "ms": ms3[1], "bytes_per_param": 2 * wire, "frac": roof(2 * wire, ms3[1])["frac"]}
+            D.lib.dlc_p2p_set_tuning(ctypes.byref(t0))
+            line["kernels_alone"]["note"] = ("each kernel alone on one GPU over local rows (no NVLink); the fold's "
+                                             "bound in the step is NVLink (nvlink_ncu)")
     # whole-step roofline: HBM bytes at the measured copy peak and
     # NVLink bytes per direction at the pool's measured 770 GB/s peer copy
     # (B200_PROFILING.md); serial = sum, bound = max (perfect overlap).
